@@ -1,0 +1,190 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * gflow_b200 — C-ABI of the B200-native gradient-synchronisation path
+ * (GradientFlow, arXiv 1902.06855). This is the drop-in boundary: the
+ * reference's C++ API (gflow::GradientPool / FusionEngine / SparseState /
+ * ring_allreduce, re-stated in paper_1902_06855_b200/csrc/include/gflow/) and
+ * the gflowpy bindings sit on top of these entry points, and any other host
+ * (ctypes, cgo, JNI) can bind them directly.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. Buffer pointers are DEVICE pointers unless
+ *    stated otherwise; `stream` is a cudaStream_t (NULL = legacy default).
+ *  - Every entry point returns gf_status (0 = OK). Errors map onto the
+ *    reference's exception taxonomy (include/gflow/errors.hpp:11-33) and the
+ *    message is available from gf_last_error() on the calling thread.
+ *  - dtype follows ElementType (include/gflow/buffer.hpp:15): 0 fp32, 1 fp16.
+ *  - Numerics are bit-exact with the reference CPU implementation: the
+ *    binary16 codec clamps instead of overflowing (half.hpp:20-59), fp16
+ *    accumulation widens to fp32 per element (buffer.hpp:60-81), no FMA.
+ *  - "Pool order": tensor id m at offset 0, id 1 last (gradient_pool.cpp:24-31).
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *  gf_encode_f16 / gf_decode_f16    float_to_half_bits / half_bits_to_float  include/gflow/half.hpp:20-87
+ *  gf_accumulate                    accumulate(ScalarBuffer, bytes)         include/gflow/buffer.hpp:60-81
+ *  gf_pack                          GradientPool::write_tensor               src/gradient_pool.cpp:78-105
+ *  gf_unpack                        dense update read g = get(i)*(1/N)       src/trainer.cpp:332-347
+ *  gf_chunk_norms                   GradientPool::chunk_l1 (+ x1/N)          src/gradient_pool.cpp:107-116, src/sparse.cpp:176-184
+ *  gf_csc_correct                   SparseState::correction_pre_allreduce    src/sparse.cpp:57-79, include/gflow/sparse.hpp:34-40
+ *  gf_csc_pack_correct              write_tensor + correction + staging pack src/gradient_pool.cpp:78-105, src/sparse.cpp:57-79,:129-140
+ *  gf_csc_compact / gf_csc_scatter  sparse_exchange staging pack/write-back  src/sparse.cpp:129-140, :162-168
+ *  gf_csc_plan                      sparse_exchange theta windows            src/sparse.cpp:142-158
+ *  gf_select_topk                   select_next_important partial_sort       src/sparse.cpp:189-201
+ *  gf_csc_sgd_update                SparseState::sgd_update / csc_update     src/sparse.cpp:206-224, include/gflow/sparse.hpp:42-51
+ *  gf_dense_sgd_update              dense momentum update loop               src/trainer.cpp:332-347
+ *  gf_comm_*                        Communicator + Transport (data plane)    include/gflow/collectives.hpp:25-61, include/gflow/transport.hpp:96-120
+ *  gf_ring_allreduce[_planned]      ring_allreduce / ring_allreduce_on       src/collectives.cpp:55-97, :174-177
+ *  gf_ring_allreduce_colocated      same, all ranks' buffers on one device   src/collectives.cpp:55-97
+ *  gf_csc_select                    select_next_important (norm allreduce + top-k) src/sparse.cpp:172-204
+ *  gf_ring_traffic                  TrafficStats record_send/recv of the ring include/gflow/transport.hpp:48-91, src/collectives.cpp:69-96
+ */
+#ifndef GFLOW_B200_H
+#define GFLOW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GF_ABI_VERSION 1
+#define GF_MAX_RANKS 16
+#define GF_IPC_HANDLE_BYTES 64
+#define GF_MAX_WINDOWS_PER_LAUNCH 256
+#define GF_THETA_INFINITE UINT64_MAX
+
+typedef enum {
+    GF_OK = 0,
+    GF_ERR_CONFIG = 1,    /* gflow::ConfigError    — bad arguments or call order */
+    GF_ERR_PROTOCOL = 2,  /* gflow::ProtocolError  — ranks disagree (sizes, important set) */
+    GF_ERR_TRANSPORT = 3, /* gflow::TransportError — peer timeout / unreachable / comm poisoned */
+    GF_ERR_TRAINING = 4,  /* gflow::TrainingError */
+    GF_ERR_CUDA = 5       /* CUDA runtime failure (reported as TransportError by the C++ layer) */
+} gf_status;
+
+typedef enum { GF_F32 = 0, GF_F16 = 1 } gf_dtype;
+
+typedef struct gf_comm gf_comm;
+
+int gf_abi_version(void);
+const char* gf_last_error(void);
+/* Number of this library's kernels launched by the calling process so far. */
+uint64_t gf_kernel_launches(void);
+
+/* ---- codec ---------------------------------------------------------------- */
+/* dst[i] = float_to_half_bits(scale * src[i]) (scale == 1 skips the multiply). */
+int gf_encode_f16(const float* src, uint16_t* dst, uint64_t n, float scale, void* stream);
+/* dst[i] = half_bits_to_float(src[i]). */
+int gf_decode_f16(const uint16_t* src, float* dst, uint64_t n, void* stream);
+/* Self-test digest of the DEVICE encoder over fp32 bit patterns [first, first+count):
+ * *digest_dev (device u64, accumulated into) += sum of splitmix64(bits<<16 | enc(bits)). */
+int gf_codec_digest(uint64_t first, uint64_t count, uint64_t* digest_dev, void* stream);
+/* dst[i] = dst[i] + src[i] in the element type (fp16: widen, add in fp32, re-encode). */
+int gf_accumulate(int dtype, void* dst, const void* src, uint64_t n, void* stream);
+
+/* ---- pack / unpack (multi-tensor, one launch per call) ----------------------- */
+/* pool[pool_off[t] + i] = enc(scale * src[t][i]) for i < count[t], t < ntensors.
+ * src/pool_off/count are HOST arrays (copied into the launch); src[t] are device ptrs. */
+int gf_pack(int dtype, void* pool, const float* const* src, const uint64_t* pool_off,
+            const uint64_t* count, int ntensors, float scale, void* stream);
+/* dst[t][i] = dec(pool[pool_off[t] + i]) * (1.0f / world). */
+int gf_unpack(int dtype, const void* pool, float* const* dst, const uint64_t* pool_off,
+              const uint64_t* count, int ntensors, int world, void* stream);
+
+/* ---- CSC kernels ----------------------------------------------------------------- */
+/* norms[c] = (float)sum_i |x_i| over chunk c (exact, as the sequential fp64 sum),
+ * times (1.0f/world) when important != NULL && important[c]. */
+int gf_chunk_norms(int dtype, const void* pool, uint64_t total, uint64_t chunk, uint64_t nc,
+                   const uint8_t* important, int world, float* norms, void* stream);
+/* In place over chunks [first_chunk, first_chunk+num_chunks):
+ * g = dec(pool)+hg ; hg = imp ? 0 : momentum*g ; pool = enc(g). */
+int gf_csc_correct(int dtype, void* pool, float* hg, const uint8_t* important, uint64_t total,
+                   uint64_t chunk, uint64_t nc, uint64_t first_chunk, uint64_t num_chunks,
+                   float momentum, void* stream);
+/* Fused pack + correction + compaction over all tensors: for pool element i in chunk c
+ *   g = dec(enc(src)) + hg ; hg = imp ? 0 : momentum*g ; pool = enc(g) ;
+ *   if imp[c]: staging[coff[c] + (i - c*chunk)] = enc(g).
+ * coff (device, nc entries) comes from gf_csc_plan. staging may be NULL (no compaction). */
+int gf_csc_pack_correct(int dtype, void* pool, float* hg, void* staging,
+                        const uint8_t* important, const uint64_t* coff, uint64_t total,
+                        uint64_t chunk, uint64_t nc, const float* const* src,
+                        const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                        float momentum, void* stream);
+int gf_csc_compact(int dtype, const void* pool, void* staging, const uint8_t* important,
+                   const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
+                   void* stream);
+int gf_csc_scatter(int dtype, void* pool, const void* staging, const uint8_t* important,
+                   const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
+                   void* stream);
+/* From important flags (device): coff[c] = sum of lengths of important chunks < c;
+ * plan[0] = staged elements, plan[1] = important chunk count, plan[2] = window count,
+ * plan[3] = elements per full window (theta policy of sparse.cpp:142-158). */
+int gf_csc_plan(const uint8_t* important, uint64_t total, uint64_t chunk, uint64_t nc,
+                int dtype, uint64_t theta, uint64_t* coff, uint64_t* plan, void* stream);
+/* flags[c] = 1 for the k chunks with largest norm (ties: lower index), else 0. */
+int gf_select_topk(const float* norms, uint64_t nc, uint64_t k, uint8_t* flags, void* stream);
+/* For important chunks: g = dec(pool)*(1/world); u = mom*hu + lr*g; hu = u; w -= u. */
+int gf_csc_sgd_update(int dtype, const void* pool, const uint8_t* important, uint64_t total,
+                      uint64_t chunk, uint64_t nc, int world, float momentum, float lr,
+                      float* hu, float* w, void* stream);
+/* Whole pool: same recurrence as above without importance (trainer.cpp:337-346). */
+int gf_dense_sgd_update(int dtype, const void* pool, uint64_t total, int world, float momentum,
+                        float lr, float* hu, float* w, void* stream);
+
+/* ---- communicator (data plane over NVLink peer memory) ---------------------------- */
+/* Allocates this rank's symmetric heap (heap_bytes, 256-B aligned base) plus flags on
+ * `device`. All ranks must create heaps of the same size. */
+int gf_comm_create(int world, int rank, int device, uint64_t heap_bytes, gf_comm** out);
+int gf_comm_destroy(gf_comm* comm);
+int gf_comm_heap(gf_comm* comm, void** base, uint64_t* bytes);
+/* Cross-process bootstrap: export this rank's handle, gather all ranks' handles
+ * (rank order, world * GF_IPC_HANDLE_BYTES) over any control plane, then connect. */
+int gf_comm_export_handle(gf_comm* comm, void* handle_out);
+int gf_comm_connect_ipc(gf_comm* comm, const void* all_handles);
+/* In-process bootstrap: comms[r] for every rank r, each on a distinct device. */
+int gf_comm_connect_local(gf_comm* const* comms, int world);
+/* Ring order (collectives.hpp:37-38): a permutation of ranks, identical on all ranks. */
+int gf_comm_set_ring_order(gf_comm* comm, const int* order);
+int gf_comm_set_timeout_ms(gf_comm* comm, uint64_t ms);
+/* GF_OK, or GF_ERR_TRANSPORT once a device-side wait timed out (comm is then poisoned). */
+int gf_comm_status(gf_comm* comm);
+int gf_comm_rank(gf_comm* comm);
+int gf_comm_world(gf_comm* comm);
+
+/* In-place allreduce (sum) of nwin windows of the symmetric buffer at heap offset
+ * heap_off. Each window [win_start[w], +win_len[w]) (elements, relative to heap_off)
+ * is split by segment_of and reduced in ring-arrival order (bit-exact with
+ * ring_allreduce). One kernel launch per <= GF_MAX_WINDOWS_PER_LAUNCH windows. */
+int gf_ring_allreduce(gf_comm* comm, int dtype, uint64_t heap_off, const uint64_t* win_start,
+                      const uint64_t* win_len, int nwin, void* stream);
+/* Same with windows described by a device plan written by gf_csc_plan / gf_csc_select. */
+int gf_ring_allreduce_planned(gf_comm* comm, int dtype, uint64_t heap_off,
+                              const uint64_t* plan_dev, void* stream);
+/* Emulation of `world` ranks whose buffers all live on the current device (no waits). */
+int gf_ring_allreduce_colocated(int dtype, void* const* bufs, int world, const int* ring_order,
+                                const uint64_t* win_start, const uint64_t* win_len, int nwin,
+                                void* stream);
+int gf_ring_allreduce_colocated_planned(int dtype, void* const* bufs, int world,
+                                        const int* ring_order, const uint64_t* plan_dev,
+                                        void* stream);
+/* Norm exchange + selection for the next iteration (sparse.cpp:185-201), one kernel:
+ * norms (nc fp32 at heap offset norms_off on every rank) are summed over ranks in
+ * ring order (as the fp32 ring_allreduce would), written back to every rank's local
+ * norms, top-k selected -> flags (device, nc bytes); then coff/plan as gf_csc_plan. */
+int gf_csc_select(gf_comm* comm, uint64_t norms_off, uint64_t nc, uint64_t k,
+                  uint8_t* flags, uint64_t total, uint64_t chunk, int dtype, uint64_t theta,
+                  uint64_t* coff, uint64_t* plan, void* stream);
+int gf_csc_select_colocated(float* const* norms, int world, const int* ring_order,
+                            uint64_t nc, uint64_t k, uint8_t* flags, uint64_t total,
+                            uint64_t chunk, int dtype, uint64_t theta, uint64_t* coff,
+                            uint64_t* plan, void* stream);
+
+/* Payload bytes the reference ring records for one allreduce of len elements at ring
+ * position `position` (collectives.cpp:69-96): 2(N-1) sends of segment_of sizes. */
+int gf_ring_traffic(uint64_t len, int world, int position, int dtype, uint64_t* bytes_sent,
+                    uint64_t* bytes_received, uint64_t* frames_sent);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GFLOW_B200_H */

@@ -1,0 +1,363 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Coarse-grained sparse communication (CSC) kernels.
+//
+//  K2 gf_csc_pack_correct  write_tensor + correction_pre_allreduce + staging pack,
+//                          fused: src/gradient_pool.cpp:78-105, src/sparse.cpp:57-79
+//                          (csc_correct sparse.hpp:34-40), src/sparse.cpp:129-140.
+//                          14 B/element of HBM traffic (4 g + 4 hg in, 2 pool + 4 hg out)
+//                          + 2 B per selected element (staging).
+//  K3 gf_chunk_norms       GradientPool::chunk_l1 (src/gradient_pool.cpp:107-116) for all
+//                          chunks, x1/N for important ones (src/sparse.cpp:176-184).
+//                          The reference sums |x| sequentially in fp64. For an fp16 pool
+//                          every |x| is an integer multiple of 2^-24, so we sum EXACTLY in
+//                          int64 units of 2^-24 (order-free, warp-shuffle + smem tree);
+//                          whenever the exact sum is < 2^53 units every fp64 partial sum
+//                          of the reference was exact too, so the float result is
+//                          bit-identical. Larger sums (|x| averaging > 12k) fall back to a
+//                          sequential fp64 pass. 2 B/element.
+//  gf_csc_compact/scatter  staging pack / write-back (src/sparse.cpp:129-140, :162-168).
+//  gf_select_topk/gf_csc_plan  see select.cuh.
+
+#include <algorithm>
+
+#include "gf_device.cuh"
+#include "gf_internal.cuh"
+#include "select.cuh"
+#include "tensor_table.cuh"
+
+namespace {
+
+constexpr int kNormThreads = 256;
+
+__device__ __forceinline__ uint64_t half_units(uint16_t h) {
+    const uint32_t e = (h >> 10) & 0x1Fu, m = h & 0x3FFu;
+    return e == 0 ? uint64_t(m) : (uint64_t(1024u + m) << (e - 1));
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+
+// One CTA per chunk (grid-stride over chunks).
+__global__ void __launch_bounds__(kNormThreads)
+norms_f16_kernel(const uint16_t* __restrict__ pool, uint64_t total, uint64_t chunk, uint64_t nc,
+                 const uint8_t* __restrict__ imp, float inv_world, float* __restrict__ norms) {
+    __shared__ uint64_t s_sum[kNormThreads / 32];
+    __shared__ int s_nan[kNormThreads / 32];
+    for (uint64_t c = blockIdx.x; c < nc; c += gridDim.x) {
+        const uint64_t b = c * chunk;
+        const uint64_t len = (c + 1 == nc) ? total - b : chunk;
+        const uint16_t* p = pool + b;
+        uint64_t acc = 0;
+        bool nan = false;
+        uint64_t done = 0;
+        if ((b % 8) == 0) {
+            const uint64_t nvec = len / 8;
+            for (uint64_t v = threadIdx.x; v < nvec; v += kNormThreads) {
+                const uint4 x = gfd::ld16_stream(p + 8 * v);
+                const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint16_t lo = uint16_t(w[k] & 0xFFFFu), hi = uint16_t(w[k] >> 16);
+                    nan |= ((lo & 0x7C00u) == 0x7C00u) | ((hi & 0x7C00u) == 0x7C00u);
+                    acc += half_units(lo) + half_units(hi);
+                }
+            }
+            done = nvec * 8;
+        }
+        for (uint64_t i = done + threadIdx.x; i < len; i += kNormThreads) {
+            const uint16_t h = p[i];
+            nan |= (h & 0x7C00u) == 0x7C00u;
+            acc += half_units(h);
+        }
+        acc = warp_sum_u64(acc);
+        const int any_nan = __any_sync(0xFFFFFFFFu, nan);
+        if ((threadIdx.x & 31) == 0) {
+            s_sum[threadIdx.x >> 5] = acc;
+            s_nan[threadIdx.x >> 5] = any_nan;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t s = 0;
+            int n = 0;
+            for (int w = 0; w < kNormThreads / 32; ++w) { s += s_sum[w]; n |= s_nan[w]; }
+            float out;
+            if (n) {
+                // fp16 pools only ever hold the codec's NaN (sign|0x7E00; inf is clamped):
+                // fabs(double) + cast gives the positive quiet NaN.
+                out = gfd::u2f(0x7FC00000u);
+            } else if (s < (1ull << 53)) {
+                out = __double2float_rn(__ull2double_rn(s) * 0x1p-24);
+            } else {
+                double d = 0.0;  // sequential fallback, exactly as the reference
+                for (uint64_t i = 0; i < len; ++i) d = __dadd_rn(d, fabs(double(gfd::dec(p[i]))));
+                out = __double2float_rn(d);
+            }
+            if (imp && imp[c]) out = gfd::mul(out, inv_world);
+            norms[c] = out;
+        }
+        __syncthreads();
+    }
+}
+
+// fp32 pools: fp64 partial sums of fp32 values are not exact in general, so the
+// reference's sequential order is reproduced: CTA stages |x| in smem, one thread adds.
+__global__ void __launch_bounds__(kNormThreads)
+norms_f32_kernel(const float* __restrict__ pool, uint64_t total, uint64_t chunk, uint64_t nc,
+                 const uint8_t* __restrict__ imp, float inv_world, float* __restrict__ norms) {
+    constexpr int kStage = 2048;
+    __shared__ double st[kStage];
+    for (uint64_t c = blockIdx.x; c < nc; c += gridDim.x) {
+        const uint64_t b = c * chunk;
+        const uint64_t len = (c + 1 == nc) ? total - b : chunk;
+        double d = 0.0;
+        for (uint64_t base = 0; base < len; base += kStage) {
+            const uint64_t n = min(uint64_t(kStage), len - base);
+            for (uint64_t i = threadIdx.x; i < n; i += kNormThreads) st[i] = fabs(double(pool[b + base + i]));
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (uint64_t i = 0; i < n; ++i) d = __dadd_rn(d, st[i]);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            float out = __double2float_rn(d);
+            if (imp && imp[c]) out = gfd::mul(out, inv_world);
+            norms[c] = out;
+        }
+    }
+}
+
+// csc_correct element (sparse.hpp:35-40 via sparse.cpp:71-77); returns the new pool value.
+__device__ __forceinline__ float correct_elem(float g, float* hg, bool imp, float mom) {
+    const float gg = gfd::add(g, *hg);
+    *hg = imp ? 0.0f : gfd::mul(mom, gg);
+    return gg;
+}
+
+template <int DT>
+__global__ void correct_kernel(void* __restrict__ pool, float* __restrict__ hg,
+                               const uint8_t* __restrict__ imp, uint64_t total, uint64_t chunk,
+                               uint64_t nc, uint64_t begin, uint64_t end, float mom) {
+    for (uint64_t i = begin + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < end;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t c = min(i / chunk, nc - 1);
+        const bool im = imp[c] != 0;
+        if (DT == GF_F16) {
+            uint16_t* p = static_cast<uint16_t*>(pool);
+            p[i] = gfd::enc(correct_elem(gfd::dec(p[i]), hg + i, im, mom));
+        } else {
+            float* p = static_cast<float*>(pool);
+            p[i] = correct_elem(p[i], hg + i, im, mom);
+        }
+    }
+}
+
+// K2: fused pack + correction + compaction.
+template <int DT>
+__global__ void __launch_bounds__(kThreads)
+pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ pool,
+                    float* __restrict__ hg, void* __restrict__ staging,
+                    const uint8_t* __restrict__ imp, const uint64_t* __restrict__ coff,
+                    uint64_t chunk, uint64_t nc, float mom, uint64_t total_tiles) {
+    for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const int t = find_tensor(T, tile);
+        const uint64_t base = (tile - T.tiles[t]) * kTile;
+        const uint64_t len = min(kTile, T.cnt[t] - base);
+        const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
+        const uint64_t po = T.off[t] + base;
+        uint64_t done = 0;
+        if (DT == GF_F16 && (reinterpret_cast<uintptr_t>(T.ptr[t]) & 15u) == 0 && po % 8 == 0 &&
+            chunk % 8 == 0) {
+            // 8 consecutive pool elements never straddle a chunk boundary here.
+            uint16_t* __restrict__ d = static_cast<uint16_t*>(pool) + po;
+            uint16_t* __restrict__ stg = static_cast<uint16_t*>(staging);
+            const int nvec = int(len / 8);
+            for (int v = threadIdx.x; v < nvec; v += kThreads) {
+                const uint64_t pi = po + 8 * uint64_t(v);
+                const uint64_t c = min(pi / chunk, nc - 1);
+                const bool im = imp[c] != 0;
+                const float4 a = gfd::ld16f_stream(s + 8 * v);
+                const float4 b = gfd::ld16f_stream(s + 8 * v + 4);
+                float4* hp = reinterpret_cast<float4*>(hg + pi);
+                float4 h0 = hp[0], h1 = hp[1];
+                const float g[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+                uint32_t o[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint16_t lo = gfd::enc(correct_elem(gfd::dec(gfd::enc(g[2 * k])), &hv[2 * k], im, mom));
+                    const uint16_t hi = gfd::enc(correct_elem(gfd::dec(gfd::enc(g[2 * k + 1])), &hv[2 * k + 1], im, mom));
+                    o[k] = uint32_t(lo) | (uint32_t(hi) << 16);
+                }
+                hp[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+                hp[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+                const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
+                gfd::st16(d + 8 * v, ov);
+                if (im && stg) gfd::st16(stg + coff[c] + (pi - c * chunk), ov);
+            }
+            done = uint64_t(nvec) * 8;
+        }
+        for (uint64_t i = done + threadIdx.x; i < len; i += kThreads) {
+            const uint64_t pi = po + i;
+            const uint64_t c = min(pi / chunk, nc - 1);
+            const bool im = imp[c] != 0;
+            if (DT == GF_F16) {
+                const uint16_t w = gfd::enc(correct_elem(gfd::dec(gfd::enc(s[i])), hg + pi, im, mom));
+                static_cast<uint16_t*>(pool)[pi] = w;
+                if (im && staging) static_cast<uint16_t*>(staging)[coff[c] + (pi - c * chunk)] = w;
+            } else {
+                const float w = correct_elem(s[i], hg + pi, im, mom);
+                static_cast<float*>(pool)[pi] = w;
+                if (im && staging) static_cast<float*>(staging)[coff[c] + (pi - c * chunk)] = w;
+            }
+        }
+    }
+}
+
+// Staging pack (dir=0) / write-back (dir=1): one CTA-row per chunk, 16-B copies.
+__global__ void compact_kernel(char* __restrict__ pool, char* __restrict__ staging,
+                               const uint8_t* __restrict__ imp, const uint64_t* __restrict__ coff,
+                               uint64_t total, uint64_t chunk, uint64_t nc, uint64_t esz, int dir) {
+    for (uint64_t c = blockIdx.y; c < nc; c += gridDim.y) {
+        if (!imp[c]) continue;
+        const uint64_t len = ((c + 1 == nc) ? total - c * chunk : chunk) * esz;
+        char* p = pool + c * chunk * esz;
+        char* s = staging + coff[c] * esz;
+        const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(s)) & 15u) == 0;
+        uint64_t done = 0;
+        if (vec) {
+            const uint64_t nv = len / 16;
+            for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < nv;
+                 v += uint64_t(gridDim.x) * blockDim.x) {
+                if (dir == 0) gfd::st16(s + 16 * v, gfd::ld16(p + 16 * v));
+                else gfd::st16(p + 16 * v, gfd::ld16(s + 16 * v));
+            }
+            done = nv * 16;
+        }
+        for (uint64_t i = done + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < len;
+             i += uint64_t(gridDim.x) * blockDim.x) {
+            if (dir == 0) s[i] = p[i]; else p[i] = s[i];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(gfs::kSelThreads)
+select_plan_kernel(const float* __restrict__ norms, uint64_t nc, uint64_t k, uint8_t* flags,
+                   int do_select, uint64_t total, uint64_t chunk, uint64_t esz, uint64_t theta,
+                   uint64_t* coff, uint64_t* plan) {
+    __shared__ gfs::SelShared sh;
+    if (do_select) gfs::block_topk(norms, nc, k, flags, sh);
+    __syncthreads();
+    if (coff && plan) gfs::block_plan(flags, total, chunk, nc, esz, theta, coff, plan, sh);
+}
+
+int compact_launch(int dtype, void* pool, const void* staging, const uint8_t* important,
+                   const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc, int dir,
+                   void* stream) {
+    if (!gfi::valid_dtype(dtype) || chunk == 0 || nc == 0)
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_compact/scatter: bad arguments");
+    const uint64_t bytes = std::max<uint64_t>(chunk, total - (nc - 1) * chunk) * gfi::esz(dtype);
+    const int gx = int(std::min<uint64_t>((bytes / 16 + 255) / 256, 16));
+    const int gy = int(std::min<uint64_t>(nc, 65535));
+    compact_kernel<<<dim3(gx, gy), 256, 0, gfi::S(stream)>>>(
+        static_cast<char*>(pool), static_cast<char*>(const_cast<void*>(staging)), important, coff,
+        total, chunk, nc, gfi::esz(dtype), dir);
+    gfi::count_launch();
+    return gfi::check_launch("gf_csc_compact");
+}
+
+}  // namespace
+
+extern "C" {
+
+int gf_chunk_norms(int dtype, const void* pool, uint64_t total, uint64_t chunk, uint64_t nc,
+                   const uint8_t* important, int world, float* norms, void* stream) {
+    if (!gfi::valid_dtype(dtype) || chunk == 0 || nc == 0 || world < 1 || (nc - 1) * chunk >= total)
+        return gfi::fail(GF_ERR_CONFIG, "gf_chunk_norms: bad arguments");
+    const float inv = 1.0f / static_cast<float>(world);
+    const int grid = int(std::min<uint64_t>(nc, uint64_t(gfi::sm_count()) * 16));
+    if (dtype == GF_F16)
+        norms_f16_kernel<<<grid, kNormThreads, 0, gfi::S(stream)>>>(
+            static_cast<const uint16_t*>(pool), total, chunk, nc, important, inv, norms);
+    else
+        norms_f32_kernel<<<grid, kNormThreads, 0, gfi::S(stream)>>>(
+            static_cast<const float*>(pool), total, chunk, nc, important, inv, norms);
+    gfi::count_launch();
+    return gfi::check_launch("gf_chunk_norms");
+}
+
+int gf_csc_correct(int dtype, void* pool, float* hg, const uint8_t* important, uint64_t total,
+                   uint64_t chunk, uint64_t nc, uint64_t first_chunk, uint64_t num_chunks,
+                   float momentum, void* stream) {
+    if (!gfi::valid_dtype(dtype) || chunk == 0 || nc == 0 || first_chunk + num_chunks > nc)
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_correct: chunk range out of bounds");
+    if (num_chunks == 0) return GF_OK;
+    const uint64_t begin = first_chunk * chunk;
+    const uint64_t end = (first_chunk + num_chunks == nc) ? total : (first_chunk + num_chunks) * chunk;
+    const uint64_t n = end - begin;
+    const int grid = grid_for(n, 256);
+    if (dtype == GF_F16)
+        correct_kernel<GF_F16><<<grid, 256, 0, gfi::S(stream)>>>(pool, hg, important, total, chunk, nc, begin, end, momentum);
+    else
+        correct_kernel<GF_F32><<<grid, 256, 0, gfi::S(stream)>>>(pool, hg, important, total, chunk, nc, begin, end, momentum);
+    gfi::count_launch();
+    return gfi::check_launch("gf_csc_correct");
+}
+
+int gf_csc_pack_correct(int dtype, void* pool, float* hg, void* staging,
+                        const uint8_t* important, const uint64_t* coff, uint64_t total,
+                        uint64_t chunk, uint64_t nc, const float* const* src,
+                        const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                        float momentum, void* stream) {
+    if (!gfi::valid_dtype(dtype) || chunk == 0 || nc == 0 || !pool || !hg || !important)
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct: bad arguments");
+    if (staging && !coff) return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct: staging needs coff");
+    (void)total;
+    return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
+                          [&](const TensorTable& T, uint64_t tiles, int grid) {
+                              if (dtype == GF_F16)
+                                  pack_correct_kernel<GF_F16><<<grid, kThreads, 0, gfi::S(stream)>>>(
+                                      T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles);
+                              else
+                                  pack_correct_kernel<GF_F32><<<grid, kThreads, 0, gfi::S(stream)>>>(
+                                      T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles);
+                          });
+}
+
+int gf_csc_compact(int dtype, const void* pool, void* staging, const uint8_t* important,
+                   const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
+                   void* stream) {
+    return compact_launch(dtype, const_cast<void*>(pool), staging, important, coff, total, chunk,
+                          nc, 0, stream);
+}
+
+int gf_csc_scatter(int dtype, void* pool, const void* staging, const uint8_t* important,
+                   const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
+                   void* stream) {
+    return compact_launch(dtype, pool, staging, important, coff, total, chunk, nc, 1, stream);
+}
+
+int gf_csc_plan(const uint8_t* important, uint64_t total, uint64_t chunk, uint64_t nc,
+                int dtype, uint64_t theta, uint64_t* coff, uint64_t* plan, void* stream) {
+    if (!gfi::valid_dtype(dtype) || chunk == 0 || nc == 0 || !coff || !plan)
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_plan: bad arguments");
+    select_plan_kernel<<<1, gfs::kSelThreads, 0, gfi::S(stream)>>>(
+        nullptr, nc, 0, const_cast<uint8_t*>(important), 0, total, chunk, gfi::esz(dtype), theta,
+        coff, plan);
+    gfi::count_launch();
+    return gfi::check_launch("gf_csc_plan");
+}
+
+int gf_select_topk(const float* norms, uint64_t nc, uint64_t k, uint8_t* flags, void* stream) {
+    if (nc == 0 || k == 0) return gfi::fail(GF_ERR_CONFIG, "gf_select_topk: empty selection");
+    select_plan_kernel<<<1, gfs::kSelThreads, 0, gfi::S(stream)>>>(
+        norms, nc, k, flags, 1, 0, 1, 2, 0, nullptr, nullptr);
+    gfi::count_launch();
+    return gfi::check_launch("gf_select_topk");
+}
+
+}  // extern "C"

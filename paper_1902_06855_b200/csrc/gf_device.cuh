@@ -1,0 +1,141 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Device-side numerics of the gradient-sync path, bit-compatible with the
+// reference's host arithmetic (GradientFlow reference, /root/reference/proj):
+//
+//  * enc()/dec(): the reference binary16 codec (include/gflow/half.hpp:20-87):
+//    round-to-nearest-even, but +-inf and overflow CLAMP to +-65504 (0x7BFF)
+//    and NaN encodes as sign|0x7E00. Hardware cvt.rn.f16.f32 does RNE
+//    (incl. subnormals) and returns inf on overflow, so we fix up inf and NaN.
+//  * add/mul/sub(): IEEE single ops with x86 SSE NaN semantics (the reference
+//    is compiled for baseline x86-64 with no FMA): a NaN operand propagates
+//    quieted (first operand first); an invalid op (inf-inf, 0*inf) yields the
+//    x86 "default NaN" 0xFFC00000. __fadd_rn/__fmul_rn are never contracted
+//    into FMA (P2 in SURVEY.md).
+#pragma once
+
+#include <cstdint>
+#include <cuda_fp16.h>
+
+namespace gfd {
+
+__device__ __forceinline__ float u2f(uint32_t u) { return __uint_as_float(u); }
+__device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
+__device__ __forceinline__ bool isnan_(float f) { return (f2u(f) & 0x7FFFFFFFu) > 0x7F800000u; }
+__device__ __forceinline__ float quiet(float f) { return u2f(f2u(f) | 0x00400000u); }
+
+// half.hpp:20-59
+__device__ __forceinline__ uint16_t enc(float v) {
+    const uint32_t b = f2u(v);
+    uint16_t h = __half_as_ushort(__float2half_rn(v));
+    if ((h & 0x7FFFu) >= 0x7C00u) {
+        // inf after rounding (overflow or inf input) clamps; NaN keeps only its sign.
+        const uint16_t sign = static_cast<uint16_t>((b >> 16) & 0x8000u);
+        h = ((b & 0x7FFFFFFFu) > 0x7F800000u) ? static_cast<uint16_t>(sign | 0x7E00u)
+                                               : static_cast<uint16_t>(sign | 0x7BFFu);
+    }
+    return h;
+}
+
+// half.hpp:61-87 (exact; NaN payload and sign preserved)
+__device__ __forceinline__ float dec(uint16_t h) {
+    if ((h & 0x7C00u) == 0x7C00u) {
+        return u2f((static_cast<uint32_t>(h & 0x8000u) << 16) | 0x7F800000u |
+                   (static_cast<uint32_t>(h & 0x3FFu) << 13));
+    }
+    return __half2float(__ushort_as_half(h));
+}
+
+__device__ __forceinline__ float nan_result(float a, float b) {
+    if (isnan_(a)) return quiet(a);
+    if (isnan_(b)) return quiet(b);
+    return u2f(0xFFC00000u);  // x86 default NaN for invalid operations
+}
+__device__ __forceinline__ float add(float a, float b) {
+    const float s = __fadd_rn(a, b);
+    return isnan_(s) ? nan_result(a, b) : s;
+}
+__device__ __forceinline__ float sub(float a, float b) {
+    const float s = __fsub_rn(a, b);
+    return isnan_(s) ? nan_result(a, b) : s;
+}
+__device__ __forceinline__ float mul(float a, float b) {
+    const float s = __fmul_rn(a, b);
+    return isnan_(s) ? nan_result(a, b) : s;
+}
+
+// accumulate (buffer.hpp:71-79): local + incoming, widened and rounded back.
+__device__ __forceinline__ uint16_t acc16(uint16_t local, uint16_t incoming) {
+    return enc(add(dec(local), dec(incoming)));
+}
+
+// 8 x fp16 in a 16-byte vector.
+struct alignas(16) H8 {
+    uint32_t w[4];
+    __device__ __forceinline__ uint16_t get(int i) const {
+        return static_cast<uint16_t>((w[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu);
+    }
+    __device__ __forceinline__ void set(int i, uint16_t v) {
+        const int s = (i & 1) * 16;
+        w[i >> 1] = (w[i >> 1] & ~(0xFFFFu << s)) | (static_cast<uint32_t>(v) << s);
+    }
+};
+
+__device__ __forceinline__ uint4 ld16(const void* p) {
+    return *reinterpret_cast<const uint4*>(p);
+}
+__device__ __forceinline__ void st16(void* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
+// streaming (evict-first) variants for data touched once
+__device__ __forceinline__ uint4 ld16_stream(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float4 ld16f_stream(const float* p) {
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+// fp16 vector accumulate: acc[i] = enc(add(dec(local[i]), dec(acc[i])))
+__device__ __forceinline__ uint4 acc16x8(uint4 local, uint4 acc) {
+    const uint32_t* l = reinterpret_cast<const uint32_t*>(&local);
+    uint32_t* a = reinterpret_cast<uint32_t*>(&acc);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint16_t lo = acc16(static_cast<uint16_t>(l[k] & 0xFFFFu), static_cast<uint16_t>(a[k] & 0xFFFFu));
+        const uint16_t hi = acc16(static_cast<uint16_t>(l[k] >> 16), static_cast<uint16_t>(a[k] >> 16));
+        a[k] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+    }
+    return acc;
+}
+// fp32 vector accumulate: acc[i] = add(local[i], acc[i])
+__device__ __forceinline__ uint4 acc32x4(uint4 local, uint4 acc) {
+    uint4 r;
+    r.x = f2u(add(u2f(local.x), u2f(acc.x)));
+    r.y = f2u(add(u2f(local.y), u2f(acc.y)));
+    r.z = f2u(add(u2f(local.z), u2f(acc.z)));
+    r.w = f2u(add(u2f(local.w), u2f(acc.w)));
+    return r;
+}
+
+// ---- system-scope flags for cross-GPU barriers --------------------------------
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+}  // namespace gfd

@@ -1,0 +1,332 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K1 pack (fp32 per-layer gradients -> fp16/fp32 fusion pool) and K6 unpack
+// (pool -> fp32 per-layer g_avg = dec(pool) * 1/N), plus the elementwise codec,
+// accumulate and momentum-SGD kernels.
+//
+// Reference: GradientPool::write_tensor (src/gradient_pool.cpp:78-105) does one
+// ScalarBuffer::set per element (a software float_to_half_bits, half.hpp:20-59);
+// the dense update loop (src/trainer.cpp:332-347) reads get(i) * inv_world.
+// Here all tensors of a call go out in ONE launch: a tensor table in kernel
+// parameter space, 8192-element tiles per CTA iteration, 128-bit loads/stores
+// (two float4 -> one 16-B fp16 vector), streaming cache hints on data read once.
+// HBM roofline: 6 B/element (4 read + 2 write) for pack and unpack.
+
+#include <algorithm>
+#include <vector>
+
+#include "gf_device.cuh"
+#include "gf_internal.cuh"
+#include "tensor_table.cuh"
+
+namespace {
+
+__device__ __forceinline__ float scaled(float g, float scale, bool do_scale) {
+    return do_scale ? gfd::mul(g, scale) : g;
+}
+
+// ---- K1: pack -----------------------------------------------------------------
+template <int DT>
+__global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ TensorTable T,
+                                                        void* __restrict__ pool, float scale,
+                                                        uint64_t total_tiles) {
+    const bool do_scale = scale != 1.0f;
+    for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const int t = find_tensor(T, tile);
+        const uint64_t base = (tile - T.tiles[t]) * kTile;
+        const uint64_t len = min(kTile, T.cnt[t] - base);
+        const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
+        const uint64_t po = T.off[t] + base;
+        const bool fast = ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 15u) == 0) && (po % 8 == 0);
+        if (DT == GF_F16) {
+            uint16_t* __restrict__ d = static_cast<uint16_t*>(pool) + po;
+            uint64_t done = 0;
+            if (fast) {
+                const int nvec = int(len / 8);
+                float4 a[kVecPerThread], b[kVecPerThread];
+#pragma unroll
+                for (int k = 0; k < kVecPerThread; ++k) {
+                    const int v = threadIdx.x + k * kThreads;
+                    if (v < nvec) {
+                        a[k] = gfd::ld16f_stream(s + 8 * v);
+                        b[k] = gfd::ld16f_stream(s + 8 * v + 4);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < kVecPerThread; ++k) {
+                    const int v = threadIdx.x + k * kThreads;
+                    if (v < nvec) {
+                        uint4 o;
+                        o.x = gfd::enc(scaled(a[k].x, scale, do_scale)) |
+                              (uint32_t(gfd::enc(scaled(a[k].y, scale, do_scale))) << 16);
+                        o.y = gfd::enc(scaled(a[k].z, scale, do_scale)) |
+                              (uint32_t(gfd::enc(scaled(a[k].w, scale, do_scale))) << 16);
+                        o.z = gfd::enc(scaled(b[k].x, scale, do_scale)) |
+                              (uint32_t(gfd::enc(scaled(b[k].y, scale, do_scale))) << 16);
+                        o.w = gfd::enc(scaled(b[k].z, scale, do_scale)) |
+                              (uint32_t(gfd::enc(scaled(b[k].w, scale, do_scale))) << 16);
+                        gfd::st16(d + 8 * v, o);
+                    }
+                }
+                done = uint64_t(nvec) * 8;
+            }
+            for (uint64_t i = done + threadIdx.x; i < len; i += kThreads) {
+                d[i] = gfd::enc(scaled(s[i], scale, do_scale));
+            }
+        } else {
+            float* __restrict__ d = static_cast<float*>(pool) + po;
+            uint64_t done = 0;
+            if (fast) {
+                const int nvec = int(len / 4);
+                for (int v = threadIdx.x; v < nvec; v += kThreads) {
+                    float4 x = gfd::ld16f_stream(s + 4 * v);
+                    if (do_scale) {
+                        x.x = gfd::mul(x.x, scale); x.y = gfd::mul(x.y, scale);
+                        x.z = gfd::mul(x.z, scale); x.w = gfd::mul(x.w, scale);
+                    }
+                    *reinterpret_cast<float4*>(d + 4 * v) = x;
+                }
+                done = uint64_t(nvec) * 4;
+            }
+            for (uint64_t i = done + threadIdx.x; i < len; i += kThreads) {
+                d[i] = scaled(s[i], scale, do_scale);
+            }
+        }
+    }
+}
+
+// ---- K6: unpack ----------------------------------------------------------------
+template <int DT>
+__global__ void __launch_bounds__(kThreads) unpack_kernel(const __grid_constant__ TensorTable T,
+                                                          const void* __restrict__ pool,
+                                                          float inv_world, uint64_t total_tiles) {
+    for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const int t = find_tensor(T, tile);
+        const uint64_t base = (tile - T.tiles[t]) * kTile;
+        const uint64_t len = min(kTile, T.cnt[t] - base);
+        float* __restrict__ d = static_cast<float*>(const_cast<void*>(T.ptr[t])) + base;
+        const uint64_t po = T.off[t] + base;
+        const bool fast = ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 15u) == 0) && (po % 8 == 0);
+        uint64_t done = 0;
+        if (DT == GF_F16) {
+            const uint16_t* __restrict__ s = static_cast<const uint16_t*>(pool) + po;
+            if (fast) {
+                const int nvec = int(len / 8);
+                uint4 x[kVecPerThread];
+#pragma unroll
+                for (int k = 0; k < kVecPerThread; ++k) {
+                    const int v = threadIdx.x + k * kThreads;
+                    if (v < nvec) x[k] = gfd::ld16_stream(s + 8 * v);
+                }
+#pragma unroll
+                for (int k = 0; k < kVecPerThread; ++k) {
+                    const int v = threadIdx.x + k * kThreads;
+                    if (v < nvec) {
+                        const uint32_t* w = reinterpret_cast<const uint32_t*>(&x[k]);
+                        float4 lo, hi;
+                        lo.x = gfd::mul(gfd::dec(uint16_t(w[0] & 0xFFFF)), inv_world);
+                        lo.y = gfd::mul(gfd::dec(uint16_t(w[0] >> 16)), inv_world);
+                        lo.z = gfd::mul(gfd::dec(uint16_t(w[1] & 0xFFFF)), inv_world);
+                        lo.w = gfd::mul(gfd::dec(uint16_t(w[1] >> 16)), inv_world);
+                        hi.x = gfd::mul(gfd::dec(uint16_t(w[2] & 0xFFFF)), inv_world);
+                        hi.y = gfd::mul(gfd::dec(uint16_t(w[2] >> 16)), inv_world);
+                        hi.z = gfd::mul(gfd::dec(uint16_t(w[3] & 0xFFFF)), inv_world);
+                        hi.w = gfd::mul(gfd::dec(uint16_t(w[3] >> 16)), inv_world);
+                        __stcs(reinterpret_cast<float4*>(d + 8 * v), lo);
+                        __stcs(reinterpret_cast<float4*>(d + 8 * v + 4), hi);
+                    }
+                }
+                done = uint64_t(nvec) * 8;
+            }
+            for (uint64_t i = done + threadIdx.x; i < len; i += kThreads) {
+                d[i] = gfd::mul(gfd::dec(s[i]), inv_world);
+            }
+        } else {
+            const float* __restrict__ s = static_cast<const float*>(pool) + po;
+            if (fast) {
+                const int nvec = int(len / 4);
+                for (int v = threadIdx.x; v < nvec; v += kThreads) {
+                    float4 x = *reinterpret_cast<const float4*>(s + 4 * v);
+                    x.x = gfd::mul(x.x, inv_world); x.y = gfd::mul(x.y, inv_world);
+                    x.z = gfd::mul(x.z, inv_world); x.w = gfd::mul(x.w, inv_world);
+                    __stcs(reinterpret_cast<float4*>(d + 4 * v), x);
+                }
+                done = uint64_t(nvec) * 4;
+            }
+            for (uint64_t i = done + threadIdx.x; i < len; i += kThreads) {
+                d[i] = gfd::mul(s[i], inv_world);
+            }
+        }
+    }
+}
+
+// ---- elementwise ----------------------------------------------------------------
+__global__ void encode_kernel(const float* __restrict__ s, uint16_t* __restrict__ d, uint64_t n,
+                              float scale) {
+    const bool do_scale = scale != 1.0f;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        d[i] = gfd::enc(scaled(s[i], scale, do_scale));
+    }
+}
+__global__ void decode_kernel(const uint16_t* __restrict__ s, float* __restrict__ d, uint64_t n) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        d[i] = gfd::dec(s[i]);
+    }
+}
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__global__ void digest_kernel(uint64_t first, uint64_t count, unsigned long long* out) {
+    uint64_t acc = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t b = uint32_t(first + i);
+        acc += splitmix64((uint64_t(b) << 16) | gfd::enc(gfd::u2f(b)));
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xFFFFFFFFu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)acc);
+}
+template <int DT>
+__global__ void accumulate_kernel(void* __restrict__ dst, const void* __restrict__ src, uint64_t n) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        if (DT == GF_F16) {
+            uint16_t* d = static_cast<uint16_t*>(dst);
+            d[i] = gfd::acc16(d[i], static_cast<const uint16_t*>(src)[i]);
+        } else {
+            float* d = static_cast<float*>(dst);
+            d[i] = gfd::add(d[i], static_cast<const float*>(src)[i]);
+        }
+    }
+}
+
+// trainer.cpp:337-346 / csc_update (sparse.hpp:42-51):
+//   g = get(i)*inv ; u = mom*hu + lr*g ; hu = u ; w -= u
+template <int DT>
+__device__ __forceinline__ void sgd_elem(const void* pool, uint64_t i, float inv_world, float mom,
+                                         float lr, float* hu, float* w) {
+    const float x = DT == GF_F16 ? gfd::dec(static_cast<const uint16_t*>(pool)[i])
+                                 : static_cast<const float*>(pool)[i];
+    const float g = gfd::mul(x, inv_world);
+    const float u = gfd::add(gfd::mul(mom, hu[i]), gfd::mul(lr, g));
+    hu[i] = u;
+    w[i] = gfd::sub(w[i], u);
+}
+template <int DT>
+__global__ void dense_sgd_kernel(const void* __restrict__ pool, uint64_t total, float inv_world,
+                                 float mom, float lr, float* __restrict__ hu, float* __restrict__ w) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        sgd_elem<DT>(pool, i, inv_world, mom, lr, hu, w);
+    }
+}
+template <int DT>
+__global__ void csc_sgd_kernel(const void* __restrict__ pool, const uint8_t* __restrict__ imp,
+                               uint64_t total, uint64_t chunk, uint64_t nc, float inv_world,
+                               float mom, float lr, float* __restrict__ hu, float* __restrict__ w) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t c = min(i / chunk, nc - 1);
+        if (imp[c]) sgd_elem<DT>(pool, i, inv_world, mom, lr, hu, w);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int gf_pack(int dtype, void* pool, const float* const* src, const uint64_t* pool_off,
+            const uint64_t* count, int ntensors, float scale, void* stream) {
+    if (!gfi::valid_dtype(dtype)) return gfi::fail(GF_ERR_CONFIG, "gf_pack: bad dtype");
+    if (!pool && ntensors > 0) return gfi::fail(GF_ERR_CONFIG, "gf_pack: null pool");
+    return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
+                          [&](const TensorTable& T, uint64_t tiles, int grid) {
+                              if (dtype == GF_F16)
+                                  pack_kernel<GF_F16><<<grid, kThreads, 0, gfi::S(stream)>>>(T, pool, scale, tiles);
+                              else
+                                  pack_kernel<GF_F32><<<grid, kThreads, 0, gfi::S(stream)>>>(T, pool, scale, tiles);
+                          });
+}
+
+int gf_unpack(int dtype, const void* pool, float* const* dst, const uint64_t* pool_off,
+              const uint64_t* count, int ntensors, int world, void* stream) {
+    if (!gfi::valid_dtype(dtype)) return gfi::fail(GF_ERR_CONFIG, "gf_unpack: bad dtype");
+    if (world < 1) return gfi::fail(GF_ERR_CONFIG, "gf_unpack: world must be >= 1");
+    const float inv_world = 1.0f / static_cast<float>(world);
+    return for_each_table(reinterpret_cast<const void* const*>(dst), pool_off, count, ntensors,
+                          [&](const TensorTable& T, uint64_t tiles, int grid) {
+                              if (dtype == GF_F16)
+                                  unpack_kernel<GF_F16><<<grid, kThreads, 0, gfi::S(stream)>>>(T, pool, inv_world, tiles);
+                              else
+                                  unpack_kernel<GF_F32><<<grid, kThreads, 0, gfi::S(stream)>>>(T, pool, inv_world, tiles);
+                          });
+}
+
+int gf_encode_f16(const float* src, uint16_t* dst, uint64_t n, float scale, void* stream) {
+    if (n == 0) return GF_OK;
+    encode_kernel<<<grid_for(n, 256), 256, 0, gfi::S(stream)>>>(src, dst, n, scale);
+    gfi::count_launch();
+    return gfi::check_launch("gf_encode_f16");
+}
+
+int gf_decode_f16(const uint16_t* src, float* dst, uint64_t n, void* stream) {
+    if (n == 0) return GF_OK;
+    decode_kernel<<<grid_for(n, 256), 256, 0, gfi::S(stream)>>>(src, dst, n);
+    gfi::count_launch();
+    return gfi::check_launch("gf_decode_f16");
+}
+
+int gf_codec_digest(uint64_t first, uint64_t count, uint64_t* digest_dev, void* stream) {
+    if (count == 0) return GF_OK;
+    digest_kernel<<<gfi::sm_count() * 8, 256, 0, gfi::S(stream)>>>(
+        first, count, reinterpret_cast<unsigned long long*>(digest_dev));
+    gfi::count_launch();
+    return gfi::check_launch("gf_codec_digest");
+}
+
+int gf_accumulate(int dtype, void* dst, const void* src, uint64_t n, void* stream) {
+    if (!gfi::valid_dtype(dtype)) return gfi::fail(GF_ERR_CONFIG, "gf_accumulate: bad dtype");
+    if (n == 0) return GF_OK;
+    if (dtype == GF_F16)
+        accumulate_kernel<GF_F16><<<grid_for(n, 256), 256, 0, gfi::S(stream)>>>(dst, src, n);
+    else
+        accumulate_kernel<GF_F32><<<grid_for(n, 256), 256, 0, gfi::S(stream)>>>(dst, src, n);
+    gfi::count_launch();
+    return gfi::check_launch("gf_accumulate");
+}
+
+int gf_dense_sgd_update(int dtype, const void* pool, uint64_t total, int world, float momentum,
+                        float lr, float* hu, float* w, void* stream) {
+    if (!gfi::valid_dtype(dtype) || world < 1)
+        return gfi::fail(GF_ERR_CONFIG, "gf_dense_sgd_update: bad arguments");
+    if (total == 0) return GF_OK;
+    const float inv = 1.0f / static_cast<float>(world);
+    if (dtype == GF_F16)
+        dense_sgd_kernel<GF_F16><<<grid_for(total, 256), 256, 0, gfi::S(stream)>>>(pool, total, inv, momentum, lr, hu, w);
+    else
+        dense_sgd_kernel<GF_F32><<<grid_for(total, 256), 256, 0, gfi::S(stream)>>>(pool, total, inv, momentum, lr, hu, w);
+    gfi::count_launch();
+    return gfi::check_launch("gf_dense_sgd_update");
+}
+
+int gf_csc_sgd_update(int dtype, const void* pool, const uint8_t* important, uint64_t total,
+                      uint64_t chunk, uint64_t nc, int world, float momentum, float lr,
+                      float* hu, float* w, void* stream) {
+    if (!gfi::valid_dtype(dtype) || world < 1 || chunk == 0 || nc == 0)
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_sgd_update: bad arguments");
+    if (total == 0) return GF_OK;
+    const float inv = 1.0f / static_cast<float>(world);
+    if (dtype == GF_F16)
+        csc_sgd_kernel<GF_F16><<<grid_for(total, 256), 256, 0, gfi::S(stream)>>>(pool, important, total, chunk, nc, inv, momentum, lr, hu, w);
+    else
+        csc_sgd_kernel<GF_F32><<<grid_for(total, 256), 256, 0, gfi::S(stream)>>>(pool, important, total, chunk, nc, inv, momentum, lr, hu, w);
+    gfi::count_launch();
+    return gfi::check_launch("gf_csc_sgd_update");
+}
+
+}  // extern "C"

@@ -1,0 +1,667 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K4: ring allreduce over NVLink/NVSwitch peer memory, and K5: the fused
+// norm exchange + top-k selection — plus the communicator (symmetric heap,
+// IPC / in-process bootstrap, cross-GPU flags).
+//
+// Reference: detail::ring_allreduce_on (src/collectives.cpp:55-97) runs n-1
+// reduce-scatter steps (send segment p-s, receive p-s-1, accumulate) and n-1
+// all-gather steps over a Transport. Segment j (segment_of, :47-53) is summed
+// starting at ring position j: ((x_j + x_{j+1}) + ...) + x_{j-1}, rounding to
+// the element type after every add (accumulate, buffer.hpp:60-81).
+//
+// B200 design: no store-and-forward. The rank at ring position p owns segment
+// p of every window: it LOADS that segment from all N ranks' buffers directly
+// over NVLink (in ring order, so the sum is bit-identical to the reference),
+// and STORES the result into all N buffers (the all-gather becomes posted
+// remote writes). Per rank: (N-1)/N*K bytes pulled + (N-1)/N*K pushed — the
+// same 2(N-1)/N*K bus bytes as the ring — in ONE kernel with two cross-GPU
+// barriers (entry: peers' inputs are ready; exit: all pushes into my buffer
+// landed). Each CTA b only pairs with CTA b on the peers, through monotonic
+// 64-bit flags written with st.release.sys and polled with ld.acquire.sys.
+// Waits are bounded (globaltimer) and a timeout poisons the communicator,
+// surfacing as TransportError like the reference's recv timeout (inproc.cpp:28-36).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "gf_device.cuh"
+#include "gf_internal.cuh"
+#include "select.cuh"
+
+namespace {
+
+constexpr int kMaxBlocks = 1024;
+constexpr int kMaxW = GF_MAX_WINDOWS_PER_LAUNCH;
+constexpr int kRingThreads = 512;
+constexpr uint64_t kFlagBytes = uint64_t(kMaxBlocks) * GF_MAX_RANKS * sizeof(uint64_t);
+
+struct RingArgs {
+    char* bufs[GF_MAX_RANKS];            // buffer base of each RANK (peer-mapped)
+    int ring[GF_MAX_RANKS];              // rank at each ring position
+    int world, rank, pos;
+    int nwin;                            // >= 0 explicit windows; -1: read plan
+    uint64_t* flags_local;
+    uint64_t* flags_peer[GF_MAX_RANKS];  // by rank
+    uint64_t entry_val, exit_val, timeout_ns;
+    int* err;
+    const uint64_t* plan;
+    uint64_t wstart[kMaxW];
+    uint64_t wlen[kMaxW];
+};
+
+struct SelArgs {
+    float* norms[GF_MAX_RANKS];          // by rank
+    int ring[GF_MAX_RANKS];
+    int world, rank, p2p;
+    uint64_t nc, k, total, chunk, esz, theta;
+    uint8_t* flags;
+    uint64_t* coff;
+    uint64_t* plan;
+    uint64_t* flags_local;
+    uint64_t* flags_peer[GF_MAX_RANKS];
+    uint64_t entry_val, exit_val, timeout_ns;
+    int* err;
+};
+
+// ---- cross-GPU barrier (CTA b <-> CTA b of every peer) ------------------------
+template <typename A>
+__device__ bool cross_barrier(const A& a, uint64_t val, int* s_ok) {
+    __threadfence_system();  // this thread's prior (remote) stores are performed
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < a.world && t != a.rank) {
+        gfd::st_release_sys(a.flags_peer[t] + blockIdx.x * GF_MAX_RANKS + a.rank, val);
+        const uint64_t* f = a.flags_local + blockIdx.x * GF_MAX_RANKS + t;
+        if (gfd::ld_acquire_sys(f) < val) {
+            const uint64_t t0 = gfd::globaltimer_ns();
+            uint32_t spins = 0;
+            while (gfd::ld_acquire_sys(f) < val) {
+                if ((++spins & 255u) == 0) {
+                    if (*reinterpret_cast<volatile int*>(a.err) != 0) { *s_ok = 0; break; }
+                    if (gfd::globaltimer_ns() - t0 > a.timeout_ns) {
+                        *reinterpret_cast<volatile int*>(a.err) = 1;
+                        *s_ok = 0;
+                        break;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    return *s_ok != 0;
+}
+
+// ---- reduction of one element range [e0, e1) -----------------------------------
+template <int DT>
+struct Vec;
+template <>
+struct Vec<GF_F16> {
+    static constexpr int kElems = 8;
+    __device__ static uint4 acc(uint4 local, uint4 a) { return gfd::acc16x8(local, a); }
+    __device__ static void scalar(const RingArgs& a, const char* const* src, int n, uint64_t e) {
+        uint16_t acc = reinterpret_cast<const uint16_t*>(src[0])[e];
+        for (int t = 1; t < n; ++t) acc = gfd::acc16(reinterpret_cast<const uint16_t*>(src[t])[e], acc);
+        for (int r = 0; r < a.world; ++r) reinterpret_cast<uint16_t*>(a.bufs[r])[e] = acc;
+    }
+};
+template <>
+struct Vec<GF_F32> {
+    static constexpr int kElems = 4;
+    __device__ static uint4 acc(uint4 local, uint4 a) { return gfd::acc32x4(local, a); }
+    __device__ static void scalar(const RingArgs& a, const char* const* src, int n, uint64_t e) {
+        float acc = reinterpret_cast<const float*>(src[0])[e];
+        for (int t = 1; t < n; ++t) acc = gfd::add(reinterpret_cast<const float*>(src[t])[e], acc);
+        for (int r = 0; r < a.world; ++r) reinterpret_cast<float*>(a.bufs[r])[e] = acc;
+    }
+};
+
+template <int DT, int NT>
+__device__ __forceinline__ void reduce_range(const RingArgs& a, int n, int p, uint64_t e0,
+                                             uint64_t e1) {
+    constexpr int VE = Vec<DT>::kElems;
+    constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
+    constexpr int U = NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1);
+    const char* src[NMAX];
+#pragma unroll
+    for (int t = 0; t < NMAX; ++t) src[t] = (t < n) ? a.bufs[a.ring[(p + t) % n]] : nullptr;
+
+    const uint64_t v0 = (e0 + VE - 1) / VE, v1 = e1 / VE;
+    if (v0 >= v1) {  // no aligned vector inside: all scalar, CTA 0
+        if (blockIdx.x == 0)
+            for (uint64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
+        return;
+    }
+    if (blockIdx.x == 0) {
+        for (uint64_t e = e0 + threadIdx.x; e < v0 * VE; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
+        for (uint64_t e = v1 * VE + threadIdx.x; e < e1; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
+    }
+    const uint64_t nv = v1 - v0;
+    const uint64_t per = (nv + gridDim.x - 1) / gridDim.x;
+    const uint64_t vb = v0 + min(nv, per * blockIdx.x);
+    const uint64_t ve = v0 + min(nv, per * (blockIdx.x + 1));
+    for (uint64_t v = vb + threadIdx.x; v < ve; v += uint64_t(blockDim.x) * U) {
+        uint4 x[U][NMAX];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t vv = v + uint64_t(u) * blockDim.x;
+            if (vv < ve) {
+#pragma unroll
+                for (int t = 0; t < NMAX; ++t)
+                    if (t < n) x[u][t] = gfd::ld16(src[t] + vv * 16);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t vv = v + uint64_t(u) * blockDim.x;
+            if (vv < ve) {
+                uint4 acc = x[u][0];
+#pragma unroll
+                for (int t = 1; t < NMAX; ++t)
+                    if (t < n) acc = Vec<DT>::acc(x[u][t], acc);
+#pragma unroll
+                for (int r = 0; r < NMAX; ++r)
+                    if (r < a.world) gfd::st16(a.bufs[r] + vv * 16, acc);
+            }
+        }
+    }
+}
+
+template <int DT, int NT, bool P2P>
+__global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constant__ RingArgs a) {
+    __shared__ int s_ok;
+    if (threadIdx.x == 0) s_ok = 1;
+    const int n = NT > 0 ? NT : a.world;
+    const int p = P2P ? a.pos : int(blockIdx.y);
+    if (P2P && !cross_barrier(a, a.entry_val, &s_ok)) return;
+    int nwin;
+    uint64_t staged = 0, stride = 0;
+    if (a.nwin >= 0) {
+        nwin = a.nwin;
+    } else {
+        staged = a.plan[0];
+        nwin = int(a.plan[2]);
+        stride = a.plan[3];
+    }
+    for (int w = 0; w < nwin; ++w) {
+        uint64_t ws, wl;
+        if (a.nwin >= 0) {
+            ws = a.wstart[w];
+            wl = a.wlen[w];
+        } else {
+            ws = uint64_t(w) * stride;
+            wl = (w == nwin - 1) ? staged - ws : stride;
+        }
+        const uint64_t base = wl / uint64_t(n), rem = wl % uint64_t(n), up = uint64_t(p);
+        const uint64_t so = up * base + min(up, rem);
+        const uint64_t sc = base + (up < rem ? 1 : 0);
+        reduce_range<DT, NT>(a, n, p, ws + so, ws + so + sc);
+    }
+    if (P2P) cross_barrier(a, a.exit_val, &s_ok);
+}
+
+// ---- K5: norm exchange + selection (one CTA) -----------------------------------
+__global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_constant__ SelArgs a) {
+    extern __shared__ float red[];
+    __shared__ int s_ok;
+    __shared__ gfs::SelShared sh;
+    if (threadIdx.x == 0) s_ok = 1;
+    const int n = a.world;
+    if (a.p2p && !cross_barrier(a, a.entry_val, &s_ok)) return;
+    const uint64_t base = a.nc / uint64_t(n), rem = a.nc % uint64_t(n);
+    for (uint64_t i = threadIdx.x; i < a.nc; i += gfs::kSelThreads) {
+        // segment index of element i under segment_of(nc, n, .) (collectives.cpp:47-53)
+        const uint64_t big = rem * (base + 1);
+        const int j = int(i < big ? i / (base + 1) : rem + (i - big) / base);
+        float acc = a.norms[a.ring[j]][i];
+        for (int t = 1; t < n; ++t) acc = gfd::add(a.norms[a.ring[(j + t) % n]][i], acc);
+        red[i] = acc;
+    }
+    if (a.p2p && !cross_barrier(a, a.exit_val, &s_ok)) return;
+    __syncthreads();
+    for (uint64_t i = threadIdx.x; i < a.nc; i += gfs::kSelThreads) {
+        if (a.p2p) {
+            a.norms[a.rank][i] = red[i];
+        } else {
+            for (int r = 0; r < n; ++r) a.norms[r][i] = red[i];
+        }
+    }
+    gfs::block_topk(red, a.nc, a.k, a.flags, sh);
+    if (a.coff && a.plan) gfs::block_plan(a.flags, a.total, a.chunk, a.nc, a.esz, a.theta, a.coff, a.plan, sh);
+}
+
+template <int DT, bool P2P>
+void launch_ring_dt(const RingArgs& a, dim3 grid, cudaStream_t s) {
+    switch (a.world) {
+        case 2: ring_kernel<DT, 2, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
+        case 3: ring_kernel<DT, 3, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
+        case 4: ring_kernel<DT, 4, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
+        case 5: ring_kernel<DT, 5, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
+        case 6: ring_kernel<DT, 6, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
+        case 7: ring_kernel<DT, 7, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
+        case 8: ring_kernel<DT, 8, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
+        default: ring_kernel<DT, 0, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
+    }
+}
+void launch_ring(int dtype, bool p2p, const RingArgs& a, dim3 grid, cudaStream_t s) {
+    if (dtype == GF_F16) {
+        if (p2p) launch_ring_dt<GF_F16, true>(a, grid, s); else launch_ring_dt<GF_F16, false>(a, grid, s);
+    } else {
+        if (p2p) launch_ring_dt<GF_F32, true>(a, grid, s); else launch_ring_dt<GF_F32, false>(a, grid, s);
+    }
+}
+
+// CTAs per rank: enough 512-thread CTAs to keep ~2 MB of NVLink loads in flight,
+// capped at 2 per SM (and by the flag table). Depends only on values identical
+// on every rank, so all ranks launch the same grid (CTA b pairs with CTA b).
+int ring_blocks(uint64_t max_seg_bytes) {
+    const uint64_t per_cta = uint64_t(kRingThreads) * 16 * 4;
+    const uint64_t want = (max_seg_bytes + per_cta - 1) / per_cta;
+    const uint64_t cap = std::min<uint64_t>(kMaxBlocks, uint64_t(gfi::sm_count()) * 2);
+    return int(std::max<uint64_t>(1, std::min(want, cap)));
+}
+
+bool valid_ring(const int* order, int world) {
+    bool seen[GF_MAX_RANKS] = {};
+    for (int i = 0; i < world; ++i) {
+        if (order[i] < 0 || order[i] >= world || seen[order[i]]) return false;
+        seen[order[i]] = true;
+    }
+    return true;
+}
+
+}  // namespace
+
+struct gf_comm {
+    int world = 0, rank = 0, device = 0, pos = 0;
+    int ring[GF_MAX_RANKS] = {};
+    uint64_t heap_bytes = 0;
+    char* alloc = nullptr;                       // [flags | heap]
+    char* peer_alloc[GF_MAX_RANKS] = {};
+    bool ipc_opened[GF_MAX_RANKS] = {};
+    int* err_host = nullptr;
+    int* err_dev = nullptr;
+    uint64_t seq = 0;
+    uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;  // transport.hpp:25 kDefaultTimeout
+    bool connected = false;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int comm_ready(gf_comm* c) {
+    if (!c) return gfi::fail(GF_ERR_CONFIG, "null communicator");
+    if (!c->connected) return gfi::fail(GF_ERR_CONFIG, "communicator not connected");
+    if (c->err_host && *reinterpret_cast<volatile int*>(c->err_host) != 0)
+        return gfi::fail(GF_ERR_TRANSPORT, "communicator poisoned by an earlier peer timeout (rank " +
+                                               std::to_string(c->rank) + ")");
+    return GF_OK;
+}
+
+void fill_common(gf_comm* c, RingArgs& a, uint64_t heap_off) {
+    a.world = c->world;
+    a.rank = c->rank;
+    a.pos = c->pos;
+    for (int r = 0; r < c->world; ++r) {
+        a.bufs[r] = c->peer_alloc[r] + kFlagBytes + heap_off;
+        a.flags_peer[r] = reinterpret_cast<uint64_t*>(c->peer_alloc[r]);
+        a.ring[r] = c->ring[r];
+    }
+    a.flags_local = reinterpret_cast<uint64_t*>(c->alloc);
+    a.timeout_ns = c->timeout_ns;
+    a.err = c->err_dev;
+    c->seq++;
+    a.entry_val = 2 * c->seq + 1;
+    a.exit_val = 2 * c->seq + 2;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gf_comm_create(int world, int rank, int device, uint64_t heap_bytes, gf_comm** out) {
+    if (!out) return gfi::fail(GF_ERR_CONFIG, "gf_comm_create: null out");
+    *out = nullptr;
+    if (world < 1 || world > GF_MAX_RANKS) return gfi::fail(GF_ERR_CONFIG, "world size out of range [1,16]");
+    if (rank < 0 || rank >= world) return gfi::fail(GF_ERR_CONFIG, "rank " + std::to_string(rank) + " outside world");
+    DeviceGuard g(device);
+    auto* c = new gf_comm();
+    c->world = world;
+    c->rank = rank;
+    c->device = device;
+    c->heap_bytes = (heap_bytes + 255) & ~uint64_t(255);
+    for (int i = 0; i < world; ++i) c->ring[i] = i;
+    c->pos = rank;
+    cudaError_t e = cudaMalloc(&c->alloc, kFlagBytes + c->heap_bytes);
+    if (e == cudaSuccess) e = cudaMemset(c->alloc, 0, kFlagBytes);
+    if (e == cudaSuccess) e = cudaHostAlloc(&c->err_host, sizeof(int), cudaHostAllocMapped);
+    if (e == cudaSuccess) {
+        *c->err_host = 0;
+        e = cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0);
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        if (c->alloc) cudaFree(c->alloc);
+        if (c->err_host) cudaFreeHost(c->err_host);
+        delete c;
+        return gfi::cuda_fail(e, "gf_comm_create");
+    }
+    c->peer_alloc[rank] = c->alloc;
+    if (world == 1) c->connected = true;
+    *out = c;
+    return GF_OK;
+}
+
+int gf_comm_destroy(gf_comm* c) {
+    if (!c) return GF_OK;
+    DeviceGuard g(c->device);
+    cudaDeviceSynchronize();
+    for (int r = 0; r < c->world; ++r)
+        if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->peer_alloc[r]);
+    cudaFree(c->alloc);
+    cudaFreeHost(c->err_host);
+    delete c;
+    return GF_OK;
+}
+
+int gf_comm_heap(gf_comm* c, void** base, uint64_t* bytes) {
+    if (!c) return gfi::fail(GF_ERR_CONFIG, "null communicator");
+    if (base) *base = c->alloc + kFlagBytes;
+    if (bytes) *bytes = c->heap_bytes;
+    return GF_OK;
+}
+
+int gf_comm_export_handle(gf_comm* c, void* handle_out) {
+    if (!c || !handle_out) return gfi::fail(GF_ERR_CONFIG, "gf_comm_export_handle: null argument");
+    DeviceGuard g(c->device);
+    cudaIpcMemHandle_t h;
+    GF_CHECK_CUDA(cudaIpcGetMemHandle(&h, c->alloc));
+    static_assert(sizeof(cudaIpcMemHandle_t) == GF_IPC_HANDLE_BYTES, "ipc handle size");
+    std::memcpy(handle_out, &h, GF_IPC_HANDLE_BYTES);
+    return GF_OK;
+}
+
+int gf_comm_connect_ipc(gf_comm* c, const void* all_handles) {
+    if (!c || !all_handles) return gfi::fail(GF_ERR_CONFIG, "gf_comm_connect_ipc: null argument");
+    DeviceGuard g(c->device);
+    const char* hs = static_cast<const char*>(all_handles);
+    for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, hs + size_t(r) * GF_IPC_HANDLE_BYTES, GF_IPC_HANDLE_BYTES);
+        void* p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            gfi::cuda_fail(e, "cudaIpcOpenMemHandle");
+            return gfi::fail(GF_ERR_TRANSPORT, "rank " + std::to_string(c->rank) +
+                                                   ": cannot map peer " + std::to_string(r) +
+                                                   " heap: " + cudaGetErrorString(e));
+        }
+        c->peer_alloc[r] = static_cast<char*>(p);
+        c->ipc_opened[r] = true;
+    }
+    c->connected = true;
+    return GF_OK;
+}
+
+int gf_comm_connect_local(gf_comm* const* comms, int world) {
+    if (!comms || world < 1) return gfi::fail(GF_ERR_CONFIG, "gf_comm_connect_local: bad arguments");
+    for (int r = 0; r < world; ++r) {
+        if (!comms[r] || comms[r]->world != world || comms[r]->rank != r)
+            return gfi::fail(GF_ERR_CONFIG, "gf_comm_connect_local: comms[r] must be rank r of this world");
+        for (int q = 0; q < r; ++q)
+            if (comms[q]->device == comms[r]->device)
+                return gfi::fail(GF_ERR_CONFIG, "gf_comm_connect_local: ranks must use distinct devices "
+                                                "(use the colocated entry points to emulate ranks on one device)");
+    }
+    for (int r = 0; r < world; ++r) {
+        DeviceGuard g(comms[r]->device);
+        for (int q = 0; q < world; ++q) {
+            if (q == r) continue;
+            int can = 0;
+            GF_CHECK_CUDA(cudaDeviceCanAccessPeer(&can, comms[r]->device, comms[q]->device));
+            if (!can)
+                return gfi::fail(GF_ERR_TRANSPORT, "device " + std::to_string(comms[r]->device) +
+                                                       " cannot access peer " + std::to_string(comms[q]->device));
+            cudaError_t e = cudaDeviceEnablePeerAccess(comms[q]->device, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else if (e != cudaSuccess) return gfi::cuda_fail(e, "cudaDeviceEnablePeerAccess");
+            comms[r]->peer_alloc[q] = comms[q]->alloc;
+        }
+        comms[r]->connected = true;
+    }
+    return GF_OK;
+}
+
+int gf_comm_set_ring_order(gf_comm* c, const int* order) {
+    if (!c || !order) return gfi::fail(GF_ERR_CONFIG, "gf_comm_set_ring_order: null argument");
+    if (!valid_ring(order, c->world)) return gfi::fail(GF_ERR_CONFIG, "ring order is not a permutation of ranks");
+    for (int i = 0; i < c->world; ++i) {
+        c->ring[i] = order[i];
+        if (order[i] == c->rank) c->pos = i;
+    }
+    return GF_OK;
+}
+
+int gf_comm_set_timeout_ms(gf_comm* c, uint64_t ms) {
+    if (!c) return gfi::fail(GF_ERR_CONFIG, "null communicator");
+    c->timeout_ns = ms * 1000ull * 1000ull;
+    return GF_OK;
+}
+
+int gf_comm_status(gf_comm* c) {
+    if (!c) return gfi::fail(GF_ERR_CONFIG, "null communicator");
+    if (c->err_host && *reinterpret_cast<volatile int*>(c->err_host) != 0)
+        return gfi::fail(GF_ERR_TRANSPORT, "recv timeout at rank " + std::to_string(c->rank) +
+                                               " (peer did not reach the collective barrier)");
+    return GF_OK;
+}
+
+int gf_comm_rank(gf_comm* c) { return c ? c->rank : -1; }
+int gf_comm_world(gf_comm* c) { return c ? c->world : -1; }
+
+int gf_ring_allreduce(gf_comm* c, int dtype, uint64_t heap_off, const uint64_t* win_start,
+                      const uint64_t* win_len, int nwin, void* stream) {
+    if (int rc = comm_ready(c)) return rc;
+    if (!gfi::valid_dtype(dtype) || nwin < 0 || (nwin > 0 && (!win_start || !win_len)))
+        return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce: bad arguments");
+    if (c->world == 1) return GF_OK;  // collectives.cpp:59
+    const uint64_t es = gfi::esz(dtype);
+    for (int w = 0; w < nwin; ++w)
+        if (heap_off + (win_start[w] + win_len[w]) * es > c->heap_bytes)
+            return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce: window outside the symmetric heap");
+    DeviceGuard g(c->device);
+    for (int first = 0; first < nwin; first += kMaxW) {
+        RingArgs a;
+        std::memset(&a, 0, sizeof(a));
+        a.nwin = std::min(kMaxW, nwin - first);
+        uint64_t max_seg = 0;
+        for (int w = 0; w < a.nwin; ++w) {
+            a.wstart[w] = win_start[first + w];
+            a.wlen[w] = win_len[first + w];
+            max_seg += (a.wlen[w] + c->world - 1) / c->world;
+        }
+        fill_common(c, a, heap_off);
+        launch_ring(dtype, true, a, dim3(ring_blocks(max_seg * es)), gfi::S(stream));
+        gfi::count_launch();
+        if (int rc = gfi::check_launch("gf_ring_allreduce")) return rc;
+    }
+    return GF_OK;
+}
+
+int gf_ring_allreduce_planned(gf_comm* c, int dtype, uint64_t heap_off, const uint64_t* plan_dev,
+                              void* stream) {
+    if (int rc = comm_ready(c)) return rc;
+    if (!gfi::valid_dtype(dtype) || !plan_dev) return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_planned: bad arguments");
+    if (c->world == 1) return GF_OK;
+    DeviceGuard g(c->device);
+    RingArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.nwin = -1;
+    a.plan = plan_dev;
+    fill_common(c, a, heap_off);
+    const uint64_t bound = c->heap_bytes > heap_off ? (c->heap_bytes - heap_off) / c->world : 0;
+    launch_ring(dtype, true, a, dim3(ring_blocks(bound)), gfi::S(stream));
+    gfi::count_launch();
+    return gfi::check_launch("gf_ring_allreduce_planned");
+}
+
+int gf_ring_allreduce_colocated(int dtype, void* const* bufs, int world, const int* ring_order,
+                                const uint64_t* win_start, const uint64_t* win_len, int nwin,
+                                void* stream) {
+    if (!gfi::valid_dtype(dtype) || world < 1 || world > GF_MAX_RANKS || !bufs || nwin < 0)
+        return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_colocated: bad arguments");
+    if (ring_order && !valid_ring(ring_order, world))
+        return gfi::fail(GF_ERR_CONFIG, "ring order is not a permutation of ranks");
+    if (world == 1) return GF_OK;
+    for (int first = 0; first < nwin; first += kMaxW) {
+        RingArgs a;
+        std::memset(&a, 0, sizeof(a));
+        a.world = world;
+        a.nwin = std::min(kMaxW, nwin - first);
+        uint64_t max_seg = 0;
+        for (int w = 0; w < a.nwin; ++w) {
+            a.wstart[w] = win_start[first + w];
+            a.wlen[w] = win_len[first + w];
+            max_seg += (a.wlen[w] + world - 1) / world;
+        }
+        for (int r = 0; r < world; ++r) {
+            a.bufs[r] = static_cast<char*>(bufs[r]);
+            a.ring[r] = ring_order ? ring_order[r] : r;
+        }
+        launch_ring(dtype, false, a, dim3(ring_blocks(max_seg * gfi::esz(dtype)), world), gfi::S(stream));
+        gfi::count_launch();
+        if (int rc = gfi::check_launch("gf_ring_allreduce_colocated")) return rc;
+    }
+    return GF_OK;
+}
+
+int gf_ring_allreduce_colocated_planned(int dtype, void* const* bufs, int world,
+                                        const int* ring_order, const uint64_t* plan_dev,
+                                        void* stream) {
+    if (!gfi::valid_dtype(dtype) || world < 1 || world > GF_MAX_RANKS || !bufs || !plan_dev)
+        return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_colocated_planned: bad arguments");
+    if (ring_order && !valid_ring(ring_order, world))
+        return gfi::fail(GF_ERR_CONFIG, "ring order is not a permutation of ranks");
+    if (world == 1) return GF_OK;
+    RingArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.world = world;
+    a.nwin = -1;
+    a.plan = plan_dev;
+    for (int r = 0; r < world; ++r) {
+        a.bufs[r] = static_cast<char*>(bufs[r]);
+        a.ring[r] = ring_order ? ring_order[r] : r;
+    }
+    launch_ring(dtype, false, a, dim3(gfi::sm_count(), world), gfi::S(stream));
+    gfi::count_launch();
+    return gfi::check_launch("gf_ring_allreduce_colocated_planned");
+}
+
+static int select_launch(SelArgs& a, cudaStream_t s) {
+    const size_t smem = size_t(a.nc) * sizeof(float);
+    if (smem > 200u * 1024u) return gfi::fail(GF_ERR_CONFIG, "gf_csc_select: too many chunks (max 51200)");
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_set[dev]) {
+        GF_CHECK_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_set[dev] = true;
+    }
+    select_kernel<<<1, gfs::kSelThreads, smem, s>>>(a);
+    gfi::count_launch();
+    return gfi::check_launch("gf_csc_select");
+}
+
+int gf_csc_select(gf_comm* c, uint64_t norms_off, uint64_t nc, uint64_t k, uint8_t* flags,
+                  uint64_t total, uint64_t chunk, int dtype, uint64_t theta, uint64_t* coff,
+                  uint64_t* plan, void* stream) {
+    if (int rc = comm_ready(c)) return rc;
+    if (nc == 0 || k == 0 || !flags || !gfi::valid_dtype(dtype) || chunk == 0)
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_select: bad arguments");
+    if (norms_off + nc * 4 > c->heap_bytes) return gfi::fail(GF_ERR_CONFIG, "gf_csc_select: norms outside heap");
+    DeviceGuard g(c->device);
+    SelArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.world = c->world;
+    a.rank = c->rank;
+    a.p2p = c->world > 1 ? 1 : 0;
+    for (int r = 0; r < c->world; ++r) {
+        a.norms[r] = reinterpret_cast<float*>(c->peer_alloc[r] + kFlagBytes + norms_off);
+        a.flags_peer[r] = reinterpret_cast<uint64_t*>(c->peer_alloc[r]);
+        a.ring[r] = c->ring[r];
+    }
+    a.nc = nc; a.k = k; a.total = total; a.chunk = chunk; a.esz = gfi::esz(dtype); a.theta = theta;
+    a.flags = flags; a.coff = coff; a.plan = plan;
+    a.flags_local = reinterpret_cast<uint64_t*>(c->alloc);
+    a.timeout_ns = c->timeout_ns;
+    a.err = c->err_dev;
+    c->seq++;
+    a.entry_val = 2 * c->seq + 1;
+    a.exit_val = 2 * c->seq + 2;
+    return select_launch(a, gfi::S(stream));
+}
+
+int gf_csc_select_colocated(float* const* norms, int world, const int* ring_order, uint64_t nc,
+                            uint64_t k, uint8_t* flags, uint64_t total, uint64_t chunk, int dtype,
+                            uint64_t theta, uint64_t* coff, uint64_t* plan, void* stream) {
+    if (!norms || world < 1 || world > GF_MAX_RANKS || nc == 0 || k == 0 || !flags ||
+        !gfi::valid_dtype(dtype) || chunk == 0)
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_select_colocated: bad arguments");
+    if (ring_order && !valid_ring(ring_order, world))
+        return gfi::fail(GF_ERR_CONFIG, "ring order is not a permutation of ranks");
+    SelArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.world = world;
+    a.p2p = 0;
+    for (int r = 0; r < world; ++r) {
+        a.norms[r] = norms[r];
+        a.ring[r] = ring_order ? ring_order[r] : r;
+    }
+    a.nc = nc; a.k = k; a.total = total; a.chunk = chunk; a.esz = gfi::esz(dtype); a.theta = theta;
+    a.flags = flags; a.coff = coff; a.plan = plan;
+    return select_launch(a, gfi::S(stream));
+}
+
+int gf_ring_traffic(uint64_t len, int world, int position, int dtype, uint64_t* bytes_sent,
+                    uint64_t* bytes_received, uint64_t* frames_sent) {
+    if (world < 1 || position < 0 || position >= world || !gfi::valid_dtype(dtype))
+        return gfi::fail(GF_ERR_CONFIG, "gf_ring_traffic: bad arguments");
+    const uint64_t es = gfi::esz(dtype), n = uint64_t(world);
+    auto seg = [&](int i) {
+        const uint64_t base = len / n, rem = len % n, idx = uint64_t(i);
+        return base + (idx < rem ? 1 : 0);
+    };
+    uint64_t sent = 0, recv = 0, frames = 0;
+    if (world > 1) {
+        const int p = position;
+        for (int s = 0; s < world - 1; ++s) {
+            sent += seg((p - s + world) % world) * es;          // RS send p-s
+            recv += seg((p - s - 1 + world) % world) * es;      // RS recv p-s-1
+            sent += seg((p + 1 - s + world) % world) * es;      // AG send p+1-s
+            recv += seg((p - s + world) % world) * es;          // AG recv p-s
+            frames += 2;
+        }
+    }
+    if (bytes_sent) *bytes_sent = sent;
+    if (bytes_received) *bytes_received = recv;
+    if (frames_sent) *frames_sent = frames;
+    return GF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// SPDX-License-Identifier: Apache-2.0
+// Multi-tensor launch table: the per-layer gradient tensors of one call travel in
+// kernel parameter space (no H2D copy of pointer arrays); CTAs walk 8192-element
+// tiles and binary-search the tile prefix to find their tensor.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+
+#include "gf_internal.cuh"
+
+namespace {
+
+constexpr int kMaxT = 256;
+constexpr int kThreads = 256;
+constexpr uint64_t kTile = 8192;
+constexpr int kVecPerThread = int(kTile / 8 / kThreads);  // 4 x 8-element vectors
+
+struct TensorTable {
+    int n;
+    int pad;
+    uint64_t tiles[kMaxT + 1];  // prefix of tile counts
+    const void* ptr[kMaxT];     // per-tensor device pointer (src for pack, dst for unpack)
+    uint64_t off[kMaxT];        // pool offset (elements)
+    uint64_t cnt[kMaxT];        // element count
+};
+
+__device__ __forceinline__ int find_tensor(const TensorTable& T, uint64_t tile) {
+    int lo = 0, hi = T.n;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (T.tiles[mid] <= tile) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+int grid_for(uint64_t n, int threads) {
+    const uint64_t want = (n + threads - 1) / threads;
+    const uint64_t cap = uint64_t(gfi::sm_count()) * 16;
+    return int(std::max<uint64_t>(1, std::min(want, cap)));
+}
+
+// Splits a host tensor list into tables of <= kMaxT tensors and launches each.
+template <typename Launch>
+int for_each_table(const void* const* ptrs, const uint64_t* off, const uint64_t* cnt, int n,
+                   Launch&& launch) {
+    if (n < 0) return gfi::fail(GF_ERR_CONFIG, "negative tensor count");
+    for (int first = 0; first < n; first += kMaxT) {
+        TensorTable T{};
+        T.n = 0;
+        uint64_t tiles = 0;
+        for (int t = first; t < std::min(n, first + kMaxT); ++t) {
+            if (cnt[t] == 0) continue;
+            if (ptrs[t] == nullptr) return gfi::fail(GF_ERR_CONFIG, "null tensor pointer");
+            T.tiles[T.n] = tiles;
+            T.ptr[T.n] = ptrs[t];
+            T.off[T.n] = off[t];
+            T.cnt[T.n] = cnt[t];
+            tiles += (cnt[t] + kTile - 1) / kTile;
+            T.n++;
+        }
+        T.tiles[T.n] = tiles;
+        if (T.n == 0) continue;
+        const int grid = int(std::min<uint64_t>(tiles, uint64_t(gfi::sm_count()) * 8));
+        launch(T, tiles, grid);
+        gfi::count_launch();
+        if (int rc = gfi::check_launch("multi-tensor kernel")) return rc;
+    }
+    return GF_OK;
+}
+
+
+}  // namespace

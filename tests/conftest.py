@@ -1,0 +1,64 @@
+# SPDX-License-Identifier: Apache-2.0
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs the sm_100a kernels)")
+    config.addinivalue_line("markers", "multigpu(n): needs n GPUs on one box")
+
+
+def _cuda_ok():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        return False
+
+
+def pytest_runtest_setup(item):
+    if item.get_closest_marker("gpu") and not _cuda_ok():
+        pytest.skip("no CUDA device in this container (run under gpurun)")
+    m = item.get_closest_marker("multigpu")
+    if m:
+        import torch
+        need = m.args[0]
+        if torch.cuda.device_count() < need:
+            pytest.skip(f"needs {need} GPUs, have {torch.cuda.device_count()}")
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    from oracle.oracle import Oracle
+    return Oracle()
+
+
+@pytest.fixture(scope="session")
+def reference():
+    from oracle.oracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    return Reference()
+
+
+@pytest.fixture(scope="session")
+def golden():
+    def load(name):
+        return np.load(os.path.join(GOLDEN, name))
+    return load
+
+
+@pytest.fixture(scope="session")
+def gf():
+    """The product's C-ABI (fails loudly if the native library is missing)."""
+    from paper_1902_06855_b200 import capi
+    capi.lib()
+    return capi
