@@ -98,14 +98,31 @@ uint64_t go_codec_digest(uint64_t first, uint64_t count, int nthreads) {
     return acc;
 }
 
+/* x86 SSE addss semantics made explicit (so the oracle does not depend on which operand
+ * its own compiler puts in the destination register): a NaN operand propagates quieted;
+ * if both are NaN the DESTINATION operand wins; an invalid op yields the default NaN
+ * 0xFFC00000 (the hardware produces that itself). The reference's fp16 accumulate has
+ * the incoming value as destination, its fp32 accumulate the local one (measured). */
+static int isnan_f(float x) { return (f2u(x) & 0x7FFFFFFFu) > 0x7F800000u; }
+static float addss(float dst, float src) {
+    if (isnan_f(dst) && isnan_f(src)) return u2f(f2u(dst) | 0x400000u);
+    return dst + src;
+}
+/* buffer.hpp:71-79 */
+static uint16_t acc16(uint16_t local, uint16_t incoming) {
+    return go_f2h(addss(go_h2f(incoming), go_h2f(local)));
+}
+/* buffer.hpp:63-69 */
+static float acc32(float local, float incoming) { return addss(local, incoming); }
+
 /* buffer.hpp:60-81 — dst[i] = dst[i] + src[i]; fp16 widened to fp32 and re-encoded. */
 void go_accumulate(int dtype, void* dst, const void* src, uint64_t n) {
     if (dtype == 0) {
         float* d = (float*)dst; const float* s = (const float*)src;
-        for (uint64_t i = 0; i < n; ++i) d[i] = d[i] + s[i];
+        for (uint64_t i = 0; i < n; ++i) d[i] = acc32(d[i], s[i]);
     } else {
         uint16_t* d = (uint16_t*)dst; const uint16_t* s = (const uint16_t*)src;
-        for (uint64_t i = 0; i < n; ++i) d[i] = go_f2h(go_h2f(d[i]) + go_h2f(s[i]));
+        for (uint64_t i = 0; i < n; ++i) d[i] = acc16(d[i], s[i]);
     }
 }
 
@@ -172,14 +189,15 @@ static void ring_one(int dtype, void* const* bufs, int n, uint64_t base, uint64_
         uint64_t off, cnt;
         go_segment_of(len, n, j, &off, &cnt);
         for (uint64_t e = base + off; e < base + off + cnt; ++e) {
-            float acc = load_el(dtype, bufs[ring[j]], e);
-            if (dtype == 1) acc = go_h2f(go_f2h(acc));
-            for (int t = 1; t < n; ++t) {
-                const float local = load_el(dtype, bufs[ring[(j + t) % n]], e);
-                const float s = local + acc;
-                acc = (dtype == 1) ? go_h2f(go_f2h(s)) : s;
+            if (dtype == 1) {
+                uint16_t acc = ((const uint16_t*)bufs[ring[j]])[e];
+                for (int t = 1; t < n; ++t) acc = acc16(((const uint16_t*)bufs[ring[(j + t) % n]])[e], acc);
+                for (int r = 0; r < n; ++r) ((uint16_t*)bufs[r])[e] = acc;
+            } else {
+                float acc = ((const float*)bufs[ring[j]])[e];
+                for (int t = 1; t < n; ++t) acc = acc32(((const float*)bufs[ring[(j + t) % n]])[e], acc);
+                for (int r = 0; r < n; ++r) ((float*)bufs[r])[e] = acc;
             }
-            for (int r = 0; r < n; ++r) store_el(dtype, bufs[r], e, acc);
         }
     }
 }
@@ -265,7 +283,7 @@ void go_csc_correct(int dtype, void* pool, float* hg, const uint8_t* imp, uint64
         const uint64_t b = c * chunk, len = go_chunk_len(total, chunk, nc, c);
         for (uint64_t i = b; i < b + len; ++i) {
             float g = load_el(dtype, pool, i);
-            g += hg[i];
+            g = addss(g, hg[i]); /* g[i] += hg[i] (sparse.hpp:37) */
             hg[i] = imp[c] ? 0.0f : momentum * g;
             store_el(dtype, pool, i, g);
         }

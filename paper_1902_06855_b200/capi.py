@@ -101,7 +101,7 @@ _RET = {"gf_last_error": C.c_char_p, "gf_kernel_launches": C.c_uint64}
 def header_symbols() -> list[str]:
     """Every function the public header declares."""
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(gf_[a-z0-9_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"^(?:int|const char\*|uint64_t)\s+(gf_[a-z0-9_]+)\s*\(", txt, re.M)))
 
 
 _lib = None

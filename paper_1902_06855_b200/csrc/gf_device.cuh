@@ -65,8 +65,11 @@ __device__ __forceinline__ float mul(float a, float b) {
 }
 
 // accumulate (buffer.hpp:71-79): local + incoming, widened and rounded back.
+// The reference binary (g++ -O2, x86-64) emits addss with the INCOMING value as the
+// destination operand here, so when both are NaN the incoming NaN wins (measured
+// against oracle/_ref). The fp32 branch (buffer.hpp:63-69, `a += b`) keeps the local one.
 __device__ __forceinline__ uint16_t acc16(uint16_t local, uint16_t incoming) {
-    return enc(add(dec(local), dec(incoming)));
+    return enc(add(dec(incoming), dec(local)));
 }
 
 // 8 x fp16 in a 16-byte vector.

@@ -185,3 +185,25 @@ def test_windows_vs_live_reference(oracle, reference):
         _, _, wb, _ = reference.dense_sync(grads, sizes, dtype=1, theta=theta)
         _, wl = oracle.dense_windows(sizes, 2, theta)
         assert list(wl * 2) == list(wb)
+
+
+def test_nan_propagation_vs_live_reference(oracle, reference):
+    """Both-NaN accumulations keep the operand the reference's binary keeps (fp16: incoming,
+    fp32: local) — pinned on NaN-dense data with both signs."""
+    rng = np.random.default_rng(0)
+
+    def nan_dense(n):
+        x = rng.uniform(-1, 1, n).astype(np.float32)
+        m = rng.random(n) < 0.3
+        b = x.view(np.uint32).copy()
+        b[m] = 0x7FC00000 | (rng.integers(0, 2, int(m.sum())).astype(np.uint32) << 31)
+        return b.view(np.float32)
+    for n in (2, 3, 4, 8):
+        for dt in (0, 1):
+            v = [nan_dense(5000) for _ in range(n)]
+            a = [oracle.f2h(z) if dt else z.copy() for z in v]
+            b = [z.copy() for z in a]
+            oracle.ring_allreduce(a, dtype=dt)
+            reference.allreduce(b, dtype=dt)
+            for r in range(n):
+                assert (bits(a[r]) == bits(b[r])).all()
