@@ -37,7 +37,13 @@ namespace {
 constexpr int kMaxBlocks = 1024;
 constexpr int kMaxW = GF_MAX_WINDOWS_PER_LAUNCH;
 constexpr int kRingThreads = 512;
-constexpr uint64_t kFlagBytes = uint64_t(kMaxBlocks) * GF_MAX_RANKS * sizeof(uint64_t);
+// Per-rank flag area at the head of the heap allocation: kMaxBlocks x GF_MAX_RANKS
+// barrier flags (written by peers) followed by kMaxBlocks epoch counters (local only).
+// The epochs live on the device and advance inside the kernels, so a captured CUDA
+// graph can replay the collective: every rank runs the same launch sequence, hence
+// CTA b's epoch is identical on all ranks.
+constexpr uint64_t kFlagWords = uint64_t(kMaxBlocks) * GF_MAX_RANKS;
+constexpr uint64_t kFlagBytes = (kFlagWords + kMaxBlocks) * sizeof(uint64_t);
 
 struct RingArgs {
     char* bufs[GF_MAX_RANKS];            // buffer base of each RANK (peer-mapped)
@@ -46,7 +52,8 @@ struct RingArgs {
     int nwin;                            // >= 0 explicit windows; -1: read plan
     uint64_t* flags_local;
     uint64_t* flags_peer[GF_MAX_RANKS];  // by rank
-    uint64_t entry_val, exit_val, timeout_ns;
+    uint64_t* epochs;                    // local, one per CTA
+    uint64_t timeout_ns;
     int* err;
     const uint64_t* plan;
     uint64_t wstart[kMaxW];
@@ -63,7 +70,8 @@ struct SelArgs {
     uint64_t* plan;
     uint64_t* flags_local;
     uint64_t* flags_peer[GF_MAX_RANKS];
-    uint64_t entry_val, exit_val, timeout_ns;
+    uint64_t* epochs;
+    uint64_t timeout_ns;
     int* err;
 };
 
@@ -173,10 +181,12 @@ __device__ __forceinline__ void reduce_range(const RingArgs& a, int n, int p, ui
 template <int DT, int NT, bool P2P>
 __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constant__ RingArgs a) {
     __shared__ int s_ok;
+    uint64_t epoch = 0;
+    if (P2P) epoch = a.epochs[blockIdx.x];
     if (threadIdx.x == 0) s_ok = 1;
     const int n = NT > 0 ? NT : a.world;
     const int p = P2P ? a.pos : int(blockIdx.y);
-    if (P2P && !cross_barrier(a, a.entry_val, &s_ok)) return;
+    if (P2P && !cross_barrier(a, epoch + 1, &s_ok)) return;
     int nwin;
     uint64_t staged = 0, stride = 0;
     if (a.nwin >= 0) {
@@ -200,7 +210,7 @@ __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constan
         const uint64_t sc = base + (up < rem ? 1 : 0);
         reduce_range<DT, NT>(a, n, p, ws + so, ws + so + sc);
     }
-    if (P2P) cross_barrier(a, a.exit_val, &s_ok);
+    if (P2P && cross_barrier(a, epoch + 2, &s_ok) && threadIdx.x == 0) a.epochs[blockIdx.x] = epoch + 2;
 }
 
 // ---- K5: norm exchange + selection (one CTA) -----------------------------------
@@ -210,7 +220,8 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
     __shared__ gfs::SelShared sh;
     if (threadIdx.x == 0) s_ok = 1;
     const int n = a.world;
-    if (a.p2p && !cross_barrier(a, a.entry_val, &s_ok)) return;
+    const uint64_t epoch = a.p2p ? a.epochs[0] : 0;
+    if (a.p2p && !cross_barrier(a, epoch + 1, &s_ok)) return;
     const uint64_t base = a.nc / uint64_t(n), rem = a.nc % uint64_t(n);
     for (uint64_t i = threadIdx.x; i < a.nc; i += gfs::kSelThreads) {
         // segment index of element i under segment_of(nc, n, .) (collectives.cpp:47-53)
@@ -220,7 +231,10 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
         for (int t = 1; t < n; ++t) acc = gfd::add(a.norms[a.ring[(j + t) % n]][i], acc);
         red[i] = acc;
     }
-    if (a.p2p && !cross_barrier(a, a.exit_val, &s_ok)) return;
+    if (a.p2p) {
+        if (!cross_barrier(a, epoch + 2, &s_ok)) return;
+        if (threadIdx.x == 0) a.epochs[0] = epoch + 2;
+    }
     __syncthreads();
     for (uint64_t i = threadIdx.x; i < a.nc; i += gfs::kSelThreads) {
         if (a.p2p) {
@@ -284,7 +298,6 @@ struct gf_comm {
     bool ipc_opened[GF_MAX_RANKS] = {};
     int* err_host = nullptr;
     int* err_dev = nullptr;
-    uint64_t seq = 0;
     uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;  // transport.hpp:25 kDefaultTimeout
     bool connected = false;
 };
@@ -323,11 +336,9 @@ void fill_common(gf_comm* c, RingArgs& a, uint64_t heap_off) {
         a.ring[r] = c->ring[r];
     }
     a.flags_local = reinterpret_cast<uint64_t*>(c->alloc);
+    a.epochs = a.flags_local + kFlagWords;
     a.timeout_ns = c->timeout_ns;
     a.err = c->err_dev;
-    c->seq++;
-    a.entry_val = 2 * c->seq + 1;
-    a.exit_val = 2 * c->seq + 2;
 }
 
 }  // namespace
@@ -609,11 +620,9 @@ int gf_csc_select(gf_comm* c, uint64_t norms_off, uint64_t nc, uint64_t k, uint8
     a.nc = nc; a.k = k; a.total = total; a.chunk = chunk; a.esz = gfi::esz(dtype); a.theta = theta;
     a.flags = flags; a.coff = coff; a.plan = plan;
     a.flags_local = reinterpret_cast<uint64_t*>(c->alloc);
+    a.epochs = a.flags_local + kFlagWords;
     a.timeout_ns = c->timeout_ns;
     a.err = c->err_dev;
-    c->seq++;
-    a.entry_val = 2 * c->seq + 1;
-    a.exit_val = 2 * c->seq + 2;
     return select_launch(a, gfi::S(stream));
 }
 

@@ -1,0 +1,225 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Multi-GPU parity of the NVLink peer-memory path (one process per GPU, IPC-mapped heaps,
+exactly the bench's launch model), plus the in-process multi-device bootstrap.
+
+Each worker builds every rank's inputs deterministically, so it can compute the oracle
+result for the whole world locally and compare its own rank bit-for-bit.
+"""
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu]
+
+F16, F32 = 1, 0
+HEAP = 256 << 20
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _setup(rank, world, port):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    from paper_1902_06855_b200 import capi, cudart
+    torch.cuda.set_device(rank)
+    cudart.set_device(rank)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    comm = C.c_void_p()
+    capi.call("gf_comm_create", world, rank, rank, HEAP, C.byref(comm))
+    h = (C.c_char * capi.GF_IPC_HANDLE_BYTES)()
+    capi.call("gf_comm_export_handle", comm, h)
+    hs = [None] * world
+    dist.all_gather_object(hs, bytes(h))
+    capi.call("gf_comm_connect_ipc", comm, b"".join(hs))
+    base = C.c_void_p()
+    capi.call("gf_comm_heap", comm, C.byref(base), None)
+    return comm, base.value, capi, cudart, dist
+
+
+def _put(cudart, base, off, arr):
+    arr = np.ascontiguousarray(arr)
+    cudart.memcpy(base + off, arr.ctypes.data, arr.nbytes)
+    cudart.sync_device()
+
+
+def _get(cudart, base, off, like):
+    out = np.empty_like(like)
+    cudart.memcpy(out.ctypes.data, base + off, out.nbytes)
+    cudart.sync_device()
+    return out
+
+
+def _bits(a):
+    return a.view(np.uint16) if a.itemsize == 2 else a.view(np.uint32)
+
+
+def _worker_ring(rank, world, port):
+    comm, base, capi, cudart, dist = _setup(rank, world, port)
+    from oracle.oracle import RESNET50, Oracle
+    o = Oracle()
+    # (1) ResNet-50 fp16 pool, theta = 1 MiB windows (bit-exact vs the oracle ring)
+    pools = [o.pack(o.gen_grads(50 + r, RESNET50), RESNET50, dtype=F16) for r in range(world)]
+    ws, wl = o.dense_windows(RESNET50, 2, 1 << 20)
+    _put(cudart, base, 0, pools[rank])
+    capi.call("gf_ring_allreduce", comm, F16, 0, capi.u64_array(ws), capi.u64_array(wl), len(ws), None)
+    got = _get(cudart, base, 0, pools[rank])
+    want = o.ring_allreduce([p.copy() for p in pools], dtype=F16, windows=(ws, wl))
+    assert (got == want[rank]).all(), "resnet windows"
+    # (2) random lengths, both dtypes, a non-identity ring order, NaN-bearing data
+    rng = np.random.default_rng(7)
+    order = rng.permutation(world).astype(np.int32)
+    capi.call("gf_comm_set_ring_order", comm, capi.int_array(order))
+    for L in (1, 5, 8, 97, 4099, 1 << 20, 3_000_001):
+        for dt in (F16, F32):
+            vals = []
+            for r in range(world):
+                rr = np.random.default_rng(1000 * L + 10 * r + dt)
+                x = rr.uniform(-100, 100, L).astype(np.float32)
+                x[rr.random(L) < 0.001] = np.nan
+                vals.append(o.f2h(x) if dt == F16 else x)
+            _put(cudart, base, 4096, vals[rank])
+            capi.call("gf_ring_allreduce", comm, dt, 4096, capi.u64_array([0]), capi.u64_array([L]),
+                      1, None)
+            got = _get(cudart, base, 4096, vals[rank])
+            want = o.ring_allreduce([v.copy() for v in vals], dtype=dt, ring_order=order)
+            assert (_bits(got) == _bits(want[rank])).all(), (L, dt)
+    # (3) back-to-back small collectives, fresh data each time (epoch protocol under reuse)
+    capi.call("gf_comm_set_ring_order", comm, capi.int_array(range(world)))
+    for it in range(60):
+        vals = [np.random.default_rng(10_000 + 31 * it + r).uniform(-4, 4, 67).astype(np.float32)
+                for r in range(world)]
+        _put(cudart, base, 0, vals[rank])
+        capi.call("gf_ring_allreduce", comm, F32, 0, capi.u64_array([0]), capi.u64_array([67]), 1, None)
+        got = _get(cudart, base, 0, vals[rank])
+        want = o.ring_allreduce([v.copy() for v in vals], dtype=F32)
+        assert (_bits(got) == _bits(want[rank])).all(), it
+    capi.call("gf_comm_status", comm)
+    dist.barrier()
+
+
+def _worker_csc(rank, world, port):
+    comm, base, capi, cudart, dist = _setup(rank, world, port)
+    from oracle.oracle import Oracle
+    o = Oracle()
+    import torch
+    nc, k = 1909, 191
+    norms = [np.random.default_rng(r).uniform(0, 5, nc).astype(np.float32) for r in range(world)]
+    for r in range(world):
+        norms[r][:32] = 2.5  # ties across the threshold region
+    noff = 1 << 20
+    _put(cudart, base, noff, norms[rank])
+    flags = torch.zeros(nc, dtype=torch.uint8, device="cuda")
+    coff = torch.zeros(nc, dtype=torch.int64, device="cuda")
+    plan = torch.zeros(4, dtype=torch.int64, device="cuda")
+    total = nc * 32000 + 12840
+    capi.call("gf_csc_select", comm, noff, nc, k, flags.data_ptr(), total, 32000, F16,
+              capi.THETA_INF, coff.data_ptr(), plan.data_ptr(), None)
+    torch.cuda.synchronize()
+    want_sum = o.ring_allreduce([x.copy() for x in norms], dtype=F32)
+    got_sum = _get(cudart, base, noff, norms[rank])
+    assert (_bits(got_sum) == _bits(want_sum[rank])).all()
+    want = o.select_topk(want_sum[0], k)
+    assert (flags.cpu().numpy() == want).all()
+    # planned ring over a staging buffer laid out by the plan (CSC exchange path)
+    staged = int(plan[0].item())
+    stg = [o.f2h(np.random.default_rng(90 + r).uniform(-1, 1, staged).astype(np.float32))
+           for r in range(world)]
+    soff = 8 << 20
+    _put(cudart, base, soff, stg[rank])
+    capi.call("gf_ring_allreduce_planned", comm, F16, soff, plan.data_ptr(), None)
+    got = _get(cudart, base, soff, stg[rank])
+    wantr = o.ring_allreduce([s.copy() for s in stg], dtype=F16)
+    assert (got == wantr[rank]).all()
+    dist.barrier()
+
+
+def _worker_timeout(rank, world, port):
+    comm, base, capi, cudart, dist = _setup(rank, world, port)
+    capi.call("gf_comm_set_timeout_ms", comm, 1500)
+    if rank == 0:
+        capi.call("gf_ring_allreduce", comm, F32, 0, capi.u64_array([0]), capi.u64_array([1024]),
+                  1, None)
+        cudart.sync_device()
+        with pytest.raises(capi.TransportError):
+            capi.call("gf_comm_status", comm)
+        with pytest.raises(capi.TransportError):  # poisoned: later collectives fail fast
+            capi.call("gf_ring_allreduce", comm, F32, 0, capi.u64_array([0]), capi.u64_array([8]),
+                      1, None)
+    dist.barrier()
+
+
+def _spawn(fn, world):
+    import torch.multiprocessing as mp
+    mp.spawn(fn, args=(world, _free_port()), nprocs=world, join=True)
+
+
+def _world():
+    import torch
+    return min(torch.cuda.device_count(), 8)
+
+
+@pytest.mark.multigpu(2)
+def test_p2p_ring_bit_exact():
+    _spawn(_worker_ring, _world())
+
+
+@pytest.mark.multigpu(2)
+def test_p2p_csc_select_and_planned_ring():
+    _spawn(_worker_csc, _world())
+
+
+@pytest.mark.multigpu(2)
+def test_p2p_timeout_is_transport_error():
+    _spawn(_worker_timeout, 2)
+
+
+@pytest.mark.multigpu(2)
+def test_inprocess_local_connect():
+    """One process driving every GPU (the reference's ranks-as-threads model)."""
+    import torch
+    from oracle.oracle import Oracle
+    from paper_1902_06855_b200 import capi, cudart
+    o = Oracle()
+    world = _world()
+    comms = []
+    for r in range(world):
+        c = C.c_void_p()
+        capi.call("gf_comm_create", world, r, r, 64 << 20, C.byref(c))
+        comms.append(c)
+    capi.call("gf_comm_connect_local", (C.c_void_p * world)(*[c.value for c in comms]), world)
+    L = 1_000_003
+    vals = [o.f2h(np.random.default_rng(r).uniform(-9, 9, L).astype(np.float32)) for r in range(world)]
+    bases = []
+    for r in range(world):
+        b = C.c_void_p()
+        capi.call("gf_comm_heap", comms[r], C.byref(b), None)
+        bases.append(b.value)
+        cudart.set_device(r)
+        cudart.memcpy(b.value, vals[r].ctypes.data, vals[r].nbytes)
+        cudart.sync_device()
+    for r in range(world):  # asynchronous launches on every device from one thread
+        cudart.set_device(r)
+        capi.call("gf_ring_allreduce", comms[r], F16, 0, capi.u64_array([0]), capi.u64_array([L]), 1, None)
+    want = o.ring_allreduce([v.copy() for v in vals], dtype=F16)
+    for r in range(world):
+        cudart.set_device(r)
+        cudart.sync_device()
+        out = np.empty_like(vals[r])
+        cudart.memcpy(out.ctypes.data, bases[r], out.nbytes)
+        cudart.sync_device()
+        assert (out == want[r]).all()
+    for c in comms:
+        capi.call("gf_comm_destroy", c)
+    torch.cuda.synchronize()
