@@ -1,0 +1,469 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Benchmark of the B200 gradient-sync path (GradientFlow, arXiv 1902.06855).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU, NCCL plumbing)
+
+A step = one data-parallel gradient synchronisation of one iteration's gradients:
+dense: pack (fp32 -> fp16 pool) + NVLink ring allreduce of the theta windows + unpack
+(g_avg = sum/N per tensor); CSC: pack+correct+compact, ring over the staging buffer,
+write-back, exact chunk L1, norm exchange + top-k, unpack+momentum update.
+Prints ONE JSON line (rank 0). See DESIGN.md for the roofline accounting.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALEXNET = [23232, 64, 307200, 192, 663552, 384, 884736, 256, 589824, 256, 37748736, 4096,
+           16777216, 4096, 4096000, 1000]
+RESNET50 = [
+    9408, 64, 64, 4096, 64, 64, 36864, 64, 64, 16384, 256, 256, 16384, 256, 256, 16384, 64, 64,
+    36864, 64, 64, 16384, 256, 256, 16384, 64, 64, 36864, 64, 64, 16384, 256, 256, 32768, 128,
+    128, 147456, 128, 128, 65536, 512, 512, 131072, 512, 512, 65536, 128, 128, 147456, 128, 128,
+    65536, 512, 512, 65536, 128, 128, 147456, 128, 128, 65536, 512, 512, 65536, 128, 128, 147456,
+    128, 128, 65536, 512, 512, 131072, 256, 256, 589824, 256, 256, 262144, 1024, 1024, 524288,
+    1024, 1024, 262144, 256, 256, 589824, 256, 256, 262144, 1024, 1024, 262144, 256, 256, 589824,
+    256, 256, 262144, 1024, 1024, 262144, 256, 256, 589824, 256, 256, 262144, 1024, 1024, 262144,
+    256, 256, 589824, 256, 256, 262144, 1024, 1024, 262144, 256, 256, 589824, 256, 256, 262144,
+    1024, 1024, 524288, 512, 512, 2359296, 512, 512, 1048576, 2048, 2048, 2097152, 2048, 2048,
+    1048576, 512, 512, 2359296, 512, 512, 1048576, 2048, 2048, 1048576, 512, 512, 2359296, 512,
+    512, 1048576, 2048, 2048, 2048000, 1000]
+THETA_INF = (1 << 64) - 1
+L2_BYTES = 126 << 20
+
+WORKLOADS = {
+    # BASELINE.json configs[1]: ResNet-50 gradient set, dense lazy allreduce, fp16 wire.
+    "resnet50-dense": dict(sizes=RESNET50, model="resnet50", csc=False, theta=64 << 20),
+    "alexnet-dense": dict(sizes=ALEXNET, model="alexnet", csc=False, theta=64 << 20),
+    # configs[2]: AlexNet CSC, chunk 32000, keep top 10% by norm, residual accumulation.
+    "alexnet-csc": dict(sizes=ALEXNET, model="alexnet", csc=True, theta=THETA_INF, sparsity=0.9),
+    # configs[3]: ResNet-50 CSC with a lazy-fusion threshold (sweep via --theta).
+    "resnet50-csc": dict(sizes=RESNET50, model="resnet50", csc=True, theta=64 << 20, sparsity=0.9),
+}
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """SM clocks + throttle reasons while the timed work executes.
+
+    sample_now() is called by the main thread right after the timed steps are enqueued
+    (the GPU is still executing them) — no sampling thread competes for the GIL with the
+    launch loop. A separate nvidia-smi process (-lms 50) records the whole run for reasons."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self.proc = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        try:
+            import subprocess
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={device_index}",
+                 "--query-gpu=clocks.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def sample_now(self):
+        if self.nv is None:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def stop(self):
+        smi = 0
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                for line in out.splitlines():
+                    f = [x.strip() for x in line.split(",")]
+                    if len(f) != 5:
+                        continue
+                    smi += 1
+                    for name, v in zip(names, f[1:]):
+                        if v.lower() == "active":
+                            self.reasons.add(name)
+            except Exception:
+                pass
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "smi_samples_whole_run": smi}
+
+
+def ring_bus_bytes(layout, esz, world, windows):
+    """NCCL busBw convention: 2(N-1)/N * K per rank (K = window bytes)."""
+    if world == 1:
+        return 0
+    return sum(2 * (world - 1) * (wl * esz) / world for wl in windows)
+
+
+def reference_arm(args, wl, world, rank):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref, unmodified
+    library compiled from /root/reference) on the host cores, ranks as threads."""
+    if rank != 0:
+        return 0
+    from oracle.oracle import Reference
+    ref = Reference()
+    steps = max(1, args.steps)
+    st = ref.time_step(world, wl["sizes"], chunk=32000, dtype=1, theta=wl["theta"],
+                       csc=wl["csc"], final_sparsity=wl.get("sparsity", 0.9), steps=steps,
+                       warmup=max(1, args.warmup if args.warmup < 3 else 1))
+    line = {
+        "metric": "grad-sync ms/step", "value": round(st["total"], 3), "unit": "ms",
+        "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": round(st["total"], 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
+        "data": "synthetic", "impl": "reference",
+        "config": config_of(args, wl, world),
+        "stages_ms": {k: round(v, 3) for k, v in st.items()},
+        "cpu_baseline": {"value": round(st["total"], 3), "unit": "ms", "cores": world,
+                         "kind": "reference",
+                         "sample": f"{steps} timed steps (+1 warm-up) of the full workload, "
+                                   f"{world} rank thread(s) over InprocTransport"},
+        "e2e": {"value": round(st["total"], 3), "unit": "ms", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_of(args, wl, world):
+    theta = wl["theta"]
+    return {"workload": args.workload, "gradient_set": wl["model"],
+            "tensors": len(wl["sizes"]), "elements": sum(wl["sizes"]),
+            "wire": "fp16", "chunk": 32000,
+            "theta_bytes": "inf" if theta == THETA_INF else theta,
+            "csc_sparsity": wl.get("sparsity") if wl["csc"] else None,
+            "parallelism": f"dp{world}", "global_batch": None, "seq_len": None}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="resnet50-dense", choices=sorted(WORKLOADS))
+    ap.add_argument("--theta", type=int, default=None, help="override theta bytes (-1 = inf)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--trace", action="store_true", help="report ring CTA-0 timestamps (diagnostic)")
+    args = ap.parse_args()
+
+    wl = dict(WORKLOADS[args.workload])
+    if args.theta is not None:
+        wl["theta"] = THETA_INF if args.theta < 0 else args.theta
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return reference_arm(args, wl, world, rank)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1902_06855_b200 import capi
+    from paper_1902_06855_b200.engine import GradSync, dense_windows
+
+    torch.cuda.set_device(local)
+    from paper_1902_06855_b200 import cudart
+    cudart.set_device(local)  # the library's CUDA runtime (may differ from torch's) on the same GPU
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def allgather(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+
+    sizes = wl["sizes"]
+    csc = wl["csc"]
+    sync = GradSync(sizes, rank=rank, world=world, device=local, theta=wl["theta"], csc=csc,
+                    final_sparsity=wl.get("sparsity", 0.9), allgather=allgather)
+    L = sync.layout
+    total = L.total
+    esz = 2
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    # ---- synthetic gradients: rotating input sets so every step reads inputs not in L2 ------
+    in_bytes = total * 4
+    n_sets = max(2, math.ceil(2 * L2_BYTES / in_bytes) + 1)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    scales = torch.cat([torch.full((s,), 2.0 ** -((i + 1) % 7), device=dev) for i, s in enumerate(sizes)])
+    inputs = [(torch.rand(total, device=dev, generator=g) * 2 - 1) * scales for _ in range(n_sets)]
+    bounds = np.concatenate([[0], np.cumsum(sizes)])
+
+    def views(flat):
+        return [flat[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
+
+    import ctypes as C
+    in_ptrs = [(C.c_void_p * len(sizes))(*views(x)) for x in inputs]  # prebuilt launch tables
+    outs = [torch.empty(total, device=dev) for _ in range(2)]
+    out_ptrs = [(C.c_void_p * len(sizes))(*views(x)) for x in outs]
+    if csc:
+        nc = L.num_chunks
+        hg = torch.zeros(total, device=dev)
+        imp = [torch.ones(nc, dtype=torch.uint8, device=dev), torch.zeros(nc, dtype=torch.uint8, device=dev)]
+        coff = [torch.zeros(nc, dtype=torch.int64, device=dev) for _ in range(2)]
+        plan = [torch.zeros(4, dtype=torch.int64, device=dev) for _ in range(2)]
+        hu = torch.zeros(total, device=dev)
+        w = torch.zeros(total, device=dev)
+        sync.attach_csc_state(hg.data_ptr(), [t.data_ptr() for t in imp], [t.data_ptr() for t in coff],
+                              [t.data_ptr() for t in plan], hu.data_ptr(), w.data_ptr())
+        sync.init_csc_plan(sp)
+
+    marks = []
+
+    def mark_factory(record):
+        def mark(name):
+            if record:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                marks.append((name, e))
+        return mark
+
+    def step(i, record=False):
+        m = mark_factory(record)
+        if csc:
+            sync.csc_step(in_ptrs[i % n_sets], stream=sp, mark=m)
+        else:
+            sync.dense_step(in_ptrs[i % n_sets], out_ptrs[i % 2], stream=sp, mark=m)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    warm = max(args.warmup, 0)
+    for i in range(warm):
+        step(i)
+    barrier()
+    launches0 = capi.lib().gf_kernel_launches()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    t0.record(stream)
+    h0 = time.perf_counter()
+    for i in range(args.steps):
+        step(warm + i, record=True)
+    t1.record(stream)
+    clocks.sample_now()  # the GPU is still executing the queued timed steps here
+    host_enqueue_ms = (time.perf_counter() - h0) * 1e3 / max(args.steps, 1)
+    torch.cuda.synchronize()
+    barrier()
+    launches = capi.lib().gf_kernel_launches() - launches0
+    sync.status()
+    ms_local = t0.elapsed_time(t1) / max(args.steps, 1)
+
+    # per-kernel durations (events on the launching stream, same timed region)
+    seg = {}
+    for (name, e0), (_, e1) in zip(marks, marks[1:]):
+        if name is not None:
+            seg.setdefault(name, []).append(e0.elapsed_time(e1))
+    seg_ms = {k: sum(v) / len(v) for k, v in seg.items()}
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = allmax(ms_local)
+    seg_ms = {k: allmax(v) for k, v in sorted(seg_ms.items())}
+
+    # ---- roofline of the dominant kernel ------------------------------------------------
+    hbm_peak, peak_src = load_peaks()
+    ws, wlen = dense_windows(L, esz, wl["theta"])
+    algo = {  # algorithmic bytes per launch
+        "pack": total * 6, "unpack": total * 6, "pack_correct": total * 14,
+        "norms": total * 2, "scatter": None, "select": None, "sgd_update": None,
+        "ring": None,
+    }
+    if csc:
+        # staged elements of the last timed (sparse) iteration, read back after timing
+        staged = int(plan[(sync.iteration - 1) & 1][0].item())
+        algo["pack_correct"] = total * 14 + staged * 2   # g, hg in; pool, hg, staging out
+        algo["scatter"] = staged * 4                      # staging in, pool out
+        algo["sgd_update"] = staged * 18                  # pool in; hu, w in+out
+        ring_bytes = ring_bus_bytes(L, esz, world, [staged])
+    else:
+        ring_bytes = ring_bus_bytes(L, esz, world, wlen)
+    algo["ring"] = ring_bytes if world > 1 else None
+    dom = max(seg_ms, key=lambda k: seg_ms[k]) if seg_ms else None
+    roof = None
+    if dom is not None and algo.get(dom):
+        t_s = seg_ms[dom] / 1e3
+        if dom == "ring":
+            ach = algo[dom] / t_s / 1e9
+            roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": 900.0, "unit": "GB/s",
+                    "frac": round(ach / 900.0, 3), "traffic": None, "kernel": "ring_kernel",
+                    "peak_src": "NVLink 5 nominal 900 GB/s/direction (measured peer copy 770)",
+                    "frac_of_measured_770": round(ach / 770.0, 3)}
+        else:
+            ach = algo[dom] / t_s / 1e9
+            roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(ach / hbm_peak, 3), "traffic": None, "kernel": dom,
+                    "peak_src": peak_src}
+    kernels = {}
+    for k, v in seg_ms.items():
+        d = {"ms": round(v, 4)}
+        if algo.get(k):
+            d["GBps"] = round(algo[k] / (v / 1e3) / 1e9, 1)
+            if k != "ring":
+                d["frac_hbm"] = round(d["GBps"] / hbm_peak, 3)
+            else:
+                d["busbw_frac_900"] = round(d["GBps"] / 900, 3)
+        kernels[k] = d
+
+    # ---- ring trace (diagnostic, outside the timed region): device timestamps of CTA 0 ----
+    ring_trace = None
+    if args.trace and world > 1:
+        import ctypes as _C
+        capi.call("gf_comm_set_trace", sync.comm, 1)
+        rec = []
+        for i in range(args.steps):
+            barrier()
+            step(i)
+            torch.cuda.synchronize()
+            t = (_C.c_uint64 * 4)()
+            capi.call("gf_comm_trace", sync.comm, t)
+            rec.append([t[1] - t[0], t[2] - t[1], t[3] - t[2]])
+        capi.call("gf_comm_set_trace", sync.comm, 0)
+        med = [statistics.median(r[j] for r in rec) / 1e3 for j in range(3)]
+        ring_trace = {"entry_wait_us": round(allmax(med[0]), 2), "body_us": round(allmax(med[1]), 2),
+                      "exit_wait_us": round(allmax(med[2]), 2)}
+
+    # ---- NCCL allreduce on the same fp16 volume (comparison only) ---------------------------
+    nccl = None
+    if world > 1:
+        x = torch.zeros(total, dtype=torch.float16, device=dev)
+        for _ in range(3):
+            dist.all_reduce(x)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            dist.all_reduce(x)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        nms = allmax(e0.elapsed_time(e1) / max(args.steps, 1))
+        nccl = {"ms": round(nms, 4), "busbw_GBps": round(2 * (world - 1) / world * total * 2 / (nms / 1e3) / 1e9, 1)}
+
+    # ---- end-to-end through the C-ABI with host buffers ---------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        h_in = torch.empty(total, dtype=torch.float32, pin_memory=True)
+        h_in.copy_(inputs[0].cpu())
+        h_out = torch.empty(total, dtype=torch.float32, pin_memory=True)
+        res_dev = outs[0] if not csc else w
+        d2h = total * 4
+        for i in range(2):
+            inputs[0].copy_(h_in, non_blocking=True)
+            step(0)
+            h_out.copy_(res_dev, non_blocking=True)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            inputs[0].copy_(h_in, non_blocking=True)
+            step(0)
+            h_out.copy_(res_dev, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = allmax(e0.elapsed_time(e1) / max(args.steps, 1))
+        e2e = {"value": round(ems, 4), "unit": "ms", "h2d_bytes_per_step": total * 4,
+               "d2h_bytes_per_step": d2h, "path": "C-ABI gf_* with pinned host grads in / results out"}
+    sync.status()
+
+    clk = clocks.stop()
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            from oracle.oracle import Reference
+            if Reference.available():
+                st = Reference().time_step(1, sizes, chunk=32000, dtype=1, theta=wl["theta"],
+                                           csc=csc, final_sparsity=wl.get("sparsity", 0.9),
+                                           steps=3, warmup=1)
+                cpu = {"value": round(st["total"], 3), "unit": "ms", "cores": 1, "kind": "reference",
+                       "sample": "3 timed steps (+1 warm-up) of the full workload, 1 rank thread",
+                       "stages_ms": {k: round(v, 2) for k, v in st.items()}}
+        except Exception as e:  # pragma: no cover
+            cpu = {"error": str(e)[:200]}
+
+    if rank == 0:
+        bus = None
+        if world > 1 and "ring" in seg_ms:
+            bus = round(ring_bytes / (seg_ms["ring"] / 1e3) / 1e9, 1)
+        line = {
+            "metric": "grad-sync ms/step", "value": round(ms, 4), "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
+            "data": "synthetic", "config": dict(config_of(args, wl, world),
+                                                l2=f"{n_sets} rotating input sets of {in_bytes >> 20} MiB "
+                                                   f"(> 126 MB L2)"),
+            "bus_gbs": bus, "kernels": kernels, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "nccl_allreduce": nccl, "gpu_launches": int(launches), "clocks": clk,
+            "ring_trace": ring_trace, "host_enqueue_ms_per_step": round(host_enqueue_ms, 4),
+        }
+        print(json.dumps(line), flush=True)
+    sync.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -148,6 +148,11 @@ int gf_comm_set_ring_order(gf_comm* comm, const int* order);
 int gf_comm_set_timeout_ms(gf_comm* comm, uint64_t ms);
 /* GF_OK, or GF_ERR_TRANSPORT once a device-side wait timed out (comm is then poisoned). */
 int gf_comm_status(gf_comm* comm);
+/* Tracing: when on, CTA 0 of every NVLink ring launch stamps %globaltimer (ns) into a
+ * host-mapped record [kernel start, entry barrier passed, exit barrier begin, end];
+ * gf_comm_trace copies the latest record (call after the launch completed). */
+int gf_comm_set_trace(gf_comm* comm, int on);
+int gf_comm_trace(gf_comm* comm, uint64_t* out4);
 int gf_comm_rank(gf_comm* comm);
 int gf_comm_world(gf_comm* comm);
 

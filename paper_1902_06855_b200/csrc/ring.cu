@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -55,6 +56,7 @@ struct RingArgs {
     uint64_t* epochs;                    // local, one per CTA
     uint64_t timeout_ns;
     int* err;
+    uint64_t* trace;                     // host-mapped [start, entered, exit_begin, end] or null
     const uint64_t* plan;
     uint64_t wstart[kMaxW];
     uint64_t wlen[kMaxW];
@@ -73,6 +75,7 @@ struct SelArgs {
     uint64_t* epochs;
     uint64_t timeout_ns;
     int* err;
+    uint64_t* trace;
 };
 
 // ---- cross-GPU barrier (CTA b <-> CTA b of every peer) ------------------------
@@ -186,7 +189,10 @@ __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constan
     if (threadIdx.x == 0) s_ok = 1;
     const int n = NT > 0 ? NT : a.world;
     const int p = P2P ? a.pos : int(blockIdx.y);
+    const bool tr = P2P && a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    if (tr) a.trace[0] = gfd::globaltimer_ns();
     if (P2P && !cross_barrier(a, epoch + 1, &s_ok)) return;
+    if (tr) a.trace[1] = gfd::globaltimer_ns();
     int nwin;
     uint64_t staged = 0, stride = 0;
     if (a.nwin >= 0) {
@@ -210,7 +216,9 @@ __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constan
         const uint64_t sc = base + (up < rem ? 1 : 0);
         reduce_range<DT, NT>(a, n, p, ws + so, ws + so + sc);
     }
+    if (tr) a.trace[2] = gfd::globaltimer_ns();
     if (P2P && cross_barrier(a, epoch + 2, &s_ok) && threadIdx.x == 0) a.epochs[blockIdx.x] = epoch + 2;
+    if (tr) a.trace[3] = gfd::globaltimer_ns();
 }
 
 // ---- K5: norm exchange + selection (one CTA) -----------------------------------
@@ -272,6 +280,11 @@ void launch_ring(int dtype, bool p2p, const RingArgs& a, dim3 grid, cudaStream_t
 // capped at 2 per SM (and by the flag table). Depends only on values identical
 // on every rank, so all ranks launch the same grid (CTA b pairs with CTA b).
 int ring_blocks(uint64_t max_seg_bytes) {
+    static const int forced = [] {
+        const char* e = std::getenv("GF_RING_BLOCKS");  // tuning override (must match on all ranks)
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced > 0) return std::min(forced, kMaxBlocks);
     const uint64_t per_cta = uint64_t(kRingThreads) * 16 * 4;
     const uint64_t want = (max_seg_bytes + per_cta - 1) / per_cta;
     const uint64_t cap = std::min<uint64_t>(kMaxBlocks, uint64_t(gfi::sm_count()) * 2);
@@ -296,8 +309,9 @@ struct gf_comm {
     char* alloc = nullptr;                       // [flags | heap]
     char* peer_alloc[GF_MAX_RANKS] = {};
     bool ipc_opened[GF_MAX_RANKS] = {};
-    int* err_host = nullptr;
+    int* err_host = nullptr;   // mapped pinned page: [0] error word, trace at +64 B
     int* err_dev = nullptr;
+    bool trace = false;
     uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;  // transport.hpp:25 kDefaultTimeout
     bool connected = false;
 };
@@ -339,6 +353,7 @@ void fill_common(gf_comm* c, RingArgs& a, uint64_t heap_off) {
     a.epochs = a.flags_local + kFlagWords;
     a.timeout_ns = c->timeout_ns;
     a.err = c->err_dev;
+    a.trace = c->trace ? reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(c->err_dev) + 64) : nullptr;
 }
 
 }  // namespace
@@ -360,9 +375,9 @@ int gf_comm_create(int world, int rank, int device, uint64_t heap_bytes, gf_comm
     c->pos = rank;
     cudaError_t e = cudaMalloc(&c->alloc, kFlagBytes + c->heap_bytes);
     if (e == cudaSuccess) e = cudaMemset(c->alloc, 0, kFlagBytes);
-    if (e == cudaSuccess) e = cudaHostAlloc(&c->err_host, sizeof(int), cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostAlloc(&c->err_host, 128, cudaHostAllocMapped);
     if (e == cudaSuccess) {
-        *c->err_host = 0;
+        std::memset(c->err_host, 0, 128);
         e = cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0);
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -480,6 +495,20 @@ int gf_comm_status(gf_comm* c) {
     if (c->err_host && *reinterpret_cast<volatile int*>(c->err_host) != 0)
         return gfi::fail(GF_ERR_TRANSPORT, "recv timeout at rank " + std::to_string(c->rank) +
                                                " (peer did not reach the collective barrier)");
+    return GF_OK;
+}
+
+int gf_comm_set_trace(gf_comm* c, int on) {
+    if (!c) return gfi::fail(GF_ERR_CONFIG, "null communicator");
+    c->trace = on != 0;
+    return GF_OK;
+}
+
+int gf_comm_trace(gf_comm* c, uint64_t* out4) {
+    if (!c || !out4) return gfi::fail(GF_ERR_CONFIG, "gf_comm_trace: null argument");
+    const volatile uint64_t* t =
+        reinterpret_cast<const volatile uint64_t*>(reinterpret_cast<char*>(c->err_host) + 64);
+    for (int i = 0; i < 4; ++i) out4[i] = t[i];
     return GF_OK;
 }
 

@@ -1,0 +1,223 @@
+# SPDX-License-Identifier: Apache-2.0
+"""GradSync: one rank's device-resident gradient-synchronisation step over the C-ABI.
+
+This is the launch sequence a data-parallel trainer runs per iteration, with the
+reference's semantics (paths relative to /root/reference/proj):
+
+  dense (lazy allreduce, src/trainer.cpp:297-347 + src/fusion.cpp:72-109):
+      gf_pack            all tensors -> fp16 pool in the symmetric heap   (K1)
+      gf_ring_allreduce  the FusionEngine theta windows, one launch        (K4)
+      gf_unpack          pool -> per-tensor fp32 g_avg = sum * 1/N        (K6)
+  CSC (src/sparse.cpp, Algorithm 1):
+      gf_csc_pack_correct   pack + residual correction + compaction        (K2)
+      gf_ring_allreduce_planned   over the staging buffer                   (K4)
+      gf_csc_scatter        staging -> pool (global sums)
+      gf_chunk_norms        exact chunk L1 (+ x1/N for important chunks)    (K3)
+      gf_csc_select         fp32 norm exchange + top-k + next plan          (K5)
+      gf_csc_sgd_update     unpack + momentum update, important chunks      (K6')
+
+Every launch is asynchronous on the caller's stream; nothing here synchronises or
+reads device memory, so a step can be captured into a CUDA graph.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+from . import capi
+
+F32, F16 = capi.GF_F32, capi.GF_F16
+THETA_INF = capi.THETA_INF
+
+
+def _align(x: int, a: int = 256) -> int:
+    return (x + a - 1) // a * a
+
+
+def llround_pos(x: float) -> int:
+    """C llround for x >= 0 (half away from zero), exact for doubles < 2^52."""
+    r = math.floor(x)
+    return r + 1 if x - r >= 0.5 else r
+
+
+@dataclass(frozen=True)
+class PoolLayout:
+    """GradientPool layout (src/gradient_pool.cpp:11-41): tensor m at offset 0, id 1 last;
+    num_chunks = max(1, llround(total / chunk)), the last chunk absorbs the remainder."""
+
+    sizes: tuple
+    chunk: int
+    offsets: tuple  # offsets[id-1]
+    total: int
+    num_chunks: int
+
+    @staticmethod
+    def build(sizes, chunk=32000) -> "PoolLayout":
+        sizes = tuple(int(s) for s in sizes)
+        if not sizes:
+            raise capi.ConfigError("gradient pool needs at least one tensor")
+        if chunk <= 0:
+            raise capi.ConfigError("chunk_size must be positive")
+        if any(s <= 0 for s in sizes):
+            raise capi.ConfigError("tensor sizes must be positive")
+        offs = [0] * len(sizes)
+        o = 0
+        for tid in range(len(sizes), 0, -1):
+            offs[tid - 1] = o
+            o += sizes[tid - 1]
+        nc = max(1, llround_pos(o / chunk))
+        return PoolLayout(sizes, chunk, tuple(offs), o, nc)
+
+    def chunk_length(self, c: int) -> int:
+        return self.total - c * self.chunk if c + 1 == self.num_chunks else self.chunk
+
+
+def dense_windows(layout: PoolLayout, esz: int, theta: int):
+    """FusionEngine windows of one iteration (src/fusion.cpp:72-109): tensors complete in
+    descending id, a window closes when its bytes reach theta, finalize flushes the rest."""
+    starts, lens = [], []
+    ws = we = 0
+    m = len(layout.sizes)
+    for tid in range(m, -1, -1):
+        flush = tid == 0
+        if not flush:
+            we = layout.offsets[tid - 1] + layout.sizes[tid - 1]
+        hit = theta != THETA_INF and (we - ws) * esz >= theta
+        if we > ws and (hit or flush):
+            starts.append(ws)
+            lens.append(we - ws)
+            ws = we
+    return starts, lens
+
+
+def sparsity_at(t: int, warmup: int, final: float) -> float:
+    """src/sparse.cpp:13-17"""
+    if warmup == 0:
+        return final
+    return final * min(1.0, t / warmup)
+
+
+def selection_count(sparsity: float, nc: int) -> int:
+    """src/sparse.cpp:19-24 (llround, floor of one chunk)."""
+    k = llround_pos((1.0 - sparsity) * nc)
+    return max(1, min(k, nc))
+
+
+class GradSync:
+    """Device-resident sync path of one rank. `allgather(bytes) -> list[bytes]` exchanges the
+    IPC handles when world > 1 (any control plane: torch.distributed, a TCP store, ...)."""
+
+    def __init__(self, sizes, rank=0, world=1, device=0, dtype=F16, theta=64 << 20,
+                 chunk=32000, csc=False, final_sparsity=0.9, warmup_iters=0, momentum=0.9,
+                 lr=0.01, allgather=None, timeout_ms=30000):
+        self.layout = PoolLayout.build(sizes, chunk)
+        self.rank, self.world, self.device, self.dtype = rank, world, device, dtype
+        self.esz = 2 if dtype == F16 else 4
+        self.theta, self.csc = theta, csc
+        self.final_sparsity, self.warmup_iters = final_sparsity, warmup_iters
+        self.momentum, self.lr = momentum, lr
+        L = self.layout
+        self.pool_off = 0
+        self.stage_off = _align(L.total * self.esz)
+        self.norms_off = self.stage_off + (_align(L.total * self.esz) if csc else 0)
+        heap = self.norms_off + _align(L.num_chunks * 4)
+        self.comm = C.c_void_p()
+        capi.call("gf_comm_create", world, rank, device, heap, C.byref(self.comm))
+        if world > 1:
+            if allgather is None:
+                raise capi.ConfigError("world > 1 needs an allgather for the IPC handles")
+            h = (C.c_char * capi.GF_IPC_HANDLE_BYTES)()
+            capi.call("gf_comm_export_handle", self.comm, h)
+            handles = allgather(bytes(h))
+            capi.call("gf_comm_connect_ipc", self.comm, b"".join(handles))
+        capi.call("gf_comm_set_timeout_ms", self.comm, timeout_ms)
+        base = C.c_void_p()
+        capi.call("gf_comm_heap", self.comm, C.byref(base), None)
+        self.heap_base = base.value
+        self.pool_ptr = self.heap_base + self.pool_off
+        self.stage_ptr = self.heap_base + self.stage_off
+        self.norms_ptr = self.heap_base + self.norms_off
+        ws, wl = dense_windows(L, self.esz, theta)
+        self._win = (capi.u64_array(ws), capi.u64_array(wl), len(ws))
+        self._offs = capi.u64_array(L.offsets)
+        self._cnts = capi.u64_array(L.sizes)
+        self.iteration = 0
+        self._csc_bufs = None
+
+    # ---- state for CSC (allocated by the caller's allocator: torch or cudaMalloc) -------
+    def attach_csc_state(self, hg, imp, coff, plan, hu, w):
+        """Device buffers: hg (total fp32), imp[2] (nc u8), coff[2] (nc u64), plan[2] (4 u64),
+        hu/w (total fp32). imp[0]/coff[0]/plan[0] must describe iteration 0 (all ones)."""
+        self._csc_bufs = dict(hg=hg, imp=imp, coff=coff, plan=plan, hu=hu, w=w)
+
+    def init_csc_plan(self, stream=None):
+        b = self._csc_bufs
+        L = self.layout
+        capi.call("gf_csc_plan", b["imp"][0], L.total, L.chunk, L.num_chunks, self.dtype,
+                  self.theta, b["coff"][0], b["plan"][0], stream)
+
+    # ---- steps ------------------------------------------------------------------------
+    @staticmethod
+    def _ptrs(ptrs):
+        """Per-tensor pointer table; a prebuilt ctypes array is passed through as is."""
+        if isinstance(ptrs, C.Array):
+            return ptrs
+        return (C.c_void_p * len(ptrs))(*ptrs)
+
+    def dense_step(self, grad_ptrs, out_ptrs, stream=None, mark=None):
+        """grad_ptrs/out_ptrs: per-tensor device pointers in ascending tensor id."""
+        L = self.layout
+        m = len(L.sizes)
+        mark = mark or (lambda name: None)
+        mark("pack")
+        capi.call("gf_pack", self.dtype, self.pool_ptr, self._ptrs(grad_ptrs), self._offs,
+                  self._cnts, m, 1.0, stream)
+        mark("ring")
+        if self.world > 1:
+            capi.call("gf_ring_allreduce", self.comm, self.dtype, self.pool_off, self._win[0],
+                      self._win[1], self._win[2], stream)
+        mark("unpack")
+        capi.call("gf_unpack", self.dtype, self.pool_ptr, self._ptrs(out_ptrs), self._offs,
+                  self._cnts, m, self.world, stream)
+        mark(None)
+
+    def csc_step(self, grad_ptrs, stream=None, mark=None):
+        """One CSC iteration (Algorithm 1). Uses the buffers given to attach_csc_state."""
+        b = self._csc_bufs
+        L = self.layout
+        m = len(L.sizes)
+        cur, nxt = self.iteration & 1, (self.iteration + 1) & 1
+        mark = mark or (lambda name: None)
+        mark("pack_correct")
+        capi.call("gf_csc_pack_correct", self.dtype, self.pool_ptr, b["hg"], self.stage_ptr,
+                  b["imp"][cur], b["coff"][cur], L.total, L.chunk, L.num_chunks,
+                  self._ptrs(grad_ptrs), self._offs, self._cnts, m, self.momentum, stream)
+        mark("ring")
+        if self.world > 1:
+            capi.call("gf_ring_allreduce_planned", self.comm, self.dtype, self.stage_off,
+                      b["plan"][cur], stream)
+        mark("scatter")
+        capi.call("gf_csc_scatter", self.dtype, self.pool_ptr, self.stage_ptr, b["imp"][cur],
+                  b["coff"][cur], L.total, L.chunk, L.num_chunks, stream)
+        mark("norms")
+        capi.call("gf_chunk_norms", self.dtype, self.pool_ptr, L.total, L.chunk, L.num_chunks,
+                  b["imp"][cur], self.world, self.norms_ptr, stream)
+        mark("select")
+        k = selection_count(sparsity_at(self.iteration + 1, self.warmup_iters,
+                                        self.final_sparsity), L.num_chunks)
+        capi.call("gf_csc_select", self.comm, self.norms_off, L.num_chunks, k, b["imp"][nxt],
+                  L.total, L.chunk, self.dtype, self.theta, b["coff"][nxt], b["plan"][nxt], stream)
+        mark("sgd_update")
+        capi.call("gf_csc_sgd_update", self.dtype, self.pool_ptr, b["imp"][cur], L.total, L.chunk,
+                  L.num_chunks, self.world, self.momentum, self.lr, b["hu"], b["w"], stream)
+        mark(None)
+        self.iteration += 1
+
+    def status(self):
+        capi.call("gf_comm_status", self.comm)
+
+    def close(self):
+        if self.comm:
+            capi.call("gf_comm_destroy", self.comm)
+            self.comm = C.c_void_p()
