@@ -253,7 +253,7 @@ def main():
         hg = torch.zeros(total, device=dev)
         imp = [torch.ones(nc, dtype=torch.uint8, device=dev), torch.zeros(nc, dtype=torch.uint8, device=dev)]
         coff = [torch.zeros(nc, dtype=torch.int64, device=dev) for _ in range(2)]
-        plan = [torch.zeros(4, dtype=torch.int64, device=dev) for _ in range(2)]
+        plan = [torch.zeros(4 + nc, dtype=torch.int64, device=dev) for _ in range(2)]
         hu = torch.zeros(total, device=dev)
         w = torch.zeros(total, device=dev)
         sync.attach_csc_state(hg.data_ptr(), [t.data_ptr() for t in imp], [t.data_ptr() for t in coff],

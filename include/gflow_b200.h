@@ -110,23 +110,26 @@ int gf_csc_pack_correct(int dtype, void* pool, float* hg, void* staging,
                         uint64_t chunk, uint64_t nc, const float* const* src,
                         const uint64_t* pool_off, const uint64_t* count, int ntensors,
                         float momentum, void* stream);
-int gf_csc_compact(int dtype, const void* pool, void* staging, const uint8_t* important,
+/* Staging pack / write-back over the important chunks listed in `plan` (see gf_csc_plan):
+ * staging[coff[c] + i] <-> pool[c*chunk + i]. max_chunks bounds plan[1] (launch size; nc is safe). */
+int gf_csc_compact(int dtype, const void* pool, void* staging, const uint64_t* plan,
                    const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
-                   void* stream);
-int gf_csc_scatter(int dtype, void* pool, const void* staging, const uint8_t* important,
+                   uint64_t max_chunks, void* stream);
+int gf_csc_scatter(int dtype, void* pool, const void* staging, const uint64_t* plan,
                    const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
-                   void* stream);
+                   uint64_t max_chunks, void* stream);
 /* From important flags (device): coff[c] = sum of lengths of important chunks < c;
- * plan[0] = staged elements, plan[1] = important chunk count, plan[2] = window count,
- * plan[3] = elements per full window (theta policy of sparse.cpp:142-158). */
+ * plan (device, 4 + nc uint64): plan[0] = staged elements, plan[1] = important chunk
+ * count, plan[2] = window count, plan[3] = elements per full window (theta policy of
+ * sparse.cpp:142-158), plan[4 .. 4+plan[1]) = the important chunk indices, ascending. */
 int gf_csc_plan(const uint8_t* important, uint64_t total, uint64_t chunk, uint64_t nc,
                 int dtype, uint64_t theta, uint64_t* coff, uint64_t* plan, void* stream);
 /* flags[c] = 1 for the k chunks with largest norm (ties: lower index), else 0. */
 int gf_select_topk(const float* norms, uint64_t nc, uint64_t k, uint8_t* flags, void* stream);
-/* For important chunks: g = dec(pool)*(1/world); u = mom*hu + lr*g; hu = u; w -= u. */
-int gf_csc_sgd_update(int dtype, const void* pool, const uint8_t* important, uint64_t total,
-                      uint64_t chunk, uint64_t nc, int world, float momentum, float lr,
-                      float* hu, float* w, void* stream);
+/* For the important chunks of `plan`: g = dec(pool)*(1/world); u = mom*hu + lr*g; hu = u; w -= u. */
+int gf_csc_sgd_update(int dtype, const void* pool, const uint64_t* plan, uint64_t total,
+                      uint64_t chunk, uint64_t nc, uint64_t max_chunks, int world, float momentum,
+                      float lr, float* hu, float* w, void* stream);
 /* Whole pool: same recurrence as above without importance (trainer.cpp:337-346). */
 int gf_dense_sgd_update(int dtype, const void* pool, uint64_t total, int world, float momentum,
                         float lr, float* hu, float* w, void* stream);

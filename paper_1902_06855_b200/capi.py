@@ -67,11 +67,11 @@ SIGNATURES = {
     "gf_chunk_norms": [_i, _vp, _u64, _u64, _u64, _vp, _i, _vp, _vp],
     "gf_csc_correct": [_i, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _u64, _f, _vp],
     "gf_csc_pack_correct": [_i, _vp, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _vp, _vp, _vp, _i, _f, _vp],
-    "gf_csc_compact": [_i, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _vp],
-    "gf_csc_scatter": [_i, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _vp],
+    "gf_csc_compact": [_i, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _vp],
+    "gf_csc_scatter": [_i, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _vp],
     "gf_csc_plan": [_vp, _u64, _u64, _u64, _i, _u64, _vp, _vp, _vp],
     "gf_select_topk": [_vp, _u64, _u64, _vp, _vp],
-    "gf_csc_sgd_update": [_i, _vp, _vp, _u64, _u64, _u64, _i, _f, _f, _vp, _vp, _vp],
+    "gf_csc_sgd_update": [_i, _vp, _vp, _u64, _u64, _u64, _u64, _i, _f, _f, _vp, _vp, _vp],
     "gf_dense_sgd_update": [_i, _vp, _u64, _i, _f, _f, _vp, _vp, _vp],
     "gf_comm_create": [_i, _i, _i, _u64, C.POINTER(_vp)],
     "gf_comm_destroy": [_vp],

@@ -56,14 +56,21 @@ norms_f16_kernel(const uint16_t* __restrict__ pool, uint64_t total, uint64_t chu
         uint64_t done = 0;
         if ((b % 8) == 0) {
             const uint64_t nvec = len / 8;
-            for (uint64_t v = threadIdx.x; v < nvec; v += kNormThreads) {
-                const uint4 x = gfd::ld16_stream(p + 8 * v);
-                const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+            constexpr int U = 4;
+            for (uint64_t v0 = threadIdx.x; v0 < nvec; v0 += uint64_t(kNormThreads) * U) {
+                uint4 x[U];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint16_t lo = uint16_t(w[k] & 0xFFFFu), hi = uint16_t(w[k] >> 16);
-                    nan |= ((lo & 0x7C00u) == 0x7C00u) | ((hi & 0x7C00u) == 0x7C00u);
-                    acc += half_units(lo) + half_units(hi);
+                for (int u = 0; u < U; ++u) {
+                    const uint64_t v = v0 + uint64_t(u) * kNormThreads;
+                    x[u] = v < nvec ? gfd::ld16_stream(p + 8 * v) : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    nan |= gfd::any_special(x[u]);
+                    const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        acc += half_units(uint16_t(w[k] & 0xFFFFu)) + half_units(uint16_t(w[k] >> 16));
                 }
             }
             done = nvec * 8;
@@ -218,12 +225,14 @@ pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ po
     }
 }
 
-// Staging pack (dir=0) / write-back (dir=1): one CTA-row per chunk, 16-B copies.
+// Staging pack (dir=0) / write-back (dir=1) over the important chunks listed in the plan
+// (plan[4+j], j < plan[1]): grid.y walks the list, grid.x tiles a chunk; 16-B copies.
 __global__ void compact_kernel(char* __restrict__ pool, char* __restrict__ staging,
-                               const uint8_t* __restrict__ imp, const uint64_t* __restrict__ coff,
+                               const uint64_t* __restrict__ plan, const uint64_t* __restrict__ coff,
                                uint64_t total, uint64_t chunk, uint64_t nc, uint64_t esz, int dir) {
-    for (uint64_t c = blockIdx.y; c < nc; c += gridDim.y) {
-        if (!imp[c]) continue;
+    const uint64_t kc = plan[1];
+    for (uint64_t j = blockIdx.y; j < kc; j += gridDim.y) {
+        const uint64_t c = plan[4 + j];
         const uint64_t len = ((c + 1 == nc) ? total - c * chunk : chunk) * esz;
         char* p = pool + c * chunk * esz;
         char* s = staging + coff[c] * esz;
@@ -233,14 +242,63 @@ __global__ void compact_kernel(char* __restrict__ pool, char* __restrict__ stagi
             const uint64_t nv = len / 16;
             for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < nv;
                  v += uint64_t(gridDim.x) * blockDim.x) {
-                if (dir == 0) gfd::st16(s + 16 * v, gfd::ld16(p + 16 * v));
-                else gfd::st16(p + 16 * v, gfd::ld16(s + 16 * v));
+                if (dir == 0) gfd::st16(s + 16 * v, gfd::ld16_stream(p + 16 * v));
+                else gfd::st16(p + 16 * v, gfd::ld16_stream(s + 16 * v));
             }
             done = nv * 16;
         }
         for (uint64_t i = done + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < len;
              i += uint64_t(gridDim.x) * blockDim.x) {
             if (dir == 0) s[i] = p[i]; else p[i] = s[i];
+        }
+    }
+}
+
+// CSC unpack + momentum update (sparse.cpp:206-224, csc_update sparse.hpp:42-51) over the
+// important chunks of the plan: g = dec(pool)*(1/N); u = mom*hu + lr*g; hu = u; w -= u.
+template <int DT>
+__global__ void __launch_bounds__(256)
+csc_sgd_kernel(const void* __restrict__ pool, const uint64_t* __restrict__ plan, uint64_t total,
+               uint64_t chunk, uint64_t nc, float inv_world, float mom, float lr,
+               float* __restrict__ hu, float* __restrict__ w) {
+    const uint64_t kc = plan[1];
+    for (uint64_t j = blockIdx.y; j < kc; j += gridDim.y) {
+        const uint64_t c = plan[4 + j];
+        const uint64_t b = c * chunk;
+        const uint64_t len = (c + 1 == nc) ? total - b : chunk;
+        uint64_t done = 0;
+        if (DT == GF_F16 && b % 8 == 0 && (reinterpret_cast<uintptr_t>(hu) & 31u) == 0 &&
+            (reinterpret_cast<uintptr_t>(w) & 31u) == 0) {
+            const uint64_t nv = len / 8;
+            const uint16_t* p = static_cast<const uint16_t*>(pool) + b;
+            for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < nv;
+                 v += uint64_t(gridDim.x) * blockDim.x) {
+                const uint4 x = gfd::ld16_stream(p + 8 * v);
+                gfd::F8 h = gfd::ld32f(hu + b + 8 * v), ww = gfd::ld32f(w + b + 8 * v);
+                float* hp = reinterpret_cast<float*>(&h);
+                float* wp = reinterpret_cast<float*>(&ww);
+                const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint16_t hv = uint16_t((xs[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu);
+                    const float g = gfd::mul(gfd::dec(hv), inv_world);
+                    const float u = gfd::add(gfd::mul(mom, hp[k]), gfd::mul(lr, g));
+                    hp[k] = u;
+                    wp[k] = gfd::sub(wp[k], u);
+                }
+                gfd::st32f(hu + b + 8 * v, h.lo, h.hi);
+                gfd::st32f(w + b + 8 * v, ww.lo, ww.hi);
+            }
+            done = nv * 8;
+        }
+        for (uint64_t i = b + done + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < b + len;
+             i += uint64_t(gridDim.x) * blockDim.x) {
+            const float x = DT == GF_F16 ? gfd::dec(static_cast<const uint16_t*>(pool)[i])
+                                         : static_cast<const float*>(pool)[i];
+            const float g = gfd::mul(x, inv_world);
+            const float u = gfd::add(gfd::mul(mom, hu[i]), gfd::mul(lr, g));
+            hu[i] = u;
+            w[i] = gfd::sub(w[i], u);
         }
     }
 }
@@ -255,16 +313,19 @@ select_plan_kernel(const float* __restrict__ norms, uint64_t nc, uint64_t k, uin
     if (coff && plan) gfs::block_plan(flags, total, chunk, nc, esz, theta, coff, plan, sh);
 }
 
-int compact_launch(int dtype, void* pool, const void* staging, const uint8_t* important,
-                   const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc, int dir,
-                   void* stream) {
-    if (!gfi::valid_dtype(dtype) || chunk == 0 || nc == 0)
+int grid_y(uint64_t max_chunks, uint64_t nc) {
+    return int(std::max<uint64_t>(1, std::min<uint64_t>(std::min(max_chunks, nc), 65535)));
+}
+
+int compact_launch(int dtype, void* pool, const void* staging, const uint64_t* plan,
+                   const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
+                   uint64_t max_chunks, int dir, void* stream) {
+    if (!gfi::valid_dtype(dtype) || chunk == 0 || nc == 0 || !plan || !coff)
         return gfi::fail(GF_ERR_CONFIG, "gf_csc_compact/scatter: bad arguments");
     const uint64_t bytes = std::max<uint64_t>(chunk, total - (nc - 1) * chunk) * gfi::esz(dtype);
-    const int gx = int(std::min<uint64_t>((bytes / 16 + 255) / 256, 16));
-    const int gy = int(std::min<uint64_t>(nc, 65535));
-    compact_kernel<<<dim3(gx, gy), 256, 0, gfi::S(stream)>>>(
-        static_cast<char*>(pool), static_cast<char*>(const_cast<void*>(staging)), important, coff,
+    const int gx = int(std::max<uint64_t>(1, std::min<uint64_t>((bytes / 16 + 511) / 512, 64)));
+    compact_kernel<<<dim3(gx, grid_y(max_chunks, nc)), 512, 0, gfi::S(stream)>>>(
+        static_cast<char*>(pool), static_cast<char*>(const_cast<void*>(staging)), plan, coff,
         total, chunk, nc, gfi::esz(dtype), dir);
     gfi::count_launch();
     return gfi::check_launch("gf_csc_compact");
@@ -328,17 +389,35 @@ int gf_csc_pack_correct(int dtype, void* pool, float* hg, void* staging,
                           });
 }
 
-int gf_csc_compact(int dtype, const void* pool, void* staging, const uint8_t* important,
+int gf_csc_compact(int dtype, const void* pool, void* staging, const uint64_t* plan,
                    const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
-                   void* stream) {
-    return compact_launch(dtype, const_cast<void*>(pool), staging, important, coff, total, chunk,
-                          nc, 0, stream);
+                   uint64_t max_chunks, void* stream) {
+    return compact_launch(dtype, const_cast<void*>(pool), staging, plan, coff, total, chunk, nc,
+                          max_chunks, 0, stream);
 }
 
-int gf_csc_scatter(int dtype, void* pool, const void* staging, const uint8_t* important,
+int gf_csc_scatter(int dtype, void* pool, const void* staging, const uint64_t* plan,
                    const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
-                   void* stream) {
-    return compact_launch(dtype, pool, staging, important, coff, total, chunk, nc, 1, stream);
+                   uint64_t max_chunks, void* stream) {
+    return compact_launch(dtype, pool, staging, plan, coff, total, chunk, nc, max_chunks, 1, stream);
+}
+
+int gf_csc_sgd_update(int dtype, const void* pool, const uint64_t* plan, uint64_t total,
+                      uint64_t chunk, uint64_t nc, uint64_t max_chunks, int world, float momentum,
+                      float lr, float* hu, float* w, void* stream) {
+    if (!gfi::valid_dtype(dtype) || world < 1 || chunk == 0 || nc == 0 || !plan)
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_sgd_update: bad arguments");
+    if (total == 0) return GF_OK;
+    const float inv = 1.0f / static_cast<float>(world);
+    const uint64_t longest = std::max<uint64_t>(chunk, total - (nc - 1) * chunk);
+    const int gx = int(std::max<uint64_t>(1, std::min<uint64_t>((longest / 8 + 255) / 256, 64)));
+    const dim3 grid(gx, grid_y(max_chunks, nc));
+    if (dtype == GF_F16)
+        csc_sgd_kernel<GF_F16><<<grid, 256, 0, gfi::S(stream)>>>(pool, plan, total, chunk, nc, inv, momentum, lr, hu, w);
+    else
+        csc_sgd_kernel<GF_F32><<<grid, 256, 0, gfi::S(stream)>>>(pool, plan, total, chunk, nc, inv, momentum, lr, hu, w);
+    gfi::count_launch();
+    return gfi::check_launch("gf_csc_sgd_update");
 }
 
 int gf_csc_plan(const uint8_t* important, uint64_t total, uint64_t chunk, uint64_t nc,

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ 
         const uint64_t len = min(kTile, T.cnt[t] - base);
         const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
         const uint64_t po = T.off[t] + base;
-        const bool fast = ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 15u) == 0) && (po % 8 == 0);
+        const bool fast = ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0) && (po % 8 == 0);
         if (DT == GF_F16) {
             uint16_t* __restrict__ d = static_cast<uint16_t*>(pool) + po;
             uint64_t done = 0;
@@ -48,24 +48,22 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ 
                 for (int k = 0; k < kVecPerThread; ++k) {
                     const int v = threadIdx.x + k * kThreads;
                     if (v < nvec) {
-                        a[k] = gfd::ld16f_stream(s + 8 * v);
-                        b[k] = gfd::ld16f_stream(s + 8 * v + 4);
+                        const gfd::F8 f = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
+                        a[k] = f.lo;
+                        b[k] = f.hi;
                     }
                 }
 #pragma unroll
                 for (int k = 0; k < kVecPerThread; ++k) {
                     const int v = threadIdx.x + k * kThreads;
                     if (v < nvec) {
-                        uint4 o;
-                        o.x = gfd::enc(scaled(a[k].x, scale, do_scale)) |
-                              (uint32_t(gfd::enc(scaled(a[k].y, scale, do_scale))) << 16);
-                        o.y = gfd::enc(scaled(a[k].z, scale, do_scale)) |
-                              (uint32_t(gfd::enc(scaled(a[k].w, scale, do_scale))) << 16);
-                        o.z = gfd::enc(scaled(b[k].x, scale, do_scale)) |
-                              (uint32_t(gfd::enc(scaled(b[k].y, scale, do_scale))) << 16);
-                        o.w = gfd::enc(scaled(b[k].z, scale, do_scale)) |
-                              (uint32_t(gfd::enc(scaled(b[k].w, scale, do_scale))) << 16);
-                        gfd::st16(d + 8 * v, o);
+                        if (do_scale) {
+                            a[k] = make_float4(gfd::mul(a[k].x, scale), gfd::mul(a[k].y, scale),
+                                               gfd::mul(a[k].z, scale), gfd::mul(a[k].w, scale));
+                            b[k] = make_float4(gfd::mul(b[k].x, scale), gfd::mul(b[k].y, scale),
+                                               gfd::mul(b[k].z, scale), gfd::mul(b[k].w, scale));
+                        }
+                        gfd::st16(d + 8 * v, gfd::enc8(a[k], b[k]));
                     }
                 }
                 done = uint64_t(nvec) * 8;
@@ -106,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) unpack_kernel(const __grid_constant_
         const uint64_t len = min(kTile, T.cnt[t] - base);
         float* __restrict__ d = static_cast<float*>(const_cast<void*>(T.ptr[t])) + base;
         const uint64_t po = T.off[t] + base;
-        const bool fast = ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 15u) == 0) && (po % 8 == 0);
+        const bool fast = ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0) && (po % 8 == 0);
         uint64_t done = 0;
         if (DT == GF_F16) {
             const uint16_t* __restrict__ s = static_cast<const uint16_t*>(pool) + po;
@@ -121,7 +119,16 @@ __global__ void __launch_bounds__(kThreads) unpack_kernel(const __grid_constant_
 #pragma unroll
                 for (int k = 0; k < kVecPerThread; ++k) {
                     const int v = threadIdx.x + k * kThreads;
-                    if (v < nvec) {
+                    if (v < nvec && !gfd::any_special(x[k])) {
+                        // fast path: finite halves, x * (1/N) cannot produce NaN
+                        const float2 f0 = gfd::h2f2(x[k].x), f1 = gfd::h2f2(x[k].y);
+                        const float2 f2 = gfd::h2f2(x[k].z), f3 = gfd::h2f2(x[k].w);
+                        gfd::st32f_stream(d + 8 * v,  // STG.E.256
+                               make_float4(__fmul_rn(f0.x, inv_world), __fmul_rn(f0.y, inv_world),
+                                           __fmul_rn(f1.x, inv_world), __fmul_rn(f1.y, inv_world)),
+                               make_float4(__fmul_rn(f2.x, inv_world), __fmul_rn(f2.y, inv_world),
+                                           __fmul_rn(f3.x, inv_world), __fmul_rn(f3.y, inv_world)));
+                    } else if (v < nvec) {
                         const uint32_t* w = reinterpret_cast<const uint32_t*>(&x[k]);
                         float4 lo, hi;
                         lo.x = gfd::mul(gfd::dec(uint16_t(w[0] & 0xFFFF)), inv_world);
@@ -132,8 +139,7 @@ __global__ void __launch_bounds__(kThreads) unpack_kernel(const __grid_constant_
                         hi.y = gfd::mul(gfd::dec(uint16_t(w[2] >> 16)), inv_world);
                         hi.z = gfd::mul(gfd::dec(uint16_t(w[3] & 0xFFFF)), inv_world);
                         hi.w = gfd::mul(gfd::dec(uint16_t(w[3] >> 16)), inv_world);
-                        __stcs(reinterpret_cast<float4*>(d + 8 * v), lo);
-                        __stcs(reinterpret_cast<float4*>(d + 8 * v + 4), hi);
+                        gfd::st32f_stream(d + 8 * v, lo, hi);
                     }
                 }
                 done = uint64_t(nvec) * 8;
@@ -225,17 +231,6 @@ __global__ void dense_sgd_kernel(const void* __restrict__ pool, uint64_t total, 
         sgd_elem<DT>(pool, i, inv_world, mom, lr, hu, w);
     }
 }
-template <int DT>
-__global__ void csc_sgd_kernel(const void* __restrict__ pool, const uint8_t* __restrict__ imp,
-                               uint64_t total, uint64_t chunk, uint64_t nc, float inv_world,
-                               float mom, float lr, float* __restrict__ hu, float* __restrict__ w) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t c = min(i / chunk, nc - 1);
-        if (imp[c]) sgd_elem<DT>(pool, i, inv_world, mom, lr, hu, w);
-    }
-}
-
 }  // namespace
 
 extern "C" {
@@ -312,21 +307,6 @@ int gf_dense_sgd_update(int dtype, const void* pool, uint64_t total, int world, 
         dense_sgd_kernel<GF_F32><<<grid_for(total, 256), 256, 0, gfi::S(stream)>>>(pool, total, inv, momentum, lr, hu, w);
     gfi::count_launch();
     return gfi::check_launch("gf_dense_sgd_update");
-}
-
-int gf_csc_sgd_update(int dtype, const void* pool, const uint8_t* important, uint64_t total,
-                      uint64_t chunk, uint64_t nc, int world, float momentum, float lr,
-                      float* hu, float* w, void* stream) {
-    if (!gfi::valid_dtype(dtype) || world < 1 || chunk == 0 || nc == 0)
-        return gfi::fail(GF_ERR_CONFIG, "gf_csc_sgd_update: bad arguments");
-    if (total == 0) return GF_OK;
-    const float inv = 1.0f / static_cast<float>(world);
-    if (dtype == GF_F16)
-        csc_sgd_kernel<GF_F16><<<grid_for(total, 256), 256, 0, gfi::S(stream)>>>(pool, important, total, chunk, nc, inv, momentum, lr, hu, w);
-    else
-        csc_sgd_kernel<GF_F32><<<grid_for(total, 256), 256, 0, gfi::S(stream)>>>(pool, important, total, chunk, nc, inv, momentum, lr, hu, w);
-    gfi::count_launch();
-    return gfi::check_launch("gf_csc_sgd_update");
 }
 
 }  // extern "C"

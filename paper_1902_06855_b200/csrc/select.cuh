@@ -85,15 +85,35 @@ inline __device__ void block_topk(const float* norms, uint64_t nc, uint64_t k, u
             if (match) atomicAdd(&sh.hist[(key >> shift) & 255u], 1u);
         }
         __syncthreads();
-        if (tid == 0) {
-            unsigned long long cum = 0;
-            int d = 255;
-            for (; d > 0; --d) {
-                if (cum + sh.hist[d] >= remaining) break;
-                cum += sh.hist[d];
+        if (tid < 32) {
+            // warp 0: lane l owns digits 255-8l .. 248-8l (descending); find the digit where
+            // the descending cumulative count first reaches `remaining`.
+            unsigned c[8];
+            unsigned tot = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                c[j] = sh.hist[255 - 8 * tid - j];
+                tot += c[j];
             }
-            sh.digit = unsigned(d);
-            sh.rem = remaining - cum;
+            unsigned incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (tid >= o) incl += y;
+            }
+            const unsigned excl = incl - tot;
+            const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl >= remaining);
+            const int L = hit ? __ffs(hit) - 1 : 31;
+            if (tid == L) {
+                unsigned long long cum = excl;
+                int d = 255 - 8 * L;
+                for (int j = 0; j < 8; ++j, --d) {
+                    if (cum + c[j] >= remaining || d == 0) break;
+                    cum += c[j];
+                }
+                sh.digit = unsigned(d);
+                sh.rem = remaining - cum;
+            }
         }
         __syncthreads();
         prefix = (prefix << 8) | sh.digit;
@@ -117,7 +137,7 @@ inline __device__ void block_topk(const float* norms, uint64_t nc, uint64_t k, u
 }
 
 // plan[0] staged elements, plan[1] important chunks, plan[2] windows, plan[3] window
-// stride (elements). Windows: sparse.cpp:142-158 cuts after the selected chunk at which
+// stride (elements), plan[4 .. 4+plan[1]) the important chunk indices, ascending. Windows: sparse.cpp:142-158 cuts after the selected chunk at which
 // pending bytes >= theta; since only the final pool chunk differs in length, every
 // window holds m = max(1, ceil(theta / (chunk*esz))) chunks except the last.
 inline __device__ void block_plan(const uint8_t* flags, uint64_t total, uint64_t chunk, uint64_t nc,
@@ -134,8 +154,9 @@ inline __device__ void block_plan(const uint8_t* flags, uint64_t total, uint64_t
         }
         uint64_t tot_len, tot_cnt;
         const uint64_t ex = block_excl_scan<uint64_t>(len, &tot_len, sh.u64s);
-        block_excl_scan<uint64_t>(one, &tot_cnt, sh.u64s);
+        const uint64_t exc = block_excl_scan<uint64_t>(one, &tot_cnt, sh.u64s);
         if (c < nc) coff[c] = carry_len + ex;
+        if (one) plan[4 + carry_cnt + exc] = c;  // ascending list of important chunks
         carry_len += tot_len;
         carry_cnt += tot_cnt;
     }

@@ -147,8 +147,8 @@ class GradSync:
 
     # ---- state for CSC (allocated by the caller's allocator: torch or cudaMalloc) -------
     def attach_csc_state(self, hg, imp, coff, plan, hu, w):
-        """Device buffers: hg (total fp32), imp[2] (nc u8), coff[2] (nc u64), plan[2] (4 u64),
-        hu/w (total fp32). imp[0]/coff[0]/plan[0] must describe iteration 0 (all ones)."""
+        """Device buffers: hg (total fp32), imp[2] (nc u8), coff[2] (nc u64), plan[2]
+        (4 + nc u64), hu/w (total fp32). imp[0] must hold iteration 0's set (all ones)."""
         self._csc_bufs = dict(hg=hg, imp=imp, coff=coff, plan=plan, hu=hu, w=w)
 
     def init_csc_plan(self, stream=None):
@@ -197,9 +197,12 @@ class GradSync:
         if self.world > 1:
             capi.call("gf_ring_allreduce_planned", self.comm, self.dtype, self.stage_off,
                       b["plan"][cur], stream)
+        # chunks selected for this iteration (iteration 0 is dense, sparse.cpp:45-51)
+        k_cur = L.num_chunks if self.iteration == 0 else selection_count(
+            sparsity_at(self.iteration, self.warmup_iters, self.final_sparsity), L.num_chunks)
         mark("scatter")
-        capi.call("gf_csc_scatter", self.dtype, self.pool_ptr, self.stage_ptr, b["imp"][cur],
-                  b["coff"][cur], L.total, L.chunk, L.num_chunks, stream)
+        capi.call("gf_csc_scatter", self.dtype, self.pool_ptr, self.stage_ptr, b["plan"][cur],
+                  b["coff"][cur], L.total, L.chunk, L.num_chunks, k_cur, stream)
         mark("norms")
         capi.call("gf_chunk_norms", self.dtype, self.pool_ptr, L.total, L.chunk, L.num_chunks,
                   b["imp"][cur], self.world, self.norms_ptr, stream)
@@ -209,8 +212,8 @@ class GradSync:
         capi.call("gf_csc_select", self.comm, self.norms_off, L.num_chunks, k, b["imp"][nxt],
                   L.total, L.chunk, self.dtype, self.theta, b["coff"][nxt], b["plan"][nxt], stream)
         mark("sgd_update")
-        capi.call("gf_csc_sgd_update", self.dtype, self.pool_ptr, b["imp"][cur], L.total, L.chunk,
-                  L.num_chunks, self.world, self.momentum, self.lr, b["hu"], b["w"], stream)
+        capi.call("gf_csc_sgd_update", self.dtype, self.pool_ptr, b["plan"][cur], L.total, L.chunk,
+                  L.num_chunks, k_cur, self.world, self.momentum, self.lr, b["hu"], b["w"], stream)
         mark(None)
         self.iteration += 1
 

@@ -266,7 +266,7 @@ def test_csc_correct_and_fused(gf, oracle, G, dtype):
     assert (G.bits(G.host(hg_d)) == G.bits(hg_w)).all()
     # (b) plan + fused pack/correct/compact
     coff = G.zeros(nc, np.uint64)
-    plan = G.zeros(4, np.uint64)
+    plan = G.zeros(4 + nc, np.uint64)
     gf.call("gf_csc_plan", imp_d.data_ptr(), total, chunk, nc, dtype, THETA_INF,
             coff.data_ptr(), plan.data_ptr(), None)
     fd = G.dev(flat)
@@ -285,13 +285,13 @@ def test_csc_correct_and_fused(gf, oracle, G, dtype):
     assert (G.bits(G.host(stage, et)[: stage_w.size]) == G.bits(stage_w)).all()
     # (c) stand-alone compact and scatter round trip
     stage3 = G.zeros(total, et)
-    gf.call("gf_csc_compact", dtype, pool2.data_ptr(), stage3.data_ptr(), imp_d.data_ptr(),
-            coff.data_ptr(), total, chunk, nc, None)
+    gf.call("gf_csc_compact", dtype, pool2.data_ptr(), stage3.data_ptr(), plan.data_ptr(),
+            coff.data_ptr(), total, chunk, nc, nc, None)
     G.sync()
     assert (G.bits(G.host(stage3, et)[: stage_w.size]) == G.bits(stage_w)).all()
     pool3 = G.zeros(total, et)
-    gf.call("gf_csc_scatter", dtype, pool3.data_ptr(), stage3.data_ptr(), imp_d.data_ptr(),
-            coff.data_ptr(), total, chunk, nc, None)
+    gf.call("gf_csc_scatter", dtype, pool3.data_ptr(), stage3.data_ptr(), plan.data_ptr(),
+            coff.data_ptr(), total, chunk, nc, nc, None)
     G.sync()
     want3 = np.zeros(total, et)
     oracle.csc_scatter(want3, imp, chunk, stage_w, dtype=dtype)
@@ -318,13 +318,14 @@ def test_select_topk_and_plan(gf, oracle, G):
             for theta in (0, 1000, 64000 * 3, THETA_INF):
                 total = nc * 32 + 17
                 coff = G.zeros(nc, np.uint64)
-                plan = G.zeros(4, np.uint64)
+                plan = G.zeros(4 + nc, np.uint64)
                 gf.call("gf_csc_plan", flags.data_ptr(), total, 32, nc, F16, theta,
                         coff.data_ptr(), plan.data_ptr(), None)
                 G.sync()
                 pl = G.host(plan, np.uint64).astype(np.int64)
                 ws, wl = oracle.csc_windows(want, total, 32, 2, theta)
-                staged, kc, nwin, stride = (int(v) for v in pl)
+                staged, kc, nwin, stride = (int(v) for v in pl[:4])
+                assert list(pl[4:4 + kc]) == list(np.nonzero(want)[0])
                 assert nwin == len(ws)
                 dev_w = [(w * stride, (staged - w * stride) if w == nwin - 1 else stride)
                          for w in range(nwin)]
@@ -346,7 +347,7 @@ def test_select_colocated_norm_exchange(gf, oracle, G):
         dn = [G.dev(x) for x in norms]
         flags = G.zeros(nc, np.uint8)
         coff = G.zeros(nc, np.uint64)
-        plan = G.zeros(4, np.uint64)
+        plan = G.zeros(4 + nc, np.uint64)
         gf.call("gf_csc_select_colocated", gf.ptr_array(dn), n, None, nc, 191, flags.data_ptr(),
                 nc * 32000, 32000, F16, THETA_INF, coff.data_ptr(), plan.data_ptr(), None)
         G.sync()
@@ -365,15 +366,18 @@ def test_sgd_updates(gf, oracle, golden, G, dtype):
         n, dt, theta, chunk, T = (int(x) for x in g[p + "meta"])
     total = int(g[p + "sizes"].sum())
     nc = oracle.pool_layout(g[p + "sizes"], chunk)[1]
+    coff = G.zeros(nc, np.uint64)
+    plan = G.zeros(4 + nc, np.uint64)
     for r in range(n):
         hu = G.zeros(total, np.float32)
         w = G.dev(g[p + "w0"])
         for t in range(T):
             pool = G.dev(g[p + "pool_x"][t][r])
             impd = G.dev(g[p + "imp"][t][r])
-            gf.call("gf_csc_sgd_update", dt, pool.data_ptr(), impd.data_ptr(),
-                    total, chunk, nc, n, np.float32(0.9), np.float32(0.01), hu.data_ptr(),
-                    w.data_ptr(), None)
+            gf.call("gf_csc_plan", impd.data_ptr(), total, chunk, nc, dt, THETA_INF,
+                    coff.data_ptr(), plan.data_ptr(), None)
+            gf.call("gf_csc_sgd_update", dt, pool.data_ptr(), plan.data_ptr(), total, chunk, nc,
+                    nc, n, np.float32(0.9), np.float32(0.01), hu.data_ptr(), w.data_ptr(), None)
             G.sync()
             assert (G.bits(G.host(hu)) == G.bits(g[p + "hu"][t][r])).all()
             assert (G.bits(G.host(w)) == G.bits(g[p + "w"][t][r])).all()
@@ -382,9 +386,11 @@ def test_sgd_updates(gf, oracle, golden, G, dtype):
     hu1, w1 = G.zeros(total, np.float32), G.dev(g[p + "w0"])
     hu2, w2 = G.zeros(total, np.float32), G.dev(g[p + "w0"])
     ones = G.dev(np.ones(nc, np.uint8))
+    gf.call("gf_csc_plan", ones.data_ptr(), total, chunk, nc, dt, THETA_INF, coff.data_ptr(),
+            plan.data_ptr(), None)
     gf.call("gf_dense_sgd_update", dt, pool.data_ptr(), total, n, np.float32(0.9),
             np.float32(0.01), hu1.data_ptr(), w1.data_ptr(), None)
-    gf.call("gf_csc_sgd_update", dt, pool.data_ptr(), ones.data_ptr(), total, chunk, nc, n,
+    gf.call("gf_csc_sgd_update", dt, pool.data_ptr(), plan.data_ptr(), total, chunk, nc, nc, n,
             np.float32(0.9), np.float32(0.01), hu2.data_ptr(), w2.data_ptr(), None)
     G.sync()
     assert (G.bits(G.host(w1)) == G.bits(G.host(w2))).all()
@@ -406,7 +412,7 @@ def test_csc_multistep_colocated_vs_reference_golden(gf, golden, oracle, G):
         norms = [G.zeros(nc, np.float32) for _ in range(n)]
         imp = G.dev(np.ones(nc, np.uint8))
         coff = G.zeros(nc, np.uint64)
-        plan = G.zeros(4, np.uint64)
+        plan = G.zeros(4 + nc, np.uint64)
         gf.call("gf_csc_plan", imp.data_ptr(), total, chunk, nc, dt, theta, coff.data_ptr(),
                 plan.data_ptr(), None)
         for t in range(T):
@@ -421,7 +427,7 @@ def test_csc_multistep_colocated_vs_reference_golden(gf, golden, oracle, G):
                     plan.data_ptr(), None)
             for r in range(n):
                 gf.call("gf_csc_scatter", dt, pools[r].data_ptr(), stages[r].data_ptr(),
-                        imp.data_ptr(), coff.data_ptr(), total, chunk, nc, None)
+                        plan.data_ptr(), coff.data_ptr(), total, chunk, nc, nc, None)
                 gf.call("gf_chunk_norms", dt, pools[r].data_ptr(), total, chunk, nc,
                         imp.data_ptr(), n, norms[r].data_ptr(), None)
             k = oracle.selection_count(oracle.sparsity_at(t + 1, 2, 0.75), nc)

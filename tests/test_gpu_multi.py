@@ -122,7 +122,7 @@ def _worker_csc(rank, world, port):
     _put(cudart, base, noff, norms[rank])
     flags = torch.zeros(nc, dtype=torch.uint8, device="cuda")
     coff = torch.zeros(nc, dtype=torch.int64, device="cuda")
-    plan = torch.zeros(4, dtype=torch.int64, device="cuda")
+    plan = torch.zeros(4 + nc, dtype=torch.int64, device="cuda")
     total = nc * 32000 + 12840
     capi.call("gf_csc_select", comm, noff, nc, k, flags.data_ptr(), total, 32000, F16,
               capi.THETA_INF, coff.data_ptr(), plan.data_ptr(), None)
