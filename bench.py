@@ -256,8 +256,10 @@ def main():
         plan = [torch.zeros(4 + nc, dtype=torch.int64, device=dev) for _ in range(2)]
         hu = torch.zeros(total, device=dev)
         w = torch.zeros(total, device=dev)
+        nacc = torch.zeros(nc, dtype=torch.int64, device=dev)
         sync.attach_csc_state(hg.data_ptr(), [t.data_ptr() for t in imp], [t.data_ptr() for t in coff],
-                              [t.data_ptr() for t in plan], hu.data_ptr(), w.data_ptr())
+                              [t.data_ptr() for t in plan], hu.data_ptr(), w.data_ptr(),
+                              nacc=nacc.data_ptr())
         sync.init_csc_plan(sp)
 
     marks = []
@@ -333,7 +335,7 @@ def main():
         # staged elements of the last timed (sparse) iteration, read back after timing
         staged = int(plan[(sync.iteration - 1) & 1][0].item())
         algo["pack_correct"] = total * 14 + staged * 2   # g, hg in; pool, hg, staging out
-        algo["scatter"] = staged * 4                      # staging in, pool out
+        algo["scatter"] = staged * 4                      # staging in, pool out (+ exact L1)
         algo["sgd_update"] = staged * 18                  # pool in; hu, w in+out
         ring_bytes = ring_bus_bytes(L, esz, world, [staged])
     else:

@@ -104,20 +104,23 @@ int gf_csc_correct(int dtype, void* pool, float* hg, const uint8_t* important, u
 /* Fused pack + correction + compaction over all tensors: for pool element i in chunk c
  *   g = dec(enc(src)) + hg ; hg = imp ? 0 : momentum*g ; pool = enc(g) ;
  *   if imp[c]: staging[coff[c] + (i - c*chunk)] = enc(g).
- * coff (device, nc entries) comes from gf_csc_plan. staging may be NULL (no compaction). */
+ * coff (device, nc entries) comes from gf_csc_plan. staging may be NULL (no compaction).
+ * nacc (device, nc uint64, fp16 pools only, nullable): the exact sum of |pool| of every
+ * UNIMPORTANT chunk is added in units of 2^-24 (bit 63 = NaN seen) — K3 fused into K2. */
 int gf_csc_pack_correct(int dtype, void* pool, float* hg, void* staging,
                         const uint8_t* important, const uint64_t* coff, uint64_t total,
                         uint64_t chunk, uint64_t nc, const float* const* src,
                         const uint64_t* pool_off, const uint64_t* count, int ntensors,
-                        float momentum, void* stream);
+                        float momentum, uint64_t* nacc, void* stream);
 /* Staging pack / write-back over the important chunks listed in `plan` (see gf_csc_plan):
  * staging[coff[c] + i] <-> pool[c*chunk + i]. max_chunks bounds plan[1] (launch size; nc is safe). */
 int gf_csc_compact(int dtype, const void* pool, void* staging, const uint64_t* plan,
                    const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
                    uint64_t max_chunks, void* stream);
+/* nacc (nullable, fp16): adds the exact |x| sums of the written-back important chunks. */
 int gf_csc_scatter(int dtype, void* pool, const void* staging, const uint64_t* plan,
                    const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
-                   uint64_t max_chunks, void* stream);
+                   uint64_t max_chunks, uint64_t* nacc, void* stream);
 /* From important flags (device): coff[c] = sum of lengths of important chunks < c;
  * plan (device, 4 + nc uint64): plan[0] = staged elements, plan[1] = important chunk
  * count, plan[2] = window count, plan[3] = elements per full window (theta policy of
@@ -179,13 +182,17 @@ int gf_ring_allreduce_colocated_planned(int dtype, void* const* bufs, int world,
  * norms (nc fp32 at heap offset norms_off on every rank) are summed over ranks in
  * ring order (as the fp32 ring_allreduce would), written back to every rank's local
  * norms, top-k selected -> flags (device, nc bytes); then coff/plan as gf_csc_plan. */
+/* With nacc != NULL the local norms are first finalized from the exact accumulators
+ * (float(sum), x1/N where imp_cur[c]) and nacc is zeroed for the next iteration. */
 int gf_csc_select(gf_comm* comm, uint64_t norms_off, uint64_t nc, uint64_t k,
                   uint8_t* flags, uint64_t total, uint64_t chunk, int dtype, uint64_t theta,
-                  uint64_t* coff, uint64_t* plan, void* stream);
+                  uint64_t* coff, uint64_t* plan, uint64_t* nacc, const void* pool,
+                  const uint8_t* imp_cur, void* stream);
 int gf_csc_select_colocated(float* const* norms, int world, const int* ring_order,
                             uint64_t nc, uint64_t k, uint8_t* flags, uint64_t total,
                             uint64_t chunk, int dtype, uint64_t theta, uint64_t* coff,
-                            uint64_t* plan, void* stream);
+                            uint64_t* plan, uint64_t* const* nacc, const void* const* pools,
+                            const uint8_t* imp_cur, void* stream);
 
 /* Payload bytes the reference ring records for one allreduce of len elements at ring
  * position `position` (collectives.cpp:69-96): 2(N-1) sends of segment_of sizes. */

@@ -66,9 +66,9 @@ SIGNATURES = {
     "gf_unpack": [_i, _vp, _vp, _vp, _vp, _i, _i, _vp],
     "gf_chunk_norms": [_i, _vp, _u64, _u64, _u64, _vp, _i, _vp, _vp],
     "gf_csc_correct": [_i, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _u64, _f, _vp],
-    "gf_csc_pack_correct": [_i, _vp, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _vp, _vp, _vp, _i, _f, _vp],
+    "gf_csc_pack_correct": [_i, _vp, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _vp, _vp, _vp, _i, _f, _vp, _vp],
     "gf_csc_compact": [_i, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _vp],
-    "gf_csc_scatter": [_i, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _vp],
+    "gf_csc_scatter": [_i, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _vp, _vp],
     "gf_csc_plan": [_vp, _u64, _u64, _u64, _i, _u64, _vp, _vp, _vp],
     "gf_select_topk": [_vp, _u64, _u64, _vp, _vp],
     "gf_csc_sgd_update": [_i, _vp, _vp, _u64, _u64, _u64, _u64, _i, _f, _f, _vp, _vp, _vp],
@@ -90,8 +90,9 @@ SIGNATURES = {
     "gf_ring_allreduce_planned": [_vp, _i, _u64, _vp, _vp],
     "gf_ring_allreduce_colocated": [_i, _vp, _i, _vp, _vp, _vp, _i, _vp],
     "gf_ring_allreduce_colocated_planned": [_i, _vp, _i, _vp, _vp, _vp],
-    "gf_csc_select": [_vp, _u64, _u64, _u64, _vp, _u64, _u64, _i, _u64, _vp, _vp, _vp],
-    "gf_csc_select_colocated": [_vp, _i, _vp, _u64, _u64, _vp, _u64, _u64, _i, _u64, _vp, _vp, _vp],
+    "gf_csc_select": [_vp, _u64, _u64, _u64, _vp, _u64, _u64, _i, _u64, _vp, _vp, _vp, _vp, _vp, _vp],
+    "gf_csc_select_colocated": [_vp, _i, _vp, _u64, _u64, _vp, _u64, _u64, _i, _u64, _vp, _vp, _vp,
+                                _vp, _vp, _vp],
     "gf_ring_traffic": [_u64, _i, _i, _i, _u64p, _u64p, _u64p],
     "gf_abi_version": [],
     "gf_last_error": [],

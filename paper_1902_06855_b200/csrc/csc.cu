@@ -163,13 +163,49 @@ __global__ void correct_kernel(void* __restrict__ pool, float* __restrict__ hg,
     }
 }
 
-// K2: fused pack + correction + compaction.
+// Exact |x| sum of 8 halves in units of 2^-24 (see gf_chunk_norms); NaN-free input.
+__device__ __forceinline__ uint64_t units8(uint4 v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint64_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc += half_units(uint16_t(w[k] & 0xFFFFu)) + half_units(uint16_t(w[k] >> 16));
+    return acc;
+}
+
+constexpr uint64_t kNaccNaN = 1ull << 63;  // NaN marker in an exact-norm accumulator
+
+// Adds a per-thread (chunk, units) contribution with warp aggregation: lanes whose chunk
+// equals the first active lane's chunk are summed with shuffles, the others add directly.
+// Must be called by all 32 lanes.
+__device__ __forceinline__ void nacc_add(uint64_t* nacc, uint64_t c, uint64_t u, bool nan, bool active) {
+    const unsigned full = 0xFFFFFFFFu;
+    const unsigned act = __ballot_sync(full, active);
+    if (!act) return;
+    const int leader = __ffs(act) - 1;
+    const uint64_t c0 = __shfl_sync(full, c, leader);
+    const bool same = active && c == c0;
+    uint64_t v = same ? u : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(full, v, o);
+    const bool anynan_same = __any_sync(full, same && nan);
+    if ((threadIdx.x & 31) == unsigned(leader)) {
+        if (v) atomicAdd(reinterpret_cast<unsigned long long*>(nacc + c0), (unsigned long long)v);
+        if (anynan_same) atomicOr(reinterpret_cast<unsigned long long*>(nacc + c0), (unsigned long long)kNaccNaN);
+    }
+    if (active && !same) {
+        if (u) atomicAdd(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)u);
+        if (nan) atomicOr(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)kNaccNaN);
+    }
+}
+
+// K2: fused pack + correction + compaction (+ exact norms of the unimportant chunks).
 template <int DT>
 __global__ void __launch_bounds__(kThreads)
 pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ pool,
                     float* __restrict__ hg, void* __restrict__ staging,
                     const uint8_t* __restrict__ imp, const uint64_t* __restrict__ coff,
-                    uint64_t chunk, uint64_t nc, float mom, uint64_t total_tiles) {
+                    uint64_t chunk, uint64_t nc, float mom, uint64_t total_tiles,
+                    uint64_t* __restrict__ nacc) {
     for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int t = find_tensor(T, tile);
         const uint64_t base = (tile - T.tiles[t]) * kTile;
@@ -177,34 +213,64 @@ pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ po
         const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
         const uint64_t po = T.off[t] + base;
         uint64_t done = 0;
-        if (DT == GF_F16 && (reinterpret_cast<uintptr_t>(T.ptr[t]) & 15u) == 0 && po % 8 == 0 &&
-            chunk % 8 == 0) {
+        if (DT == GF_F16 && (reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0 && po % 8 == 0 &&
+            chunk % 8 == 0 && (reinterpret_cast<uintptr_t>(hg) & 31u) == 0) {
             // 8 consecutive pool elements never straddle a chunk boundary here.
             uint16_t* __restrict__ d = static_cast<uint16_t*>(pool) + po;
             uint16_t* __restrict__ stg = static_cast<uint16_t*>(staging);
             const int nvec = int(len / 8);
-            for (int v = threadIdx.x; v < nvec; v += kThreads) {
-                const uint64_t pi = po + 8 * uint64_t(v);
-                const uint64_t c = min(pi / chunk, nc - 1);
-                const bool im = imp[c] != 0;
-                const float4 a = gfd::ld16f_stream(s + 8 * v);
-                const float4 b = gfd::ld16f_stream(s + 8 * v + 4);
-                float4* hp = reinterpret_cast<float4*>(hg + pi);
-                float4 h0 = hp[0], h1 = hp[1];
-                const float g[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-                float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-                uint32_t o[4];
+            for (int v0 = 0; v0 < nvec; v0 += kThreads) {
+                const int v = v0 + threadIdx.x;
+                const bool act = v < nvec;
+                uint64_t c = 0, units = 0;
+                bool im = true, nan = false;
+                if (act) {
+                    const uint64_t pi = po + 8 * uint64_t(v);
+                    c = min(pi / chunk, nc - 1);
+                    im = imp[c] != 0;
+                    const gfd::F8 gv = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
+                    gfd::F8 hv = gfd::ld32f(hg + pi);
+                    float* hp = reinterpret_cast<float*>(&hv);
+                    const uint4 h1 = gfd::enc8(gv.lo, gv.hi);  // pack (write_tensor)
+                    uint4 ov;
+                    bool slow = gfd::any_special(h1);
+                    float hn[8];
+                    if (!slow) {
+                        const uint32_t hw[4] = {h1.x, h1.y, h1.z, h1.w};
+                        uint32_t o[4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint16_t lo = gfd::enc(correct_elem(gfd::dec(gfd::enc(g[2 * k])), &hv[2 * k], im, mom));
-                    const uint16_t hi = gfd::enc(correct_elem(gfd::dec(gfd::enc(g[2 * k + 1])), &hv[2 * k + 1], im, mom));
-                    o[k] = uint32_t(lo) | (uint32_t(hi) << 16);
+                        for (int k = 0; k < 4; ++k) {
+                            const float2 g1 = gfd::h2f2(hw[k]);
+                            const float a0 = __fadd_rn(g1.x, hp[2 * k]);
+                            const float a1 = __fadd_rn(g1.y, hp[2 * k + 1]);
+                            hn[2 * k] = im ? 0.0f : __fmul_rn(mom, a0);
+                            hn[2 * k + 1] = im ? 0.0f : __fmul_rn(mom, a1);
+                            o[k] = gfd::f22h2(a0, a1);
+                        }
+                        ov = make_uint4(o[0], o[1], o[2], o[3]);
+                        slow = gfd::any_special(ov);  // non-finite or clamped sum: exact slow path
+                    }
+                    if (slow) {
+                        const float g[8] = {gv.lo.x, gv.lo.y, gv.lo.z, gv.lo.w, gv.hi.x, gv.hi.y, gv.hi.z, gv.hi.w};
+                        uint32_t o[4];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) hn[k] = hp[k];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint16_t lo = gfd::enc(correct_elem(gfd::dec(gfd::enc(g[2 * k])), &hn[2 * k], im, mom));
+                            const uint16_t hi = gfd::enc(correct_elem(gfd::dec(gfd::enc(g[2 * k + 1])), &hn[2 * k + 1], im, mom));
+                            o[k] = uint32_t(lo) | (uint32_t(hi) << 16);
+                        }
+                        ov = make_uint4(o[0], o[1], o[2], o[3]);
+                        nan = gfd::any_special(ov);  // the pool holds no inf, so special == NaN
+                    }
+                    gfd::st32f(hg + pi, make_float4(hn[0], hn[1], hn[2], hn[3]),
+                               make_float4(hn[4], hn[5], hn[6], hn[7]));
+                    gfd::st16(d + 8 * v, ov);
+                    if (im && stg) gfd::st16(stg + coff[c] + (pi - c * chunk), ov);
+                    if (!im && nacc) units = units8(nan ? make_uint4(0, 0, 0, 0) : ov);
                 }
-                hp[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
-                hp[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
-                const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
-                gfd::st16(d + 8 * v, ov);
-                if (im && stg) gfd::st16(stg + coff[c] + (pi - c * chunk), ov);
+                if (nacc) nacc_add(nacc, c, units, nan, act && !im);
             }
             done = uint64_t(nvec) * 8;
         }
@@ -216,6 +282,12 @@ pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ po
                 const uint16_t w = gfd::enc(correct_elem(gfd::dec(gfd::enc(s[i])), hg + pi, im, mom));
                 static_cast<uint16_t*>(pool)[pi] = w;
                 if (im && staging) static_cast<uint16_t*>(staging)[coff[c] + (pi - c * chunk)] = w;
+                if (!im && nacc) {
+                    if ((w & 0x7C00u) == 0x7C00u)
+                        atomicOr(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)kNaccNaN);
+                    else if (half_units(w))
+                        atomicAdd(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)half_units(w));
+                }
             } else {
                 const float w = correct_elem(s[i], hg + pi, im, mom);
                 static_cast<float*>(pool)[pi] = w;
@@ -227,9 +299,12 @@ pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ po
 
 // Staging pack (dir=0) / write-back (dir=1) over the important chunks listed in the plan
 // (plan[4+j], j < plan[1]): grid.y walks the list, grid.x tiles a chunk; 16-B copies.
+// On write-back of an fp16 pool, the exact |x| sums of the (now global) chunk values are
+// accumulated into nacc — the norms of the important chunks, without re-reading the pool.
 __global__ void compact_kernel(char* __restrict__ pool, char* __restrict__ staging,
                                const uint64_t* __restrict__ plan, const uint64_t* __restrict__ coff,
-                               uint64_t total, uint64_t chunk, uint64_t nc, uint64_t esz, int dir) {
+                               uint64_t total, uint64_t chunk, uint64_t nc, uint64_t esz, int dir,
+                               uint64_t* __restrict__ nacc) {
     const uint64_t kc = plan[1];
     for (uint64_t j = blockIdx.y; j < kc; j += gridDim.y) {
         const uint64_t c = plan[4 + j];
@@ -237,19 +312,45 @@ __global__ void compact_kernel(char* __restrict__ pool, char* __restrict__ stagi
         char* p = pool + c * chunk * esz;
         char* s = staging + coff[c] * esz;
         const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(s)) & 15u) == 0;
-        uint64_t done = 0;
+        uint64_t done = 0, units = 0;
+        bool nan = false;
         if (vec) {
             const uint64_t nv = len / 16;
             for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < nv;
                  v += uint64_t(gridDim.x) * blockDim.x) {
-                if (dir == 0) gfd::st16(s + 16 * v, gfd::ld16_stream(p + 16 * v));
-                else gfd::st16(p + 16 * v, gfd::ld16_stream(s + 16 * v));
+                if (dir == 0) {
+                    gfd::st16(s + 16 * v, gfd::ld16_stream(p + 16 * v));
+                } else {
+                    const uint4 x = gfd::ld16_stream(s + 16 * v);
+                    gfd::st16(p + 16 * v, x);
+                    if (nacc) {
+                        if (gfd::any_special(x)) nan = true; else units += units8(x);
+                    }
+                }
             }
             done = nv * 16;
         }
         for (uint64_t i = done + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < len;
              i += uint64_t(gridDim.x) * blockDim.x) {
-            if (dir == 0) s[i] = p[i]; else p[i] = s[i];
+            if (dir == 0) {
+                s[i] = p[i];
+            } else {
+                p[i] = s[i];
+                if (nacc && (i & 1)) {  // fp16: the element completes at its high byte
+                    const uint16_t h = uint16_t(uint8_t(s[i - 1])) | (uint16_t(uint8_t(s[i])) << 8);
+                    if ((h & 0x7C00u) == 0x7C00u) nan = true; else units += half_units(h);
+                }
+            }
+        }
+        if (nacc) {
+            uint64_t v = units;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+            const bool an = __any_sync(0xFFFFFFFFu, nan);
+            if ((threadIdx.x & 31) == 0) {
+                if (v) atomicAdd(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)v);
+                if (an) atomicOr(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)kNaccNaN);
+            }
         }
     }
 }
@@ -319,14 +420,15 @@ int grid_y(uint64_t max_chunks, uint64_t nc) {
 
 int compact_launch(int dtype, void* pool, const void* staging, const uint64_t* plan,
                    const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
-                   uint64_t max_chunks, int dir, void* stream) {
+                   uint64_t max_chunks, int dir, uint64_t* nacc, void* stream) {
+    if (nacc && dtype != GF_F16) return gfi::fail(GF_ERR_CONFIG, "exact norm accumulation needs an fp16 pool");
     if (!gfi::valid_dtype(dtype) || chunk == 0 || nc == 0 || !plan || !coff)
         return gfi::fail(GF_ERR_CONFIG, "gf_csc_compact/scatter: bad arguments");
     const uint64_t bytes = std::max<uint64_t>(chunk, total - (nc - 1) * chunk) * gfi::esz(dtype);
     const int gx = int(std::max<uint64_t>(1, std::min<uint64_t>((bytes / 16 + 511) / 512, 64)));
     compact_kernel<<<dim3(gx, grid_y(max_chunks, nc)), 512, 0, gfi::S(stream)>>>(
         static_cast<char*>(pool), static_cast<char*>(const_cast<void*>(staging)), plan, coff,
-        total, chunk, nc, gfi::esz(dtype), dir);
+        total, chunk, nc, gfi::esz(dtype), dir, nacc);
     gfi::count_launch();
     return gfi::check_launch("gf_csc_compact");
 }
@@ -373,19 +475,20 @@ int gf_csc_pack_correct(int dtype, void* pool, float* hg, void* staging,
                         const uint8_t* important, const uint64_t* coff, uint64_t total,
                         uint64_t chunk, uint64_t nc, const float* const* src,
                         const uint64_t* pool_off, const uint64_t* count, int ntensors,
-                        float momentum, void* stream) {
+                        float momentum, uint64_t* nacc, void* stream) {
     if (!gfi::valid_dtype(dtype) || chunk == 0 || nc == 0 || !pool || !hg || !important)
         return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct: bad arguments");
+    if (nacc && dtype != GF_F16) return gfi::fail(GF_ERR_CONFIG, "exact norm accumulation needs an fp16 pool");
     if (staging && !coff) return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct: staging needs coff");
     (void)total;
     return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
                           [&](const TensorTable& T, uint64_t tiles, int grid) {
                               if (dtype == GF_F16)
                                   pack_correct_kernel<GF_F16><<<grid, kThreads, 0, gfi::S(stream)>>>(
-                                      T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles);
+                                      T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc);
                               else
                                   pack_correct_kernel<GF_F32><<<grid, kThreads, 0, gfi::S(stream)>>>(
-                                      T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles);
+                                      T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc);
                           });
 }
 
@@ -393,13 +496,14 @@ int gf_csc_compact(int dtype, const void* pool, void* staging, const uint64_t* p
                    const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
                    uint64_t max_chunks, void* stream) {
     return compact_launch(dtype, const_cast<void*>(pool), staging, plan, coff, total, chunk, nc,
-                          max_chunks, 0, stream);
+                          max_chunks, 0, nullptr, stream);
 }
 
 int gf_csc_scatter(int dtype, void* pool, const void* staging, const uint64_t* plan,
                    const uint64_t* coff, uint64_t total, uint64_t chunk, uint64_t nc,
-                   uint64_t max_chunks, void* stream) {
-    return compact_launch(dtype, pool, staging, plan, coff, total, chunk, nc, max_chunks, 1, stream);
+                   uint64_t max_chunks, uint64_t* nacc, void* stream) {
+    return compact_launch(dtype, pool, staging, plan, coff, total, chunk, nc, max_chunks, 1, nacc,
+                          stream);
 }
 
 int gf_csc_sgd_update(int dtype, const void* pool, const uint64_t* plan, uint64_t total,

@@ -64,6 +64,9 @@ struct RingArgs {
 
 struct SelArgs {
     float* norms[GF_MAX_RANKS];          // by rank
+    uint64_t* nacc[GF_MAX_RANKS];        // exact |x| sums (units 2^-24) to finalize, or null
+    const uint16_t* pool[GF_MAX_RANKS];  // fp16 pools (sequential fallback for huge sums)
+    const uint8_t* imp_cur;              // this iteration's important set (x1/N)
     int ring[GF_MAX_RANKS];
     int world, rank, p2p;
     uint64_t nc, k, total, chunk, esz, theta;
@@ -229,6 +232,32 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
     if (threadIdx.x == 0) s_ok = 1;
     const int n = a.world;
     const uint64_t epoch = a.p2p ? a.epochs[0] : 0;
+    // Finalize this iteration's local norms from the exact accumulators written by
+    // pack_correct (unimportant chunks) and scatter (important chunks): chunk_l1 +
+    // x1/N (sparse.cpp:176-184), then re-arm the accumulators for the next iteration.
+    if (a.nacc[0] || a.nacc[a.rank]) {
+        const float inv_world = 1.0f / float(n);
+        for (int r = a.p2p ? a.rank : 0; r < (a.p2p ? a.rank + 1 : n); ++r) {
+            for (uint64_t i = threadIdx.x; i < a.nc; i += gfs::kSelThreads) {
+                const uint64_t S = a.nacc[r][i];
+                float v;
+                if (S >> 63) {
+                    v = gfd::u2f(0x7FC00000u);
+                } else if (S < (1ull << 53)) {
+                    v = __double2float_rn(__ull2double_rn(S) * 0x1p-24);
+                } else {  // inexact fp64 partial sums in the reference: replay its order
+                    const uint64_t b = i * a.chunk, len = (i + 1 == a.nc) ? a.total - b : a.chunk;
+                    double d = 0.0;
+                    for (uint64_t e = 0; e < len; ++e) d = __dadd_rn(d, fabs(double(gfd::dec(a.pool[r][b + e]))));
+                    v = __double2float_rn(d);
+                }
+                if (a.imp_cur[i]) v = gfd::mul(v, inv_world);
+                a.norms[r][i] = v;
+                a.nacc[r][i] = 0;
+            }
+        }
+        __syncthreads();
+    }
     if (a.p2p && !cross_barrier(a, epoch + 1, &s_ok)) return;
     const uint64_t base = a.nc / uint64_t(n), rem = a.nc % uint64_t(n);
     for (uint64_t i = threadIdx.x; i < a.nc; i += gfs::kSelThreads) {
@@ -630,7 +659,10 @@ static int select_launch(SelArgs& a, cudaStream_t s) {
 
 int gf_csc_select(gf_comm* c, uint64_t norms_off, uint64_t nc, uint64_t k, uint8_t* flags,
                   uint64_t total, uint64_t chunk, int dtype, uint64_t theta, uint64_t* coff,
-                  uint64_t* plan, void* stream) {
+                  uint64_t* plan, uint64_t* nacc, const void* pool, const uint8_t* imp_cur,
+                  void* stream) {
+    if (nacc && (!pool || !imp_cur || dtype != GF_F16))
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_select: nacc needs an fp16 pool and the current set");
     if (int rc = comm_ready(c)) return rc;
     if (nc == 0 || k == 0 || !flags || !gfi::valid_dtype(dtype) || chunk == 0)
         return gfi::fail(GF_ERR_CONFIG, "gf_csc_select: bad arguments");
@@ -648,6 +680,9 @@ int gf_csc_select(gf_comm* c, uint64_t norms_off, uint64_t nc, uint64_t k, uint8
     }
     a.nc = nc; a.k = k; a.total = total; a.chunk = chunk; a.esz = gfi::esz(dtype); a.theta = theta;
     a.flags = flags; a.coff = coff; a.plan = plan;
+    a.nacc[c->rank] = nacc;
+    a.pool[c->rank] = static_cast<const uint16_t*>(pool);
+    a.imp_cur = imp_cur;
     a.flags_local = reinterpret_cast<uint64_t*>(c->alloc);
     a.epochs = a.flags_local + kFlagWords;
     a.timeout_ns = c->timeout_ns;
@@ -657,7 +692,10 @@ int gf_csc_select(gf_comm* c, uint64_t norms_off, uint64_t nc, uint64_t k, uint8
 
 int gf_csc_select_colocated(float* const* norms, int world, const int* ring_order, uint64_t nc,
                             uint64_t k, uint8_t* flags, uint64_t total, uint64_t chunk, int dtype,
-                            uint64_t theta, uint64_t* coff, uint64_t* plan, void* stream) {
+                            uint64_t theta, uint64_t* coff, uint64_t* plan, uint64_t* const* nacc,
+                            const void* const* pools, const uint8_t* imp_cur, void* stream) {
+    if (nacc && (!pools || !imp_cur || dtype != GF_F16))
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_select_colocated: nacc needs fp16 pools and the current set");
     if (!norms || world < 1 || world > GF_MAX_RANKS || nc == 0 || k == 0 || !flags ||
         !gfi::valid_dtype(dtype) || chunk == 0)
         return gfi::fail(GF_ERR_CONFIG, "gf_csc_select_colocated: bad arguments");
@@ -670,7 +708,12 @@ int gf_csc_select_colocated(float* const* norms, int world, const int* ring_orde
     for (int r = 0; r < world; ++r) {
         a.norms[r] = norms[r];
         a.ring[r] = ring_order ? ring_order[r] : r;
+        if (nacc) {
+            a.nacc[r] = nacc[r];
+            a.pool[r] = static_cast<const uint16_t*>(pools[r]);
+        }
     }
+    a.imp_cur = imp_cur;
     a.nc = nc; a.k = k; a.total = total; a.chunk = chunk; a.esz = gfi::esz(dtype); a.theta = theta;
     a.flags = flags; a.coff = coff; a.plan = plan;
     return select_launch(a, gfi::S(stream));

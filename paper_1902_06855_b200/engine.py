@@ -11,9 +11,9 @@ reference's semantics (paths relative to /root/reference/proj):
   CSC (src/sparse.cpp, Algorithm 1):
       gf_csc_pack_correct   pack + residual correction + compaction        (K2)
       gf_ring_allreduce_planned   over the staging buffer                   (K4)
-      gf_csc_scatter        staging -> pool (global sums)
-      gf_chunk_norms        exact chunk L1 (+ x1/N for important chunks)    (K3)
-      gf_csc_select         fp32 norm exchange + top-k + next plan          (K5)
+      gf_csc_scatter        staging -> pool (global sums) + exact L1 of those chunks
+      (K3 is fused: pack_correct/scatter accumulate exact chunk |x| sums for fp16 pools)
+      gf_csc_select         finalize norms, fp32 norm exchange, top-k, next plan (K5)
       gf_csc_sgd_update     unpack + momentum update, important chunks      (K6')
 
 Every launch is asynchronous on the caller's stream; nothing here synchronises or
@@ -146,10 +146,13 @@ class GradSync:
         self._csc_bufs = None
 
     # ---- state for CSC (allocated by the caller's allocator: torch or cudaMalloc) -------
-    def attach_csc_state(self, hg, imp, coff, plan, hu, w):
+    def attach_csc_state(self, hg, imp, coff, plan, hu, w, nacc=None):
         """Device buffers: hg (total fp32), imp[2] (nc u8), coff[2] (nc u64), plan[2]
-        (4 + nc u64), hu/w (total fp32). imp[0] must hold iteration 0's set (all ones)."""
-        self._csc_bufs = dict(hg=hg, imp=imp, coff=coff, plan=plan, hu=hu, w=w)
+        (4 + nc u64), hu/w (total fp32), nacc (nc u64, zeroed; fp16 pools: exact chunk norms
+        fused into pack/scatter). imp[0] must hold iteration 0's set (all ones)."""
+        if self.dtype != F16:
+            nacc = None
+        self._csc_bufs = dict(hg=hg, imp=imp, coff=coff, plan=plan, hu=hu, w=w, nacc=nacc)
 
     def init_csc_plan(self, stream=None):
         b = self._csc_bufs
@@ -190,9 +193,10 @@ class GradSync:
         cur, nxt = self.iteration & 1, (self.iteration + 1) & 1
         mark = mark or (lambda name: None)
         mark("pack_correct")
+        nacc = b["nacc"]
         capi.call("gf_csc_pack_correct", self.dtype, self.pool_ptr, b["hg"], self.stage_ptr,
                   b["imp"][cur], b["coff"][cur], L.total, L.chunk, L.num_chunks,
-                  self._ptrs(grad_ptrs), self._offs, self._cnts, m, self.momentum, stream)
+                  self._ptrs(grad_ptrs), self._offs, self._cnts, m, self.momentum, nacc, stream)
         mark("ring")
         if self.world > 1:
             capi.call("gf_ring_allreduce_planned", self.comm, self.dtype, self.stage_off,
@@ -202,15 +206,17 @@ class GradSync:
             sparsity_at(self.iteration, self.warmup_iters, self.final_sparsity), L.num_chunks)
         mark("scatter")
         capi.call("gf_csc_scatter", self.dtype, self.pool_ptr, self.stage_ptr, b["plan"][cur],
-                  b["coff"][cur], L.total, L.chunk, L.num_chunks, k_cur, stream)
-        mark("norms")
-        capi.call("gf_chunk_norms", self.dtype, self.pool_ptr, L.total, L.chunk, L.num_chunks,
-                  b["imp"][cur], self.world, self.norms_ptr, stream)
+                  b["coff"][cur], L.total, L.chunk, L.num_chunks, k_cur, nacc, stream)
+        if nacc is None:  # fp32 pool: separate norm pass (sequential fp64, as the reference)
+            mark("norms")
+            capi.call("gf_chunk_norms", self.dtype, self.pool_ptr, L.total, L.chunk, L.num_chunks,
+                      b["imp"][cur], self.world, self.norms_ptr, stream)
         mark("select")
         k = selection_count(sparsity_at(self.iteration + 1, self.warmup_iters,
                                         self.final_sparsity), L.num_chunks)
         capi.call("gf_csc_select", self.comm, self.norms_off, L.num_chunks, k, b["imp"][nxt],
-                  L.total, L.chunk, self.dtype, self.theta, b["coff"][nxt], b["plan"][nxt], stream)
+                  L.total, L.chunk, self.dtype, self.theta, b["coff"][nxt], b["plan"][nxt],
+                  nacc, self.pool_ptr if nacc else None, b["imp"][cur] if nacc else None, stream)
         mark("sgd_update")
         capi.call("gf_csc_sgd_update", self.dtype, self.pool_ptr, b["plan"][cur], L.total, L.chunk,
                   L.num_chunks, k_cur, self.world, self.momentum, self.lr, b["hu"], b["w"], stream)

@@ -273,11 +273,18 @@ def test_csc_correct_and_fused(gf, oracle, G, dtype):
     pool2 = G.zeros(total, et)
     hg2 = G.dev(hg0)
     stage = G.zeros(total, et)
+    nacc = G.zeros(nc, np.uint64)
     ptrs, offs, cnts = G.table(G.pool_tensors(fd, sizes, off))
     gf.call("gf_csc_pack_correct", dtype, pool2.data_ptr(), hg2.data_ptr(), stage.data_ptr(),
             imp_d.data_ptr(), coff.data_ptr(), total, chunk, nc, ptrs, offs, cnts, len(sizes),
-            mom, None)
+            mom, nacc.data_ptr() if dtype == F16 else None, None)
     G.sync()
+    if dtype == F16:  # K3 fused into K2: exact L1 of every unimportant chunk
+        want_l1 = oracle.chunk_norms(pool_w, chunk, nc, None, 1, dtype=dtype)
+        got_u = G.host(nacc, np.uint64)
+        for c in np.nonzero(imp == 0)[0]:
+            assert np.float32(float(got_u[c]) * 2.0 ** -24) == want_l1[c], c
+        assert not got_u[imp == 1].any()
     pl = G.host(plan, np.uint64)
     assert int(pl[0]) == stage_w.size and int(pl[1]) == int(imp.sum())
     assert (G.bits(G.host(pool2, et)) == G.bits(pool_w)).all()
@@ -291,7 +298,7 @@ def test_csc_correct_and_fused(gf, oracle, G, dtype):
     assert (G.bits(G.host(stage3, et)[: stage_w.size]) == G.bits(stage_w)).all()
     pool3 = G.zeros(total, et)
     gf.call("gf_csc_scatter", dtype, pool3.data_ptr(), stage3.data_ptr(), plan.data_ptr(),
-            coff.data_ptr(), total, chunk, nc, nc, None)
+            coff.data_ptr(), total, chunk, nc, nc, None, None)
     G.sync()
     want3 = np.zeros(total, et)
     oracle.csc_scatter(want3, imp, chunk, stage_w, dtype=dtype)
@@ -349,7 +356,8 @@ def test_select_colocated_norm_exchange(gf, oracle, G):
         coff = G.zeros(nc, np.uint64)
         plan = G.zeros(4 + nc, np.uint64)
         gf.call("gf_csc_select_colocated", gf.ptr_array(dn), n, None, nc, 191, flags.data_ptr(),
-                nc * 32000, 32000, F16, THETA_INF, coff.data_ptr(), plan.data_ptr(), None)
+                nc * 32000, 32000, F16, THETA_INF, coff.data_ptr(), plan.data_ptr(), None, None,
+                None, None)
         G.sync()
         assert (G.host(flags) == want).all()
         for r in range(n):
@@ -397,11 +405,17 @@ def test_sgd_updates(gf, oracle, golden, G, dtype):
 
 
 # ---- whole CSC iterations, colocated ranks, vs the reference's own multi-step run -------------
-def test_csc_multistep_colocated_vs_reference_golden(gf, golden, oracle, G):
+@pytest.mark.parametrize("fused_norms", [True, False])
+def test_csc_multistep_colocated_vs_reference_golden(gf, golden, oracle, G, fused_norms):
+    """Full CSC iterations (pack+correct+compact, ring, write-back, norms, exchange+top-k)
+    for n colocated ranks against the reference's own multi-step run. fused_norms: exact
+    chunk L1 accumulated inside pack_correct/scatter (fp16) instead of gf_chunk_norms."""
     g = golden("csc_run.npz")
     for ci in range(int(g["csc_cases"][0])):
         p = f"c{ci}_"
         n, dt, theta, chunk, T = (int(x) for x in g[p + "meta"])
+        if fused_norms and dt != F16:
+            continue
         sizes = [int(s) for s in g[p + "sizes"]]
         total = sum(sizes)
         off, nc, _ = oracle.pool_layout(sizes, chunk)
@@ -410,6 +424,7 @@ def test_csc_multistep_colocated_vs_reference_golden(gf, golden, oracle, G):
         stages = [G.zeros(total, et) for _ in range(n)]
         hgs = [G.zeros(total, np.float32) for _ in range(n)]
         norms = [G.zeros(nc, np.float32) for _ in range(n)]
+        naccs = [G.zeros(nc, np.uint64) for _ in range(n)] if fused_norms else None
         imp = G.dev(np.ones(nc, np.uint8))
         coff = G.zeros(nc, np.uint64)
         plan = G.zeros(4 + nc, np.uint64)
@@ -421,23 +436,33 @@ def test_csc_multistep_colocated_vs_reference_golden(gf, golden, oracle, G):
                 ptrs, offs, cnts = G.table(G.pool_tensors(fd, sizes, off))
                 gf.call("gf_csc_pack_correct", dt, pools[r].data_ptr(), hgs[r].data_ptr(),
                         stages[r].data_ptr(), imp.data_ptr(), coff.data_ptr(), total, chunk, nc,
-                        ptrs, offs, cnts, len(sizes), np.float32(0.9), None)
+                        ptrs, offs, cnts, len(sizes), np.float32(0.9),
+                        naccs[r].data_ptr() if fused_norms else None, None)
                 G.sync()
             gf.call("gf_ring_allreduce_colocated_planned", dt, gf.ptr_array(stages), n, None,
                     plan.data_ptr(), None)
             for r in range(n):
                 gf.call("gf_csc_scatter", dt, pools[r].data_ptr(), stages[r].data_ptr(),
-                        plan.data_ptr(), coff.data_ptr(), total, chunk, nc, nc, None)
-                gf.call("gf_chunk_norms", dt, pools[r].data_ptr(), total, chunk, nc,
-                        imp.data_ptr(), n, norms[r].data_ptr(), None)
+                        plan.data_ptr(), coff.data_ptr(), total, chunk, nc, nc,
+                        naccs[r].data_ptr() if fused_norms else None, None)
+                if not fused_norms:
+                    gf.call("gf_chunk_norms", dt, pools[r].data_ptr(), total, chunk, nc,
+                            imp.data_ptr(), n, norms[r].data_ptr(), None)
             k = oracle.selection_count(oracle.sparsity_at(t + 1, 2, 0.75), nc)
             nxt = G.zeros(nc, np.uint8)
+            nxt_plan = G.zeros(4 + nc, np.uint64)
+            nxt_coff = G.zeros(nc, np.uint64)
             gf.call("gf_csc_select_colocated", gf.ptr_array(norms), n, None, nc, k,
-                    nxt.data_ptr(), total, chunk, dt, theta, coff.data_ptr(), plan.data_ptr(), None)
+                    nxt.data_ptr(), total, chunk, dt, theta, nxt_coff.data_ptr(), nxt_plan.data_ptr(),
+                    gf.ptr_array(naccs) if fused_norms else None,
+                    gf.ptr_array(pools) if fused_norms else None,
+                    imp.data_ptr() if fused_norms else None, None)
             G.sync()
             for r in range(n):
                 assert (G.bits(G.host(hgs[r])) == G.bits(g[p + "hg"][t][r])).all(), (ci, t, r)
                 assert (G.bits(G.host(pools[r], et)) == G.bits(g[p + "pool_x"][t][r])).all(), (ci, t, r)
                 assert (G.bits(G.host(norms[r])) == G.bits(g[p + "norms_sum"][t][r])).all(), (ci, t, r)
+                if fused_norms:
+                    assert not G.host(naccs[r], np.uint64).any()  # re-armed for the next step
             assert (G.host(nxt) == g[p + "next_imp"][t][0]).all(), (ci, t)
-            imp = nxt
+            imp, coff, plan = nxt, nxt_coff, nxt_plan

@@ -125,7 +125,7 @@ def _worker_csc(rank, world, port):
     plan = torch.zeros(4 + nc, dtype=torch.int64, device="cuda")
     total = nc * 32000 + 12840
     capi.call("gf_csc_select", comm, noff, nc, k, flags.data_ptr(), total, 32000, F16,
-              capi.THETA_INF, coff.data_ptr(), plan.data_ptr(), None)
+              capi.THETA_INF, coff.data_ptr(), plan.data_ptr(), None, None, None, None)
     torch.cuda.synchronize()
     want_sum = o.ring_allreduce([x.copy() for x in norms], dtype=F32)
     got_sum = _get(cudart, base, noff, norms[rank])
