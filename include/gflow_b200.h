@@ -168,6 +168,17 @@ int gf_comm_world(gf_comm* comm);
  * ring_allreduce). One kernel launch per <= GF_MAX_WINDOWS_PER_LAUNCH windows. */
 int gf_ring_allreduce(gf_comm* comm, int dtype, uint64_t heap_off, const uint64_t* win_start,
                       const uint64_t* win_len, int nwin, void* stream);
+/* Same over explicit per-rank buffers (rank_bufs[r] = rank r's buffer as mapped on THIS
+ * rank's GPU, 16-byte aligned; windows relative to each buffer start). Used for
+ * registered user buffers (e.g. a GradientPool) instead of the symmetric heap. */
+int gf_ring_allreduce_ptrs(gf_comm* comm, int dtype, void* const* rank_bufs,
+                           const uint64_t* win_start, const uint64_t* win_len, int nwin,
+                           void* stream);
+/* Buffer registration across processes: export the IPC handle of the allocation holding
+ * dev_ptr (+ its offset), open a peer's handle (mapped base on this rank's GPU), close. */
+int gf_ipc_export(const void* dev_ptr, void* handle_out, uint64_t* offset_out);
+int gf_ipc_open(gf_comm* comm, const void* handle, void** base_out);
+int gf_ipc_close(gf_comm* comm, void* base);
 /* Same with windows described by a device plan written by gf_csc_plan / gf_csc_select. */
 int gf_ring_allreduce_planned(gf_comm* comm, int dtype, uint64_t heap_off,
                               const uint64_t* plan_dev, void* stream);
@@ -193,6 +204,13 @@ int gf_csc_select_colocated(float* const* norms, int world, const int* ring_orde
                             uint64_t chunk, int dtype, uint64_t theta, uint64_t* coff,
                             uint64_t* plan, uint64_t* const* nacc, const void* const* pools,
                             const uint8_t* imp_cur, void* stream);
+
+/* Rooted helpers over peer-addressable per-rank buffers, launched by ONE rank after the
+ * others signalled readiness over the control plane (host-orchestrated collectives):
+ * oracle_allreduce (collectives.cpp:203-226): every buffer = ((b0 + b1) + ...) + b[N-1];
+ * broadcast: every buffer = bufs[root]. */
+int gf_oracle_allreduce_ptrs(int dtype, void* const* bufs, int world, uint64_t len, void* stream);
+int gf_broadcast_ptrs(void* const* bufs, int world, int root, uint64_t bytes, void* stream);
 
 /* Payload bytes the reference ring records for one allreduce of len elements at ring
  * position `position` (collectives.cpp:69-96): 2(N-1) sends of segment_of sizes. */

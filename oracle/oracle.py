@@ -384,6 +384,25 @@ class Reference:
         self.L.refd_gen_grads(r, t, np_ptr(s), len(s), np_ptr(out))
         return out
 
+    def train(self, ranks=2, model_dims=(64, 32, 1), task="linear", iterations=50, n_examples=1024,
+              batch=16, learning_rate=0.01, momentum=0.9, seed=1, algo=0, precision="fp32",
+              theta_bytes=64 << 20, csc=False, final_sparsity=0.0, warmup_iters=0, chunk_size=1000):
+        d = u64(model_dims)
+        nparams = sum(model_dims[i] * model_dims[i - 1] + model_dims[i] for i in range(1, len(model_dims)))
+        losses = np.zeros(iterations, np.float64)
+        gb = np.zeros(iterations, np.uint64)
+        w = np.zeros(nparams, np.float32)
+        npo = np.zeros(1, np.uint64)
+        self.L.refd_train.restype = C.c_int
+        self._check(self.L.refd_train(
+            C.c_int(ranks), np_ptr(d), C.c_int(len(d)), C.c_int(task == "logistic"),
+            C.c_uint64(iterations), C.c_uint64(n_examples), C.c_uint64(batch), C.c_double(learning_rate),
+            C.c_double(momentum), C.c_uint64(seed), C.c_int(algo), C.c_int(precision == "fp16"),
+            C.c_uint64(theta_bytes), C.c_int(int(csc)), C.c_double(final_sparsity),
+            C.c_uint64(warmup_iters), C.c_uint64(chunk_size), np_ptr(losses), np_ptr(gb), np_ptr(w),
+            C.c_uint64(nparams), np_ptr(npo)))
+        return dict(loss=losses, grad_payload_bytes=gb, final_weights=w)
+
     def time_step(self, n, sizes, chunk=32000, dtype=1, theta=64 << 20, csc=False,
                   final_sparsity=0.9, steps=3, warmup=1):
         s = u64(sizes)

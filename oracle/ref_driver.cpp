@@ -29,6 +29,7 @@
 #include "gflow/harness.hpp"
 #include "gflow/inproc.hpp"
 #include "gflow/sparse.hpp"
+#include "gflow/trainer.hpp"
 
 using namespace gflow;
 
@@ -301,6 +302,43 @@ int refd_bench_allreduce(int ranks, std::uint64_t bytes, int algo, int group_siz
         *sent = r.per_rank_payload_sent;
         *predicted = r.predicted_payload;
         *matches = r.matches_oracle ? 1 : 0;
+    });
+}
+
+// ---- whole training runs (trainer.cpp:264-382), ranks as threads -------------------
+// dims: model_dims (nd entries). Outputs (rank 0): losses[iterations], grad_bytes[iterations],
+// weights[n_params] (final); returns the parameter count in *n_params.
+int refd_train(int ranks, const std::uint64_t* dims, int nd, int logistic, std::uint64_t iterations,
+               std::uint64_t n_examples, std::uint64_t batch, double lr, double momentum, std::uint64_t seed,
+               int algo, int dtype, std::uint64_t theta, int csc, double final_sparsity, std::uint64_t warmup,
+               std::uint64_t chunk, double* losses, std::uint64_t* grad_bytes, float* weights,
+               std::uint64_t cap, std::uint64_t* n_params) {
+    return guarded([&] {
+        TrainOptions o;
+        o.model_dims.assign(dims, dims + nd);
+        o.task = logistic ? Task::kLogistic : Task::kLinearRegression;
+        o.iterations = iterations;
+        o.n_examples = n_examples;
+        o.batch = batch;
+        o.learning_rate = lr;
+        o.momentum = momentum;
+        o.seed = seed;
+        o.algorithm = algo_of(algo);
+        o.wire_precision = dtype == 1 ? ElementType::kF16 : ElementType::kF32;
+        o.theta_bytes = theta;
+        o.csc = csc != 0;
+        o.final_sparsity = final_sparsity;
+        o.warmup_iters = warmup;
+        o.chunk_size = chunk;
+        std::vector<TrainResult> res(static_cast<std::size_t>(ranks));
+        run_world(ranks, [&](int r, Transport& tp) { res[static_cast<std::size_t>(r)] = train_worker(o, tp); });
+        const auto& r0 = res[0];
+        for (std::size_t t = 0; t < r0.metrics.size(); ++t) {
+            losses[t] = r0.metrics[t].loss;
+            grad_bytes[t] = r0.metrics[t].grad_payload_bytes;
+        }
+        *n_params = r0.final_weights.size();
+        for (std::size_t i = 0; i < r0.final_weights.size() && i < cap; ++i) weights[i] = r0.final_weights[i];
     });
 }
 

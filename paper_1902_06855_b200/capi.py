@@ -88,12 +88,18 @@ SIGNATURES = {
     "gf_comm_world": [_vp],
     "gf_ring_allreduce": [_vp, _i, _u64, _vp, _vp, _i, _vp],
     "gf_ring_allreduce_planned": [_vp, _i, _u64, _vp, _vp],
+    "gf_ring_allreduce_ptrs": [_vp, _i, _vp, _vp, _vp, _i, _vp],
+    "gf_ipc_export": [_vp, _vp, _u64p],
+    "gf_ipc_open": [_vp, _vp, C.POINTER(_vp)],
+    "gf_ipc_close": [_vp, _vp],
     "gf_ring_allreduce_colocated": [_i, _vp, _i, _vp, _vp, _vp, _i, _vp],
     "gf_ring_allreduce_colocated_planned": [_i, _vp, _i, _vp, _vp, _vp],
     "gf_csc_select": [_vp, _u64, _u64, _u64, _vp, _u64, _u64, _i, _u64, _vp, _vp, _vp, _vp, _vp, _vp],
     "gf_csc_select_colocated": [_vp, _i, _vp, _u64, _u64, _vp, _u64, _u64, _i, _u64, _vp, _vp, _vp,
                                 _vp, _vp, _vp],
     "gf_ring_traffic": [_u64, _i, _i, _i, _u64p, _u64p, _u64p],
+    "gf_oracle_allreduce_ptrs": [_i, _vp, _i, _u64, _vp],
+    "gf_broadcast_ptrs": [_vp, _i, _i, _u64, _vp],
     "gf_abi_version": [],
     "gf_last_error": [],
     "gf_kernel_launches": [],

@@ -1,0 +1,461 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// gflowpy — Python bindings of the B200 gradient-sync path. The module-level functions
+// keep the reference's gflowpy names, keyword arguments and defaults
+// (reference: bindings/module.cpp:158-199; ConfigError -> ValueError); the classes expose
+// the C++ API (GradientPool, FusionEngine, SparseState, Communicator, collectives) so that
+// parity tests can drive it the way the reference's C++ tests do, ranks as threads.
+#include <pybind11/functional.h>
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <thread>
+
+#include "gflow/collectives.hpp"
+#include "gflow/fusion.hpp"
+#include "gflow/gradient_pool.hpp"
+#include "gflow/half.hpp"
+#include "gflow/inproc.hpp"
+#include "gflow/sparse.hpp"
+#include "gflow/trainer.hpp"
+
+namespace py = pybind11;
+using namespace gflow;
+
+namespace {
+
+using release = py::call_guard<py::gil_scoped_release>;
+
+Algo algo_from_name(const std::string& name) {
+    if (name == "ring") return Algo::kRing;
+    if (name == "hierarchical") return Algo::kHierarchical;
+    if (name == "oracle") return Algo::kOracle;
+    throw ConfigError("unknown algorithm: " + name);
+}
+
+ElementType precision_from_name(const std::string& name) {
+    if (name == "fp32") return ElementType::kF32;
+    if (name == "fp16") return ElementType::kF16;
+    throw ConfigError("unknown precision: " + name);
+}
+
+// Layout only (no device allocation): gradient_pool.cpp:11-41 semantics.
+py::dict pool_info(const std::vector<std::size_t>& sizes, std::size_t chunk_size) {
+    if (sizes.empty()) throw ConfigError("gradient pool needs at least one tensor");
+    if (chunk_size == 0) throw ConfigError("chunk_size must be positive");
+    std::size_t total = 0;
+    for (auto s : sizes) {
+        if (s == 0) throw ConfigError("tensor sizes must be positive");
+        total += s;
+    }
+    const std::size_t nc = std::max<std::size_t>(
+        1, static_cast<std::size_t>(std::llround(static_cast<double>(total) / static_cast<double>(chunk_size))));
+    py::dict offsets;
+    std::size_t off = 0;
+    for (int id = static_cast<int>(sizes.size()); id >= 1; --id) {
+        offsets[py::int_(id)] = off;
+        off += sizes[static_cast<std::size_t>(id - 1)];
+    }
+    std::vector<std::size_t> lens(nc, chunk_size);
+    lens.back() = total - (nc - 1) * chunk_size;
+    py::dict out;
+    out["total_elements"] = total;
+    out["num_chunks"] = nc;
+    out["tensor_offsets"] = offsets;
+    out["chunk_lengths"] = lens;
+    return out;
+}
+
+// harness.cpp:132-159 (analytic payload; dense 2(N-1)/N * pool bytes, CSC over the k
+// selected chunks plus the fp32 norm vector; the reference uses ceil for the chunk count here)
+py::dict predict_traffic(std::uint64_t pool_elements, std::size_t element_bytes, int ranks, double sparsity,
+                         std::size_t chunk_size, bool csc) {
+    const double n = ranks, factor = ranks > 1 ? 2.0 * (n - 1.0) / n : 0.0;
+    const double pool_bytes = static_cast<double>(pool_elements) * static_cast<double>(element_bytes);
+    double grad = factor * pool_bytes, norm = 0.0;
+    if (csc) {
+        const std::size_t nc = (pool_elements + chunk_size - 1) / chunk_size;
+        const std::size_t k = selection_count(sparsity, nc);
+        grad = factor * std::min(pool_bytes, static_cast<double>(k) * chunk_size * element_bytes);
+        norm = factor * static_cast<double>(nc) * 4.0;
+    }
+    py::dict out;
+    out["grad_bytes"] = grad;
+    out["norm_bytes"] = norm;
+    out["total_bytes"] = grad + norm;
+    return out;
+}
+
+int device_count() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// Rank r's GPU when ranks are threads: its own GPU if there are enough, else all share GPU 0.
+int rank_device(int rank, int ranks) {
+    const int n = device_count();
+    return n >= ranks ? rank : 0;
+}
+
+template <typename F>
+void run_ranks(int ranks, F body) {
+    auto world = make_inproc_world(ranks);
+    std::vector<std::thread> ts;
+    std::vector<std::exception_ptr> errors(static_cast<std::size_t>(ranks));
+    for (int r = 0; r < ranks; ++r) {
+        ts.emplace_back([&, r] {
+            try {
+                cudaSetDevice(rank_device(r, ranks));
+                body(r, *world[static_cast<std::size_t>(r)]);
+            } catch (...) {
+                errors[static_cast<std::size_t>(r)] = std::current_exception();
+            }
+        });
+    }
+    for (auto& t : ts) t.join();
+    for (auto& e : errors)
+        if (e) std::rethrow_exception(e);
+}
+
+// harness.cpp:245-339 semantics, ranks as threads, the allreduce on the GPU.
+py::dict bench_allreduce(int ranks, std::uint64_t bytes, const std::string& algo, int group_size,
+                         const std::string& precision) {
+    const Algo a = algo_from_name(algo);
+    const ElementType et = precision_from_name(precision);
+    if (ranks < 1) throw ConfigError("ranks must be >= 1");
+    const std::size_t esz = element_size(et), n = bytes / esz;
+    if (n == 0) throw ConfigError("buffer too small for element type");
+    if (a == Algo::kHierarchical && (group_size < 1 || ranks % group_size != 0))
+        throw ConfigError("group size " + std::to_string(group_size) + " must divide world " + std::to_string(ranks));
+    std::uint64_t sent0 = 0, phase2 = 0;
+    std::vector<std::vector<float>> got(static_cast<std::size_t>(ranks)), want(static_cast<std::size_t>(ranks));
+    {
+        py::gil_scoped_release nogil;
+        run_ranks(ranks, [&](int r, Transport& tp) {
+            Communicator comm(tp, group_size);
+            std::mt19937_64 rng(1234 + static_cast<std::uint64_t>(r));
+            std::uniform_real_distribution<float> uni(-1.0f, 1.0f);
+            std::vector<float> v(n);
+            for (auto& x : v) x = uni(rng);
+            auto buf = OwnedBuffer::from_floats(et, v);
+            auto ref = OwnedBuffer::from_floats(et, v);
+            switch (a) {
+                case Algo::kRing: ring_allreduce(comm, buf.view()); break;
+                case Algo::kHierarchical: hierarchical_allreduce(comm, buf.view()); break;
+                case Algo::kOracle: oracle_allreduce(comm, buf.view()); break;
+            }
+            oracle_allreduce(comm, ref.view());
+            got[static_cast<std::size_t>(r)] = buf.to_floats();
+            want[static_cast<std::size_t>(r)] = ref.to_floats();
+            if (r == 0) {
+                for (const auto& [label, c] : tp.stats().snapshot())
+                    if (label != "oracle") sent0 += c.payload_bytes_sent;
+                const auto segs = comm.phase2_segment_bytes();
+                phase2 = segs.empty() ? 0 : segs.front();
+            }
+        });
+    }
+    std::uint64_t predicted = 0;
+    if (a == Algo::kRing && ranks > 1) {
+        for (int s = 0; s < ranks - 1; ++s) {
+            predicted += (detail::segment_of(n, ranks, (ranks - s) % ranks).length +
+                          detail::segment_of(n, ranks, (1 - s + ranks) % ranks).length) * esz;
+        }
+    }
+    double max_rel = 0.0;
+    for (int r = 0; r < ranks; ++r)
+        for (std::size_t i = 0; i < n; ++i) {
+            const double w = want[static_cast<std::size_t>(r)][i], g = got[static_cast<std::size_t>(r)][i];
+            max_rel = std::max(max_rel, std::fabs(g - w) / std::max(1.0, std::fabs(w)));
+        }
+    py::dict out;
+    out["per_rank_payload_sent"] = sent0;
+    out["predicted_payload"] = predicted;
+    out["phase2_segment_bytes"] = phase2;
+    out["matches_oracle"] = max_rel <= (et == ElementType::kF32 ? 1e-6 : 1e-2);
+    return out;
+}
+
+py::dict train(int ranks, const std::vector<std::size_t>& model_dims, const std::string& task,
+               std::uint64_t iterations, std::size_t n_examples, std::size_t batch, double learning_rate,
+               double momentum, std::uint64_t seed, const std::string& algo, int group_size,
+               const std::string& precision, std::uint64_t theta_bytes, bool csc, double final_sparsity,
+               std::uint64_t warmup_iters, std::size_t chunk_size) {
+    TrainOptions o;
+    o.model_dims = model_dims;
+    o.task = task == "logistic" ? Task::kLogistic : Task::kLinearRegression;
+    o.iterations = iterations;
+    o.n_examples = n_examples;
+    o.batch = batch;
+    o.learning_rate = learning_rate;
+    o.momentum = momentum;
+    o.seed = seed;
+    o.algorithm = algo_from_name(algo);
+    o.group_size = group_size;
+    o.wire_precision = precision_from_name(precision);
+    o.theta_bytes = theta_bytes;
+    o.csc = csc;
+    o.final_sparsity = final_sparsity;
+    o.warmup_iters = warmup_iters;
+    o.chunk_size = chunk_size;
+    std::vector<TrainResult> res(static_cast<std::size_t>(ranks));
+    {
+        py::gil_scoped_release nogil;
+        run_ranks(ranks, [&](int r, Transport& tp) { res[static_cast<std::size_t>(r)] = train_worker(o, tp); });
+    }
+    const auto& r0 = res[0];
+    std::vector<double> losses, sparsity;
+    std::vector<std::uint64_t> gb;
+    for (const auto& m : r0.metrics) {
+        losses.push_back(m.loss);
+        gb.push_back(m.grad_payload_bytes);
+        sparsity.push_back(m.sparsity);
+    }
+    py::dict out;
+    out["final_loss"] = r0.final_loss;
+    out["final_weights"] = r0.final_weights;
+    out["loss"] = losses;
+    out["grad_payload_bytes"] = gb;
+    out["sparsity"] = sparsity;
+    return out;
+}
+
+// ---- array helpers for the class API ------------------------------------------------------
+struct Span {
+    float* ptr;
+    std::size_t n;
+};
+// numpy float32 array (host) or any object with data_ptr()/numel() (torch CUDA tensor)
+Span as_float_span(py::object o) {
+    if (py::hasattr(o, "data_ptr") && py::hasattr(o, "numel")) {
+        return {reinterpret_cast<float*>(o.attr("data_ptr")().cast<std::uintptr_t>()),
+                o.attr("numel")().cast<std::size_t>()};
+    }
+    auto a = o.cast<py::array_t<float, py::array::c_style>>();
+    return {a.mutable_data(), static_cast<std::size_t>(a.size())};
+}
+
+ScalarBuffer as_buffer(py::array a) {
+    if (!(a.flags() & py::array::c_style)) throw ConfigError("buffer must be C-contiguous");
+    if (a.dtype().is(py::dtype::of<float>()))
+        return {ElementType::kF32, static_cast<std::byte*>(a.mutable_data()), static_cast<std::size_t>(a.size())};
+    if (a.dtype().is(py::dtype::of<std::uint16_t>()))
+        return {ElementType::kF16, static_cast<std::byte*>(a.mutable_data()), static_cast<std::size_t>(a.size())};
+    throw ConfigError("buffer must be float32 (fp32) or uint16 (fp16 bits)");
+}
+
+py::dict stats_dict(const TrafficStats& s) {
+    py::dict out;
+    for (const auto& [label, c] : s.snapshot()) {
+        py::dict d;
+        d["payload_bytes_sent"] = c.payload_bytes_sent;
+        d["payload_bytes_received"] = c.payload_bytes_received;
+        d["frames_sent"] = c.frames_sent;
+        out[py::str(label)] = d;
+    }
+    return out;
+}
+
+// futures of the fusion engine, opaque to Python
+struct Handles {
+    std::vector<FusedHandle> h;
+    Handles() = default;
+    explicit Handles(std::vector<FusedHandle> v) : h(std::move(v)) {}
+    Handles(const Handles&) = delete;
+    Handles& operator=(const Handles&) = delete;
+    Handles(Handles&&) = default;
+    Handles& operator=(Handles&&) = default;
+};
+
+}  // namespace
+
+PYBIND11_MODULE(gflowpy, m) {
+    m.doc() = "GradientFlow gradient synchronisation on B200 (sm_100a kernels, NVLink peer memory)";
+
+    auto config_error = py::register_exception<ConfigError>(m, "ConfigError", PyExc_ValueError);
+    py::register_exception<ProtocolError>(m, "ProtocolError", PyExc_RuntimeError);
+    py::register_exception<TransportError>(m, "TransportError", PyExc_RuntimeError);
+    py::register_exception<TrainingError>(m, "TrainingError", PyExc_RuntimeError);
+    (void)config_error;
+
+    // ---- the reference's module functions (bindings/module.cpp:158-199) --------------
+    m.def("float_to_half_bits", &float_to_half_bits, py::arg("value"));
+    m.def("half_bits_to_float", &half_bits_to_float, py::arg("bits"));
+    m.def("encode_half", [](const std::vector<float>& v) {
+        const auto b = encode_half(v);
+        return py::bytes(reinterpret_cast<const char*>(b.data()), b.size());
+    }, py::arg("values"));
+    m.def("decode_half", [](const py::bytes& raw) {
+        std::string s = raw;
+        return decode_half(std::span<const std::byte>(reinterpret_cast<const std::byte*>(s.data()), s.size()));
+    }, py::arg("data"));
+    m.def("pool_info", &pool_info, py::arg("tensor_sizes"), py::arg("chunk_size") = 32000);
+    m.def("sparsity_at", &sparsity_at, py::arg("iteration"), py::arg("warmup_iters"), py::arg("final_sparsity"));
+    m.def("selection_count", &selection_count, py::arg("sparsity"), py::arg("num_chunks"));
+    m.def("predict_traffic", &predict_traffic, py::arg("pool_elements"), py::arg("element_bytes"),
+          py::arg("ranks"), py::arg("sparsity") = 0.0, py::arg("chunk_size") = 32000, py::arg("csc") = false);
+    m.def("bench_allreduce", &bench_allreduce, py::arg("ranks"), py::arg("bytes"), py::arg("algo") = "ring",
+          py::arg("group_size") = 1, py::arg("precision") = "fp32");
+    m.def("train", &train, py::arg("ranks") = 2, py::arg("model_dims") = std::vector<std::size_t>{64, 32, 1},
+          py::arg("task") = "linear", py::arg("iterations") = 50, py::arg("n_examples") = 1024,
+          py::arg("batch") = 16, py::arg("learning_rate") = 0.01, py::arg("momentum") = 0.9,
+          py::arg("seed") = 1, py::arg("algo") = "ring", py::arg("group_size") = 1,
+          py::arg("precision") = "fp32", py::arg("theta_bytes") = 64ull << 20, py::arg("csc") = false,
+          py::arg("final_sparsity") = 0.0, py::arg("warmup_iters") = 0, py::arg("chunk_size") = 1000);
+
+    // ---- the C++ API ----------------------------------------------------------------
+    py::enum_<ElementType>(m, "ElementType").value("kF32", ElementType::kF32).value("kF16", ElementType::kF16);
+    py::enum_<Algo>(m, "Algo").value("kRing", Algo::kRing).value("kHierarchical", Algo::kHierarchical)
+        .value("kOracle", Algo::kOracle);
+    m.attr("THETA_INFINITE") = py::int_(kThetaInfinite);
+    m.def("device_count", &device_count);
+    m.def("set_device", [](int d) {
+        if (cudaSetDevice(d) != cudaSuccess) throw ConfigError("cudaSetDevice(" + std::to_string(d) + ") failed");
+    });
+
+    py::class_<Transport, std::shared_ptr<Transport>>(m, "Transport")
+        .def_property_readonly("rank", &Transport::rank)
+        .def_property_readonly("world_size", &Transport::world_size)
+        .def("barrier", &Transport::barrier, release())
+        .def("stats", [](Transport& t) { return stats_dict(t.stats()); })
+        .def("total_payload_sent", [](Transport& t) { return t.stats().total().payload_bytes_sent; })
+        .def("set_timeout_ms", [](Transport& t, int ms) { t.set_timeout(std::chrono::milliseconds(ms)); });
+    m.def("make_inproc_world", [](int n) {
+        std::vector<std::shared_ptr<Transport>> out;
+        for (auto& t : make_inproc_world(n)) out.emplace_back(t.release());
+        return out;
+    }, py::arg("world_size"));
+
+    py::class_<Communicator>(m, "Communicator")
+        .def(py::init<Transport&, int>(), py::arg("transport"), py::arg("group_size") = 1, py::keep_alive<1, 2>())
+        .def_property_readonly("rank", &Communicator::rank)
+        .def_property_readonly("world_size", &Communicator::world_size)
+        .def_property_readonly("ring_order", &Communicator::ring_order)
+        .def("set_ring_order", &Communicator::set_ring_order)
+        .def("set_device", &Communicator::set_device)
+        .def("device_mode", [](Communicator& c) { return std::string(c.device().mode_name()); }, release())
+        .def("device", [](Communicator& c) { return c.device().device(); }, release());
+
+    m.def("ring_allreduce", [](Communicator& c, py::array a) {
+        ScalarBuffer b = as_buffer(a);
+        py::gil_scoped_release nogil;
+        ring_allreduce(c, b);
+    }, py::arg("comm"), py::arg("buf"));
+    m.def("oracle_allreduce", [](Communicator& c, py::array a) {
+        ScalarBuffer b = as_buffer(a);
+        py::gil_scoped_release nogil;
+        oracle_allreduce(c, b);
+    }, py::arg("comm"), py::arg("buf"));
+    m.def("broadcast", [](Communicator& c, py::array a, int root) {
+        ScalarBuffer b = as_buffer(a);
+        py::gil_scoped_release nogil;
+        broadcast(c, b, root);
+    }, py::arg("comm"), py::arg("buf"), py::arg("root"));
+    m.def("hierarchical_allreduce", [](Communicator& c, py::array a) {
+        ScalarBuffer b = as_buffer(a);
+        py::gil_scoped_release nogil;
+        hierarchical_allreduce(c, b);
+    }, py::arg("comm"), py::arg("buf"));
+    m.def("segment_of", [](std::size_t len, int n, int i) {
+        auto s = detail::segment_of(len, n, i);
+        return py::make_tuple(s.offset, s.length);
+    });
+
+    py::class_<GradientPool>(m, "GradientPool")
+        .def(py::init<const std::vector<std::size_t>&, std::size_t, ElementType>(), py::arg("tensor_sizes"),
+             py::arg("chunk_size") = kDefaultChunkSize, py::arg("element_type") = ElementType::kF32)
+        .def_property_readonly("total_elements", &GradientPool::total_elements)
+        .def_property_readonly("chunk_size", &GradientPool::chunk_size)
+        .def_property_readonly("num_chunks", &GradientPool::num_chunks)
+        .def_property_readonly("num_tensors", &GradientPool::num_tensors)
+        .def_property_readonly("device", &GradientPool::device)
+        .def("desc", [](const GradientPool& p, int id) {
+            const auto& d = p.desc(id);
+            return py::make_tuple(d.tensor_id, d.element_count, d.pool_offset);
+        })
+        .def("chunk_begin", &GradientPool::chunk_begin)
+        .def("chunk_length", &GradientPool::chunk_length)
+        .def("begin_iteration", &GradientPool::begin_iteration)
+        .def("write_tensor", [](GradientPool& p, int id, py::object values) {
+            Span s = as_float_span(values);
+            py::gil_scoped_release nogil;
+            return p.write_tensor(id, std::span<const float>(s.ptr, s.n));
+        })
+        .def_property_readonly("written_elements", &GradientPool::written_elements)
+        .def("iteration_complete", &GradientPool::iteration_complete)
+        .def("get", &GradientPool::get)
+        .def("set", &GradientPool::set)
+        .def("chunk_l1", &GradientPool::chunk_l1, release())
+        .def("device_ptr", [](GradientPool& p) { return reinterpret_cast<std::uintptr_t>(p.device_data()); })
+        .def("to_numpy", [](GradientPool& p) {
+            const std::size_t n = p.total_elements();
+            if (p.element_type() == ElementType::kF16) {
+                py::array_t<std::uint16_t> a(n);
+                p.invalidate_host();
+                if (cudaMemcpy(a.mutable_data(), p.device_data(), n * 2, cudaMemcpyDeviceToHost) != cudaSuccess)
+                    throw TransportError("pool D2H");
+                return py::array(a);
+            }
+            py::array_t<float> a(n);
+            if (cudaMemcpy(a.mutable_data(), p.device_data(), n * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+                throw TransportError("pool D2H");
+            return py::array(a);
+        });
+
+    py::class_<Handles>(m, "FusedHandles")
+        .def("__len__", [](const Handles& h) { return h.h.size(); })
+        .def("extend", [](Handles& a, Handles& b) {
+            for (auto& x : b.h) a.h.push_back(std::move(x));
+            b.h.clear();
+        })
+        .def("wait_all", [](Handles& h) { FusionEngine::wait_all(h.h); }, release());
+    py::class_<FusionEngine>(m, "FusionEngine")
+        .def(py::init([](GradientPool& p, Communicator& c, std::uint64_t theta, Algo a) {
+                 return new FusionEngine(p, c, FusionConfig{theta, a});
+             }),
+             py::arg("pool"), py::arg("comm"), py::arg("threshold_bytes") = 64ull << 20,
+             py::arg("algorithm") = Algo::kRing, py::keep_alive<1, 2>(), py::keep_alive<1, 3>())
+        .def("begin_iteration", &FusionEngine::begin_iteration)
+        .def("on_tensor_complete", [](FusionEngine& e, int id) { return Handles{e.on_tensor_complete(id)}; })
+        .def("finalize_iteration", [](FusionEngine& e) {
+            Handles h;
+            if (auto f = e.finalize_iteration()) h.h.push_back(std::move(*f));
+            return h;
+        })
+        .def("window_bytes", [](const FusionEngine& e) { return e.last_log().window_bytes; })
+        .def("log_csv_line", &FusionEngine::log_csv_line);
+
+    py::class_<SparseState>(m, "SparseState")
+        .def(py::init([](GradientPool& p, double mom, double lr, double s, std::uint64_t w) {
+                 return new SparseState(p, SparseConfig{mom, lr, s, w});
+             }),
+             py::arg("pool"), py::arg("momentum") = 0.9, py::arg("learning_rate") = 0.01,
+             py::arg("final_sparsity") = 0.0, py::arg("warmup_iters") = 0, py::keep_alive<1, 2>())
+        .def("begin_iteration", &SparseState::begin_iteration)
+        .def("correction_pre_allreduce", &SparseState::correction_pre_allreduce)
+        .def("sparse_exchange", &SparseState::sparse_exchange, release())
+        .def("select_next_important", &SparseState::select_next_important, release())
+        .def("sgd_update", [](SparseState& s, py::object w, int world) {
+            Span sp = as_float_span(w);
+            py::gil_scoped_release nogil;
+            s.sgd_update(std::span<float>(sp.ptr, sp.n), world);
+        })
+        .def_property_readonly("important", &SparseState::important)
+        .def("hg", [](const SparseState& s) { auto v = s.hg(); return std::vector<float>(v.begin(), v.end()); })
+        .def("hu", [](const SparseState& s) { auto v = s.hu(); return std::vector<float>(v.begin(), v.end()); })
+        .def("selected_chunks", &SparseState::selected_chunks)
+        .def("selected_payload_bytes", &SparseState::selected_payload_bytes)
+        .def_property_readonly("current_sparsity", &SparseState::current_sparsity)
+        .def_property_readonly("last_exchange_windows", &SparseState::last_exchange_windows)
+        .def("checksum", &SparseState::checksum);
+}

@@ -54,7 +54,7 @@ norms_f16_kernel(const uint16_t* __restrict__ pool, uint64_t total, uint64_t chu
         uint64_t acc = 0;
         bool nan = false;
         uint64_t done = 0;
-        if ((b % 8) == 0) {
+        if ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) {
             const uint64_t nvec = len / 8;
             constexpr int U = 4;
             for (uint64_t v0 = threadIdx.x; v0 < nvec; v0 += uint64_t(kNormThreads) * U) {
@@ -214,7 +214,9 @@ pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ po
         const uint64_t po = T.off[t] + base;
         uint64_t done = 0;
         if (DT == GF_F16 && (reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0 && po % 8 == 0 &&
-            chunk % 8 == 0 && (reinterpret_cast<uintptr_t>(hg) & 31u) == 0) {
+            chunk % 8 == 0 && (reinterpret_cast<uintptr_t>(hg) & 31u) == 0 &&
+            (reinterpret_cast<uintptr_t>(pool) & 15u) == 0 &&
+            (reinterpret_cast<uintptr_t>(staging) & 15u) == 0) {
             // 8 consecutive pool elements never straddle a chunk boundary here.
             uint16_t* __restrict__ d = static_cast<uint16_t*>(pool) + po;
             uint16_t* __restrict__ stg = static_cast<uint16_t*>(staging);
@@ -368,7 +370,8 @@ csc_sgd_kernel(const void* __restrict__ pool, const uint64_t* __restrict__ plan,
         const uint64_t b = c * chunk;
         const uint64_t len = (c + 1 == nc) ? total - b : chunk;
         uint64_t done = 0;
-        if (DT == GF_F16 && b % 8 == 0 && (reinterpret_cast<uintptr_t>(hu) & 31u) == 0 &&
+        if (DT == GF_F16 && b % 8 == 0 && (reinterpret_cast<uintptr_t>(pool) & 15u) == 0 &&
+            (reinterpret_cast<uintptr_t>(hu) & 31u) == 0 &&
             (reinterpret_cast<uintptr_t>(w) & 31u) == 0) {
             const uint64_t nv = len / 8;
             const uint16_t* p = static_cast<const uint16_t*>(pool) + b;

@@ -37,7 +37,8 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ 
         const uint64_t len = min(kTile, T.cnt[t] - base);
         const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
         const uint64_t po = T.off[t] + base;
-        const bool fast = ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0) && (po % 8 == 0);
+        const bool fast = ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0) && (po % 8 == 0) &&
+                          ((reinterpret_cast<uintptr_t>(pool) & 15u) == 0);
         if (DT == GF_F16) {
             uint16_t* __restrict__ d = static_cast<uint16_t*>(pool) + po;
             uint64_t done = 0;
@@ -104,7 +105,8 @@ __global__ void __launch_bounds__(kThreads) unpack_kernel(const __grid_constant_
         const uint64_t len = min(kTile, T.cnt[t] - base);
         float* __restrict__ d = static_cast<float*>(const_cast<void*>(T.ptr[t])) + base;
         const uint64_t po = T.off[t] + base;
-        const bool fast = ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0) && (po % 8 == 0);
+        const bool fast = ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0) && (po % 8 == 0) &&
+                          ((reinterpret_cast<uintptr_t>(pool) & 15u) == 0);
         uint64_t done = 0;
         if (DT == GF_F16) {
             const uint16_t* __restrict__ s = static_cast<const uint16_t*>(pool) + po;
@@ -307,6 +309,70 @@ int gf_dense_sgd_update(int dtype, const void* pool, uint64_t total, int world, 
         dense_sgd_kernel<GF_F32><<<grid_for(total, 256), 256, 0, gfi::S(stream)>>>(pool, total, inv, momentum, lr, hu, w);
     gfi::count_launch();
     return gfi::check_launch("gf_dense_sgd_update");
+}
+
+}  // extern "C"
+
+// ---- rooted helpers for the host-orchestrated oracle/broadcast collectives ---------------
+namespace {
+template <int DT>
+__global__ void oracle_sum_kernel(char* const* __restrict__ bufs_in, int world, uint64_t len) {
+    // bufs_in: device array of world pointers (peer-mapped). oracle_allreduce
+    // (collectives.cpp:203-226): rank 0 accumulates ranks 1..N-1 in order, then all get it.
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < len;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        if (DT == GF_F16) {
+            uint16_t acc = reinterpret_cast<const uint16_t*>(bufs_in[0])[i];
+            for (int r = 1; r < world; ++r) acc = gfd::acc16(acc, reinterpret_cast<const uint16_t*>(bufs_in[r])[i]);
+            for (int r = 0; r < world; ++r) reinterpret_cast<uint16_t*>(bufs_in[r])[i] = acc;
+        } else {
+            float acc = reinterpret_cast<const float*>(bufs_in[0])[i];
+            for (int r = 1; r < world; ++r) acc = gfd::add(acc, reinterpret_cast<const float*>(bufs_in[r])[i]);
+            for (int r = 0; r < world; ++r) reinterpret_cast<float*>(bufs_in[r])[i] = acc;
+        }
+    }
+}
+__global__ void bcast_kernel(char* const* __restrict__ bufs_in, int world, int root, uint64_t bytes) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < bytes;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const char v = bufs_in[root][i];
+        for (int r = 0; r < world; ++r)
+            if (r != root) bufs_in[r][i] = v;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int gf_oracle_allreduce_ptrs(int dtype, void* const* bufs, int world, uint64_t len, void* stream) {
+    if (!gfi::valid_dtype(dtype) || !bufs || world < 1 || world > GF_MAX_RANKS)
+        return gfi::fail(GF_ERR_CONFIG, "gf_oracle_allreduce_ptrs: bad arguments");
+    if (world == 1 || len == 0) return GF_OK;
+    char** dptrs = nullptr;
+    GF_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dptrs), sizeof(char*) * world, gfi::S(stream)));
+    GF_CHECK_CUDA(cudaMemcpyAsync(dptrs, bufs, sizeof(char*) * world, cudaMemcpyHostToDevice, gfi::S(stream)));
+    if (dtype == GF_F16)
+        oracle_sum_kernel<GF_F16><<<grid_for(len, 256), 256, 0, gfi::S(stream)>>>(dptrs, world, len);
+    else
+        oracle_sum_kernel<GF_F32><<<grid_for(len, 256), 256, 0, gfi::S(stream)>>>(dptrs, world, len);
+    gfi::count_launch();
+    const int rc = gfi::check_launch("gf_oracle_allreduce_ptrs");
+    cudaFreeAsync(dptrs, gfi::S(stream));
+    return rc;
+}
+
+int gf_broadcast_ptrs(void* const* bufs, int world, int root, uint64_t bytes, void* stream) {
+    if (!bufs || world < 1 || world > GF_MAX_RANKS || root < 0 || root >= world)
+        return gfi::fail(GF_ERR_CONFIG, "gf_broadcast_ptrs: bad arguments");
+    if (world == 1 || bytes == 0) return GF_OK;
+    char** dptrs = nullptr;
+    GF_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dptrs), sizeof(char*) * world, gfi::S(stream)));
+    GF_CHECK_CUDA(cudaMemcpyAsync(dptrs, bufs, sizeof(char*) * world, cudaMemcpyHostToDevice, gfi::S(stream)));
+    bcast_kernel<<<grid_for(bytes, 256), 256, 0, gfi::S(stream)>>>(dptrs, world, root, bytes);
+    gfi::count_launch();
+    const int rc = gfi::check_launch("gf_broadcast_ptrs");
+    cudaFreeAsync(dptrs, gfi::S(stream));
+    return rc;
 }
 
 }  // extern "C"

@@ -22,6 +22,7 @@
 // Waits are bounded (globaltimer) and a timeout poisons the communicator,
 // surfacing as TransportError like the reference's recv timeout (inproc.cpp:28-36).
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -570,6 +571,84 @@ int gf_ring_allreduce(gf_comm* c, int dtype, uint64_t heap_off, const uint64_t* 
         gfi::count_launch();
         if (int rc = gfi::check_launch("gf_ring_allreduce")) return rc;
     }
+    return GF_OK;
+}
+
+int gf_ring_allreduce_ptrs(gf_comm* c, int dtype, void* const* rank_bufs, const uint64_t* win_start,
+                           const uint64_t* win_len, int nwin, void* stream) {
+    if (int rc = comm_ready(c)) return rc;
+    if (!gfi::valid_dtype(dtype) || !rank_bufs || nwin < 0 || (nwin > 0 && (!win_start || !win_len)))
+        return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_ptrs: bad arguments");
+    if (c->world == 1) return GF_OK;
+    const uint64_t es = gfi::esz(dtype);
+    for (int r = 0; r < c->world; ++r) {
+        if (!rank_bufs[r]) return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_ptrs: null rank buffer");
+        if ((reinterpret_cast<uintptr_t>(rank_bufs[r]) & 15u) != 0)
+            return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_ptrs: rank buffers must be 16-byte aligned");
+    }
+    DeviceGuard g(c->device);
+    for (int first = 0; first < nwin; first += kMaxW) {
+        RingArgs a;
+        std::memset(&a, 0, sizeof(a));
+        a.nwin = std::min(kMaxW, nwin - first);
+        uint64_t max_seg = 0;
+        for (int w = 0; w < a.nwin; ++w) {
+            a.wstart[w] = win_start[first + w];
+            a.wlen[w] = win_len[first + w];
+            max_seg += (a.wlen[w] + c->world - 1) / c->world;
+        }
+        fill_common(c, a, 0);
+        for (int r = 0; r < c->world; ++r) a.bufs[r] = static_cast<char*>(rank_bufs[r]);
+        launch_ring(dtype, true, a, dim3(ring_blocks(max_seg * es)), gfi::S(stream));
+        gfi::count_launch();
+        if (int rc = gfi::check_launch("gf_ring_allreduce_ptrs")) return rc;
+    }
+    return GF_OK;
+}
+
+int gf_ipc_export(const void* dev_ptr, void* handle_out, uint64_t* offset_out) {
+    if (!dev_ptr || !handle_out || !offset_out) return gfi::fail(GF_ERR_CONFIG, "gf_ipc_export: null argument");
+    // driver entry point fetched through the runtime: no link-time libcuda dependency
+    using range_fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static range_fn get_range = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<range_fn>(fn);
+    }();
+    if (!get_range) return gfi::fail(GF_ERR_CUDA, "gf_ipc_export: cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+        return gfi::fail(GF_ERR_CONFIG, "gf_ipc_export: not a device allocation");
+    cudaIpcMemHandle_t h;
+    GF_CHECK_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    std::memcpy(handle_out, &h, GF_IPC_HANDLE_BYTES);
+    *offset_out = reinterpret_cast<CUdeviceptr>(dev_ptr) - base;
+    return GF_OK;
+}
+
+int gf_ipc_open(gf_comm* c, const void* handle, void** base_out) {
+    if (!c || !handle || !base_out) return gfi::fail(GF_ERR_CONFIG, "gf_ipc_open: null argument");
+    DeviceGuard g(c->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, GF_IPC_HANDLE_BYTES);
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        gfi::cuda_fail(e, "cudaIpcOpenMemHandle");
+        return gfi::fail(GF_ERR_TRANSPORT, std::string("gf_ipc_open: ") + cudaGetErrorString(e));
+    }
+    *base_out = p;
+    return GF_OK;
+}
+
+int gf_ipc_close(gf_comm* c, void* base) {
+    if (!c || !base) return GF_OK;
+    DeviceGuard g(c->device);
+    GF_CHECK_CUDA(cudaIpcCloseMemHandle(base));
     return GF_OK;
 }
 

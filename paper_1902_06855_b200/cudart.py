@@ -10,8 +10,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-_CANDIDATES = ["/usr/local/cuda/lib64/libcudart.so.12", "/usr/local/cuda/lib64/libcudart.so",
-               "libcudart.so.12", "libcudart.so"]
+# soname first: resolves to the runtime instance torch / libgflow_b200 already loaded
+_CANDIDATES = ["libcudart.so.12", "/usr/local/cuda/lib64/libcudart.so.12", "libcudart.so"]
 cudaMemcpyDefault = 4
 _rt = None
 

@@ -13,6 +13,7 @@ self-contained and travel to the GPU box with the repo.
 from __future__ import annotations
 
 import concurrent.futures as cf
+import json
 import os
 import sys
 
@@ -139,6 +140,29 @@ def hand_traces(ref: Reference, out):
     out["trace_ties"] = r["next_imp"][0][0]
 
 
+TRAIN_CASES = [
+    dict(ranks=2, model_dims=[8, 1], task="logistic", iterations=40, n_examples=128, batch=16,
+         learning_rate=0.3, seed=7),
+    dict(ranks=4, iterations=12, chunk_size=100),
+    dict(ranks=4, iterations=12, chunk_size=100, csc=True, final_sparsity=0.85, warmup_iters=3),
+    dict(ranks=2, iterations=10, precision="fp16", theta_bytes=2048),
+    dict(ranks=3, model_dims=[16, 24, 8, 1], iterations=8, precision="fp16", csc=True,
+         final_sparsity=0.75, warmup_iters=2, chunk_size=64, n_examples=96, batch=8),
+    dict(ranks=4, model_dims=[32, 16, 1], iterations=6, theta_bytes=0),
+]
+
+
+def train_runs(ref: Reference, out):
+    """Whole training runs of the reference trainer (train_worker), rank 0's view."""
+    for i, c in enumerate(TRAIN_CASES):
+        r = ref.train(**c)
+        out[f"t{i}_loss"] = r["loss"]
+        out[f"t{i}_grad_bytes"] = r["grad_payload_bytes"]
+        out[f"t{i}_weights"] = r["final_weights"]
+    out["train_cases"] = np.array([len(TRAIN_CASES)])
+    out["cases_json"] = np.array(json.dumps(TRAIN_CASES))
+
+
 def main():
     ref = Reference()
     out: dict = {}
@@ -152,7 +176,10 @@ def main():
     c: dict = {}
     csc(ref, c)
     np.savez_compressed(os.path.join(HERE, "csc_run.npz"), **c)
-    for f in ("codec_layout.npz", "dense_sync.npz", "csc_run.npz"):
+    t: dict = {}
+    train_runs(ref, t)
+    np.savez_compressed(os.path.join(HERE, "train.npz"), **t)
+    for f in ("codec_layout.npz", "dense_sync.npz", "csc_run.npz", "train.npz"):
         print(f, os.path.getsize(os.path.join(HERE, f)))
 
 
