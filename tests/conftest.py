@@ -51,8 +51,14 @@ def reference():
 
 @pytest.fixture(scope="session")
 def golden():
+    cache = {}
+
     def load(name):
-        return np.load(os.path.join(GOLDEN, name))
+        # eager dict: NpzFile reads lazily and is not safe to share across rank threads
+        if name not in cache:
+            with np.load(os.path.join(GOLDEN, name)) as z:
+                cache[name] = {k: z[k] for k in z.files}
+        return cache[name]
     return load
 
 
