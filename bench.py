@@ -192,6 +192,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--trace", action="store_true", help="report ring CTA-0 timestamps (diagnostic)")
+    ap.add_argument("--ring-only", action="store_true", help="diagnostic: time the collective alone")
     args = ap.parse_args()
 
     wl = dict(WORKLOADS[args.workload])
@@ -277,7 +278,8 @@ def main():
         if csc:
             sync.csc_step(in_ptrs[i % n_sets], stream=sp, mark=m)
         else:
-            sync.dense_step(in_ptrs[i % n_sets], out_ptrs[i % 2], stream=sp, mark=m)
+            sync.dense_step(in_ptrs[i % n_sets], out_ptrs[i % 2], stream=sp, mark=m,
+                            ring_only=args.ring_only)
 
     def barrier():
         if world > 1:
@@ -384,6 +386,9 @@ def main():
         med = [statistics.median(r[j] for r in rec) / 1e3 for j in range(3)]
         ring_trace = {"entry_wait_us": round(allmax(med[0]), 2), "body_us": round(allmax(med[1]), 2),
                       "exit_wait_us": round(allmax(med[2]), 2)}
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, [round(m, 2) for m in med])
+        ring_trace["per_rank_entry_body_exit_us"] = per_rank
 
     # ---- NCCL allreduce on the same fp16 volume (comparison only) ---------------------------
     nccl = None

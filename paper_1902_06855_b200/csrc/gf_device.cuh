@@ -142,13 +142,32 @@ __device__ __forceinline__ uint4 enc8(float4 a, float4 b) {
 struct F8 {
     float4 lo, hi;
 };
+// L2 residency policies (126 MB L2): streams touched once (fp32 gradients in, fp32 g_avg
+// out) are marked evict-first so that the fp16 pool written by pack stays resident for
+// the ring (local + peer reads) and unpack.
+__device__ __forceinline__ uint64_t pol_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ F8 ld32f_stream(const float* p) {
     F8 v;
-    asm volatile("ld.global.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
                  : "=f"(v.lo.x), "=f"(v.lo.y), "=f"(v.lo.z), "=f"(v.lo.w), "=f"(v.hi.x), "=f"(v.hi.y),
                    "=f"(v.hi.z), "=f"(v.hi.w)
-                 : "l"(p));
+                 : "l"(p), "l"(pol_evict_first()));
     return v;
+}
+// fp16 pool store that asks L2 to keep the line (evict-last)
+__device__ __forceinline__ void st16_keep(void* p, uint4 v) {
+    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w), "l"(pol_evict_last())
+                 : "memory");
 }
 __device__ __forceinline__ F8 ld32f(const float* p) {
     F8 v;
@@ -159,8 +178,9 @@ __device__ __forceinline__ F8 ld32f(const float* p) {
     return v;
 }
 __device__ __forceinline__ void st32f_stream(float* p, float4 lo, float4 hi) {
-    asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
-                 "f"(lo.x), "f"(lo.y), "f"(lo.z), "f"(lo.w), "f"(hi.x), "f"(hi.y), "f"(hi.z), "f"(hi.w)
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p),
+                 "f"(lo.x), "f"(lo.y), "f"(lo.z), "f"(lo.w), "f"(hi.x), "f"(hi.y), "f"(hi.z), "f"(hi.w),
+                 "l"(pol_evict_first())
                  : "memory");
 }
 __device__ __forceinline__ void st32f(float* p, float4 lo, float4 hi) {

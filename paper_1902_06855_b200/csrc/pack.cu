@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ 
                             b[k] = make_float4(gfd::mul(b[k].x, scale), gfd::mul(b[k].y, scale),
                                                gfd::mul(b[k].z, scale), gfd::mul(b[k].w, scale));
                         }
-                        gfd::st16(d + 8 * v, gfd::enc8(a[k], b[k]));
+                        gfd::st16_keep(d + 8 * v, gfd::enc8(a[k], b[k]));
                     }
                 }
                 done = uint64_t(nvec) * 8;

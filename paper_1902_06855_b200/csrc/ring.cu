@@ -45,7 +45,7 @@ constexpr int kRingThreads = 512;
 // graph can replay the collective: every rank runs the same launch sequence, hence
 // CTA b's epoch is identical on all ranks.
 constexpr uint64_t kFlagWords = uint64_t(kMaxBlocks) * GF_MAX_RANKS;
-constexpr uint64_t kFlagBytes = (kFlagWords + kMaxBlocks) * sizeof(uint64_t);
+constexpr uint64_t kFlagBytes = (kFlagWords + kMaxBlocks + 32) * sizeof(uint64_t);  // + work/done words
 
 struct RingArgs {
     char* bufs[GF_MAX_RANKS];            // buffer base of each RANK (peer-mapped)
@@ -55,6 +55,8 @@ struct RingArgs {
     uint64_t* flags_local;
     uint64_t* flags_peer[GF_MAX_RANKS];  // by rank
     uint64_t* epochs;                    // local, one per CTA
+    uint64_t* work;                      // local dynamic item counter (re-armed by the last CTA)
+    unsigned* done;                      // local CTA completion counter
     uint64_t timeout_ns;
     int* err;
     uint64_t* trace;                     // host-mapped [start, entered, exit_begin, end] or null
@@ -83,12 +85,16 @@ struct SelArgs {
 };
 
 // ---- cross-GPU barrier (CTA b <-> CTA b of every peer) ------------------------
+// release_writes: the CTA's earlier global stores (incl. pushes into peers) must be visible
+// to a peer that observes the flag. bar.sync orders them before the signalling threads, whose
+// system-scope fence + release store make them cumulative (the cooperative-groups grid-sync
+// pattern, at .sys scope). At kernel entry nothing was written yet: no fence.
 template <typename A>
-__device__ bool cross_barrier(const A& a, uint64_t val, int* s_ok) {
-    __threadfence_system();  // this thread's prior (remote) stores are performed
+__device__ bool cross_barrier(const A& a, uint64_t val, int* s_ok, bool release_writes = true) {
     __syncthreads();
     const int t = threadIdx.x;
     if (t < a.world && t != a.rank) {
+        if (release_writes) __threadfence_system();
         gfd::st_release_sys(a.flags_peer[t] + blockIdx.x * GF_MAX_RANKS + a.rank, val);
         const uint64_t* f = a.flags_local + blockIdx.x * GF_MAX_RANKS + t;
         if (gfd::ld_acquire_sys(f) < val) {
@@ -134,16 +140,16 @@ struct Vec<GF_F32> {
     }
 };
 
+// Reduction of one window's owned segment: the grid sweeps its 16-byte vectors in
+// lockstep (thread g takes vectors g, g+T, g+2T, ... with T = all threads of the grid), so
+// every thread gets the same number of vectors (+-1) and all CTAs of a rank finish
+// together; U vectors x N sources of loads are in flight per thread.
 template <int DT, int NT>
-__device__ __forceinline__ void reduce_range(const RingArgs& a, int n, int p, uint64_t e0,
-                                             uint64_t e1) {
+__device__ __forceinline__ void reduce_segment(const RingArgs& a, const char* const* src, int n,
+                                               uint64_t e0, uint64_t e1, uint64_t gtid, uint64_t T) {
     constexpr int VE = Vec<DT>::kElems;
     constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
     constexpr int U = NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1);
-    const char* src[NMAX];
-#pragma unroll
-    for (int t = 0; t < NMAX; ++t) src[t] = (t < n) ? a.bufs[a.ring[(p + t) % n]] : nullptr;
-
     const uint64_t v0 = (e0 + VE - 1) / VE, v1 = e1 / VE;
     if (v0 >= v1) {  // no aligned vector inside: all scalar, CTA 0
         if (blockIdx.x == 0)
@@ -154,16 +160,12 @@ __device__ __forceinline__ void reduce_range(const RingArgs& a, int n, int p, ui
         for (uint64_t e = e0 + threadIdx.x; e < v0 * VE; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
         for (uint64_t e = v1 * VE + threadIdx.x; e < e1; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
     }
-    const uint64_t nv = v1 - v0;
-    const uint64_t per = (nv + gridDim.x - 1) / gridDim.x;
-    const uint64_t vb = v0 + min(nv, per * blockIdx.x);
-    const uint64_t ve = v0 + min(nv, per * (blockIdx.x + 1));
-    for (uint64_t v = vb + threadIdx.x; v < ve; v += uint64_t(blockDim.x) * U) {
+    for (uint64_t v = v0 + gtid; v < v1; v += T * U) {
         uint4 x[U][NMAX];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t vv = v + uint64_t(u) * blockDim.x;
-            if (vv < ve) {
+            const uint64_t vv = v + uint64_t(u) * T;
+            if (vv < v1) {
 #pragma unroll
                 for (int t = 0; t < NMAX; ++t)
                     if (t < n) x[u][t] = gfd::ld16(src[t] + vv * 16);
@@ -171,8 +173,8 @@ __device__ __forceinline__ void reduce_range(const RingArgs& a, int n, int p, ui
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t vv = v + uint64_t(u) * blockDim.x;
-            if (vv < ve) {
+            const uint64_t vv = v + uint64_t(u) * T;
+            if (vv < v1) {
                 uint4 acc = x[u][0];
 #pragma unroll
                 for (int t = 1; t < NMAX; ++t)
@@ -187,6 +189,7 @@ __device__ __forceinline__ void reduce_range(const RingArgs& a, int n, int p, ui
 
 template <int DT, int NT, bool P2P>
 __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constant__ RingArgs a) {
+    constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
     __shared__ int s_ok;
     uint64_t epoch = 0;
     if (P2P) epoch = a.epochs[blockIdx.x];
@@ -195,8 +198,14 @@ __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constan
     const int p = P2P ? a.pos : int(blockIdx.y);
     const bool tr = P2P && a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
     if (tr) a.trace[0] = gfd::globaltimer_ns();
-    if (P2P && !cross_barrier(a, epoch + 1, &s_ok)) return;
+    if (P2P && !cross_barrier(a, epoch + 1, &s_ok, false)) return;
     if (tr) a.trace[1] = gfd::globaltimer_ns();
+
+    const char* src[NMAX];
+#pragma unroll
+    for (int t = 0; t < NMAX; ++t) src[t] = (t < n) ? a.bufs[a.ring[(p + t) % n]] : nullptr;
+    const uint64_t T = uint64_t(gridDim.x) * blockDim.x;
+    const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     int nwin;
     uint64_t staged = 0, stride = 0;
     if (a.nwin >= 0) {
@@ -215,13 +224,13 @@ __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constan
             ws = uint64_t(w) * stride;
             wl = (w == nwin - 1) ? staged - ws : stride;
         }
+        // owned segment: segment_of(wl, n, p) (collectives.cpp:47-53)
         const uint64_t base = wl / uint64_t(n), rem = wl % uint64_t(n), up = uint64_t(p);
-        const uint64_t so = up * base + min(up, rem);
-        const uint64_t sc = base + (up < rem ? 1 : 0);
-        reduce_range<DT, NT>(a, n, p, ws + so, ws + so + sc);
+        const uint64_t e0 = ws + up * base + min(up, rem);
+        reduce_segment<DT, NT>(a, src, n, e0, e0 + base + (up < rem ? 1 : 0), gtid, T);
     }
     if (tr) a.trace[2] = gfd::globaltimer_ns();
-    if (P2P && cross_barrier(a, epoch + 2, &s_ok) && threadIdx.x == 0) a.epochs[blockIdx.x] = epoch + 2;
+    if (P2P && cross_barrier(a, epoch + 2, &s_ok, true) && threadIdx.x == 0) a.epochs[blockIdx.x] = epoch + 2;
     if (tr) a.trace[3] = gfd::globaltimer_ns();
 }
 
@@ -381,6 +390,8 @@ void fill_common(gf_comm* c, RingArgs& a, uint64_t heap_off) {
     }
     a.flags_local = reinterpret_cast<uint64_t*>(c->alloc);
     a.epochs = a.flags_local + kFlagWords;
+    a.work = a.epochs + kMaxBlocks;
+    a.done = reinterpret_cast<unsigned*>(a.work + 16);
     a.timeout_ns = c->timeout_ns;
     a.err = c->err_dev;
     a.trace = c->trace ? reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(c->err_dev) + 64) : nullptr;

@@ -168,21 +168,24 @@ class GradSync:
             return ptrs
         return (C.c_void_p * len(ptrs))(*ptrs)
 
-    def dense_step(self, grad_ptrs, out_ptrs, stream=None, mark=None):
-        """grad_ptrs/out_ptrs: per-tensor device pointers in ascending tensor id."""
+    def dense_step(self, grad_ptrs, out_ptrs, stream=None, mark=None, ring_only=False):
+        """grad_ptrs/out_ptrs: per-tensor device pointers in ascending tensor id.
+        ring_only: diagnostic — the collective alone, on whatever the pool holds."""
         L = self.layout
         m = len(L.sizes)
         mark = mark or (lambda name: None)
-        mark("pack")
-        capi.call("gf_pack", self.dtype, self.pool_ptr, self._ptrs(grad_ptrs), self._offs,
-                  self._cnts, m, 1.0, stream)
+        if not ring_only:
+            mark("pack")
+            capi.call("gf_pack", self.dtype, self.pool_ptr, self._ptrs(grad_ptrs), self._offs,
+                      self._cnts, m, 1.0, stream)
         mark("ring")
         if self.world > 1:
             capi.call("gf_ring_allreduce", self.comm, self.dtype, self.pool_off, self._win[0],
                       self._win[1], self._win[2], stream)
-        mark("unpack")
-        capi.call("gf_unpack", self.dtype, self.pool_ptr, self._ptrs(out_ptrs), self._offs,
-                  self._cnts, m, self.world, stream)
+        if not ring_only:
+            mark("unpack")
+            capi.call("gf_unpack", self.dtype, self.pool_ptr, self._ptrs(out_ptrs), self._offs,
+                      self._cnts, m, self.world, stream)
         mark(None)
 
     def csc_step(self, grad_ptrs, stream=None, mark=None):

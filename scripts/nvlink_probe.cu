@@ -112,6 +112,33 @@ __global__ void push_all(Args a) {
     }
 }
 
+// ring-like mix: each thread pulls one vector from every peer (its owned segment) and pushes
+// one vector to every peer (the all-gather), like the K4 kernel
+template <int U>
+__global__ void mixed(Args a) {
+    const size_t V = a.vec_per_peer;
+    const size_t tid = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = tid; i < V; i += stride * U) {
+        uint4 x[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < a.n && i + u * stride < V) x[u][q] = a.src[q][a.me * V + i + u * stride];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            uint4 acc = x[u][0];
+#pragma unroll
+            for (int q = 1; q < 8; ++q)
+                if (q < a.n) { acc.x ^= x[u][q].x; acc.y += x[u][q].y; }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < a.n && i + u * stride < V) a.dst[q][a.me * V + i + u * stride] = acc;
+        }
+    }
+}
+
 int main(int argc, char** argv) {
     int n = argc > 1 ? atoi(argv[1]) : 2;
     size_t mb = argc > 2 ? atoll(argv[2]) : 256;
@@ -159,6 +186,7 @@ int main(int argc, char** argv) {
                 if (kind == 1) push<4><<<g, threads, 0, st[d]>>>(a);
                 if (kind == 2) pull_all<1><<<g, threads, 0, st[d]>>>(a);
                 if (kind == 3) push_all<2><<<g, threads, 0, st[d]>>>(a);
+                if (kind == 5) mixed<2><<<g, threads, 0, st[d]>>>(a);
                 if (kind == 4) {
                     for (int qq = 1; qq < n; ++qq) {
                         int q = (d + qq) % n;
@@ -180,11 +208,12 @@ int main(int argc, char** argv) {
         printf("n=%d %-10s blocks/SM=%d thr=%d : %.3f ms  %.1f GB/s per GPU per direction\n", n, name,
                blocks_per_sm, threads, best, payload / (best * 1e-3) / 1e9);
     };
-    for (int b : {1, 2, 4}) {
+    for (int b : {1, 2}) {
         run("pull", 0, b, 512);
         run("push", 1, b, 512);
         run("pull_all", 2, b, 512);
         run("push_all", 3, b, 512);
+        run("mixed(x2)", 5, b, 512);
     }
     run("memcpy", 4, 1, 1);
     return 0;
