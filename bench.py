@@ -193,6 +193,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--trace", action="store_true", help="report ring CTA-0 timestamps (diagnostic)")
     ap.add_argument("--ring-only", action="store_true", help="diagnostic: time the collective alone")
+    ap.add_argument("--fused", action="store_true",
+                    help="dense: one fused pack+ring+unpack kernel per step (gf_sync_step_dense)")
     args = ap.parse_args()
 
     wl = dict(WORKLOADS[args.workload])
@@ -278,8 +280,11 @@ def main():
         if csc:
             sync.csc_step(in_ptrs[i % n_sets], stream=sp, mark=m)
         else:
-            sync.dense_step(in_ptrs[i % n_sets], out_ptrs[i % 2], stream=sp, mark=m,
-                            ring_only=args.ring_only)
+            if args.fused:
+                sync.fused_step(in_ptrs[i % n_sets], out_ptrs[i % 2], stream=sp, mark=m)
+            else:
+                sync.dense_step(in_ptrs[i % n_sets], out_ptrs[i % 2], stream=sp, mark=m,
+                                ring_only=args.ring_only)
 
     def barrier():
         if world > 1:
@@ -330,6 +335,7 @@ def main():
     ws, wlen = dense_windows(L, esz, wl["theta"])
     algo = {  # algorithmic bytes per launch
         "pack": total * 6, "unpack": total * 6, "pack_correct": total * 14,
+        "fused_step": None,
         "norms": total * 2, "scatter": None, "select": None, "sgd_update": None,
         "ring": None,
     }
@@ -343,11 +349,13 @@ def main():
     else:
         ring_bytes = ring_bus_bytes(L, esz, world, wlen)
     algo["ring"] = ring_bytes if world > 1 else None
+    if args.fused:  # its binding roofline: NVLink bus bytes at N>1, HBM bytes at N=1
+        algo["fused_step"] = ring_bytes if world > 1 else total * 12
     dom = max(seg_ms, key=lambda k: seg_ms[k]) if seg_ms else None
     roof = None
     if dom is not None and algo.get(dom):
         t_s = seg_ms[dom] / 1e3
-        if dom == "ring":
+        if dom == "ring" or (dom == "fused_step" and world > 1):
             ach = algo[dom] / t_s / 1e9
             roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": 900.0, "unit": "GB/s",
                     "frac": round(ach / 900.0, 3), "traffic": None, "kernel": "ring_kernel",
@@ -363,7 +371,7 @@ def main():
         d = {"ms": round(v, 4)}
         if algo.get(k):
             d["GBps"] = round(algo[k] / (v / 1e3) / 1e9, 1)
-            if k != "ring":
+            if k != "ring" and not (k == "fused_step" and world > 1):
                 d["frac_hbm"] = round(d["GBps"] / hbm_peak, 3)
             else:
                 d["busbw_frac_900"] = round(d["GBps"] / 900, 3)
@@ -453,6 +461,8 @@ def main():
         bus = None
         if world > 1 and "ring" in seg_ms:
             bus = round(ring_bytes / (seg_ms["ring"] / 1e3) / 1e9, 1)
+        elif world > 1 and "fused_step" in seg_ms:
+            bus = round(ring_bytes / (seg_ms["fused_step"] / 1e3) / 1e9, 1)
         line = {
             "metric": "grad-sync ms/step", "value": round(ms, 4), "unit": "ms", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),

@@ -35,6 +35,8 @@
  *  gf_comm_*                        Communicator + Transport (data plane)    include/gflow/collectives.hpp:25-61, include/gflow/transport.hpp:96-120
  *  gf_ring_allreduce[_planned]      ring_allreduce / ring_allreduce_on       src/collectives.cpp:55-97, :174-177
  *  gf_ring_allreduce_colocated      same, all ranks' buffers on one device   src/collectives.cpp:55-97
+ *  gf_sync_step_dense               one dense iteration: write_tensor x m + FusionEngine windows +
+ *                                   update read (src/trainer.cpp:297-347), fused into one kernel
  *  gf_csc_select                    select_next_important (norm allreduce + top-k) src/sparse.cpp:172-204
  *  gf_ring_traffic                  TrafficStats record_send/recv of the ring include/gflow/transport.hpp:48-91, src/collectives.cpp:69-96
  */
@@ -182,6 +184,15 @@ int gf_ipc_close(gf_comm* comm, void* base);
 /* Same with windows described by a device plan written by gf_csc_plan / gf_csc_select. */
 int gf_ring_allreduce_planned(gf_comm* comm, int dtype, uint64_t heap_off,
                               const uint64_t* plan_dev, void* stream);
+/* One fused dense sync step: pack -> ring allreduce of the theta windows -> unpack, as ONE
+ * persistent kernel per rank that overlaps the three slab by slab through per-slab flags in
+ * peer memory (no global barriers). Result-identical to gf_pack + gf_ring_allreduce +
+ * gf_unpack (bit for bit). The fp16/fp32 pool lives at pool_heap_off in the symmetric heap;
+ * src/dst/pool_off/count are HOST arrays (<= 256 tensors) of device pointers / sizes. */
+int gf_sync_step_dense(gf_comm* comm, int dtype, uint64_t pool_heap_off, const float* const* src,
+                       float* const* dst, const uint64_t* pool_off, const uint64_t* count,
+                       int ntensors, const uint64_t* win_start, const uint64_t* win_len, int nwin,
+                       void* stream);
 /* Emulation of `world` ranks whose buffers all live on the current device (no waits). */
 int gf_ring_allreduce_colocated(int dtype, void* const* bufs, int world, const int* ring_order,
                                 const uint64_t* win_start, const uint64_t* win_len, int nwin,

@@ -89,6 +89,7 @@ SIGNATURES = {
     "gf_ring_allreduce": [_vp, _i, _u64, _vp, _vp, _i, _vp],
     "gf_ring_allreduce_planned": [_vp, _i, _u64, _vp, _vp],
     "gf_ring_allreduce_ptrs": [_vp, _i, _vp, _vp, _vp, _i, _vp],
+    "gf_sync_step_dense": [_vp, _i, _u64, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _vp],
     "gf_ipc_export": [_vp, _vp, _u64p],
     "gf_ipc_open": [_vp, _vp, C.POINTER(_vp)],
     "gf_ipc_close": [_vp, _vp],

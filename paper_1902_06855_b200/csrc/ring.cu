@@ -33,19 +33,11 @@
 #include "gf_device.cuh"
 #include "gf_internal.cuh"
 #include "select.cuh"
+#include "comm.cuh"
 
 namespace {
 
-constexpr int kMaxBlocks = 1024;
-constexpr int kMaxW = GF_MAX_WINDOWS_PER_LAUNCH;
-constexpr int kRingThreads = 512;
-// Per-rank flag area at the head of the heap allocation: kMaxBlocks x GF_MAX_RANKS
-// barrier flags (written by peers) followed by kMaxBlocks epoch counters (local only).
-// The epochs live on the device and advance inside the kernels, so a captured CUDA
-// graph can replay the collective: every rank runs the same launch sequence, hence
-// CTA b's epoch is identical on all ranks.
-constexpr uint64_t kFlagWords = uint64_t(kMaxBlocks) * GF_MAX_RANKS;
-constexpr uint64_t kFlagBytes = (kFlagWords + kMaxBlocks + 32) * sizeof(uint64_t);  // + work/done words
+
 
 struct RingArgs {
     char* bufs[GF_MAX_RANKS];            // buffer base of each RANK (peer-mapped)
@@ -341,43 +333,7 @@ bool valid_ring(const int* order, int world) {
 
 }  // namespace
 
-struct gf_comm {
-    int world = 0, rank = 0, device = 0, pos = 0;
-    int ring[GF_MAX_RANKS] = {};
-    uint64_t heap_bytes = 0;
-    char* alloc = nullptr;                       // [flags | heap]
-    char* peer_alloc[GF_MAX_RANKS] = {};
-    bool ipc_opened[GF_MAX_RANKS] = {};
-    int* err_host = nullptr;   // mapped pinned page: [0] error word, trace at +64 B
-    int* err_dev = nullptr;
-    bool trace = false;
-    uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;  // transport.hpp:25 kDefaultTimeout
-    bool connected = false;
-};
-
 namespace {
-
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        int cur = -1;
-        cudaGetDevice(&cur);
-        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-    }
-};
-
-int comm_ready(gf_comm* c) {
-    if (!c) return gfi::fail(GF_ERR_CONFIG, "null communicator");
-    if (!c->connected) return gfi::fail(GF_ERR_CONFIG, "communicator not connected");
-    if (c->err_host && *reinterpret_cast<volatile int*>(c->err_host) != 0)
-        return gfi::fail(GF_ERR_TRANSPORT, "communicator poisoned by an earlier peer timeout (rank " +
-                                               std::to_string(c->rank) + ")");
-    return GF_OK;
-}
 
 void fill_common(gf_comm* c, RingArgs& a, uint64_t heap_off) {
     a.world = c->world;
@@ -440,6 +396,12 @@ int gf_comm_destroy(gf_comm* c) {
     cudaDeviceSynchronize();
     for (int r = 0; r < c->world; ++r)
         if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->peer_alloc[r]);
+    for (auto& kv : c->step_plans) {
+        cudaFree(kv.second.slab_a);
+        cudaFree(kv.second.slab_b);
+        cudaFree(kv.second.slab_pos);
+        cudaFree(kv.second.mine);
+    }
     cudaFree(c->alloc);
     cudaFreeHost(c->err_host);
     delete c;

@@ -188,6 +188,16 @@ class GradSync:
                       self._cnts, m, self.world, stream)
         mark(None)
 
+    def fused_step(self, grad_ptrs, out_ptrs, stream=None, mark=None):
+        """The dense step as ONE kernel (gf_sync_step_dense): pack, NVLink ring of the theta
+        windows and unpack overlapped slab by slab; bit-identical to dense_step."""
+        mark = mark or (lambda name: None)
+        mark("fused_step")
+        capi.call("gf_sync_step_dense", self.comm, self.dtype, self.pool_off, self._ptrs(grad_ptrs),
+                  self._ptrs(out_ptrs), self._offs, self._cnts, len(self.layout.sizes),
+                  self._win[0], self._win[1], self._win[2], stream)
+        mark(None)
+
     def csc_step(self, grad_ptrs, stream=None, mark=None):
         """One CSC iteration (Algorithm 1). Uses the buffers given to attach_csc_state."""
         b = self._csc_bufs

@@ -466,3 +466,27 @@ def test_csc_multistep_colocated_vs_reference_golden(gf, golden, oracle, G, fuse
                     assert not G.host(naccs[r], np.uint64).any()  # re-armed for the next step
             assert (G.host(nxt) == g[p + "next_imp"][t][0]).all(), (ci, t)
             imp, coff, plan = nxt, nxt_coff, nxt_plan
+
+
+def test_fused_step_single_rank(gf, oracle, G):
+    """world == 1: the fused kernel's pack/unpack path (no peers) vs the oracle."""
+    import torch
+    from paper_1902_06855_b200.engine import GradSync
+    sizes = RESNET50[:40] + [13, 7]  # includes two tensors with unaligned pool offsets
+    off, _, _ = oracle.pool_layout(sizes, 32000)
+    bounds = np.concatenate([[0], np.cumsum(sizes)])
+    sync = GradSync(sizes, theta=1 << 16)
+    for it in range(3):
+        flat = oracle.gen_grads(40 + it, sizes) * np.float32(1 + it)
+        g = torch.from_numpy(flat).cuda()
+        out = torch.empty_like(g)
+        gp = [g[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
+        op = [out[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
+        sync.fused_step(gp, op)
+        torch.cuda.synchronize()
+        want = oracle.unpack(oracle.pack(flat, sizes), 1)
+        got = out.cpu().numpy()
+        for i, s in enumerate(sizes):
+            assert (got[int(bounds[i]):int(bounds[i + 1])].view(np.uint32) ==
+                    want[int(off[i]):int(off[i]) + s].view(np.uint32)).all(), (it, i)
+    sync.close()

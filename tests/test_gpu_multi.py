@@ -223,3 +223,49 @@ def test_inprocess_local_connect():
     for c in comms:
         capi.call("gf_comm_destroy", c)
     torch.cuda.synchronize()
+
+
+def _worker_fused(rank, world, port):
+    """The fused dense step (pack + NVLink ring + unpack in one kernel) over several
+    iterations and theta values, bit-exact against the oracle's unfused path."""
+    comm, base, capi, cudart, dist = _setup(rank, world, port)
+    import torch
+    from oracle.oracle import RESNET50, Oracle
+    from paper_1902_06855_b200.engine import GradSync
+    o = Oracle()
+    torch.cuda.set_device(rank)
+    sizes = RESNET50
+    off, _, _ = o.pool_layout(sizes, 32000)
+    bounds = np.concatenate([[0], np.cumsum(sizes)])
+
+    def ag(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+
+    for theta in (64 << 20, 1 << 20, 0):
+        sync = GradSync(sizes, rank=rank, world=world, device=rank, theta=theta, allgather=ag)
+        for it in range(3):
+            grads = [o.gen_grads(1000 * it + 17 * r + theta % 97, sizes) for r in range(world)]
+            g = torch.from_numpy(grads[rank]).cuda()
+            out = torch.empty_like(g)
+            gp = [g[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
+            op = [out[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
+            sync.fused_step(gp, op)
+            torch.cuda.synchronize()
+            sync.status()
+            ws, wl = o.dense_windows(sizes, 2, theta)
+            pools = o.ring_allreduce([o.pack(x, sizes) for x in grads], dtype=F16, windows=(ws, wl))
+            want_pool = o.unpack(pools[rank], world)
+            got = out.cpu().numpy()
+            for i, s in enumerate(sizes):
+                w = want_pool[int(off[i]):int(off[i]) + s]
+                assert (got[int(bounds[i]):int(bounds[i + 1])].view(np.uint32) == w.view(np.uint32)).all(), \
+                    (theta, it, i)
+        sync.close()
+    dist.barrier()
+
+
+@pytest.mark.multigpu(2)
+def test_p2p_fused_step_bit_exact():
+    _spawn(_worker_fused, _world())
