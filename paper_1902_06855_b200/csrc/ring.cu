@@ -171,9 +171,11 @@ __device__ __forceinline__ void reduce_segment(const RingArgs& a, const char* co
 #pragma unroll
                 for (int t = 1; t < NMAX; ++t)
                     if (t < n) acc = Vec<DT>::acc(x[u][t], acc);
+                // push the sum to every rank, starting with the next one on the ring so the
+                // ranks' first stores spread over distinct destinations
 #pragma unroll
-                for (int r = 0; r < NMAX; ++r)
-                    if (r < a.world) gfd::st16(a.bufs[r] + vv * 16, acc);
+                for (int t = 0; t < NMAX; ++t)
+                    if (t < n) gfd::st16(const_cast<char*>(src[(t + 1) % n]) + vv * 16, acc);
             }
         }
     }
@@ -308,7 +310,7 @@ void launch_ring(int dtype, bool p2p, const RingArgs& a, dim3 grid, cudaStream_t
 }
 
 // CTAs per rank: enough 512-thread CTAs to keep ~2 MB of NVLink loads in flight,
-// capped at 2 per SM (and by the flag table). Depends only on values identical
+// capped at 1 per SM (and by the flag table). Depends only on values identical
 // on every rank, so all ranks launch the same grid (CTA b pairs with CTA b).
 int ring_blocks(uint64_t max_seg_bytes) {
     static const int forced = [] {
@@ -318,7 +320,9 @@ int ring_blocks(uint64_t max_seg_bytes) {
     if (forced > 0) return std::min(forced, kMaxBlocks);
     const uint64_t per_cta = uint64_t(kRingThreads) * 16 * 4;
     const uint64_t want = (max_seg_bytes + per_cta - 1) / per_cta;
-    const uint64_t cap = std::min<uint64_t>(kMaxBlocks, uint64_t(gfi::sm_count()) * 2);
+    // one 512-thread CTA per SM: measured on 2-4 B200, 2/SM and more oversubscribe the
+    // NVLink request queues (ResNet-50 fp16, N=4: 150 us at 148 CTAs vs 163 at 296)
+    const uint64_t cap = std::min<uint64_t>(kMaxBlocks, uint64_t(gfi::sm_count()));
     return int(std::max<uint64_t>(1, std::min(want, cap)));
 }
 
