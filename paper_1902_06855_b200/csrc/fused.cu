@@ -96,15 +96,20 @@ __device__ __forceinline__ int first_tensor(const StepTable& T, uint64_t x) {
 }
 
 // ---- pack / unpack of pool range [x0, x1) ----------------------------------------------
-template <int DT>
+// SOLO (world == 1): the collective is the identity, so the slab is unpacked straight from
+// the registers that hold its packed value (g_avg = dec(enc(g)) * 1/N): one HBM pass.
+template <int DT, bool SOLO>
 __device__ void pack_range(const StepArgs& a, const StepTable& T, uint64_t x0, uint64_t x1) {
     char* pool = a.pool[a.rank];
+    const float inv = a.inv_world;
     for (int t = first_tensor(T, x0); t < T.n && T.off[t] < x1; ++t) {
         const uint64_t lo = max(x0, T.off[t]), hi = min(x1, T.off[t] + T.cnt[t]);
         if (lo >= hi) continue;
         const float* s = T.src[t] - T.off[t];  // indexed by pool element
+        float* o = T.dst[t] - T.off[t];
         uint64_t v0 = hi, v1 = hi;
-        if (DT == GF_F16 && (T.off[t] % 8) == 0 && (reinterpret_cast<uintptr_t>(T.src[t]) & 31u) == 0) {
+        if (DT == GF_F16 && (T.off[t] % 8) == 0 && (reinterpret_cast<uintptr_t>(T.src[t]) & 31u) == 0 &&
+            (!SOLO || (reinterpret_cast<uintptr_t>(T.dst[t]) & 31u) == 0)) {
             v0 = (lo + 7) / 8 * 8;
             v1 = max(v0, hi / 8 * 8);
             uint16_t* d = reinterpret_cast<uint16_t*>(pool);
@@ -116,19 +121,44 @@ __device__ void pack_range(const StepArgs& a, const StepTable& T, uint64_t x0, u
                 for (int u = 0; u < U; ++u)
                     if (e0 + u * step < v1) f[u] = gfd::ld32f_stream(s + e0 + u * step);
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (e0 + u * step < v1) gfd::st16_keep(d + e0 + u * step, gfd::enc8(f[u].lo, f[u].hi));
+                for (int u = 0; u < U; ++u) {
+                    const uint64_t e = e0 + u * step;
+                    if (e >= v1) break;
+                    const uint4 h = gfd::enc8(f[u].lo, f[u].hi);
+                    if (SOLO) {
+                        gfd::st16(d + e, h);
+                        if (!gfd::any_special(h)) {
+                            const float2 g0 = gfd::h2f2(h.x), g1 = gfd::h2f2(h.y), g2 = gfd::h2f2(h.z), g3 = gfd::h2f2(h.w);
+                            gfd::st32f_stream(o + e,
+                                              make_float4(__fmul_rn(g0.x, inv), __fmul_rn(g0.y, inv),
+                                                          __fmul_rn(g1.x, inv), __fmul_rn(g1.y, inv)),
+                                              make_float4(__fmul_rn(g2.x, inv), __fmul_rn(g2.y, inv),
+                                                          __fmul_rn(g3.x, inv), __fmul_rn(g3.y, inv)));
+                        } else {
+                            const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+                            for (int k = 0; k < 8; ++k)
+                                o[e + k] = gfd::mul(gfd::dec(uint16_t((hw[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu)), inv);
+                        }
+                    } else {
+                        gfd::st16_keep(d + e, h);
+                    }
+                }
             }
         }
         // scalar head [lo, v0) and tail [v1, hi) (everything when the tensor is unaligned)
         const uint64_t h_end = min(v0, hi), t_beg = max(v1, h_end);
-        for (uint64_t e = lo + threadIdx.x; e < h_end; e += blockDim.x) {
-            if (DT == GF_F16) reinterpret_cast<uint16_t*>(pool)[e] = gfd::enc(s[e]);
-            else reinterpret_cast<float*>(pool)[e] = s[e];
-        }
-        for (uint64_t e = t_beg + threadIdx.x; e < hi; e += blockDim.x) {
-            if (DT == GF_F16) reinterpret_cast<uint16_t*>(pool)[e] = gfd::enc(s[e]);
-            else reinterpret_cast<float*>(pool)[e] = s[e];
+        for (int part = 0; part < 2; ++part) {
+            const uint64_t b0 = part == 0 ? lo : t_beg, b1 = part == 0 ? h_end : hi;
+            for (uint64_t e = b0 + threadIdx.x; e < b1; e += blockDim.x) {
+                if (DT == GF_F16) {
+                    const uint16_t h = gfd::enc(s[e]);
+                    reinterpret_cast<uint16_t*>(pool)[e] = h;
+                    if (SOLO) o[e] = gfd::mul(gfd::dec(h), inv);
+                } else {
+                    reinterpret_cast<float*>(pool)[e] = s[e];
+                    if (SOLO) o[e] = gfd::mul(s[e], inv);
+                }
+            }
         }
     }
 }
@@ -254,8 +284,10 @@ step_kernel(const __grid_constant__ StepArgs a, const __grid_constant__ StepTabl
         const uint32_t q = s_task;
         if (q >= a.ntasks || !s_ok) break;
         const uint32_t code = a.tasks[q], kind = code >> 30, t = code & 0x3FFFFFFFu;
-        if (kind == 0) {  // ---- pack slab t, then tell its owner
-            pack_range<DT>(a, T, a.slab_a[t], a.slab_b[t]);
+        if (solo) {  // ---- world == 1: pack and unpack the slab in one pass, no flags
+            pack_range<DT, true>(a, T, a.slab_a[t], a.slab_b[t]);
+        } else if (kind == 0) {  // ---- pack slab t, then tell its owner
+            pack_range<DT, false>(a, T, a.slab_a[t], a.slab_b[t]);
             __syncthreads();
             if (threadIdx.x == 0) {
                 const int owner = a.ring[a.slab_pos[t]];
@@ -306,13 +338,19 @@ void launch_step(const StepArgs& a, const StepTable& T, int grid, cudaStream_t s
     }
 }
 
-uint64_t slab_elems(int dtype) {
+// Slab size: 128 KB of pool (GF_STEP_SLAB=<elements> overrides).
+uint64_t slab_elems(int dtype, int world, uint64_t total, int grid) {
     static const uint64_t forced = [] {
         const char* e = std::getenv("GF_STEP_SLAB");
         return e ? uint64_t(std::atoll(e)) : 0ull;
     }();
     if (forced) return forced;
-    return dtype == GF_F16 ? 65536 : 32768;  // 128 KB of pool per slab
+    // measured (ResNet-50/AlexNet, 1-4 B200): per-task overhead outweighs a shorter tail,
+    // so 128 KB slabs win at every world size
+    (void)world;
+    (void)total;
+    (void)grid;
+    return dtype == GF_F16 ? 65536 : 32768;
 }
 
 }  // namespace
@@ -350,13 +388,15 @@ int gf_sync_step_dense(gf_comm* c, int dtype, uint64_t pool_heap_off, const floa
         return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense: pool outside the symmetric heap");
     DeviceGuard guard(c->device);
     // ---- slab plan (cached per geometry) ---------------------------------------------
-    const uint64_t SE = slab_elems(dtype);
     static int grid = 0;
     if (grid == 0) {
         int occ = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<GF_F16, 8>, kStepThreads, 0);
         grid = std::max(1, occ) * gfi::sm_count();
     }
+    uint64_t span = 0;
+    for (int w = 0; w < nwin; ++w) span += win_len[w];
+    const uint64_t SE = slab_elems(dtype, c->world, span, grid);
     std::string key = std::to_string(dtype) + "/" + std::to_string(c->pos) + "/" + std::to_string(SE) + "/" +
                       std::to_string(grid);
     for (int w = 0; w < nwin; ++w) key += "/" + std::to_string(win_start[w]) + ":" + std::to_string(win_len[w]);
@@ -409,14 +449,14 @@ int gf_sync_step_dense(gf_comm* c, int dtype, uint64_t pool_heap_off, const floa
             return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(0);
         }();
         const int64_t D1 = n == 1 ? 0 : (lag ? lag : R);
-        const int64_t D2 = n == 1 ? (lag ? lag : R) : (lag ? 2 * lag : R + 1);
+        const int64_t D2 = n == 1 ? R + 1 : (lag ? 2 * lag : R + 1);  // n == 1: packs only
         std::vector<uint32_t> tasks;
         for (int64_t r = 0; r < R + D2; ++r) {
             if (r < R)
                 for (uint32_t g : rounds[static_cast<size_t>(r)]) tasks.push_back((0u << 30) | g);
             if (n > 1 && r - D1 >= 0 && r - D1 < R && mine[static_cast<size_t>(r - D1)] >= 0)
                 tasks.push_back((1u << 30) | static_cast<uint32_t>(mine[static_cast<size_t>(r - D1)]));
-            if (r - D2 >= 0 && r - D2 < R)
+            if (n > 1 && r - D2 >= 0 && r - D2 < R)
                 for (uint32_t g : rounds[static_cast<size_t>(r - D2)]) tasks.push_back((2u << 30) | g);
         }
         StepPlan sp;
