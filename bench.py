@@ -366,6 +366,20 @@ def main():
             roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
                     "frac": round(ach / hbm_peak, 3), "traffic": None, "kernel": dom,
                     "peak_src": peak_src}
+    # traffic: DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    if roof is not None:
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                tr = json.load(f)
+            kname = {"pack": "pack_kernel", "unpack": "unpack_kernel", "pack_correct": "pack_correct_kernel",
+                     "sgd_update": "csc_sgd_kernel", "scatter": "compact_kernel",
+                     "select": "select_kernel"}.get(dom)
+            ent = tr.get(args.workload, {}).get(kname or "", {})
+            if ent:
+                roof["traffic"] = ent["dram_bytes_per_launch"]
+                roof["traffic_note"] = "ncu --set full, cold cache, profiles/ncu_traffic.json"
+        except Exception:
+            pass
     kernels = {}
     for k, v in seg_ms.items():
         d = {"ms": round(v, 4)}
