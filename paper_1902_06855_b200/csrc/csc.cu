@@ -428,8 +428,9 @@ int compact_launch(int dtype, void* pool, const void* staging, const uint64_t* p
     if (!gfi::valid_dtype(dtype) || chunk == 0 || nc == 0 || !plan || !coff)
         return gfi::fail(GF_ERR_CONFIG, "gf_csc_compact/scatter: bad arguments");
     const uint64_t bytes = std::max<uint64_t>(chunk, total - (nc - 1) * chunk) * gfi::esz(dtype);
-    const int gx = int(std::max<uint64_t>(1, std::min<uint64_t>((bytes / 16 + 511) / 512, 64)));
-    compact_kernel<<<dim3(gx, grid_y(max_chunks, nc)), 512, 0, gfi::S(stream)>>>(
+    // one 1024-thread CTA per 64 KB of chunk: 4 x 16 B per thread, one wave for k ~ 2 x #SMs
+    const int gx = int(std::max<uint64_t>(1, std::min<uint64_t>((bytes + 65535) / 65536, 64)));
+    compact_kernel<<<dim3(gx, grid_y(max_chunks, nc)), 1024, 0, gfi::S(stream)>>>(
         static_cast<char*>(pool), static_cast<char*>(const_cast<void*>(staging)), plan, coff,
         total, chunk, nc, gfi::esz(dtype), dir, nacc);
     gfi::count_launch();

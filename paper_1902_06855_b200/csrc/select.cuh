@@ -65,6 +65,23 @@ struct SelShared {
 };
 
 // flags[c] = 1 iff chunk c is among the top k by (norm desc, index asc).
+// Keys of up to kSelThreads * kKeysPerThread chunks stay in registers across the passes.
+constexpr int kKeysPerThread = 4;
+
+template <typename F>
+__device__ __forceinline__ void for_each_key(const float* norms, uint64_t nc, const uint32_t* kr, bool cached,
+                                             F&& fn) {
+    if (cached) {
+#pragma unroll
+        for (int q = 0; q < kKeysPerThread; ++q) {
+            const uint64_t i = threadIdx.x + uint64_t(q) * kSelThreads;
+            if (i < nc) fn(i, kr[q]);
+        }
+    } else {
+        for (uint64_t i = threadIdx.x; i < nc; i += kSelThreads) fn(i, norm_key(norms[i]));
+    }
+}
+
 inline __device__ void block_topk(const float* norms, uint64_t nc, uint64_t k, uint8_t* flags,
                            SelShared& sh) {
     const int tid = threadIdx.x;
@@ -73,17 +90,23 @@ inline __device__ void block_topk(const float* norms, uint64_t nc, uint64_t k, u
         __syncthreads();
         return;
     }
+    const bool cached = nc <= uint64_t(kSelThreads) * kKeysPerThread;
+    uint32_t kr[kKeysPerThread];
+#pragma unroll
+    for (int q = 0; q < kKeysPerThread; ++q) {
+        const uint64_t i = tid + uint64_t(q) * kSelThreads;
+        kr[q] = (cached && i < nc) ? norm_key(norms[i]) : 0u;
+    }
     uint32_t prefix = 0;
     unsigned long long remaining = k;
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
         for (int d = tid; d < 256; d += kSelThreads) sh.hist[d] = 0;
         __syncthreads();
-        for (uint64_t i = tid; i < nc; i += kSelThreads) {
-            const uint32_t key = norm_key(norms[i]);
+        for_each_key(norms, nc, kr, cached, [&](uint64_t, uint32_t key) {
             const bool match = pass == 0 || (key >> (shift + 8)) == prefix;
             if (match) atomicAdd(&sh.hist[(key >> shift) & 255u], 1u);
-        }
+        });
         __syncthreads();
         if (tid < 32) {
             // warp 0: lane l owns digits 255-8l .. 248-8l (descending); find the digit where
@@ -126,7 +149,16 @@ inline __device__ void block_topk(const float* norms, uint64_t nc, uint64_t k, u
     for (uint64_t base = 0; base < nc; base += kSelThreads) {
         const uint64_t i = base + tid;
         uint32_t key = 0;
-        if (i < nc) key = norm_key(norms[i]);
+        const uint64_t q = base / kSelThreads;
+        if (i < nc) {
+            if (cached) {
+#pragma unroll
+                for (int z = 0; z < kKeysPerThread; ++z)
+                    if (uint64_t(z) == q) key = kr[z];
+            } else {
+                key = norm_key(norms[i]);
+            }
+        }
         const uint64_t eq = (i < nc && key == T) ? 1 : 0;
         uint64_t tot;
         const uint64_t ex = block_excl_scan<uint64_t>(eq, &tot, sh.u64s);

@@ -178,8 +178,8 @@ class GradSync:
             mark("pack")
             capi.call("gf_pack", self.dtype, self.pool_ptr, self._ptrs(grad_ptrs), self._offs,
                       self._cnts, m, 1.0, stream)
-        mark("ring")
-        if self.world > 1:
+        if self.world > 1:  # a world of one has no collective (collectives.cpp:59)
+            mark("ring")
             capi.call("gf_ring_allreduce", self.comm, self.dtype, self.pool_off, self._win[0],
                       self._win[1], self._win[2], stream)
         if not ring_only:
@@ -210,8 +210,8 @@ class GradSync:
         capi.call("gf_csc_pack_correct", self.dtype, self.pool_ptr, b["hg"], self.stage_ptr,
                   b["imp"][cur], b["coff"][cur], L.total, L.chunk, L.num_chunks,
                   self._ptrs(grad_ptrs), self._offs, self._cnts, m, self.momentum, nacc, stream)
-        mark("ring")
         if self.world > 1:
+            mark("ring")
             capi.call("gf_ring_allreduce_planned", self.comm, self.dtype, self.stage_off,
                       b["plan"][cur], stream)
         # chunks selected for this iteration (iteration 0 is dense, sparse.cpp:45-51)
