@@ -387,6 +387,9 @@ int gf_sync_step_dense(gf_comm* c, int dtype, uint64_t pool_heap_off, const floa
     if (pool_heap_off + hi * es > c->heap_bytes)
         return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense: pool outside the symmetric heap");
     DeviceGuard guard(c->device);
+    if (c->world == 1)  // no collective: pack and unpack in one streaming pass
+        return gfi::pack_unpack_solo(dtype, c->alloc + kFlagBytes + pool_heap_off, src, dst, pool_off, count,
+                                     ntensors, gfi::S(stream));
     // ---- slab plan (cached per geometry) ---------------------------------------------
     static int grid = 0;
     if (grid == 0) {

@@ -20,6 +20,10 @@ void count_launch(uint64_t n = 1);
 int sm_count();              // SMs of the current device (cached per device)
 int check_launch(const char* what);  // cudaGetLastError -> status
 
+// world == 1 dense step (pack.cu): pack and unpack in one pass (the collective is the identity)
+int pack_unpack_solo(int dtype, void* pool, const float* const* src, float* const* dst,
+                     const uint64_t* pool_off, const uint64_t* count, int ntensors, cudaStream_t stream);
+
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 inline uint64_t esz(int dtype) { return dtype == GF_F32 ? 4u : 2u; }
 inline bool valid_dtype(int d) { return d == GF_F32 || d == GF_F16; }

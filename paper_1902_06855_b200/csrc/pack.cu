@@ -13,6 +13,7 @@
 // HBM roofline: 6 B/element (4 read + 2 write) for pack and unpack.
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "gf_device.cuh"
@@ -25,20 +26,49 @@ __device__ __forceinline__ float scaled(float g, float scale, bool do_scale) {
     return do_scale ? gfd::mul(g, scale) : g;
 }
 
-// ---- K1: pack -----------------------------------------------------------------
-template <int DT>
+// ---- K1: pack (and, at world == 1, K1+K6 in one pass) ------------------------------
+// Dst = NoDst: pack only. Dst = DstTable: world == 1, where the collective is the identity
+// (src/collectives.cpp:59), so g_avg = dec(enc(g)) * 1/1 is written from the registers that
+// hold the packed value: one HBM pass of 10 B/element instead of pack + unpack's 12.
+struct NoDst {};
+struct DstTable {
+    float* ptr[kMaxT];
+};
+
+__device__ __forceinline__ void store_avg8(float* o, const uint4 h, float inv) {
+    if (!gfd::any_special(h)) {
+        const float2 g0 = gfd::h2f2(h.x), g1 = gfd::h2f2(h.y), g2 = gfd::h2f2(h.z), g3 = gfd::h2f2(h.w);
+        gfd::st32f_stream(o, make_float4(__fmul_rn(g0.x, inv), __fmul_rn(g0.y, inv), __fmul_rn(g1.x, inv),
+                                         __fmul_rn(g1.y, inv)),
+                          make_float4(__fmul_rn(g2.x, inv), __fmul_rn(g2.y, inv), __fmul_rn(g3.x, inv),
+                                      __fmul_rn(g3.y, inv)));
+    } else {
+        const uint32_t w[4] = {h.x, h.y, h.z, h.w};
+        float r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = gfd::mul(gfd::dec(uint16_t((w[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu)), inv);
+        gfd::st32f_stream(o, make_float4(r[0], r[1], r[2], r[3]), make_float4(r[4], r[5], r[6], r[7]));
+    }
+}
+
+template <int DT, class Dst>
 __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ TensorTable T,
+                                                        const __grid_constant__ Dst D,
                                                         void* __restrict__ pool, float scale,
-                                                        uint64_t total_tiles) {
+                                                        float inv_world, uint64_t total_tiles) {
+    constexpr bool SOLO = std::is_same<Dst, DstTable>::value;
     const bool do_scale = scale != 1.0f;
     for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int t = find_tensor(T, tile);
         const uint64_t base = (tile - T.tiles[t]) * kTile;
         const uint64_t len = min(kTile, T.cnt[t] - base);
         const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
+        float* __restrict__ o = nullptr;
+        if constexpr (SOLO) o = D.ptr[t] + base;
         const uint64_t po = T.off[t] + base;
         const bool fast = ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0) && (po % 8 == 0) &&
-                          ((reinterpret_cast<uintptr_t>(pool) & 15u) == 0);
+                          ((reinterpret_cast<uintptr_t>(pool) & 15u) == 0) &&
+                          (!SOLO || (reinterpret_cast<uintptr_t>(o) & 31u) == 0);
         if (DT == GF_F16) {
             uint16_t* __restrict__ d = static_cast<uint16_t*>(pool) + po;
             uint64_t done = 0;
@@ -64,13 +94,21 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ 
                             b[k] = make_float4(gfd::mul(b[k].x, scale), gfd::mul(b[k].y, scale),
                                                gfd::mul(b[k].z, scale), gfd::mul(b[k].w, scale));
                         }
-                        gfd::st16_keep(d + 8 * v, gfd::enc8(a[k], b[k]));
+                        const uint4 h = gfd::enc8(a[k], b[k]);
+                        if constexpr (SOLO) {
+                            gfd::st16(d + 8 * v, h);
+                            store_avg8(o + 8 * v, h, inv_world);
+                        } else {
+                            gfd::st16_keep(d + 8 * v, h);  // the collective / unpack reads it next
+                        }
                     }
                 }
                 done = uint64_t(nvec) * 8;
             }
             for (uint64_t i = done + threadIdx.x; i < len; i += kThreads) {
-                d[i] = gfd::enc(scaled(s[i], scale, do_scale));
+                const uint16_t h = gfd::enc(scaled(s[i], scale, do_scale));
+                d[i] = h;
+                if constexpr (SOLO) o[i] = gfd::mul(gfd::dec(h), inv_world);
             }
         } else {
             float* __restrict__ d = static_cast<float*>(pool) + po;
@@ -84,11 +122,18 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ 
                         x.z = gfd::mul(x.z, scale); x.w = gfd::mul(x.w, scale);
                     }
                     *reinterpret_cast<float4*>(d + 4 * v) = x;
+                    if constexpr (SOLO) {
+                        __stcs(reinterpret_cast<float4*>(o + 4 * v),
+                               make_float4(gfd::mul(x.x, inv_world), gfd::mul(x.y, inv_world),
+                                           gfd::mul(x.z, inv_world), gfd::mul(x.w, inv_world)));
+                    }
                 }
                 done = uint64_t(nvec) * 4;
             }
             for (uint64_t i = done + threadIdx.x; i < len; i += kThreads) {
-                d[i] = scaled(s[i], scale, do_scale);
+                const float x = scaled(s[i], scale, do_scale);
+                d[i] = x;
+                if constexpr (SOLO) o[i] = gfd::mul(x, inv_world);
             }
         }
     }
@@ -244,11 +289,35 @@ int gf_pack(int dtype, void* pool, const float* const* src, const uint64_t* pool
     return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
                           [&](const TensorTable& T, uint64_t tiles, int grid) {
                               if (dtype == GF_F16)
-                                  pack_kernel<GF_F16><<<grid, kThreads, 0, gfi::S(stream)>>>(T, pool, scale, tiles);
+                                  pack_kernel<GF_F16, NoDst><<<grid, kThreads, 0, gfi::S(stream)>>>(T, NoDst{}, pool, scale, 1.0f, tiles);
                               else
-                                  pack_kernel<GF_F32><<<grid, kThreads, 0, gfi::S(stream)>>>(T, pool, scale, tiles);
+                                  pack_kernel<GF_F32, NoDst><<<grid, kThreads, 0, gfi::S(stream)>>>(T, NoDst{}, pool, scale, 1.0f, tiles);
                           });
 }
+
+}  // extern "C"
+
+namespace gfi {
+int pack_unpack_solo(int dtype, void* pool, const float* const* src, float* const* dst,
+                     const uint64_t* pool_off, const uint64_t* count, int ntensors, cudaStream_t stream) {
+    if (!valid_dtype(dtype)) return fail(GF_ERR_CONFIG, "pack_unpack: bad dtype");
+    if (!pool && ntensors > 0) return fail(GF_ERR_CONFIG, "pack_unpack: null pool");
+    for (int t = 0; t < ntensors; ++t)
+        if (count[t] && !dst[t]) return fail(GF_ERR_CONFIG, "pack_unpack: null output tensor");
+    return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
+                          [&](const TensorTable& T, uint64_t tiles, int grid, int first) {
+                              DstTable D{};
+                              for (int t = first, j = 0; j < T.n; ++t)
+                                  if (count[t]) D.ptr[j++] = dst[t];
+                              if (dtype == GF_F16)
+                                  pack_kernel<GF_F16, DstTable><<<grid, kThreads, 0, stream>>>(T, D, pool, 1.0f, 1.0f, tiles);
+                              else
+                                  pack_kernel<GF_F32, DstTable><<<grid, kThreads, 0, stream>>>(T, D, pool, 1.0f, 1.0f, tiles);
+                          });
+}
+}  // namespace gfi
+
+extern "C" {
 
 int gf_unpack(int dtype, const void* pool, float* const* dst, const uint64_t* pool_off,
               const uint64_t* count, int ntensors, int world, void* stream) {

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "gf_internal.cuh"
 
@@ -62,7 +63,10 @@ int for_each_table(const void* const* ptrs, const uint64_t* off, const uint64_t*
         T.tiles[T.n] = tiles;
         if (T.n == 0) continue;
         const int grid = int(std::min<uint64_t>(tiles, uint64_t(gfi::sm_count()) * 8));
-        launch(T, tiles, grid);
+        if constexpr (std::is_invocable_v<Launch, const TensorTable&, uint64_t, int, int>)
+            launch(T, tiles, grid, first);  // first: index of the table's first caller tensor
+        else
+            launch(T, tiles, grid);
         gfi::count_launch();
         if (int rc = gfi::check_launch("multi-tensor kernel")) return rc;
     }

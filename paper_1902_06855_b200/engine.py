@@ -174,6 +174,14 @@ class GradSync:
         L = self.layout
         m = len(L.sizes)
         mark = mark or (lambda name: None)
+        if self.world == 1 and not ring_only:
+            # no collective (collectives.cpp:59): gf_sync_step_dense packs and unpacks in one pass
+            mark("pack_unpack")
+            capi.call("gf_sync_step_dense", self.comm, self.dtype, self.pool_off, self._ptrs(grad_ptrs),
+                      self._ptrs(out_ptrs), self._offs, self._cnts, m, self._win[0], self._win[1],
+                      self._win[2], stream)
+            mark(None)
+            return
         if not ring_only:
             mark("pack")
             capi.call("gf_pack", self.dtype, self.pool_ptr, self._ptrs(grad_ptrs), self._offs,

@@ -490,3 +490,40 @@ def test_fused_step_single_rank(gf, oracle, G):
             assert (got[int(bounds[i]):int(bounds[i + 1])].view(np.uint32) ==
                     want[int(off[i]):int(off[i]) + s].view(np.uint32)).all(), (it, i)
     sync.close()
+
+
+@pytest.mark.parametrize("dtype", [F16, F32])
+@pytest.mark.parametrize("aligned", [True, False])
+def test_sync_step_world1_one_pass(gf, oracle, G, dtype, aligned):
+    """world == 1: gf_sync_step_dense packs and unpacks in ONE pass (pack_kernel<DstTable>).
+    Pool and g_avg vs the oracle, with special values; aligned=False shifts every output
+    tensor by one element so the scalar path runs too."""
+    import torch
+    from paper_1902_06855_b200 import cudart
+    from paper_1902_06855_b200.engine import GradSync
+    sizes = RESNET50[:30] + [13, 7, 40000]
+    off, _, _ = oracle.pool_layout(sizes, 32000)
+    bounds = np.concatenate([[0], np.cumsum(sizes)])
+    sync = GradSync(sizes, dtype=dtype, theta=1 << 16)
+    total = int(bounds[-1])
+    esz = 2 if dtype == F16 else 4
+    rng = np.random.default_rng(7 + dtype)
+    for it in range(2):
+        flat = G.specials(rng, total) * np.float32(8 ** it)
+        g = torch.from_numpy(flat).cuda()
+        shift = 0 if aligned else 1
+        out = torch.full((total + 1,), -1.0, device="cuda")
+        gp = [g[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
+        op = [out[shift + int(bounds[i]):shift + int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
+        sync.dense_step(gp, op)
+        torch.cuda.synchronize()
+        want_pool = oracle.pack(flat, sizes, dtype=dtype)
+        want = oracle.unpack(want_pool, 1, dtype=dtype)
+        pool = np.empty(total * esz, np.uint8)
+        cudart.memcpy(pool.ctypes.data, sync.pool_ptr, total * esz)
+        assert (pool.view(np.uint16 if dtype == F16 else np.uint32) == G.bits(want_pool)).all()
+        got = out.cpu().numpy()[shift:shift + total]
+        for i, s in enumerate(sizes):
+            assert (got[int(bounds[i]):int(bounds[i + 1])].view(np.uint32) ==
+                    want[int(off[i]):int(off[i]) + s].view(np.uint32)).all(), (it, i)
+    sync.close()
