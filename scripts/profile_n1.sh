@@ -8,4 +8,5 @@ run() {  # $1 workload  $2 kernel regex
   echo "$W rc=$?"
 }
 run resnet50-dense "pack_kernel|unpack_kernel"
+run alexnet-dense "pack_kernel|unpack_kernel"
 run alexnet-csc "pack_correct|select_kernel|compact_kernel|csc_sgd"
