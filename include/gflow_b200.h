@@ -39,6 +39,9 @@
  *                                   update read (src/trainer.cpp:297-347), fused into one kernel
  *  gf_csc_select                    select_next_important (norm allreduce + top-k) src/sparse.cpp:172-204
  *  gf_ring_traffic                  TrafficStats record_send/recv of the ring include/gflow/transport.hpp:48-91, src/collectives.cpp:69-96
+ *  gf_oracle_allreduce_ptrs         oracle_allreduce                         src/collectives.cpp:203-226
+ *  gf_broadcast_ptrs                broadcast / broadcast_on                 src/collectives.cpp:146-170, :237-242
+ *  gf_ring_reduce_ptrs              reduce / ring_reduce_on (+ hierarchical)  src/collectives.cpp:99-144, :179-201, :229-235
  */
 #ifndef GFLOW_B200_H
 #define GFLOW_B200_H
@@ -222,6 +225,12 @@ int gf_csc_select_colocated(float* const* norms, int world, const int* ring_orde
  * broadcast: every buffer = bufs[root]. */
 int gf_oracle_allreduce_ptrs(int dtype, void* const* bufs, int world, uint64_t len, void* stream);
 int gf_broadcast_ptrs(void* const* bufs, int world, int root, uint64_t bytes, void* stream);
+/* Rooted ring reduce (reduce(), collectives.cpp:99-144, 229-235), bufs in RING-POSITION
+ * order: the root position gets every full sum; position j+k keeps segment j's partial sum
+ * of positions j..j+k (the reference's reduce-scatter state), position j its raw segment j.
+ * hierarchical_allreduce (collectives.cpp:179-201) = this per group + ring allreduce over
+ * the masters + broadcast. */
+int gf_ring_reduce_ptrs(int dtype, void* const* bufs, int n, int root_pos, uint64_t len, void* stream);
 
 /* Payload bytes the reference ring records for one allreduce of len elements at ring
  * position `position` (collectives.cpp:69-96): 2(N-1) sends of segment_of sizes. */

@@ -214,6 +214,52 @@ void go_ring_allreduce(int dtype, void* const* bufs, int n, uint64_t len, const 
     go_ring_allreduce_windows(dtype, bufs, n, &s, &len, 1, ring_order);
 }
 
+/* collectives.cpp:99-144 ring_reduce_on: the RS of ring_allreduce_on, then every position
+ * but the root sends its owned segment to the root. End state: position j+k (k = 1..n-1)
+ * holds segment j's partial chain (positions j..j+k), position j keeps its raw segment j,
+ * and the root holds every full sum. bufs[t] = buffer of ring position t. */
+void go_ring_reduce(int dtype, void* const* bufs, int n, int root_pos, uint64_t len) {
+    if (n <= 1) return; /* collectives.cpp:104 */
+    for (int j = 0; j < n; ++j) {
+        uint64_t off, cnt;
+        go_segment_of(len, n, j, &off, &cnt);
+        for (uint64_t e = off; e < off + cnt; ++e) {
+            if (dtype == 1) {
+                uint16_t acc = ((const uint16_t*)bufs[j])[e];
+                for (int k = 1; k < n; ++k) {
+                    uint16_t* b = (uint16_t*)bufs[(j + k) % n];
+                    acc = acc16(b[e], acc);
+                    b[e] = acc;
+                }
+                ((uint16_t*)bufs[root_pos])[e] = acc;
+            } else {
+                float acc = ((const float*)bufs[j])[e];
+                for (int k = 1; k < n; ++k) {
+                    float* b = (float*)bufs[(j + k) % n];
+                    acc = acc32(b[e], acc);
+                    b[e] = acc;
+                }
+                ((float*)bufs[root_pos])[e] = acc;
+            }
+        }
+    }
+}
+
+/* collectives.cpp:179-201 hierarchical_allreduce: ring_reduce_on inside each group of m
+ * consecutive ranks to its master (rank g*m), ring_allreduce_on over the masters in
+ * group order, broadcast_on from each master to its group. bufs[r] = rank r. */
+void go_hier_allreduce(int dtype, void* const* bufs, int n, int m, uint64_t len) {
+    const int k = n / m;
+    const size_t es = dtype == 1 ? 2u : 4u;
+    for (int g = 0; g < k; ++g) go_ring_reduce(dtype, bufs + (size_t)g * (size_t)m, m, 0, len);
+    void** masters = (void**)malloc(sizeof(void*) * (size_t)k);
+    for (int g = 0; g < k; ++g) masters[g] = bufs[(size_t)g * (size_t)m];
+    go_ring_allreduce(dtype, masters, k, len, NULL);
+    for (int g = 0; g < k; ++g)
+        for (int r = 1; r < m; ++r) memcpy(bufs[(size_t)g * (size_t)m + (size_t)r], masters[g], len * es);
+    free(masters);
+}
+
 /* fusion.cpp:72-109: on_tensor_complete extends [start,end) to the tensor's end;
  * maybe_launch fires when pending bytes >= theta (theta != kThetaInfinite);
  * finalize flushes the residual. */

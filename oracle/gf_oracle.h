@@ -58,6 +58,12 @@ void go_ring_allreduce(int dtype, void* const* bufs, int n, uint64_t len, const 
 void go_ring_allreduce_windows(int dtype, void* const* bufs, int n, const uint64_t* wstart,
                                const uint64_t* wlen, int nwin, const int* ring_order);
 
+/* Rooted ring reduce (collectives.cpp:99-144), end state of every position; bufs[t] is
+ * ring position t's buffer. In place. */
+void go_ring_reduce(int dtype, void* const* bufs, int n, int root_pos, uint64_t len);
+/* hierarchical_allreduce (collectives.cpp:179-201) with groups of m ranks; bufs[r] = rank r. */
+void go_hier_allreduce(int dtype, void* const* bufs, int n, int m, uint64_t len);
+
 /* FusionEngine windows for one iteration (fusion.cpp:72-109): tensors complete in
  * descending id; window [start,end) launched when bytes >= theta (theta = UINT64_MAX
  * means never), residual at finalize. Returns window count; fills start/len (elements). */

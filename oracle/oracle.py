@@ -94,6 +94,8 @@ class Oracle:
             "go_unpack": [C.c_int, _vp, C.c_uint64, C.c_int, _vp],
             "go_ring_allreduce": [C.c_int, _vp, C.c_int, C.c_uint64, _vp],
             "go_ring_allreduce_windows": [C.c_int, _vp, C.c_int, _vp, _vp, C.c_int, _vp],
+            "go_ring_reduce": [C.c_int, _vp, C.c_int, C.c_int, C.c_uint64],
+            "go_hier_allreduce": [C.c_int, _vp, C.c_int, C.c_int, C.c_uint64],
             "go_chunk_norms": [C.c_int, _vp, C.c_uint64, C.c_uint64, C.c_uint64, _vp, C.c_int, _vp],
             "go_csc_correct": [C.c_int, _vp, _vp, _vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_float],
             "go_csc_scatter": [C.c_int, _vp, _vp, C.c_uint64, C.c_uint64, C.c_uint64, _vp],
@@ -174,6 +176,20 @@ class Oracle:
             ws, wl = u64(windows[0]), u64(windows[1])
             self.L.go_ring_allreduce_windows(dtype, ptr_array(bufs), n, np_ptr(ws), np_ptr(wl),
                                              len(ws), None if ro is None else np_ptr(ro))
+        return bufs
+
+    def ring_reduce(self, bufs, root, dtype=1, ring_order=None):
+        """reduce(comm, buf, root) end state (collectives.cpp:99-144, 229-235), in place on
+        per-RANK buffers; ring_order maps ring position -> rank (identity when None)."""
+        n = len(bufs)
+        ring = list(range(n)) if ring_order is None else [int(x) for x in ring_order]
+        by_pos = [bufs[ring[t]] for t in range(n)]
+        self.L.go_ring_reduce(dtype, ptr_array(by_pos), n, ring.index(root), bufs[0].size)
+        return bufs
+
+    def hier_allreduce(self, bufs, group_size, dtype=1):
+        """hierarchical_allreduce (collectives.cpp:179-201), in place on per-rank buffers."""
+        self.L.go_hier_allreduce(dtype, ptr_array(bufs), len(bufs), group_size, bufs[0].size)
         return bufs
 
     def chunk_norms(self, pool, chunk, nc, imp, world, dtype=1):
@@ -269,7 +285,7 @@ class Reference:
         L.refd_selection_count.argtypes = [C.c_double, C.c_uint64]
         L.refd_sparsity_at.restype = C.c_double
         L.refd_sparsity_at.argtypes = [C.c_uint64, C.c_uint64, C.c_double]
-        for name in ["refd_pool_layout", "refd_allreduce", "refd_dense_sync", "refd_csc_run",
+        for name in ["refd_pool_layout", "refd_allreduce", "refd_reduce", "refd_dense_sync", "refd_csc_run",
                      "refd_bench_allreduce", "refd_time_step"]:
             getattr(L, name).restype = C.c_int
         L.refd_time_step.argtypes = [C.c_int, _vp, C.c_int, C.c_uint64, C.c_int, C.c_uint64,
@@ -318,6 +334,16 @@ class Reference:
         self._check(self.L.refd_allreduce(C.c_int(n), C.c_int(dtype), C.c_uint64(bufs[0].size),
                                           ptr_array(bufs), C.c_int(algo), C.c_int(group_size),
                                           None if ro is None else np_ptr(ro), np_ptr(sent)))
+        return sent
+
+    def reduce(self, bufs, root, dtype=1, ring_order=None):
+        """The reference's reduce() with ranks as threads, in place; returns payload sent."""
+        n = len(bufs)
+        sent = np.zeros(n, np.uint64)
+        ro = None if ring_order is None else np.ascontiguousarray(ring_order, dtype=np.int32)
+        self._check(self.L.refd_reduce(C.c_int(n), C.c_int(dtype), C.c_uint64(bufs[0].size),
+                                       ptr_array(bufs), C.c_int(root),
+                                       None if ro is None else np_ptr(ro), np_ptr(sent)))
         return sent
 
     def dense_sync(self, grads, sizes, dtype=1, theta=64 << 20, chunk=32000, algo=0, group_size=1):

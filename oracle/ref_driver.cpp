@@ -174,6 +174,21 @@ int refd_allreduce(int n, int dtype, std::uint64_t len, void* const* bufs, int a
     });
 }
 
+// ---- rooted ring reduce on raw arrays (collectives.cpp:99-144, 229-235) ----------
+int refd_reduce(int n, int dtype, std::uint64_t len, void* const* bufs, int root,
+                const int* ring_order, std::uint64_t* sent_out) {
+    return guarded([&] {
+        run_world(n, [&](int r, Transport& tp) {
+            Communicator comm(tp);
+            if (ring_order) comm.set_ring_order(std::vector<int>(ring_order, ring_order + n));
+            ScalarBuffer b{dtype == 1 ? ElementType::kF16 : ElementType::kF32,
+                           static_cast<std::byte*>(bufs[r]), len};
+            reduce(comm, b, root);
+            if (sent_out) sent_out[r] = tp.stats().total().payload_bytes_sent;
+        });
+    });
+}
+
 // ---- dense lazy-allreduce step (trainer.cpp:297-347 without the model) ---------
 // grads[r]: rank r's gradients, flat in ASCENDING tensor id. Outputs (nullable):
 // pools_out[r] raw pool bytes after the fused windows, gavg_out[r] pool-ordered

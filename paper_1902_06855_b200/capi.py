@@ -101,6 +101,7 @@ SIGNATURES = {
     "gf_ring_traffic": [_u64, _i, _i, _i, _u64p, _u64p, _u64p],
     "gf_oracle_allreduce_ptrs": [_i, _vp, _i, _u64, _vp],
     "gf_broadcast_ptrs": [_vp, _i, _i, _u64, _vp],
+    "gf_ring_reduce_ptrs": [_i, _vp, _i, _i, _u64, _vp],
     "gf_abi_version": [],
     "gf_last_error": [],
     "gf_kernel_launches": [],

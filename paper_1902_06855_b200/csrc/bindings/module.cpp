@@ -343,6 +343,8 @@ PYBIND11_MODULE(gflowpy, m) {
         .def_property_readonly("ring_order", &Communicator::ring_order)
         .def("set_ring_order", &Communicator::set_ring_order)
         .def("set_device", &Communicator::set_device)
+        .def_property_readonly("group_size", &Communicator::group_size)
+        .def("phase2_segment_bytes", &Communicator::phase2_segment_bytes)
         .def("device_mode", [](Communicator& c) { return std::string(c.device().mode_name()); }, release())
         .def("device", [](Communicator& c) { return c.device().device(); }, release());
 
@@ -360,6 +362,11 @@ PYBIND11_MODULE(gflowpy, m) {
         ScalarBuffer b = as_buffer(a);
         py::gil_scoped_release nogil;
         broadcast(c, b, root);
+    }, py::arg("comm"), py::arg("buf"), py::arg("root"));
+    m.def("reduce", [](Communicator& c, py::array a, int root) {
+        ScalarBuffer b = as_buffer(a);
+        py::gil_scoped_release nogil;
+        reduce(c, b, root);
     }, py::arg("comm"), py::arg("buf"), py::arg("root"));
     m.def("hierarchical_allreduce", [](Communicator& c, py::array a) {
         ScalarBuffer b = as_buffer(a);

@@ -170,20 +170,104 @@ void broadcast(Communicator& comm, ScalarBuffer buf, int root) {
     if (hop > 0) comm.transport().stats().record_recv("bcast", buf.byte_length());
 }
 
-void reduce(Communicator& comm, ScalarBuffer buf, int root) {
-    if (root < 0 || root >= comm.world_size()) throw ConfigError("reduce root " + std::to_string(root) + " outside group");
-    throw ConfigError("reduce: rooted ring reduce is not part of the B200 hot path (SURVEY.md §8f); "
-                      "use ring_allreduce");
+namespace {
+
+// Payload of ring_reduce_on (collectives.cpp:99-144) at ring position p of n, root at rp:
+// the n-1 reduce-scatter sends, then every non-root position sends its owned segment.
+void record_ring_reduce(TrafficStats& st, const std::string& label, std::size_t len, std::size_t es, int n,
+                        int p, int rp) {
+    if (n <= 1) return;
+    auto seg = [&](int i) { return detail::segment_of(len, n, i).length * es; };
+    std::uint64_t sent = 0, recvd = 0, frames = 0;
+    for (int s = 0; s < n - 1; ++s) {
+        sent += seg((p - s + n) % n);
+        recvd += seg((p - s - 1 + n) % n);
+        ++frames;
+    }
+    const int owned = (p + 1) % n;
+    if (p != rp) {
+        sent += seg(owned);
+        ++frames;
+    } else {
+        for (int i = 0; i < n; ++i)
+            if (i != owned && (i - 1 + n) % n != rp) recvd += seg(i);
+    }
+    st.record_send(label, sent, frames);
+    st.record_recv(label, recvd);
 }
 
+int position_of(const std::vector<int>& ring, int rank) {
+    return static_cast<int>(std::find(ring.begin(), ring.end(), rank) - ring.begin());
+}
+
+}  // namespace
+
+void reduce(Communicator& comm, ScalarBuffer buf, int root) {
+    if (root < 0 || root >= comm.world_size()) throw ConfigError("reduce root " + std::to_string(root) + " outside group");
+    const int n = comm.world_size();
+    if (n == 1) return;
+    const auto ring = comm.ring_order();
+    const int rp = position_of(ring, root);
+    DeviceContext& ctx = comm.device();
+    with_device_view(ctx, buf, [&](ScalarBuffer dev) {
+        rooted(comm, dev, root, [&](std::vector<void*>& ptrs) {
+            std::vector<void*> by_pos(static_cast<std::size_t>(n));
+            for (int t = 0; t < n; ++t) by_pos[static_cast<std::size_t>(t)] = ptrs[static_cast<std::size_t>(ring[t])];
+            check(gf_ring_reduce_ptrs(static_cast<int>(dev.type), by_pos.data(), n, rp, dev.length, nullptr),
+                  "reduce");
+        });
+    });
+    record_ring_reduce(comm.transport().stats(), "reduce", buf.length, element_size(buf.type), n,
+                       position_of(ring, comm.rank()), rp);
+}
+
+// collectives.cpp:179-201: ring_reduce_on inside each group of m consecutive ranks to its
+// master, ring_allreduce_on over the masters, broadcast_on from each master. On the device
+// the root launches: the group reduces, a rooted reduce over the masters (its root holds the
+// masters' ring-allreduce sums: same chains) and one broadcast of that buffer to every rank.
 void hierarchical_allreduce(Communicator& comm, ScalarBuffer buf) {
     const int n = comm.world_size(), m = comm.group_size();
     if (m < 1 || n % m != 0) {
         throw ConfigError("group size " + std::to_string(m) + " must divide world " + std::to_string(n));
     }
-    (void)buf;
-    throw ConfigError("hierarchical_allreduce: not on the B200 path — one NVSwitch domain gives every "
-                      "GPU full bandwidth to every peer (SURVEY.md §8f); use Algo::kRing");
+    if (n == 1) return;
+    const int k = n / m;
+    DeviceContext& ctx = comm.device();
+    with_device_view(ctx, buf, [&](ScalarBuffer dev) {
+        rooted(comm, dev, 0, [&](std::vector<void*>& ptrs) {
+            const int dt = static_cast<int>(dev.type);
+            if (m > 1)
+                for (int g = 0; g < k; ++g)
+                    check(gf_ring_reduce_ptrs(dt, ptrs.data() + static_cast<std::size_t>(g) * m, m, 0, dev.length,
+                                              nullptr),
+                          "hierarchical_allreduce (groups)");
+            if (k > 1) {
+                std::vector<void*> masters;
+                for (int g = 0; g < k; ++g) masters.push_back(ptrs[static_cast<std::size_t>(g) * m]);
+                check(gf_ring_reduce_ptrs(dt, masters.data(), k, 0, dev.length, nullptr),
+                      "hierarchical_allreduce (masters)");
+            }
+            check(gf_broadcast_ptrs(ptrs.data(), n, 0, dev.byte_length(), nullptr), "hierarchical_allreduce (bcast)");
+        });
+    });
+    // payload of the three phases as the reference moves it (labels hier1/hier2/hier3)
+    auto& st = comm.transport().stats();
+    const std::size_t es = element_size(buf.type), len = buf.length;
+    const int g = comm.rank() / m, q = comm.rank() % m;
+    record_ring_reduce(st, "hier1", len, es, m, q, 0);
+    if (q == 0 && k > 1) {
+        std::uint64_t sent = 0, recvd = 0, frames = 0;
+        check(gf_ring_traffic(len, k, g, static_cast<int>(buf.type), &sent, &recvd, &frames), "traffic");
+        st.record_send("hier2", sent, frames);
+        st.record_recv("hier2", recvd);
+        auto seg = [&](int i) { return detail::segment_of(len, k, i).length * es; };
+        for (int s = 0; s < k - 1; ++s) comm.log_phase2_segment(seg((g - s + k) % k));      // RS sends
+        for (int s = 0; s < k - 1; ++s) comm.log_phase2_segment(seg((g + 1 - s + k) % k));  // AG sends
+    }
+    if (m > 1) {
+        if (q < m - 1) st.record_send("hier3", buf.byte_length(), 1);
+        if (q > 0) st.record_recv("hier3", buf.byte_length());
+    }
 }
 
 }  // namespace gflow

@@ -401,6 +401,34 @@ __global__ void oracle_sum_kernel(char* const* __restrict__ bufs_in, int world, 
         }
     }
 }
+// ring_reduce_on (collectives.cpp:99-144) end state, one pass over every position's buffer
+// (bufs in ring-position order): segment j's chain starts raw at position j; position j+k
+// keeps the partial sum of positions j..j+k (what its RS step left), the root every full sum.
+template <int DT>
+__global__ void ring_reduce_kernel(char* const* __restrict__ bufs, int n, int root, uint64_t len) {
+    const uint64_t base = len / uint64_t(n), rem = len % uint64_t(n), big = rem * (base + 1);
+    for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < len;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const int j = int(e < big ? e / (base + 1) : rem + (e - big) / base);
+        if (DT == GF_F16) {
+            uint16_t acc = reinterpret_cast<const uint16_t*>(bufs[j])[e];
+            for (int k = 1; k < n; ++k) {
+                uint16_t* b = reinterpret_cast<uint16_t*>(bufs[(j + k) % n]);
+                acc = gfd::acc16(b[e], acc);
+                b[e] = acc;
+            }
+            reinterpret_cast<uint16_t*>(bufs[root])[e] = acc;
+        } else {
+            float acc = reinterpret_cast<const float*>(bufs[j])[e];
+            for (int k = 1; k < n; ++k) {
+                float* b = reinterpret_cast<float*>(bufs[(j + k) % n]);
+                acc = gfd::add(b[e], acc);
+                b[e] = acc;
+            }
+            reinterpret_cast<float*>(bufs[root])[e] = acc;
+        }
+    }
+}
 __global__ void bcast_kernel(char* const* __restrict__ bufs_in, int world, int root, uint64_t bytes) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < bytes;
          i += uint64_t(gridDim.x) * blockDim.x) {
@@ -426,6 +454,23 @@ int gf_oracle_allreduce_ptrs(int dtype, void* const* bufs, int world, uint64_t l
         oracle_sum_kernel<GF_F32><<<grid_for(len, 256), 256, 0, gfi::S(stream)>>>(dptrs, world, len);
     gfi::count_launch();
     const int rc = gfi::check_launch("gf_oracle_allreduce_ptrs");
+    cudaFreeAsync(dptrs, gfi::S(stream));
+    return rc;
+}
+
+int gf_ring_reduce_ptrs(int dtype, void* const* bufs, int n, int root_pos, uint64_t len, void* stream) {
+    if (!gfi::valid_dtype(dtype) || !bufs || n < 1 || n > GF_MAX_RANKS || root_pos < 0 || root_pos >= n)
+        return gfi::fail(GF_ERR_CONFIG, "gf_ring_reduce_ptrs: bad arguments");
+    if (n == 1 || len == 0) return GF_OK;
+    char** dptrs = nullptr;
+    GF_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dptrs), sizeof(char*) * n, gfi::S(stream)));
+    GF_CHECK_CUDA(cudaMemcpyAsync(dptrs, bufs, sizeof(char*) * n, cudaMemcpyHostToDevice, gfi::S(stream)));
+    if (dtype == GF_F16)
+        ring_reduce_kernel<GF_F16><<<grid_for(len, 256), 256, 0, gfi::S(stream)>>>(dptrs, n, root_pos, len);
+    else
+        ring_reduce_kernel<GF_F32><<<grid_for(len, 256), 256, 0, gfi::S(stream)>>>(dptrs, n, root_pos, len);
+    gfi::count_launch();
+    const int rc = gfi::check_launch("gf_ring_reduce_ptrs");
     cudaFreeAsync(dptrs, gfi::S(stream));
     return rc;
 }

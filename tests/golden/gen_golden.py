@@ -163,8 +163,49 @@ def train_runs(ref: Reference, out):
     out["cases_json"] = np.array(json.dumps(TRAIN_CASES))
 
 
+REDUCE_CASES = [  # (n, dtype, len, root, ring_order or None)
+    (2, 0, 37, 0, None), (2, 1, 1000, 1, None), (3, 0, 1001, 2, None), (4, 1, 4099, 1, [2, 0, 3, 1]),
+    (5, 1, 3, 4, None), (8, 0, 777, 5, [7, 6, 5, 4, 3, 2, 1, 0]), (8, 1, 8192, 0, None),
+]
+HIER_CASES = [  # (n, group_size, dtype, len)
+    (4, 2, 0, 1000), (4, 2, 1, 4099), (6, 3, 1, 777), (6, 2, 0, 9), (8, 2, 0, 16384), (8, 4, 1, 5000),
+    (4, 1, 1, 100), (4, 4, 0, 100),
+]
+
+
+def rooted(ref: Reference, out):
+    """reduce() end states of every rank and hierarchical_allreduce results + payloads."""
+    rng = np.random.default_rng(21)
+
+    def inputs(n, dt, length):
+        xs = [specials(rng, length) * np.float32(4.0) for _ in range(n)]
+        return [ref.f2h(x) if dt == 1 else x for x in xs]
+
+    for i, (n, dt, length, root, ring) in enumerate(REDUCE_CASES):
+        bufs = inputs(n, dt, length)
+        out[f"r{i}_in"] = np.stack(bufs)
+        work = [b.copy() for b in bufs]
+        out[f"r{i}_sent"] = ref.reduce(work, root, dtype=dt, ring_order=ring)
+        out[f"r{i}_out"] = np.stack(work)
+    for i, (n, m, dt, length) in enumerate(HIER_CASES):
+        bufs = inputs(n, dt, length)
+        out[f"h{i}_in"] = np.stack(bufs)
+        work = [b.copy() for b in bufs]
+        out[f"h{i}_sent"] = ref.allreduce(work, dtype=dt, algo=1, group_size=m)
+        out[f"h{i}_out"] = np.stack(work)
+    out["cases_json"] = np.array(json.dumps({"reduce": REDUCE_CASES, "hier": HIER_CASES}))
+
+
 def main():
     ref = Reference()
+    only = set(sys.argv[1:])
+    if only:  # e.g. `gen_golden.py rooted`: regenerate just those fixtures
+        if "rooted" in only:
+            r: dict = {}
+            rooted(ref, r)
+            np.savez_compressed(os.path.join(HERE, "rooted.npz"), **r)
+            print("rooted.npz", os.path.getsize(os.path.join(HERE, "rooted.npz")))
+        return
     out: dict = {}
     codec(ref, out)
     layouts(ref, out)
@@ -179,7 +220,10 @@ def main():
     t: dict = {}
     train_runs(ref, t)
     np.savez_compressed(os.path.join(HERE, "train.npz"), **t)
-    for f in ("codec_layout.npz", "dense_sync.npz", "csc_run.npz", "train.npz"):
+    r: dict = {}
+    rooted(ref, r)
+    np.savez_compressed(os.path.join(HERE, "rooted.npz"), **r)
+    for f in ("codec_layout.npz", "dense_sync.npz", "csc_run.npz", "train.npz", "rooted.npz"):
         print(f, os.path.getsize(os.path.join(HERE, f)))
 
 

@@ -207,3 +207,22 @@ def test_nan_propagation_vs_live_reference(oracle, reference):
             reference.allreduce(b, dtype=dt)
             for r in range(n):
                 assert (bits(a[r]) == bits(b[r])).all()
+
+
+# ---- rooted collectives: reduce() and hierarchical_allreduce() ---------------------------
+def test_rooted_golden(oracle, golden):
+    """Oracle restatement vs the reference's reduce() end state on EVERY rank (the root's
+    sums and the reduce-scatter partials elsewhere) and its hierarchical_allreduce."""
+    import json
+    g = golden("rooted.npz")
+    cases = json.loads(str(g["cases_json"]))
+    for i, (n, dt, length, root, ring) in enumerate(cases["reduce"]):
+        bufs = [x.copy() for x in g[f"r{i}_in"]]
+        oracle.ring_reduce(bufs, root, dtype=dt, ring_order=ring)
+        for r in range(n):
+            assert (bits(bufs[r]) == bits(g[f"r{i}_out"][r])).all(), (i, r)
+    for i, (n, m, dt, length) in enumerate(cases["hier"]):
+        bufs = [x.copy() for x in g[f"h{i}_in"]]
+        oracle.hier_allreduce(bufs, m, dtype=dt)
+        for r in range(n):
+            assert (bits(bufs[r]) == bits(g[f"h{i}_out"][r])).all(), (i, r)
