@@ -446,28 +446,59 @@ def main():
     # ---- end-to-end through the C-ABI with host buffers ---------------------------------------
     e2e = None
     if not args.no_e2e:
-        h_in = torch.empty(total, dtype=torch.float32, pin_memory=True)
-        h_in.copy_(inputs[0].cpu())
-        h_out = torch.empty(total, dtype=torch.float32, pin_memory=True)
-        res_dev = outs[0] if not csc else w
+        # Every step: H2D of the step's gradients from pinned host memory, the sync step
+        # through the C-ABI, D2H of its result (g_avg, or the updated weights for CSC).
+        # Double-buffered on three streams, as a training loop would run it: the H2D of
+        # step i+1 overlaps the D2H of step i (PCIe is full duplex); a step starts once its
+        # input landed and the previous result left the device (CSC updates w in place).
+        h_in = [torch.empty(total, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        for h in h_in:
+            h.copy_(inputs[0].cpu())
+        h_out = [torch.empty(total, dtype=torch.float32, pin_memory=True) for _ in range(2)]
         d2h = total * 4
-        for i in range(2):
-            inputs[0].copy_(h_in, non_blocking=True)
-            step(0)
-            h_out.copy_(res_dev, non_blocking=True)
+        s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+        def result(slot):
+            return outs[slot] if not csc else w
+
+        def run_e2e(k):
+            ev_in = [torch.cuda.Event() for _ in range(k)]
+            ev_comp = [torch.cuda.Event() for _ in range(k)]
+            ev_out = [torch.cuda.Event() for _ in range(k)]
+            for i in range(k):
+                slot = i % 2
+                if i >= 2:
+                    s_in.wait_event(ev_comp[i - 2])  # step i-2 finished reading this input slot
+                with torch.cuda.stream(s_in):
+                    inputs[slot].copy_(h_in[slot], non_blocking=True)
+                ev_in[i].record(s_in)
+                stream.wait_event(ev_in[i])
+                if i >= 1:
+                    stream.wait_event(ev_out[i - 1])
+                step(slot)
+                ev_comp[i].record(stream)
+                s_out.wait_event(ev_comp[i])
+                with torch.cuda.stream(s_out):
+                    h_out[slot].copy_(result(slot), non_blocking=True)
+                ev_out[i].record(s_out)
+            return ev_out[-1]
+
+        run_e2e(3)
+        torch.cuda.synchronize()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(args.steps):
-            inputs[0].copy_(h_in, non_blocking=True)
-            step(0)
-            h_out.copy_(res_dev, non_blocking=True)
-        e1.record(stream)
+        e0.record(s_in)
+        stream.wait_event(e0)
+        last = run_e2e(args.steps)
+        s_out.wait_event(last)
+        e1.record(s_out)
         torch.cuda.synchronize()
         ems = allmax(e0.elapsed_time(e1) / max(args.steps, 1))
         e2e = {"value": round(ems, 4), "unit": "ms", "h2d_bytes_per_step": total * 4,
-               "d2h_bytes_per_step": d2h, "path": "C-ABI gf_* with pinned host grads in / results out"}
+               "d2h_bytes_per_step": d2h,
+               "path": "C-ABI gf_* with pinned host grads in / results out, double-buffered: "
+                       "H2D of step i+1 overlaps D2H of step i"}
     sync.status()
 
     clk = clocks.stop()
