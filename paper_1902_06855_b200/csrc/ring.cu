@@ -268,8 +268,15 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
         // segment index of element i under segment_of(nc, n, .) (collectives.cpp:47-53)
         const uint64_t big = rem * (base + 1);
         const int j = int(i < big ? i / (base + 1) : rem + (i - big) / base);
-        float acc = a.norms[a.ring[j]][i];
-        for (int t = 1; t < n; ++t) acc = gfd::add(a.norms[a.ring[(j + t) % n]][i], acc);
+        // issue every rank's load before the first add: one NVLink round trip, not n
+        float v[GF_MAX_RANKS];
+#pragma unroll
+        for (int t = 0; t < GF_MAX_RANKS; ++t)
+            if (t < n) v[t] = a.norms[a.ring[(j + t) % n]][i];
+        float acc = v[0];
+#pragma unroll
+        for (int t = 1; t < GF_MAX_RANKS; ++t)
+            if (t < n) acc = gfd::add(v[t], acc);
         red[i] = acc;
     }
     if (a.p2p) {
