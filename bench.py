@@ -276,7 +276,7 @@ def main():
         return mark
 
     def step(i, record=False):
-        m = mark_factory(record)
+        m = mark_factory(record) if record else None  # None: the production schedule
         if csc:
             sync.csc_step(in_ptrs[i % n_sets], stream=sp, mark=m)
         else:

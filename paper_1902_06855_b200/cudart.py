@@ -35,6 +35,10 @@ def rt():
         _rt.cudaSetDevice.argtypes = [C.c_int]
         _rt.cudaHostRegister.argtypes = [C.c_void_p, C.c_size_t, C.c_uint]
         _rt.cudaHostUnregister.argtypes = [C.c_void_p]
+        _rt.cudaStreamCreateWithFlags.argtypes = [C.POINTER(C.c_void_p), C.c_uint]
+        _rt.cudaEventCreateWithFlags.argtypes = [C.POINTER(C.c_void_p), C.c_uint]
+        _rt.cudaEventRecord.argtypes = [C.c_void_p, C.c_void_p]
+        _rt.cudaStreamWaitEvent.argtypes = [C.c_void_p, C.c_void_p, C.c_uint]
     return _rt
 
 
@@ -51,6 +55,27 @@ def memcpy(dst: int, src: int, nbytes: int, stream: int | None = None) -> None:
 def memset(dst: int, value: int, nbytes: int, stream: int | None = None) -> None:
     _chk(rt().cudaMemsetAsync(C.c_void_p(dst), value, nbytes, C.c_void_p(stream or 0)),
          "cudaMemsetAsync")
+
+
+def stream_create() -> int:
+    """A non-blocking stream on the current device (never destroyed: engine lifetime)."""
+    h = C.c_void_p()
+    _chk(rt().cudaStreamCreateWithFlags(C.byref(h), 1), "cudaStreamCreateWithFlags")
+    return h.value
+
+
+def event_create() -> int:
+    h = C.c_void_p()
+    _chk(rt().cudaEventCreateWithFlags(C.byref(h), 2), "cudaEventCreateWithFlags")  # no timing
+    return h.value
+
+
+def event_record(ev: int, stream: int | None) -> None:
+    _chk(rt().cudaEventRecord(C.c_void_p(ev), C.c_void_p(stream or 0)), "cudaEventRecord")
+
+
+def stream_wait(stream: int | None, ev: int) -> None:
+    _chk(rt().cudaStreamWaitEvent(C.c_void_p(stream or 0), C.c_void_p(ev), 0), "cudaStreamWaitEvent")
 
 
 def sync_device() -> None:

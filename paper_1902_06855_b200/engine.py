@@ -25,7 +25,7 @@ import ctypes as C
 import math
 from dataclasses import dataclass
 
-from . import capi
+from . import capi, cudart
 
 F32, F16 = capi.GF_F32, capi.GF_F16
 THETA_INF = capi.THETA_INF
@@ -144,6 +144,7 @@ class GradSync:
         self._cnts = capi.u64_array(L.sizes)
         self.iteration = 0
         self._csc_bufs = None
+        self._side = None  # (stream, event, event) for the CSC update beside the selection
 
     # ---- state for CSC (allocated by the caller's allocator: torch or cudaMalloc) -------
     def attach_csc_state(self, hg, imp, coff, plan, hu, w, nacc=None):
@@ -212,6 +213,7 @@ class GradSync:
         L = self.layout
         m = len(L.sizes)
         cur, nxt = self.iteration & 1, (self.iteration + 1) & 1
+        marked = mark is not None
         mark = mark or (lambda name: None)
         mark("pack_correct")
         nacc = b["nacc"]
@@ -232,17 +234,44 @@ class GradSync:
             mark("norms")
             capi.call("gf_chunk_norms", self.dtype, self.pool_ptr, L.total, L.chunk, L.num_chunks,
                       b["imp"][cur], self.world, self.norms_ptr, stream)
-        mark("select")
         k = selection_count(sparsity_at(self.iteration + 1, self.warmup_iters,
                                         self.final_sparsity), L.num_chunks)
-        capi.call("gf_csc_select", self.comm, self.norms_off, L.num_chunks, k, b["imp"][nxt],
-                  L.total, L.chunk, self.dtype, self.theta, b["coff"][nxt], b["plan"][nxt],
-                  nacc, self.pool_ptr if nacc else None, b["imp"][cur] if nacc else None, stream)
-        mark("sgd_update")
-        capi.call("gf_csc_sgd_update", self.dtype, self.pool_ptr, b["plan"][cur], L.total, L.chunk,
-                  L.num_chunks, k_cur, self.world, self.momentum, self.lr, b["hu"], b["w"], stream)
+
+        def select():
+            capi.call("gf_csc_select", self.comm, self.norms_off, L.num_chunks, k, b["imp"][nxt],
+                      L.total, L.chunk, self.dtype, self.theta, b["coff"][nxt], b["plan"][nxt],
+                      nacc, self.pool_ptr if nacc else None, b["imp"][cur] if nacc else None, stream)
+
+        def update(s):
+            capi.call("gf_csc_sgd_update", self.dtype, self.pool_ptr, b["plan"][cur], L.total,
+                      L.chunk, L.num_chunks, k_cur, self.world, self.momentum, self.lr, b["hu"],
+                      b["w"], s)
+
+        if marked:  # per-kernel timing: one stream, kernels in order
+            mark("select")
+            select()
+            mark("sgd_update")
+            update(stream)
+        else:
+            # The update reads this iteration's pool and plan; the selection reads the
+            # pool and writes the NEXT plan and norms: independent. The one-CTA, latency-bound
+            # selection runs beside the bandwidth-bound update on a second stream; the step
+            # ends when both did (the next pack_correct overwrites the pool).
+            side, ev_a, ev_b = self._side_stream()
+            cudart.event_record(ev_a, stream)
+            cudart.stream_wait(side, ev_a)
+            update(side)
+            cudart.event_record(ev_b, side)
+            select()
+            cudart.stream_wait(stream, ev_b)
         mark(None)
         self.iteration += 1
+
+    def _side_stream(self):
+        if self._side is None:
+            cudart.set_device(self.device)
+            self._side = (cudart.stream_create(), cudart.event_create(), cudart.event_create())
+        return self._side
 
     def status(self):
         capi.call("gf_comm_status", self.comm)

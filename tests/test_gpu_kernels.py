@@ -527,3 +527,53 @@ def test_sync_step_world1_one_pass(gf, oracle, G, dtype, aligned):
             assert (got[int(bounds[i]):int(bounds[i + 1])].view(np.uint32) ==
                     want[int(off[i]):int(off[i]) + s].view(np.uint32)).all(), (it, i)
     sync.close()
+
+
+@pytest.mark.parametrize("dtype", [F16, F32])
+@pytest.mark.parametrize("theta", [400, THETA_INF])
+def test_engine_csc_world1_vs_oracle(gf, oracle, G, dtype, theta):
+    """GradSync.csc_step at world 1 (the bench's N=1 CSC path: pack_correct, scatter,
+    select beside the update on a second stream) over 5 iterations vs the oracle."""
+    import torch
+    from paper_1902_06855_b200 import cudart
+    from paper_1902_06855_b200.engine import GradSync
+    sizes, chunk = [300, 50, 1000, 7, 4000], 100
+    total = sum(sizes)
+    sync = GradSync(sizes, dtype=dtype, theta=theta, chunk=chunk, csc=True, final_sparsity=0.75,
+                    warmup_iters=2, momentum=0.9, lr=0.01)
+    nc = sync.layout.num_chunks
+    hg = torch.zeros(total, device="cuda")
+    imp = [torch.ones(nc, dtype=torch.uint8, device="cuda"), torch.zeros(nc, dtype=torch.uint8, device="cuda")]
+    coff = [torch.zeros(nc, dtype=torch.int64, device="cuda") for _ in range(2)]
+    plan = [torch.zeros(4 + nc, dtype=torch.int64, device="cuda") for _ in range(2)]
+    rng = np.random.default_rng(5 + dtype)
+    w0 = rng.uniform(-1, 1, total).astype(np.float32)
+    hu, w = torch.zeros(total, device="cuda"), torch.from_numpy(w0.copy()).cuda()
+    nacc = torch.zeros(nc, dtype=torch.int64, device="cuda")
+    sync.attach_csc_state(hg.data_ptr(), [t.data_ptr() for t in imp], [t.data_ptr() for t in coff],
+                          [t.data_ptr() for t in plan], hu.data_ptr(), w.data_ptr(), nacc=nacc.data_ptr())
+    sync.init_csc_plan()
+    bounds = np.concatenate([[0], np.cumsum(sizes)])
+    o_hg, o_hu, o_w = [np.zeros(total, np.float32)], np.zeros(total, np.float32), w0.copy()
+    o_imp = np.ones(nc, np.uint8)
+    esz = 2 if dtype == F16 else 4
+    for t in range(5):
+        x = G.specials(rng, total, nan=False) * np.float32(rng.uniform(0.1, 3))
+        xd = torch.from_numpy(x).cuda()
+        sync.csc_step([xd[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))])
+        torch.cuda.synchronize()
+        k = oracle.selection_count(oracle.sparsity_at(t + 1, 2, 0.75), nc)
+        pools, _, nxt, _ = oracle.csc_iteration([x], sizes, chunk, theta, np.float32(0.9), o_imp, k, o_hg,
+                                                dtype=dtype)
+        oracle.csc_sgd_update(pools[0], o_imp, chunk, 1, np.float32(0.9), np.float32(0.01), o_hu, o_w,
+                              dtype=dtype)
+        pool = np.empty(total * esz, np.uint8)
+        cudart.memcpy(pool.ctypes.data, sync.pool_ptr, pool.nbytes)
+        cudart.sync_device()
+        assert (pool == pools[0].view(np.uint8)).all(), t
+        assert (G.bits(hg.cpu().numpy()) == G.bits(o_hg[0])).all(), t
+        assert (imp[(t + 1) & 1].cpu().numpy() == nxt).all(), t
+        assert (G.bits(hu.cpu().numpy()) == G.bits(o_hu)).all(), t
+        assert (G.bits(w.cpu().numpy()) == G.bits(o_w)).all(), t
+        o_imp = nxt
+    sync.close()

@@ -269,3 +269,74 @@ def _worker_fused(rank, world, port):
 @pytest.mark.multigpu(2)
 def test_p2p_fused_step_bit_exact():
     _spawn(_worker_fused, _world())
+
+
+def _worker_engine_csc(rank, world, port):
+    """GradSync.csc_step — the bench's engine path, with the update running beside the
+    selection on a second stream — over the reference's own multi-step CSC runs
+    (tests/golden/csc_run.npz cases with this world size): hg, the exchanged pool, the next
+    important set, hu and w after every iteration, bit for bit."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    from paper_1902_06855_b200 import cudart
+    from paper_1902_06855_b200.engine import GradSync
+    torch.cuda.set_device(rank)
+    cudart.set_device(rank)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+
+    def ag(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "csc_run.npz"))
+    ran = 0
+    for ci in range(int(g["csc_cases"][0])):
+        p = f"c{ci}_"
+        n, dt, theta, chunk, T = (int(x) for x in g[p + "meta"])
+        if n != world:
+            continue
+        ran += 1
+        sizes = [int(x) for x in g[p + "sizes"]]
+        total = sum(sizes)
+        sync = GradSync(sizes, rank=rank, world=world, device=rank, dtype=dt, theta=theta, chunk=chunk,
+                        csc=True, final_sparsity=0.75, warmup_iters=2, momentum=0.9, lr=0.01,
+                        allgather=ag)
+        nc = sync.layout.num_chunks
+        dev = torch.device("cuda", rank)
+        hg = torch.zeros(total, device=dev)
+        imp = [torch.ones(nc, dtype=torch.uint8, device=dev), torch.zeros(nc, dtype=torch.uint8, device=dev)]
+        coff = [torch.zeros(nc, dtype=torch.int64, device=dev) for _ in range(2)]
+        plan = [torch.zeros(4 + nc, dtype=torch.int64, device=dev) for _ in range(2)]
+        hu = torch.zeros(total, device=dev)
+        w = torch.from_numpy(g[p + "w0"]).to(dev)
+        nacc = torch.zeros(nc, dtype=torch.int64, device=dev)
+        sync.attach_csc_state(hg.data_ptr(), [t.data_ptr() for t in imp], [t.data_ptr() for t in coff],
+                              [t.data_ptr() for t in plan], hu.data_ptr(), w.data_ptr(), nacc=nacc.data_ptr())
+        sync.init_csc_plan()
+        bounds = np.concatenate([[0], np.cumsum(sizes)])
+        esz = 2 if dt == F16 else 4
+        for t in range(T):
+            x = torch.from_numpy(np.ascontiguousarray(g[p + "grads"][t][rank])).to(dev)
+            sync.csc_step([x[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))])
+            torch.cuda.synchronize()
+            sync.status()
+            pool = np.empty(total * esz, np.uint8)
+            cudart.memcpy(pool.ctypes.data, sync.pool_ptr, pool.nbytes)
+            cudart.sync_device()
+            want_pool = np.ascontiguousarray(g[p + "pool_x"][t][rank])
+            assert (pool == want_pool.view(np.uint8)).all(), (ci, t)
+            assert (hg.cpu().numpy().view(np.uint32) == g[p + "hg"][t][rank].view(np.uint32)).all(), (ci, t)
+            assert (imp[(t + 1) & 1].cpu().numpy() == g[p + "next_imp"][t][rank]).all(), (ci, t)
+            assert (hu.cpu().numpy().view(np.uint32) == g[p + "hu"][t][rank].view(np.uint32)).all(), (ci, t)
+            assert (w.cpu().numpy().view(np.uint32) == g[p + "w"][t][rank].view(np.uint32)).all(), (ci, t)
+        sync.close()
+    assert ran > 0 or world not in (2, 4)
+    dist.barrier()
+
+
+@pytest.mark.multigpu(2)
+def test_p2p_engine_csc_vs_reference_golden():
+    _spawn(_worker_engine_csc, _world())
