@@ -193,6 +193,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--trace", action="store_true", help="report ring CTA-0 timestamps (diagnostic)")
     ap.add_argument("--ring-only", action="store_true", help="diagnostic: time the collective alone")
+    ap.add_argument("--overlap", type=float, default=0.0, metavar="BACKWARD_MS",
+                    help="also measure the dense sync overlapped with a synthetic backward of "
+                         "this many ms (bf16 GEMMs; tensors complete in descending id, theta "
+                         "windows launch as they close: the reference's lazy allreduce)")
     ap.add_argument("--fused", action="store_true",
                     help="dense: one fused pack+ring+unpack kernel per step (gf_sync_step_dense)")
     args = ap.parse_args()
@@ -426,6 +430,63 @@ def main():
         dist.all_gather_object(per_rank, [round(m, 2) for m in med])
         ring_trace["per_rank_entry_body_exit_us"] = per_rank
 
+    # ---- overlap with backward (fusion.cpp:72-123) -----------------------------
+    overlap = None
+    if args.overlap > 0 and not csc:
+        A = torch.randn(2048, 4096, dtype=torch.bfloat16, device=dev)
+        B = torch.randn(4096, 4096, dtype=torch.bfloat16, device=dev)
+        Cm = torch.empty(2048, 4096, dtype=torch.bfloat16, device=dev)
+        for _ in range(20):
+            torch.matmul(A, B, out=Cm)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(50):
+            torch.matmul(A, B, out=Cm)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        gemm_ms = e0.elapsed_time(e1) / 50
+        n_gemm = max(1, round(args.overlap / gemm_ms))
+        # backward work of tensor id is proportional to its size (tiny BN tensors: none)
+        reps = {tid: int(round(n_gemm * sizes[tid - 1] / total)) for tid in range(1, len(sizes) + 1)}
+
+        def backward(i, with_sync):
+            if with_sync:
+                sync.begin_iteration(in_ptrs[i % n_sets], out_ptrs[i % 2], stream=sp)
+            for tid in range(len(sizes), 0, -1):
+                for _ in range(reps[tid]):
+                    torch.matmul(A, B, out=Cm)
+                if with_sync:
+                    sync.tensor_complete(tid)
+            if with_sync:
+                sync.finalize_iteration()
+
+        host = {}
+
+        def timed(with_sync):
+            for i in range(3):
+                backward(i, with_sync)
+            barrier()
+            e0.record(stream)
+            h0 = time.perf_counter()
+            for i in range(args.steps):
+                backward(i, with_sync)
+            host[with_sync] = (time.perf_counter() - h0) * 1e3 / max(args.steps, 1)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            return allmax(e0.elapsed_time(e1) / max(args.steps, 1))
+
+        bw = timed(False)
+        both = timed(True)
+        sync.status()
+        overlap = {"backward_ms": round(bw, 4), "backward_plus_sync_ms": round(both, 4),
+                   "exposed_sync_ms": round(both - bw, 4), "sync_alone_ms": round(ms, 4),
+                   "windows": len(wlen), "theta_bytes": "inf" if wl["theta"] == THETA_INF else wl["theta"],
+                   "host_enqueue_ms": {"backward": round(host[False], 4), "backward_plus_sync": round(host[True], 4)},
+                   "backward": f"{sum(reps.values())} bf16 GEMMs 2048x4096x4096 per step, by tensor size"}
+
     # ---- NCCL allreduce on the same fp16 volume (comparison only) ---------------------------
     nccl = None
     if world > 1:
@@ -531,7 +592,7 @@ def main():
                                                    f"(> 126 MB L2)"),
             "bus_gbs": bus, "kernels": kernels, "kernel_timing": kernel_timing, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "nccl_allreduce": nccl, "gpu_launches": int(launches), "clocks": clk,
-            "ring_trace": ring_trace, "host_enqueue_ms_per_step": round(host_enqueue_ms, 4),
+            "ring_trace": ring_trace, "overlap": overlap, "host_enqueue_ms_per_step": round(host_enqueue_ms, 4),
         }
         print(json.dumps(line), flush=True)
     sync.close()

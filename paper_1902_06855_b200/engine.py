@@ -145,6 +145,8 @@ class GradSync:
         self.iteration = 0
         self._csc_bufs = None
         self._side = None  # (stream, event, event) for the CSC update beside the selection
+        self._comm_s = None  # (stream, event, event) of the overlapped dense iteration
+        self._ov = None
 
     # ---- state for CSC (allocated by the caller's allocator: torch or cudaMalloc) -------
     def attach_csc_state(self, hg, imp, coff, plan, hu, w, nacc=None):
@@ -206,6 +208,76 @@ class GradSync:
                   self._ptrs(out_ptrs), self._offs, self._cnts, len(self.layout.sizes),
                   self._win[0], self._win[1], self._win[2], stream)
         mark(None)
+
+    # ---- overlap with backward: FusionEngine on device streams (fusion.cpp:25-123) --------
+    def begin_iteration(self, grad_ptrs, out_ptrs, stream=None):
+        """Start a dense iteration whose tensors become final one by one (descending id)
+        while the caller's backward is still running on `stream`. Each theta window is
+        packed, ring-reduced and unpacked on a communication stream as soon as it closes
+        (maybe_launch, fusion.cpp:72-99), FIFO like the reference's progress thread."""
+        if self.dtype not in (F16, F32):
+            raise capi.ConfigError("bad dtype")
+        self._ov = dict(grad=list(grad_ptrs), out=list(out_ptrs), stream=stream, ws=0, we=0,
+                        ids=[], launched=0)
+
+    def tensor_complete(self, tid):
+        """FusionEngine::on_tensor_complete(tid) (fusion.cpp:72-99); tid is 1-based and
+        tensors complete in descending id order (the pool's ascending offsets)."""
+        ov = self._ov
+        L = self.layout
+        if ov is None:
+            raise capi.ConfigError("tensor_complete before begin_iteration")
+        expect = len(L.sizes) - len(ov["ids"]) - ov["launched"]
+        if tid != expect:
+            raise capi.ConfigError(f"tensor {tid} completed out of order (expected {expect})")
+        ov["ids"].append(tid)
+        ov["we"] = L.offsets[tid - 1] + L.sizes[tid - 1]
+        if self.theta != THETA_INF and (ov["we"] - ov["ws"]) * self.esz >= self.theta:
+            self._launch_window()
+
+    def finalize_iteration(self):
+        """finalize_iteration + wait_all (fusion.cpp:101-123): flush the last window and make
+        the caller's stream wait for every window's g_avg."""
+        ov = self._ov
+        if ov is None:
+            raise capi.ConfigError("finalize_iteration before begin_iteration")
+        if ov["we"] > ov["ws"]:
+            self._launch_window()
+        if ov["launched"] != len(self.layout.sizes):
+            raise capi.ConfigError("finalize_iteration before every tensor completed")
+        cs, ev_ready, ev_done = self._comm_stream()
+        cudart.stream_wait(ov["stream"], ev_done)
+        self._ov = None
+
+    def _launch_window(self):
+        ov = self._ov
+        cs, ev_ready, ev_done = self._comm_stream()
+        ids = ov["ids"]
+        n = len(ids)
+        src = (C.c_void_p * n)(*[ov["grad"][t - 1] for t in ids])
+        dst = (C.c_void_p * n)(*[ov["out"][t - 1] for t in ids])
+        offs = capi.u64_array([self.layout.offsets[t - 1] for t in ids])
+        cnts = capi.u64_array([self.layout.sizes[t - 1] for t in ids])
+        cudart.event_record(ev_ready, ov["stream"])  # the window's gradients are final
+        cudart.stream_wait(cs, ev_ready)
+        ws, wl = capi.u64_array([ov["ws"]]), capi.u64_array([ov["we"] - ov["ws"]])
+        if self.world == 1:
+            capi.call("gf_sync_step_dense", self.comm, self.dtype, self.pool_off, src, dst, offs, cnts,
+                      n, ws, wl, 1, cs)
+        else:
+            capi.call("gf_pack", self.dtype, self.pool_ptr, src, offs, cnts, n, 1.0, cs)
+            capi.call("gf_ring_allreduce", self.comm, self.dtype, self.pool_off, ws, wl, 1, cs)
+            capi.call("gf_unpack", self.dtype, self.pool_ptr, dst, offs, cnts, n, self.world, cs)
+        cudart.event_record(ev_done, cs)
+        ov["launched"] += n
+        ov["ids"] = []
+        ov["ws"] = ov["we"]
+
+    def _comm_stream(self):
+        if self._comm_s is None:
+            cudart.set_device(self.device)
+            self._comm_s = (cudart.stream_create(), cudart.event_create(), cudart.event_create())
+        return self._comm_s
 
     def csc_step(self, grad_ptrs, stream=None, mark=None):
         """One CSC iteration (Algorithm 1). Uses the buffers given to attach_csc_state."""

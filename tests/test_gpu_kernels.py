@@ -577,3 +577,38 @@ def test_engine_csc_world1_vs_oracle(gf, oracle, G, dtype, theta):
         assert (G.bits(w.cpu().numpy()) == G.bits(o_w)).all(), t
         o_imp = nxt
     sync.close()
+
+
+def test_overlap_api_world1(gf, oracle, G):
+    """begin_iteration / tensor_complete / finalize_iteration at world 1: each closed theta
+    window is packed and unpacked on the communication stream; out-of-order completion and
+    an early finalize raise ConfigError like the reference (fusion.cpp:90-94)."""
+    import torch
+    from paper_1902_06855_b200 import capi
+    from paper_1902_06855_b200.engine import GradSync
+    sizes = RESNET50[:60] + [13, 7]
+    off, _, _ = oracle.pool_layout(sizes, 32000)
+    bounds = np.concatenate([[0], np.cumsum(sizes)])
+    sync = GradSync(sizes, theta=1 << 18)
+    flat = oracle.gen_grads(99, sizes)
+    g = torch.from_numpy(flat).cuda()
+    out = torch.empty_like(g)
+    gp = [g[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
+    op = [out[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
+    sync.begin_iteration(gp, op)
+    with pytest.raises(capi.ConfigError):
+        sync.tensor_complete(1)
+    for tid in range(len(sizes), 0, -1):
+        sync.tensor_complete(tid)
+    sync.finalize_iteration()
+    torch.cuda.synchronize()
+    want = oracle.unpack(oracle.pack(flat, sizes), 1)
+    got = out.cpu().numpy()
+    for i, s in enumerate(sizes):
+        assert (got[int(bounds[i]):int(bounds[i + 1])].view(np.uint32) ==
+                want[int(off[i]):int(off[i]) + s].view(np.uint32)).all(), i
+    sync.begin_iteration(gp, op)
+    sync.tensor_complete(len(sizes))
+    with pytest.raises(capi.ConfigError):
+        sync.finalize_iteration()
+    sync.close()

@@ -340,3 +340,60 @@ def _worker_engine_csc(rank, world, port):
 @pytest.mark.multigpu(2)
 def test_p2p_engine_csc_vs_reference_golden():
     _spawn(_worker_engine_csc, _world())
+
+
+def _worker_overlap(rank, world, port):
+    """GradSync.begin_iteration / tensor_complete / finalize_iteration: theta windows
+    launched on a communication stream while 'backward' runs, one ring per window; g_avg
+    bit-exact against the oracle's windowed ring."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    from oracle.oracle import RESNET50, Oracle
+    from paper_1902_06855_b200 import cudart
+    from paper_1902_06855_b200.engine import GradSync
+    torch.cuda.set_device(rank)
+    cudart.set_device(rank)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+
+    def ag(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+
+    o = Oracle()
+    sizes = RESNET50
+    off, _, _ = o.pool_layout(sizes, 32000)
+    bounds = np.concatenate([[0], np.cumsum(sizes)])
+    stream = torch.cuda.current_stream().cuda_stream
+    for theta in (8 << 20, 1 << 20):
+        sync = GradSync(sizes, rank=rank, world=world, device=rank, theta=theta, allgather=ag)
+        for it in range(2):
+            grads = [o.gen_grads(300 * it + 7 * r + 5, sizes) for r in range(world)]
+            g = torch.from_numpy(grads[rank]).cuda()
+            out = torch.empty_like(g)
+            gp = [g[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
+            op = [out[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
+            sync.begin_iteration(gp, op, stream=stream)
+            for tid in range(len(sizes), 0, -1):
+                torch.cuda._sleep(2000)  # backward work on the caller's stream
+                sync.tensor_complete(tid)
+            sync.finalize_iteration()
+            torch.cuda.synchronize()
+            sync.status()
+            ws, wl = o.dense_windows(sizes, 2, theta)
+            assert len(ws) > 2
+            pools = o.ring_allreduce([o.pack(x, sizes) for x in grads], dtype=F16, windows=(ws, wl))
+            want = o.unpack(pools[rank], world)
+            got = out.cpu().numpy()
+            for i, s in enumerate(sizes):
+                assert (got[int(bounds[i]):int(bounds[i + 1])].view(np.uint32) ==
+                        want[int(off[i]):int(off[i]) + s].view(np.uint32)).all(), (theta, it, i)
+        sync.close()
+    dist.barrier()
+
+
+@pytest.mark.multigpu(2)
+def test_p2p_overlapped_windows_bit_exact():
+    _spawn(_worker_overlap, _world())
