@@ -462,29 +462,32 @@ def main():
             if with_sync:
                 sync.finalize_iteration()
 
-        host = {}
-
-        def timed(with_sync):
-            for i in range(3):
-                backward(i, with_sync)
-            barrier()
-            e0.record(stream)
-            h0 = time.perf_counter()
-            for i in range(args.steps):
-                backward(i, with_sync)
-            host[with_sync] = (time.perf_counter() - h0) * 1e3 / max(args.steps, 1)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            barrier()
-            return allmax(e0.elapsed_time(e1) / max(args.steps, 1))
-
-        bw = timed(False)
-        both = timed(True)
-        sync.status()
+        # Alternate the two variants step by step and take medians: GEMM throughput drifts
+        # by several % over a run (power, clocks), more than the sync itself at N=1.
+        for i in range(3):
+            backward(i, False)
+            backward(i, True)
+        barrier()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 1)]
+        h0 = time.perf_counter()
+        evs[0].record(stream)
+        for i in range(args.steps):
+            backward(i, False)
+            evs[2 * i + 1].record(stream)
+            backward(i, True)
+            evs[2 * i + 2].record(stream)
+        host_ms = (time.perf_counter() - h0) * 1e3 / max(args.steps, 1)
+        torch.cuda.synchronize()
+        barrier()
+        t_bw = [evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(args.steps)]
+        t_both = [evs[2 * i + 1].elapsed_time(evs[2 * i + 2]) for i in range(args.steps)]
+        bw = allmax(statistics.median(t_bw))
+        both = allmax(statistics.median(t_both))
         overlap = {"backward_ms": round(bw, 4), "backward_plus_sync_ms": round(both, 4),
                    "exposed_sync_ms": round(both - bw, 4), "sync_alone_ms": round(ms, 4),
                    "windows": len(wlen), "theta_bytes": "inf" if wl["theta"] == THETA_INF else wl["theta"],
-                   "host_enqueue_ms": {"backward": round(host[False], 4), "backward_plus_sync": round(host[True], 4)},
+                   "host_enqueue_ms_per_pair": round(host_ms, 4),
+                   "method": "backward-only and backward+sync steps alternate; medians, max over ranks",
                    "backward": f"{sum(reps.values())} bf16 GEMMs 2048x4096x4096 per step, by tensor size"}
 
     # ---- NCCL allreduce on the same fp16 volume (comparison only) ---------------------------
