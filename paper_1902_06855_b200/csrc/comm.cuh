@@ -7,8 +7,6 @@
 //   [0, kFlagWords)                 ring barrier flags  flags[cta][src_rank]   (peers write)
 //   [kFlagWords, +kMaxBlocks)       per-CTA epoch counters (local)
 //   [+kMaxBlocks, +32)              ring work/done counters (local)
-//   step area (uint32 words):       packed[slab][src_rank] (peers write), reduced[slab]
-//                                   (owner writes), step epoch / queue / done (local)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -25,22 +23,7 @@ constexpr int kMaxW = GF_MAX_WINDOWS_PER_LAUNCH;
 constexpr int kRingThreads = 512;
 constexpr uint64_t kFlagWords = uint64_t(kMaxBlocks) * GF_MAX_RANKS;
 constexpr uint64_t kRingFlagBytes = (kFlagWords + kMaxBlocks + 32) * sizeof(uint64_t);
-// fused step: slab-granular flags
-constexpr uint64_t kStepMaxSlabs = 16384;
-constexpr uint64_t kStepPackedWords = kStepMaxSlabs * GF_MAX_RANKS;  // uint32
-constexpr uint64_t kStepReducedWords = kStepMaxSlabs;                // uint32
-constexpr uint64_t kStepCtlWords = 64;                               // uint32: epoch, queue, done
-constexpr uint64_t kStepFlagBytes = (kStepPackedWords + kStepReducedWords + kStepCtlWords) * 4;
-constexpr uint64_t kFlagBytes = kRingFlagBytes + kStepFlagBytes;
-
-// A cached device-side work plan of the fused step (slab table), keyed by its geometry.
-struct StepPlan {
-    uint64_t* slab_a = nullptr;   // [nslab] first element
-    uint64_t* slab_b = nullptr;   // [nslab] end element
-    uint32_t* slab_pos = nullptr; // [nslab] owner's ring position
-    uint32_t* mine = nullptr;     // [nmine] this rank's task queue ((kind << 30) | slab)
-    uint32_t nslab = 0, nmine = 0;
-};
+constexpr uint64_t kFlagBytes = kRingFlagBytes;
 
 struct gf_comm {
     int world = 0, rank = 0, device = 0, pos = 0;
@@ -54,7 +37,6 @@ struct gf_comm {
     bool trace = false;
     uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;  // transport.hpp:25 kDefaultTimeout
     bool connected = false;
-    std::map<std::string, StepPlan> step_plans;
 };
 
 namespace {
@@ -80,9 +62,5 @@ inline int comm_ready(gf_comm* c) {
                                                std::to_string(c->rank) + ")");
     return GF_OK;
 }
-
-inline uint32_t* step_packed(char* alloc) { return reinterpret_cast<uint32_t*>(alloc + kRingFlagBytes); }
-inline uint32_t* step_reduced(char* alloc) { return step_packed(alloc) + kStepPackedWords; }
-inline uint32_t* step_ctl(char* alloc) { return step_reduced(alloc) + kStepReducedWords; }
 
 }  // namespace

@@ -34,28 +34,11 @@
 #include "gf_internal.cuh"
 #include "select.cuh"
 #include "comm.cuh"
+#include "ring_device.cuh"
 
 namespace {
 
 
-
-struct RingArgs {
-    char* bufs[GF_MAX_RANKS];            // buffer base of each RANK (peer-mapped)
-    int ring[GF_MAX_RANKS];              // rank at each ring position
-    int world, rank, pos;
-    int nwin;                            // >= 0 explicit windows; -1: read plan
-    uint64_t* flags_local;
-    uint64_t* flags_peer[GF_MAX_RANKS];  // by rank
-    uint64_t* epochs;                    // local, one per CTA
-    uint64_t* work;                      // local dynamic item counter (re-armed by the last CTA)
-    unsigned* done;                      // local CTA completion counter
-    uint64_t timeout_ns;
-    int* err;
-    uint64_t* trace;                     // host-mapped [start, entered, exit_begin, end] or null
-    const uint64_t* plan;
-    uint64_t wstart[kMaxW];
-    uint64_t wlen[kMaxW];
-};
 
 struct SelArgs {
     float* norms[GF_MAX_RANKS];          // by rank
@@ -75,111 +58,6 @@ struct SelArgs {
     int* err;
     uint64_t* trace;
 };
-
-// ---- cross-GPU barrier (CTA b <-> CTA b of every peer) ------------------------
-// release_writes: the CTA's earlier global stores (incl. pushes into peers) must be visible
-// to a peer that observes the flag. bar.sync orders them before the signalling threads, whose
-// system-scope fence + release store make them cumulative (the cooperative-groups grid-sync
-// pattern, at .sys scope). At kernel entry nothing was written yet: no fence.
-template <typename A>
-__device__ bool cross_barrier(const A& a, uint64_t val, int* s_ok, bool release_writes = true) {
-    __syncthreads();
-    const int t = threadIdx.x;
-    if (t < a.world && t != a.rank) {
-        if (release_writes) __threadfence_system();
-        gfd::st_release_sys(a.flags_peer[t] + blockIdx.x * GF_MAX_RANKS + a.rank, val);
-        const uint64_t* f = a.flags_local + blockIdx.x * GF_MAX_RANKS + t;
-        if (gfd::ld_acquire_sys(f) < val) {
-            const uint64_t t0 = gfd::globaltimer_ns();
-            uint32_t spins = 0;
-            while (gfd::ld_acquire_sys(f) < val) {
-                if ((++spins & 255u) == 0) {
-                    if (*reinterpret_cast<volatile int*>(a.err) != 0) { *s_ok = 0; break; }
-                    if (gfd::globaltimer_ns() - t0 > a.timeout_ns) {
-                        *reinterpret_cast<volatile int*>(a.err) = 1;
-                        *s_ok = 0;
-                        break;
-                    }
-                }
-            }
-        }
-    }
-    __syncthreads();
-    return *s_ok != 0;
-}
-
-// ---- reduction of one element range [e0, e1) -----------------------------------
-template <int DT>
-struct Vec;
-template <>
-struct Vec<GF_F16> {
-    static constexpr int kElems = 8;
-    __device__ static uint4 acc(uint4 local, uint4 a) { return gfd::acc16x8(local, a); }
-    __device__ static void scalar(const RingArgs& a, const char* const* src, int n, uint64_t e) {
-        uint16_t acc = reinterpret_cast<const uint16_t*>(src[0])[e];
-        for (int t = 1; t < n; ++t) acc = gfd::acc16(reinterpret_cast<const uint16_t*>(src[t])[e], acc);
-        for (int r = 0; r < a.world; ++r) reinterpret_cast<uint16_t*>(a.bufs[r])[e] = acc;
-    }
-};
-template <>
-struct Vec<GF_F32> {
-    static constexpr int kElems = 4;
-    __device__ static uint4 acc(uint4 local, uint4 a) { return gfd::acc32x4(local, a); }
-    __device__ static void scalar(const RingArgs& a, const char* const* src, int n, uint64_t e) {
-        float acc = reinterpret_cast<const float*>(src[0])[e];
-        for (int t = 1; t < n; ++t) acc = gfd::add(reinterpret_cast<const float*>(src[t])[e], acc);
-        for (int r = 0; r < a.world; ++r) reinterpret_cast<float*>(a.bufs[r])[e] = acc;
-    }
-};
-
-// Reduction of one window's owned segment: the grid sweeps its 16-byte vectors in
-// lockstep (thread g takes vectors g, g+T, g+2T, ... with T = all threads of the grid), so
-// every thread gets the same number of vectors (+-1) and all CTAs of a rank finish
-// together; U vectors x N sources of loads are in flight per thread.
-template <int DT, int NT>
-__device__ __forceinline__ void reduce_segment(const RingArgs& a, const char* const* src, int n,
-                                               uint64_t e0, uint64_t e1, uint64_t gtid, uint64_t T) {
-    constexpr int VE = Vec<DT>::kElems;
-    constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
-    constexpr int U = NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1);
-    const uint64_t v0 = (e0 + VE - 1) / VE, v1 = e1 / VE;
-    if (v0 >= v1) {  // no aligned vector inside: all scalar, CTA 0
-        if (blockIdx.x == 0)
-            for (uint64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
-        return;
-    }
-    if (blockIdx.x == 0) {
-        for (uint64_t e = e0 + threadIdx.x; e < v0 * VE; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
-        for (uint64_t e = v1 * VE + threadIdx.x; e < e1; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
-    }
-    for (uint64_t v = v0 + gtid; v < v1; v += T * U) {
-        uint4 x[U][NMAX];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t vv = v + uint64_t(u) * T;
-            if (vv < v1) {
-#pragma unroll
-                for (int t = 0; t < NMAX; ++t)
-                    if (t < n) x[u][t] = gfd::ld16(src[t] + vv * 16);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t vv = v + uint64_t(u) * T;
-            if (vv < v1) {
-                uint4 acc = x[u][0];
-#pragma unroll
-                for (int t = 1; t < NMAX; ++t)
-                    if (t < n) acc = Vec<DT>::acc(x[u][t], acc);
-                // push the sum to every rank, starting with the next one on the ring so the
-                // ranks' first stores spread over distinct destinations
-#pragma unroll
-                for (int t = 0; t < NMAX; ++t)
-                    if (t < n) gfd::st16(const_cast<char*>(src[(t + 1) % n]) + vv * 16, acc);
-            }
-        }
-    }
-}
 
 template <int DT, int NT, bool P2P>
 __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constant__ RingArgs a) {
@@ -319,7 +197,7 @@ void launch_ring(int dtype, bool p2p, const RingArgs& a, dim3 grid, cudaStream_t
 // CTAs per rank: enough 512-thread CTAs to keep ~2 MB of NVLink loads in flight,
 // capped at 1 per SM (and by the flag table). Depends only on values identical
 // on every rank, so all ranks launch the same grid (CTA b pairs with CTA b).
-int ring_blocks(uint64_t max_seg_bytes) {
+int ring_blocks_impl(uint64_t max_seg_bytes) {
     static const int forced = [] {
         const char* e = std::getenv("GF_RING_BLOCKS");  // tuning override (must match on all ranks)
         return e ? std::atoi(e) : 0;
@@ -345,24 +223,6 @@ bool valid_ring(const int* order, int world) {
 }  // namespace
 
 namespace {
-
-void fill_common(gf_comm* c, RingArgs& a, uint64_t heap_off) {
-    a.world = c->world;
-    a.rank = c->rank;
-    a.pos = c->pos;
-    for (int r = 0; r < c->world; ++r) {
-        a.bufs[r] = c->peer_alloc[r] + kFlagBytes + heap_off;
-        a.flags_peer[r] = reinterpret_cast<uint64_t*>(c->peer_alloc[r]);
-        a.ring[r] = c->ring[r];
-    }
-    a.flags_local = reinterpret_cast<uint64_t*>(c->alloc);
-    a.epochs = a.flags_local + kFlagWords;
-    a.work = a.epochs + kMaxBlocks;
-    a.done = reinterpret_cast<unsigned*>(a.work + 16);
-    a.timeout_ns = c->timeout_ns;
-    a.err = c->err_dev;
-    a.trace = c->trace ? reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(c->err_dev) + 64) : nullptr;
-}
 
 }  // namespace
 
@@ -407,12 +267,6 @@ int gf_comm_destroy(gf_comm* c) {
     cudaDeviceSynchronize();
     for (int r = 0; r < c->world; ++r)
         if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->peer_alloc[r]);
-    for (auto& kv : c->step_plans) {
-        cudaFree(kv.second.slab_a);
-        cudaFree(kv.second.slab_b);
-        cudaFree(kv.second.slab_pos);
-        cudaFree(kv.second.mine);
-    }
     cudaFree(c->alloc);
     cudaFreeHost(c->err_host);
     delete c;
@@ -551,7 +405,7 @@ int gf_ring_allreduce(gf_comm* c, int dtype, uint64_t heap_off, const uint64_t* 
             max_seg += (a.wlen[w] + c->world - 1) / c->world;
         }
         fill_common(c, a, heap_off);
-        launch_ring(dtype, true, a, dim3(ring_blocks(max_seg * es)), gfi::S(stream));
+        launch_ring(dtype, true, a, dim3(gfr::ring_blocks(max_seg * es)), gfi::S(stream));
         gfi::count_launch();
         if (int rc = gfi::check_launch("gf_ring_allreduce")) return rc;
     }
@@ -583,7 +437,7 @@ int gf_ring_allreduce_ptrs(gf_comm* c, int dtype, void* const* rank_bufs, const 
         }
         fill_common(c, a, 0);
         for (int r = 0; r < c->world; ++r) a.bufs[r] = static_cast<char*>(rank_bufs[r]);
-        launch_ring(dtype, true, a, dim3(ring_blocks(max_seg * es)), gfi::S(stream));
+        launch_ring(dtype, true, a, dim3(gfr::ring_blocks(max_seg * es)), gfi::S(stream));
         gfi::count_launch();
         if (int rc = gfi::check_launch("gf_ring_allreduce_ptrs")) return rc;
     }
@@ -648,7 +502,7 @@ int gf_ring_allreduce_planned(gf_comm* c, int dtype, uint64_t heap_off, const ui
     a.plan = plan_dev;
     fill_common(c, a, heap_off);
     const uint64_t bound = c->heap_bytes > heap_off ? (c->heap_bytes - heap_off) / c->world : 0;
-    launch_ring(dtype, true, a, dim3(ring_blocks(bound)), gfi::S(stream));
+    launch_ring(dtype, true, a, dim3(gfr::ring_blocks(bound)), gfi::S(stream));
     gfi::count_launch();
     return gfi::check_launch("gf_ring_allreduce_planned");
 }
@@ -676,7 +530,7 @@ int gf_ring_allreduce_colocated(int dtype, void* const* bufs, int world, const i
             a.bufs[r] = static_cast<char*>(bufs[r]);
             a.ring[r] = ring_order ? ring_order[r] : r;
         }
-        launch_ring(dtype, false, a, dim3(ring_blocks(max_seg * gfi::esz(dtype)), world), gfi::S(stream));
+        launch_ring(dtype, false, a, dim3(gfr::ring_blocks(max_seg * gfi::esz(dtype)), world), gfi::S(stream));
         gfi::count_launch();
         if (int rc = gfi::check_launch("gf_ring_allreduce_colocated")) return rc;
     }
@@ -809,3 +663,7 @@ int gf_ring_traffic(uint64_t len, int world, int position, int dtype, uint64_t* 
 }
 
 }  // extern "C"
+
+namespace gfr {
+int ring_blocks(uint64_t max_seg_bytes) { return ring_blocks_impl(max_seg_bytes); }
+}  // namespace gfr

@@ -1,0 +1,163 @@
+// SPDX-License-Identifier: Apache-2.0
+// Device pieces of the NVLink ring shared by ring.cu (K4, the collective alone) and
+// fused.cu (the dense step: pack + ring + unpack in one kernel): launch arguments, the
+// per-CTA-pair cross-GPU barrier and the segment reduction.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "comm.cuh"
+#include "gf_device.cuh"
+#include "gf_internal.cuh"
+
+namespace {
+
+struct RingArgs {
+    char* bufs[GF_MAX_RANKS];            // buffer base of each RANK (peer-mapped)
+    int ring[GF_MAX_RANKS];              // rank at each ring position
+    int world, rank, pos;
+    int nwin;                            // >= 0 explicit windows; -1: read plan
+    uint64_t* flags_local;
+    uint64_t* flags_peer[GF_MAX_RANKS];  // by rank
+    uint64_t* epochs;                    // local, one per CTA
+    uint64_t* work;                      // local dynamic item counter (re-armed by the last CTA)
+    unsigned* done;                      // local CTA completion counter
+    uint64_t timeout_ns;
+    int* err;
+    uint64_t* trace;                     // host-mapped [start, entered, exit_begin, end] or null
+    const uint64_t* plan;
+    uint64_t wstart[kMaxW];
+    uint64_t wlen[kMaxW];
+};
+
+// ---- cross-GPU barrier (CTA b <-> CTA b of every peer) ------------------------
+// release_writes: the CTA's earlier global stores (incl. pushes into peers) must be visible
+// to a peer that observes the flag. bar.sync orders them before the signalling threads, whose
+// system-scope fence + release store make them cumulative (the cooperative-groups grid-sync
+// pattern, at .sys scope). At kernel entry nothing was written yet: no fence.
+template <typename A>
+__device__ bool cross_barrier(const A& a, uint64_t val, int* s_ok, bool release_writes = true) {
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < a.world && t != a.rank) {
+        if (release_writes) __threadfence_system();
+        gfd::st_release_sys(a.flags_peer[t] + blockIdx.x * GF_MAX_RANKS + a.rank, val);
+        const uint64_t* f = a.flags_local + blockIdx.x * GF_MAX_RANKS + t;
+        if (gfd::ld_acquire_sys(f) < val) {
+            const uint64_t t0 = gfd::globaltimer_ns();
+            uint32_t spins = 0;
+            while (gfd::ld_acquire_sys(f) < val) {
+                if ((++spins & 255u) == 0) {
+                    if (*reinterpret_cast<volatile int*>(a.err) != 0) { *s_ok = 0; break; }
+                    if (gfd::globaltimer_ns() - t0 > a.timeout_ns) {
+                        *reinterpret_cast<volatile int*>(a.err) = 1;
+                        *s_ok = 0;
+                        break;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    return *s_ok != 0;
+}
+
+// ---- reduction of one element range [e0, e1) -----------------------------------
+template <int DT>
+struct Vec;
+template <>
+struct Vec<GF_F16> {
+    static constexpr int kElems = 8;
+    __device__ static uint4 acc(uint4 local, uint4 a) { return gfd::acc16x8(local, a); }
+    __device__ static void scalar(const RingArgs& a, const char* const* src, int n, uint64_t e) {
+        uint16_t acc = reinterpret_cast<const uint16_t*>(src[0])[e];
+        for (int t = 1; t < n; ++t) acc = gfd::acc16(reinterpret_cast<const uint16_t*>(src[t])[e], acc);
+        for (int r = 0; r < a.world; ++r) reinterpret_cast<uint16_t*>(a.bufs[r])[e] = acc;
+    }
+};
+template <>
+struct Vec<GF_F32> {
+    static constexpr int kElems = 4;
+    __device__ static uint4 acc(uint4 local, uint4 a) { return gfd::acc32x4(local, a); }
+    __device__ static void scalar(const RingArgs& a, const char* const* src, int n, uint64_t e) {
+        float acc = reinterpret_cast<const float*>(src[0])[e];
+        for (int t = 1; t < n; ++t) acc = gfd::add(reinterpret_cast<const float*>(src[t])[e], acc);
+        for (int r = 0; r < a.world; ++r) reinterpret_cast<float*>(a.bufs[r])[e] = acc;
+    }
+};
+
+// Reduction of one window's owned segment: the grid sweeps its 16-byte vectors in
+// lockstep (thread g takes vectors g, g+T, g+2T, ... with T = all threads of the grid), so
+// every thread gets the same number of vectors (+-1) and all CTAs of a rank finish
+// together; U vectors x N sources of loads are in flight per thread.
+template <int DT, int NT>
+__device__ __forceinline__ void reduce_segment(const RingArgs& a, const char* const* src, int n,
+                                               uint64_t e0, uint64_t e1, uint64_t gtid, uint64_t T) {
+    constexpr int VE = Vec<DT>::kElems;
+    constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
+    constexpr int U = NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1);
+    const uint64_t v0 = (e0 + VE - 1) / VE, v1 = e1 / VE;
+    if (v0 >= v1) {  // no aligned vector inside: all scalar, CTA 0
+        if (blockIdx.x == 0)
+            for (uint64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
+        return;
+    }
+    if (blockIdx.x == 0) {
+        for (uint64_t e = e0 + threadIdx.x; e < v0 * VE; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
+        for (uint64_t e = v1 * VE + threadIdx.x; e < e1; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
+    }
+    for (uint64_t v = v0 + gtid; v < v1; v += T * U) {
+        uint4 x[U][NMAX];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t vv = v + uint64_t(u) * T;
+            if (vv < v1) {
+#pragma unroll
+                for (int t = 0; t < NMAX; ++t)
+                    if (t < n) x[u][t] = gfd::ld16(src[t] + vv * 16);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t vv = v + uint64_t(u) * T;
+            if (vv < v1) {
+                uint4 acc = x[u][0];
+#pragma unroll
+                for (int t = 1; t < NMAX; ++t)
+                    if (t < n) acc = Vec<DT>::acc(x[u][t], acc);
+                // push the sum to every rank, starting with the next one on the ring so the
+                // ranks' first stores spread over distinct destinations
+#pragma unroll
+                for (int t = 0; t < NMAX; ++t)
+                    if (t < n) gfd::st16(const_cast<char*>(src[(t + 1) % n]) + vv * 16, acc);
+            }
+        }
+    }
+}
+
+inline void fill_common(gf_comm* c, RingArgs& a, uint64_t heap_off) {
+    a.world = c->world;
+    a.rank = c->rank;
+    a.pos = c->pos;
+    for (int r = 0; r < c->world; ++r) {
+        a.bufs[r] = c->peer_alloc[r] + kFlagBytes + heap_off;
+        a.flags_peer[r] = reinterpret_cast<uint64_t*>(c->peer_alloc[r]);
+        a.ring[r] = c->ring[r];
+    }
+    a.flags_local = reinterpret_cast<uint64_t*>(c->alloc);
+    a.epochs = a.flags_local + kFlagWords;
+    a.work = a.epochs + kMaxBlocks;
+    a.done = reinterpret_cast<unsigned*>(a.work + 16);
+    a.timeout_ns = c->timeout_ns;
+    a.err = c->err_dev;
+    a.trace = c->trace ? reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(c->err_dev) + 64) : nullptr;
+}
+
+}  // namespace
+
+namespace gfr {
+// CTAs per rank of a ring launch (ring.cu): identical on every rank for the same windows.
+int ring_blocks(uint64_t max_seg_bytes);
+}  // namespace gfr
