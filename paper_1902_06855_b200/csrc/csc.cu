@@ -20,6 +20,7 @@
 //  gf_select_topk/gf_csc_plan  see select.cuh.
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gf_device.cuh"
 #include "gf_internal.cuh"
@@ -199,8 +200,10 @@ __device__ __forceinline__ void nacc_add(uint64_t* nacc, uint64_t c, uint64_t u,
 }
 
 // K2: fused pack + correction + compaction (+ exact norms of the unimportant chunks).
+// 4 CTAs per SM (64 registers): measured best (AlexNet CSC: 154 us; 168 us at 78 registers
+// and 3 CTAs per SM; 160 us at 5 CTAs per SM, which spills)
 template <int DT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ pool,
                     float* __restrict__ hg, void* __restrict__ staging,
                     const uint8_t* __restrict__ imp, const uint64_t* __restrict__ coff,
