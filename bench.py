@@ -360,7 +360,8 @@ def main():
     if csc:
         # staged elements of the last timed (sparse) iteration, read back after timing
         staged = int(plan[(sync.iteration - 1) & 1][0].item())
-        algo["pack_correct"] = total * 14 + staged * 2   # g, hg in; pool, hg, staging out
+        # g, hg in; pool, hg out; + the staging copy at N>1 (N=1 has no exchange, no staging)
+        algo["pack_correct"] = total * 14 + (staged * 2 if world > 1 else 0)
         algo["scatter"] = staged * 4                      # staging in, pool out (+ exact L1)
         algo["sgd_update"] = staged * 18                  # pool in; hu, w in+out
         ring_bytes = ring_bus_bytes(L, esz, world, [staged])

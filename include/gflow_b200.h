@@ -109,9 +109,12 @@ int gf_csc_correct(int dtype, void* pool, float* hg, const uint8_t* important, u
 /* Fused pack + correction + compaction over all tensors: for pool element i in chunk c
  *   g = dec(enc(src)) + hg ; hg = imp ? 0 : momentum*g ; pool = enc(g) ;
  *   if imp[c]: staging[coff[c] + (i - c*chunk)] = enc(g).
- * coff (device, nc entries) comes from gf_csc_plan. staging may be NULL (no compaction).
+ * coff (device, nc entries) comes from gf_csc_plan.
  * nacc (device, nc uint64, fp16 pools only, nullable): the exact sum of |pool| of every
- * UNIMPORTANT chunk is added in units of 2^-24 (bit 63 = NaN seen) — K3 fused into K2. */
+ * UNIMPORTANT chunk is added in units of 2^-24 (bit 63 = NaN seen) — K3 fused into K2.
+ * staging may be NULL: no compaction. That is the world-1 step, where the exchange is the
+ * identity (collectives.cpp:59): nacc then also takes the important chunks, and no
+ * gf_csc_scatter follows. */
 int gf_csc_pack_correct(int dtype, void* pool, float* hg, void* staging,
                         const uint8_t* important, const uint64_t* coff, uint64_t total,
                         uint64_t chunk, uint64_t nc, const float* const* src,

@@ -199,7 +199,8 @@ __device__ __forceinline__ void nacc_add(uint64_t* nacc, uint64_t c, uint64_t u,
     }
 }
 
-// K2: fused pack + correction + compaction (+ exact norms of the unimportant chunks).
+// K2: fused pack + correction + compaction (+ exact norms of the unimportant chunks; of
+// every chunk when staging is null: world 1, where the pool already holds the exchanged sums).
 // 4 CTAs per SM (64 registers): measured best (AlexNet CSC: 154 us; 168 us at 78 registers
 // and 3 CTAs per SM; 160 us at 5 CTAs per SM, which spills)
 template <int DT>
@@ -273,9 +274,9 @@ pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ po
                                make_float4(hn[4], hn[5], hn[6], hn[7]));
                     gfd::st16(d + 8 * v, ov);
                     if (im && stg) gfd::st16(stg + coff[c] + (pi - c * chunk), ov);
-                    if (!im && nacc) units = units8(nan ? make_uint4(0, 0, 0, 0) : ov);
+                    if ((!im || !stg) && nacc) units = units8(nan ? make_uint4(0, 0, 0, 0) : ov);
                 }
-                if (nacc) nacc_add(nacc, c, units, nan, act && !im);
+                if (nacc) nacc_add(nacc, c, units, nan, act && (!im || !stg));
             }
             done = uint64_t(nvec) * 8;
         }
@@ -287,7 +288,7 @@ pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ po
                 const uint16_t w = gfd::enc(correct_elem(gfd::dec(gfd::enc(s[i])), hg + pi, im, mom));
                 static_cast<uint16_t*>(pool)[pi] = w;
                 if (im && staging) static_cast<uint16_t*>(staging)[coff[c] + (pi - c * chunk)] = w;
-                if (!im && nacc) {
+                if ((!im || !staging) && nacc) {
                     if ((w & 0x7C00u) == 0x7C00u)
                         atomicOr(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)kNaccNaN);
                     else if (half_units(w))

@@ -289,9 +289,11 @@ class GradSync:
         mark = mark or (lambda name: None)
         mark("pack_correct")
         nacc = b["nacc"]
-        capi.call("gf_csc_pack_correct", self.dtype, self.pool_ptr, b["hg"], self.stage_ptr,
-                  b["imp"][cur], b["coff"][cur], L.total, L.chunk, L.num_chunks,
-                  self._ptrs(grad_ptrs), self._offs, self._cnts, m, self.momentum, nacc, stream)
+        solo = self.world == 1  # the exchange is the identity: no staging, no scatter
+        capi.call("gf_csc_pack_correct", self.dtype, self.pool_ptr, b["hg"],
+                  None if solo else self.stage_ptr, b["imp"][cur], b["coff"][cur], L.total, L.chunk,
+                  L.num_chunks, self._ptrs(grad_ptrs), self._offs, self._cnts, m, self.momentum,
+                  nacc, stream)
         if self.world > 1:
             mark("ring")
             capi.call("gf_ring_allreduce_planned", self.comm, self.dtype, self.stage_off,
@@ -299,9 +301,10 @@ class GradSync:
         # chunks selected for this iteration (iteration 0 is dense, sparse.cpp:45-51)
         k_cur = L.num_chunks if self.iteration == 0 else selection_count(
             sparsity_at(self.iteration, self.warmup_iters, self.final_sparsity), L.num_chunks)
-        mark("scatter")
-        capi.call("gf_csc_scatter", self.dtype, self.pool_ptr, self.stage_ptr, b["plan"][cur],
-                  b["coff"][cur], L.total, L.chunk, L.num_chunks, k_cur, nacc, stream)
+        if not solo:
+            mark("scatter")
+            capi.call("gf_csc_scatter", self.dtype, self.pool_ptr, self.stage_ptr, b["plan"][cur],
+                      b["coff"][cur], L.total, L.chunk, L.num_chunks, k_cur, nacc, stream)
         if nacc is None:  # fp32 pool: separate norm pass (sequential fp64, as the reference)
             mark("norms")
             capi.call("gf_chunk_norms", self.dtype, self.pool_ptr, L.total, L.chunk, L.num_chunks,
