@@ -368,13 +368,14 @@ def main():
     else:
         ring_bytes = ring_bus_bytes(L, esz, world, wlen)
     algo["ring"] = ring_bytes if world > 1 else None
+    algo["ring_scatter"] = algo["ring"]  # CSC exchange with the write-back fused in
     if args.fused:  # its binding roofline: NVLink bus bytes at N>1, HBM bytes at N=1
         algo["fused_step"] = ring_bytes if world > 1 else total * 12
     dom = max(seg_ms, key=lambda k: seg_ms[k]) if seg_ms else None
     roof = None
     if dom is not None and algo.get(dom):
         t_s = seg_ms[dom] / 1e3
-        if dom == "ring" or (dom == "fused_step" and world > 1):
+        if dom in ("ring", "ring_scatter") or (dom == "fused_step" and world > 1):
             ach = algo[dom] / t_s / 1e9
             roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": 900.0, "unit": "GB/s",
                     "frac": round(ach / 900.0, 3), "traffic": None, "kernel": "ring_kernel",
@@ -404,7 +405,7 @@ def main():
         d = {"ms": round(v, 4)}
         if algo.get(k):
             d["GBps"] = round(algo[k] / (v / 1e3) / 1e9, 1)
-            if k != "ring" and not (k == "fused_step" and world > 1):
+            if k not in ("ring", "ring_scatter") and not (k == "fused_step" and world > 1):
                 d["frac_hbm"] = round(d["GBps"] / hbm_peak, 3)
             else:
                 d["busbw_frac_900"] = round(d["GBps"] / 900, 3)
@@ -583,8 +584,9 @@ def main():
 
     if rank == 0:
         bus = None
-        if world > 1 and "ring" in seg_ms:
-            bus = round(ring_bytes / (seg_ms["ring"] / 1e3) / 1e9, 1)
+        rk = "ring" if "ring" in seg_ms else "ring_scatter"
+        if world > 1 and rk in seg_ms:
+            bus = round(ring_bytes / (seg_ms[rk] / 1e3) / 1e9, 1)
         elif world > 1 and "fused_step" in seg_ms:
             bus = round(ring_bytes / (seg_ms["fused_step"] / 1e3) / 1e9, 1)
         line = {

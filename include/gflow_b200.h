@@ -190,11 +190,19 @@ int gf_ipc_close(gf_comm* comm, void* base);
 /* Same with windows described by a device plan written by gf_csc_plan / gf_csc_select. */
 int gf_ring_allreduce_planned(gf_comm* comm, int dtype, uint64_t heap_off,
                               const uint64_t* plan_dev, void* stream);
-/* One fused dense sync step: pack -> ring allreduce of the theta windows -> unpack, as ONE
- * persistent kernel per rank that overlaps the three slab by slab through per-slab flags in
- * peer memory (no global barriers). Result-identical to gf_pack + gf_ring_allreduce +
- * gf_unpack (bit for bit). The fp16/fp32 pool lives at pool_heap_off in the symmetric heap;
- * src/dst/pool_off/count are HOST arrays (<= 256 tensors) of device pointers / sizes. */
+/* The planned exchange of the staging buffer at stage_heap_off WITH the write-back fused in:
+ * after its exit barrier each CTA copies its staging vectors into `pool` (local, fp16) and
+ * adds their exact |x| units to nacc — gf_ring_allreduce_planned + gf_csc_scatter in one
+ * launch (sparse.cpp:142-168). fp16 only, chunk % 8 == 0, nc <= 6144, world > 1. */
+int gf_ring_allreduce_planned_scatter(gf_comm* comm, int dtype, uint64_t stage_heap_off,
+                                      const uint64_t* plan_dev, void* pool, uint64_t chunk,
+                                      uint64_t nc, uint64_t* nacc, void* stream);
+/* One dense sync step as ONE kernel per rank: pack -> ring allreduce of the theta windows ->
+ * unpack. Each CTA packs, reduces and unpacks one fixed strided set of pool vectors and only
+ * synchronises with its peer CTAs (entry/exit barriers); at world 1 it is a single streaming
+ * pass. Result-identical to gf_pack + gf_ring_allreduce + gf_unpack (bit for bit). The
+ * fp16/fp32 pool lives at pool_heap_off in the symmetric heap; src/dst/pool_off/count are
+ * HOST arrays (<= 256 tensors, tiling the windows) of device pointers / sizes. */
 int gf_sync_step_dense(gf_comm* comm, int dtype, uint64_t pool_heap_off, const float* const* src,
                        float* const* dst, const uint64_t* pool_off, const uint64_t* count,
                        int ntensors, const uint64_t* win_start, const uint64_t* win_len, int nwin,

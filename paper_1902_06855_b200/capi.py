@@ -88,6 +88,7 @@ SIGNATURES = {
     "gf_comm_world": [_vp],
     "gf_ring_allreduce": [_vp, _i, _u64, _vp, _vp, _i, _vp],
     "gf_ring_allreduce_planned": [_vp, _i, _u64, _vp, _vp],
+    "gf_ring_allreduce_planned_scatter": [_vp, _i, _u64, _vp, _vp, _u64, _u64, _vp, _vp],
     "gf_ring_allreduce_ptrs": [_vp, _i, _vp, _vp, _vp, _i, _vp],
     "gf_sync_step_dense": [_vp, _i, _u64, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _vp],
     "gf_ipc_export": [_vp, _vp, _u64p],

@@ -31,10 +31,8 @@ namespace {
 
 constexpr int kNormThreads = 256;
 
-__device__ __forceinline__ uint64_t half_units(uint16_t h) {
-    const uint32_t e = (h >> 10) & 0x1Fu, m = h & 0x3FFu;
-    return e == 0 ? uint64_t(m) : (uint64_t(1024u + m) << (e - 1));
-}
+using gfd::half_units;
+using gfd::units8;
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
@@ -68,10 +66,7 @@ norms_f16_kernel(const uint16_t* __restrict__ pool, uint64_t total, uint64_t chu
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     nan |= gfd::any_special(x[u]);
-                    const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        acc += half_units(uint16_t(w[k] & 0xFFFFu)) + half_units(uint16_t(w[k] >> 16));
+                    acc += units8(x[u]);
                 }
             }
             done = nvec * 8;
@@ -162,15 +157,6 @@ __global__ void correct_kernel(void* __restrict__ pool, float* __restrict__ hg,
             p[i] = correct_elem(p[i], hg + i, im, mom);
         }
     }
-}
-
-// Exact |x| sum of 8 halves in units of 2^-24 (see gf_chunk_norms); NaN-free input.
-__device__ __forceinline__ uint64_t units8(uint4 v) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    uint64_t acc = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) acc += half_units(uint16_t(w[k] & 0xFFFFu)) + half_units(uint16_t(w[k] >> 16));
-    return acc;
 }
 
 constexpr uint64_t kNaccNaN = 1ull << 63;  // NaN marker in an exact-norm accumulator

@@ -137,6 +137,24 @@ __device__ __forceinline__ uint4 enc8(float4 a, float4 b) {
     return o;
 }
 
+// ---- exact |x| of fp16 values in units of 2^-24 (the chunk L1 of gf_chunk_norms) ----------
+// |h| * 2^24 is an integer < 2^40 for every finite half, and fp32 holds it exactly (a power
+// of two times an 11-bit significand): half -> float, scale, truncate. Non-finite halves give
+// meaningless units; callers track NaN separately.
+__device__ __forceinline__ uint64_t half_units(uint16_t h) {
+    return __float2ull_rz(fabsf(__half2float(__ushort_as_half(h))) * 16777216.0f);
+}
+__device__ __forceinline__ uint64_t units8(uint4 v) {
+    const uint32_t w[4] = {v.x & 0x7FFF7FFFu, v.y & 0x7FFF7FFFu, v.z & 0x7FFF7FFFu, v.w & 0x7FFF7FFFu};
+    uint64_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float2 f = h2f2(w[k]);
+        acc += __float2ull_rz(f.x * 16777216.0f) + __float2ull_rz(f.y * 16777216.0f);
+    }
+    return acc;
+}
+
 // 256-bit (32 B per thread) global access, sm_100: one LDG.E.256 / STG.E.256 per 8 floats.
 // Requires 32-B alignment.
 struct F8 {

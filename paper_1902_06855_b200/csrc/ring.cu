@@ -59,6 +59,100 @@ struct SelArgs {
     uint64_t* trace;
 };
 
+// ---- CSC write-back fused into the planned ring (staging -> pool + exact chunk L1) -------
+using gfd::half_units;
+constexpr uint64_t kNaccNaN = 1ull << 63;
+
+// pool element of staging element s: important chunk q of the plan starts at staging q*chunk
+// (only the final pool chunk differs in length, and it is last when selected). The chunk
+// list is staged in shared memory after the exit barrier (wb_list).
+__device__ __forceinline__ uint64_t wb_target(const RingArgs& a, const uint64_t* list, uint64_t k, uint64_t s,
+                                              uint64_t& c) {
+    const uint64_t q = min(s / a.wb_chunk, k - 1);
+    c = list[q];
+    return c * a.wb_chunk + (s - q * a.wb_chunk);
+}
+
+// warp-aggregated add of (chunk, units): lanes sharing the first active lane's chunk combine
+__device__ __forceinline__ void wb_nacc_add(uint64_t* nacc, uint64_t c, uint64_t u, bool nan, bool active) {
+    const unsigned full = 0xFFFFFFFFu;
+    const unsigned act = __ballot_sync(full, active);
+    if (!act) return;
+    const int leader = __ffs(act) - 1;
+    const uint64_t c0 = __shfl_sync(full, c, leader);
+    const bool same = active && c == c0;
+    uint64_t v = same ? u : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(full, v, o);
+    const bool anynan = __any_sync(full, same && nan);
+    if ((threadIdx.x & 31) == unsigned(leader)) {
+        if (v) atomicAdd(reinterpret_cast<unsigned long long*>(nacc + c0), (unsigned long long)v);
+        if (anynan) atomicOr(reinterpret_cast<unsigned long long*>(nacc + c0), (unsigned long long)kNaccNaN);
+    }
+    if (active && !same) {
+        if (u) atomicAdd(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)u);
+        if (nan) atomicOr(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)kNaccNaN);
+    }
+}
+
+// This CTA's staging vectors of segment [e0, e1) (the reduce pattern: every segment's, since
+// the exit barrier covered the pushes of CTA b on every rank) -> pool, + units.
+__device__ void wb_segment(const RingArgs& a, const uint64_t* list, uint64_t k, uint64_t e0, uint64_t e1,
+                           uint64_t gtid, uint64_t T) {
+    const uint16_t* stg = reinterpret_cast<const uint16_t*>(a.bufs[a.rank]);
+    uint16_t* pool = reinterpret_cast<uint16_t*>(a.wb_pool);
+    const uint64_t v0 = (e0 + 7) / 8, v1 = e1 / 8;
+    auto scalar = [&](uint64_t b, uint64_t e) {
+        for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+            uint64_t c;
+            const uint64_t d = wb_target(a, list, k, i, c);
+            const uint16_t h = reinterpret_cast<const volatile uint16_t*>(stg)[i];
+            pool[d] = h;
+            if ((h & 0x7C00u) == 0x7C00u)
+                atomicOr(reinterpret_cast<unsigned long long*>(a.wb_nacc + c), (unsigned long long)kNaccNaN);
+            else if (half_units(h))
+                atomicAdd(reinterpret_cast<unsigned long long*>(a.wb_nacc + c), (unsigned long long)half_units(h));
+        }
+    };
+    if (v0 >= v1) {
+        if (blockIdx.x == 0) scalar(e0, e1);
+        return;
+    }
+    if (blockIdx.x == 0) {
+        scalar(e0, v0 * 8);
+        scalar(v1 * 8, e1);
+    }
+    // whole-warp iterations (the aggregation's shuffles need every lane), U vectors in flight
+    constexpr int U = 4;
+    const uint64_t lane = gtid & 31;
+    for (uint64_t base = v0 + gtid - lane; base < v1; base += T * U) {
+        uint4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t vv = base + uint64_t(u) * T + lane;
+            if (vv < v1)
+                asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];"  // peers wrote it: skip L1
+                             : "=r"(x[u].x), "=r"(x[u].y), "=r"(x[u].z), "=r"(x[u].w)
+                             : "l"(stg + vv * 8));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t vv = base + uint64_t(u) * T + lane;
+            if (base + uint64_t(u) * T >= v1) break;  // warp-uniform
+            const bool act = vv < v1;
+            uint64_t c = 0, un = 0;
+            bool nan = false;
+            if (act) {
+                const uint64_t d = wb_target(a, list, k, vv * 8, c);
+                gfd::st16(pool + d, x[u]);
+                nan = gfd::any_special(x[u]);
+                if (!nan) un = gfd::units8(x[u]);
+            }
+            wb_nacc_add(a.wb_nacc, c, un, nan, act);
+        }
+    }
+}
+
 template <int DT, int NT, bool P2P>
 __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constant__ RingArgs a) {
     constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
@@ -102,8 +196,23 @@ __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constan
         reduce_segment<DT, NT>(a, src, n, e0, e0 + base + (up < rem ? 1 : 0), gtid, T);
     }
     if (tr) a.trace[2] = gfd::globaltimer_ns();
-    if (P2P && cross_barrier(a, epoch + 2, &s_ok, true) && threadIdx.x == 0) a.epochs[blockIdx.x] = epoch + 2;
+    if (P2P && !cross_barrier(a, epoch + 2, &s_ok, true)) return;
+    if (P2P && threadIdx.x == 0) a.epochs[blockIdx.x] = epoch + 2;
     if (tr) a.trace[3] = gfd::globaltimer_ns();
+    if (DT == GF_F16 && P2P && a.wb_pool != nullptr && nwin > 0) {  // fused CSC write-back
+        extern __shared__ uint64_t wb_list[];  // the plan's important chunks (plan[1] <= nc)
+        const uint64_t k = a.plan[1];
+        for (uint64_t q = threadIdx.x; q < k; q += blockDim.x) wb_list[q] = a.plan[4 + q];
+        __syncthreads();
+        for (int w = 0; w < nwin; ++w) {
+            const uint64_t ws = uint64_t(w) * stride, wl = (w == nwin - 1) ? staged - ws : stride;
+            const uint64_t base = wl / uint64_t(n), rem = wl % uint64_t(n);
+            for (int j = 0; j < n; ++j) {
+                const uint64_t uj = uint64_t(j), e0 = ws + uj * base + min(uj, rem);
+                wb_segment(a, wb_list, k, e0, e0 + base + (uj < rem ? 1 : 0), gtid, T);
+            }
+        }
+    }
 }
 
 // ---- K5: norm exchange + selection (one CTA) -----------------------------------
@@ -174,23 +283,23 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
 }
 
 template <int DT, bool P2P>
-void launch_ring_dt(const RingArgs& a, dim3 grid, cudaStream_t s) {
+void launch_ring_dt(const RingArgs& a, dim3 grid, cudaStream_t s, size_t smem) {
     switch (a.world) {
-        case 2: ring_kernel<DT, 2, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
-        case 3: ring_kernel<DT, 3, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
-        case 4: ring_kernel<DT, 4, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
-        case 5: ring_kernel<DT, 5, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
-        case 6: ring_kernel<DT, 6, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
-        case 7: ring_kernel<DT, 7, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
-        case 8: ring_kernel<DT, 8, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
-        default: ring_kernel<DT, 0, P2P><<<grid, kRingThreads, 0, s>>>(a); break;
+        case 2: ring_kernel<DT, 2, P2P><<<grid, kRingThreads, smem, s>>>(a); break;
+        case 3: ring_kernel<DT, 3, P2P><<<grid, kRingThreads, smem, s>>>(a); break;
+        case 4: ring_kernel<DT, 4, P2P><<<grid, kRingThreads, smem, s>>>(a); break;
+        case 5: ring_kernel<DT, 5, P2P><<<grid, kRingThreads, smem, s>>>(a); break;
+        case 6: ring_kernel<DT, 6, P2P><<<grid, kRingThreads, smem, s>>>(a); break;
+        case 7: ring_kernel<DT, 7, P2P><<<grid, kRingThreads, smem, s>>>(a); break;
+        case 8: ring_kernel<DT, 8, P2P><<<grid, kRingThreads, smem, s>>>(a); break;
+        default: ring_kernel<DT, 0, P2P><<<grid, kRingThreads, smem, s>>>(a); break;
     }
 }
-void launch_ring(int dtype, bool p2p, const RingArgs& a, dim3 grid, cudaStream_t s) {
+void launch_ring(int dtype, bool p2p, const RingArgs& a, dim3 grid, cudaStream_t s, size_t smem = 0) {
     if (dtype == GF_F16) {
-        if (p2p) launch_ring_dt<GF_F16, true>(a, grid, s); else launch_ring_dt<GF_F16, false>(a, grid, s);
+        if (p2p) launch_ring_dt<GF_F16, true>(a, grid, s, smem); else launch_ring_dt<GF_F16, false>(a, grid, s, smem);
     } else {
-        if (p2p) launch_ring_dt<GF_F32, true>(a, grid, s); else launch_ring_dt<GF_F32, false>(a, grid, s);
+        if (p2p) launch_ring_dt<GF_F32, true>(a, grid, s, smem); else launch_ring_dt<GF_F32, false>(a, grid, s, smem);
     }
 }
 
@@ -505,6 +614,30 @@ int gf_ring_allreduce_planned(gf_comm* c, int dtype, uint64_t heap_off, const ui
     launch_ring(dtype, true, a, dim3(gfr::ring_blocks(bound)), gfi::S(stream));
     gfi::count_launch();
     return gfi::check_launch("gf_ring_allreduce_planned");
+}
+
+int gf_ring_allreduce_planned_scatter(gf_comm* c, int dtype, uint64_t stage_heap_off, const uint64_t* plan_dev,
+                                      void* pool, uint64_t chunk, uint64_t nc, uint64_t* nacc, void* stream) {
+    if (int rc = comm_ready(c)) return rc;
+    if (dtype != GF_F16 || !plan_dev || !pool || !nacc || chunk == 0 || chunk % 8 != 0 || nc == 0 ||
+        nc > 6144 || (reinterpret_cast<uintptr_t>(pool) & 15u) != 0)
+        return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_planned_scatter: fp16 pool (16-B aligned), chunk % 8 == 0, "
+                                        "nc <= 6144 (chunk list in shared memory), nacc required");
+    if (c->world == 1) return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_planned_scatter: world 1 has no exchange");
+    DeviceGuard g(c->device);
+    RingArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.nwin = -1;
+    a.plan = plan_dev;
+    fill_common(c, a, stage_heap_off);
+    a.wb_pool = static_cast<char*>(pool);
+    a.wb_nacc = nacc;
+    a.wb_chunk = chunk;
+    a.wb_nc = nc;
+    const uint64_t bound = c->heap_bytes > stage_heap_off ? (c->heap_bytes - stage_heap_off) / c->world : 0;
+    launch_ring(dtype, true, a, dim3(gfr::ring_blocks(bound)), gfi::S(stream), size_t(nc) * 8);
+    gfi::count_launch();
+    return gfi::check_launch("gf_ring_allreduce_planned_scatter");
 }
 
 int gf_ring_allreduce_colocated(int dtype, void* const* bufs, int world, const int* ring_order,

@@ -28,6 +28,12 @@ struct RingArgs {
     int* err;
     uint64_t* trace;                     // host-mapped [start, entered, exit_begin, end] or null
     const uint64_t* plan;
+    // planned (CSC) mode only: after the exit barrier every CTA writes its staging vectors
+    // back into the local fp16 pool and adds their exact |x| units to nacc (the work of
+    // gf_csc_scatter, sparse.cpp:162-168, fused into the collective). Null: no write-back.
+    char* wb_pool;
+    uint64_t* wb_nacc;
+    uint64_t wb_chunk, wb_nc;
     uint64_t wstart[kMaxW];
     uint64_t wlen[kMaxW];
 };

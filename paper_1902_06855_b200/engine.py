@@ -294,14 +294,19 @@ class GradSync:
                   None if solo else self.stage_ptr, b["imp"][cur], b["coff"][cur], L.total, L.chunk,
                   L.num_chunks, self._ptrs(grad_ptrs), self._offs, self._cnts, m, self.momentum,
                   nacc, stream)
-        if self.world > 1:
-            mark("ring")
-            capi.call("gf_ring_allreduce_planned", self.comm, self.dtype, self.stage_off,
-                      b["plan"][cur], stream)
         # chunks selected for this iteration (iteration 0 is dense, sparse.cpp:45-51)
         k_cur = L.num_chunks if self.iteration == 0 else selection_count(
             sparsity_at(self.iteration, self.warmup_iters, self.final_sparsity), L.num_chunks)
-        if not solo:
+        fused_wb = not solo and nacc is not None and L.chunk % 8 == 0 and L.num_chunks <= 6144
+        if fused_wb:  # exchange + write-back + exact L1 of the exchanged chunks, one launch
+            mark("ring_scatter")
+            capi.call("gf_ring_allreduce_planned_scatter", self.comm, self.dtype, self.stage_off,
+                      b["plan"][cur], self.pool_ptr, L.chunk, L.num_chunks, nacc, stream)
+        elif not solo:
+            mark("ring")
+            capi.call("gf_ring_allreduce_planned", self.comm, self.dtype, self.stage_off,
+                      b["plan"][cur], stream)
+        if not solo and not fused_wb:
             mark("scatter")
             capi.call("gf_csc_scatter", self.dtype, self.pool_ptr, self.stage_ptr, b["plan"][cur],
                       b["coff"][cur], L.total, L.chunk, L.num_chunks, k_cur, nacc, stream)

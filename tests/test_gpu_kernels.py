@@ -612,3 +612,20 @@ def test_overlap_api_world1(gf, oracle, G):
     with pytest.raises(capi.ConfigError):
         sync.finalize_iteration()
     sync.close()
+
+
+def test_chunk_norms_every_finite_half(gf, oracle, G):
+    """Exact-unit L1 (|h| * 2^24 via fp32, gf_device.cuh units8/half_units) over every finite
+    half, one per chunk and eight per chunk, vs the oracle's sequential fp64 chunk_l1."""
+    h = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    h = h[(h & 0x7C00) != 0x7C00]
+    for chunk in (1, 8):
+        n = (h.size // chunk) * chunk
+        pool = np.ascontiguousarray(h[:n])
+        nc = n // chunk
+        d = G.dev(pool)
+        out = G.zeros(nc, np.float32)
+        gf.call("gf_chunk_norms", F16, d.data_ptr(), n, chunk, nc, None, 1, out.data_ptr(), None)
+        G.sync()
+        want = oracle.chunk_norms(pool, chunk, nc, None, 1, dtype=F16)
+        assert (G.bits(G.host(out)) == G.bits(want)).all(), chunk
