@@ -197,6 +197,9 @@ def main():
                     help="also measure the dense sync overlapped with a synthetic backward of "
                          "this many ms (bf16 GEMMs; tensors complete in descending id, theta "
                          "windows launch as they close: the reference's lazy allreduce)")
+    ap.add_argument("--dense-mode", default="pull", choices=["pull", "push", "fused"],
+                    help="dense N>1: pull (pack + pull RS/AG fused with unpack), push (pack + "
+                         "push-pull ring + unpack) or fused (one kernel)")
     ap.add_argument("--fused", action="store_true",
                     help="dense: one fused pack+ring+unpack kernel per step (gf_sync_step_dense)")
     args = ap.parse_args()
@@ -230,8 +233,11 @@ def main():
 
     sizes = wl["sizes"]
     csc = wl["csc"]
+    if args.fused:
+        args.dense_mode = "fused"
     sync = GradSync(sizes, rank=rank, world=world, device=local, theta=wl["theta"], csc=csc,
-                    final_sparsity=wl.get("sparsity", 0.9), allgather=allgather)
+                    final_sparsity=wl.get("sparsity", 0.9), allgather=allgather,
+                    dense_mode=args.dense_mode)
     L = sync.layout
     total = L.total
     esz = 2
@@ -369,13 +375,14 @@ def main():
         ring_bytes = ring_bus_bytes(L, esz, world, wlen)
     algo["ring"] = ring_bytes if world > 1 else None
     algo["ring_scatter"] = algo["ring"]  # CSC exchange with the write-back fused in
+    algo["ring_unpack"] = algo["ring"]   # dense pull mode: RS + AG with the unpack fused in
     if args.fused:  # its binding roofline: NVLink bus bytes at N>1, HBM bytes at N=1
         algo["fused_step"] = ring_bytes if world > 1 else total * 12
     dom = max(seg_ms, key=lambda k: seg_ms[k]) if seg_ms else None
     roof = None
     if dom is not None and algo.get(dom):
         t_s = seg_ms[dom] / 1e3
-        if dom in ("ring", "ring_scatter") or (dom == "fused_step" and world > 1):
+        if dom in ("ring", "ring_scatter", "ring_unpack") or (dom == "fused_step" and world > 1):
             ach = algo[dom] / t_s / 1e9
             roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": 900.0, "unit": "GB/s",
                     "frac": round(ach / 900.0, 3), "traffic": None, "kernel": "ring_kernel",
@@ -405,7 +412,7 @@ def main():
         d = {"ms": round(v, 4)}
         if algo.get(k):
             d["GBps"] = round(algo[k] / (v / 1e3) / 1e9, 1)
-            if k not in ("ring", "ring_scatter") and not (k == "fused_step" and world > 1):
+            if k not in ("ring", "ring_scatter", "ring_unpack") and not (k == "fused_step" and world > 1):
                 d["frac_hbm"] = round(d["GBps"] / hbm_peak, 3)
             else:
                 d["busbw_frac_900"] = round(d["GBps"] / 900, 3)
@@ -584,7 +591,7 @@ def main():
 
     if rank == 0:
         bus = None
-        rk = "ring" if "ring" in seg_ms else "ring_scatter"
+        rk = next((k for k in ("ring", "ring_unpack", "ring_scatter") if k in seg_ms), "ring")
         if world > 1 and rk in seg_ms:
             bus = round(ring_bytes / (seg_ms[rk] / 1e3) / 1e9, 1)
         elif world > 1 and "fused_step" in seg_ms:

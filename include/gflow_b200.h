@@ -35,6 +35,8 @@
  *  gf_comm_*                        Communicator + Transport (data plane)    include/gflow/collectives.hpp:25-61, include/gflow/transport.hpp:96-120
  *  gf_ring_allreduce[_planned]      ring_allreduce / ring_allreduce_on       src/collectives.cpp:55-97, :174-177
  *  gf_ring_allreduce_colocated      same, all ranks' buffers on one device   src/collectives.cpp:55-97
+ *  gf_ring_allreduce_unpack         ring_allreduce of the windows + the update read g = get(i)*(1/N)
+ *                                   src/collectives.cpp:55-97, src/trainer.cpp:332-347
  *  gf_sync_step_dense               one dense iteration: write_tensor x m + FusionEngine windows +
  *                                   update read (src/trainer.cpp:297-347), fused into one kernel
  *  gf_csc_select                    select_next_important (norm allreduce + top-k) src/sparse.cpp:172-204
@@ -207,6 +209,19 @@ int gf_sync_step_dense(gf_comm* comm, int dtype, uint64_t pool_heap_off, const f
                        float* const* dst, const uint64_t* pool_off, const uint64_t* count,
                        int ntensors, const uint64_t* win_start, const uint64_t* win_len, int nwin,
                        void* stream);
+/* The allreduce of the theta windows fused with the unpack (gf_ring_allreduce + gf_unpack):
+ * the rank at ring position p sums segment p of every window by pulling it from all pools in
+ * ring order, then pulls every other segment from its owner; each value is unpacked to
+ * dst as x * (1/N) straight from registers and every pool ends holding the sums. Nothing is
+ * pushed over NVLink. dst/pool_off/count are HOST arrays (<= 256 tensors tiling the windows).
+ * flags: GF_RSAG_NO_EXIT_BARRIER skips the final "peers are done reading my pool" barrier; the
+ * caller must then not rewrite this pool before its next collective on the communicator
+ * (alternate two pools: the next collective's entry barrier orders the reuse). */
+#define GF_RSAG_NO_EXIT_BARRIER 1
+int gf_ring_allreduce_unpack(gf_comm* comm, int dtype, uint64_t pool_heap_off, float* const* dst,
+                             const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                             const uint64_t* win_start, const uint64_t* win_len, int nwin, int flags,
+                             void* stream);
 /* Emulation of `world` ranks whose buffers all live on the current device (no waits). */
 int gf_ring_allreduce_colocated(int dtype, void* const* bufs, int world, const int* ring_order,
                                 const uint64_t* win_start, const uint64_t* win_len, int nwin,

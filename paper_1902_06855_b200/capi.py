@@ -21,6 +21,7 @@ GF_OK, GF_ERR_CONFIG, GF_ERR_PROTOCOL, GF_ERR_TRANSPORT, GF_ERR_TRAINING, GF_ERR
 GF_F32, GF_F16 = 0, 1
 GF_MAX_RANKS = 16
 GF_IPC_HANDLE_BYTES = 64
+GF_RSAG_NO_EXIT_BARRIER = 1
 THETA_INF = (1 << 64) - 1
 
 
@@ -91,6 +92,7 @@ SIGNATURES = {
     "gf_ring_allreduce_planned_scatter": [_vp, _i, _u64, _vp, _vp, _u64, _u64, _vp, _vp],
     "gf_ring_allreduce_ptrs": [_vp, _i, _vp, _vp, _vp, _i, _vp],
     "gf_sync_step_dense": [_vp, _i, _u64, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _vp],
+    "gf_ring_allreduce_unpack": [_vp, _i, _u64, _vp, _vp, _vp, _i, _vp, _vp, _i, _i, _vp],
     "gf_ipc_export": [_vp, _vp, _u64p],
     "gf_ipc_open": [_vp, _vp, C.POINTER(_vp)],
     "gf_ipc_close": [_vp, _vp],

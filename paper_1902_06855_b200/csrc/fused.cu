@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cstring>
 #include <numeric>
+#include <string>
 #include <vector>
 
 #include "ring_device.cuh"
@@ -137,10 +138,42 @@ __device__ __forceinline__ void pack_vectors(const StepTable& T, char* pool, uin
     }
 }
 
+// one 16-byte pool vector vv holding x -> fp32 g_avg = x * (1/N) in its tensor(s)
+template <int DT>
+__device__ __forceinline__ void unpack_vec(const StepTable& T, uint64_t vv, uint4 x, float inv) {
+    constexpr int VE = Vec<DT>::kElems;
+    const uint64_t e = vv * VE;
+    int t = tensor_at(T, e);
+    float* d = T.dst[t] + (e - T.off[t]);
+    const bool whole = e + VE <= T.off[t] + T.cnt[t];
+    if (DT == GF_F16 && whole && (reinterpret_cast<uintptr_t>(d) & 31u) == 0 && !gfd::any_special(x)) {
+        const float2 f0 = gfd::h2f2(x.x), f1 = gfd::h2f2(x.y);
+        const float2 f2 = gfd::h2f2(x.z), f3 = gfd::h2f2(x.w);
+        gfd::st32f_stream(d,  // STG.E.256; finite halves: x * (1/N) cannot produce NaN
+                          make_float4(__fmul_rn(f0.x, inv), __fmul_rn(f0.y, inv), __fmul_rn(f1.x, inv),
+                                      __fmul_rn(f1.y, inv)),
+                          make_float4(__fmul_rn(f2.x, inv), __fmul_rn(f2.y, inv), __fmul_rn(f3.x, inv),
+                                      __fmul_rn(f3.y, inv)));
+    } else if (DT == GF_F32 && whole && (reinterpret_cast<uintptr_t>(d) & 15u) == 0) {
+        const float4 f = *reinterpret_cast<const float4*>(&x);
+        __stcs(reinterpret_cast<float4*>(d), make_float4(gfd::mul(f.x, inv), gfd::mul(f.y, inv),
+                                                        gfd::mul(f.z, inv), gfd::mul(f.w, inv)));
+    } else {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&x);
+#pragma unroll
+        for (int k = 0; k < VE; ++k) {
+            const uint64_t ek = e + k;
+            while (t + 1 < T.n && T.off[t + 1] <= ek) ++t;
+            const float xv = DT == GF_F16 ? gfd::dec(uint16_t((w[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu))
+                                          : gfd::u2f(w[k]);
+            T.dst[t][ek - T.off[t]] = gfd::mul(xv, inv);
+        }
+    }
+}
+
 template <int DT>
 __device__ __forceinline__ void unpack_vectors(const StepTable& T, const char* pool, uint64_t v0, uint64_t v1,
                                                uint64_t g, uint64_t S, float inv) {
-    constexpr int VE = Vec<DT>::kElems;
     constexpr int U = kSweepU;
     for (uint64_t v = v0 + g; v < v1; v += S * U) {
         uint4 x[U];
@@ -152,34 +185,7 @@ __device__ __forceinline__ void unpack_vectors(const StepTable& T, const char* p
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint64_t vv = v + uint64_t(u) * S;
-            if (vv >= v1) continue;
-            const uint64_t e = vv * VE;
-            int t = tensor_at(T, e);
-            float* d = T.dst[t] + (e - T.off[t]);
-            const bool whole = e + VE <= T.off[t] + T.cnt[t];
-            if (DT == GF_F16 && whole && (reinterpret_cast<uintptr_t>(d) & 31u) == 0 && !gfd::any_special(x[u])) {
-                const float2 f0 = gfd::h2f2(x[u].x), f1 = gfd::h2f2(x[u].y);
-                const float2 f2 = gfd::h2f2(x[u].z), f3 = gfd::h2f2(x[u].w);
-                gfd::st32f_stream(d,  // STG.E.256; finite halves: x * (1/N) cannot produce NaN
-                                  make_float4(__fmul_rn(f0.x, inv), __fmul_rn(f0.y, inv), __fmul_rn(f1.x, inv),
-                                              __fmul_rn(f1.y, inv)),
-                                  make_float4(__fmul_rn(f2.x, inv), __fmul_rn(f2.y, inv), __fmul_rn(f3.x, inv),
-                                              __fmul_rn(f3.y, inv)));
-            } else if (DT == GF_F32 && whole && (reinterpret_cast<uintptr_t>(d) & 15u) == 0) {
-                const float4 f = *reinterpret_cast<const float4*>(&x[u]);
-                __stcs(reinterpret_cast<float4*>(d), make_float4(gfd::mul(f.x, inv), gfd::mul(f.y, inv),
-                                                                gfd::mul(f.z, inv), gfd::mul(f.w, inv)));
-            } else {
-                const uint32_t* w = reinterpret_cast<const uint32_t*>(&x[u]);
-#pragma unroll
-                for (int k = 0; k < VE; ++k) {
-                    const uint64_t ek = e + k;
-                    while (t + 1 < T.n && T.off[t + 1] <= ek) ++t;
-                    const float xv = DT == GF_F16 ? gfd::dec(uint16_t((w[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu))
-                                                  : gfd::u2f(w[k]);
-                    T.dst[t][ek - T.off[t]] = gfd::mul(xv, inv);
-                }
-            }
+            if (vv < v1) unpack_vec<DT>(T, vv, x[u], inv);
         }
     }
 }
@@ -259,6 +265,222 @@ void launch_step(const RingArgs& a, const StepTable& T, float inv, int grid, cud
     }
 }
 
+// ---- gf_ring_allreduce_unpack: pull reduce-scatter, then pull all-gather fused with unpack ----
+// The rank at ring position p sums segment p of every window from all N pools in ring order
+// (the reference's arrival order, as reduce_segment), keeps the sum in its OWN pool only and
+// unpacks it from registers. After one barrier with its peer CTAs it PULLS every other
+// segment from the rank that owns it, writes it into its pool (every pool ends holding the
+// sums, as after ring_allreduce) and unpacks it. Nothing is pushed, so no barrier waits for
+// posted NVLink writes to drain; and the separate unpack pass (re-reading the pool) is gone.
+template <int DT>
+__device__ __forceinline__ uint4 ld16_cg(const void* p) {  // L2 only: a peer wrote it this launch
+    uint4 v;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+template <int DT, int NT>
+__device__ void rs_pull_segment(const RingArgs& a, const StepTable& T, const char* const* src, int n,
+                                uint64_t e0, uint64_t e1, uint64_t g, uint64_t S, float inv) {
+    constexpr int VE = Vec<DT>::kElems;
+    constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
+    constexpr int U = NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1);
+    char* local = const_cast<char*>(src[0]);  // ring[pos] == rank
+    uint64_t v0 = (e0 + VE - 1) / VE, v1 = e1 / VE;
+    if (v0 >= v1) v0 = v1 = e1 / VE + 1;  // no aligned vector inside: all scalar
+    if (blockIdx.x == 0) {  // unaligned edges (or the whole segment), scalar, CTA 0
+        auto edge = [&](uint64_t lo, uint64_t hi) {
+            for (uint64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+                float xv;
+                if (DT == GF_F16) {
+                    uint16_t acc = reinterpret_cast<const uint16_t*>(src[0])[e];
+                    for (int t = 1; t < n; ++t) acc = gfd::acc16(reinterpret_cast<const uint16_t*>(src[t])[e], acc);
+                    reinterpret_cast<uint16_t*>(local)[e] = acc;
+                    xv = gfd::dec(acc);
+                } else {
+                    float acc = reinterpret_cast<const float*>(src[0])[e];
+                    for (int t = 1; t < n; ++t) acc = gfd::add(reinterpret_cast<const float*>(src[t])[e], acc);
+                    reinterpret_cast<float*>(local)[e] = acc;
+                    xv = acc;
+                }
+                const int t = tensor_at(T, e);
+                T.dst[t][e - T.off[t]] = gfd::mul(xv, inv);
+            }
+        };
+        if (v0 < v1) {
+            edge(e0, v0 * VE);
+            edge(v1 * VE, e1);
+        } else {
+            edge(e0, e1);
+        }
+    }
+    for (uint64_t v = v0 + g; v < v1; v += S * U) {
+        uint4 x[U][NMAX];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t vv = v + uint64_t(u) * S;
+            if (vv < v1) {
+#pragma unroll
+                for (int t = 0; t < NMAX; ++t)
+                    if (t < n) x[u][t] = gfd::ld16(src[t] + vv * 16);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t vv = v + uint64_t(u) * S;
+            if (vv < v1) {
+                uint4 acc = x[u][0];
+#pragma unroll
+                for (int t = 1; t < NMAX; ++t)
+                    if (t < n) acc = Vec<DT>::acc(x[u][t], acc);
+                gfd::st16_keep(local + vv * 16, acc);  // the peers pull it next
+                unpack_vec<DT>(T, vv, acc, inv);
+            }
+        }
+    }
+}
+
+template <int DT>
+__device__ void ag_pull_segment(const StepTable& T, const char* owner, char* local, uint64_t e0, uint64_t e1,
+                                uint64_t g, uint64_t S, float inv) {
+    constexpr int VE = Vec<DT>::kElems;
+    constexpr int U = 8;
+    uint64_t v0 = (e0 + VE - 1) / VE, v1 = e1 / VE;
+    if (v0 >= v1) v0 = v1 = e1 / VE + 1;
+    if (blockIdx.x == 0) {
+        auto edge = [&](uint64_t lo, uint64_t hi) {
+            for (uint64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+                float xv;
+                if (DT == GF_F16) {
+                    const uint16_t h = reinterpret_cast<const volatile uint16_t*>(owner)[e];
+                    reinterpret_cast<uint16_t*>(local)[e] = h;
+                    xv = gfd::dec(h);
+                } else {
+                    xv = reinterpret_cast<const volatile float*>(owner)[e];
+                    reinterpret_cast<float*>(local)[e] = xv;
+                }
+                const int t = tensor_at(T, e);
+                T.dst[t][e - T.off[t]] = gfd::mul(xv, inv);
+            }
+        };
+        if (v0 < v1) {
+            edge(e0, v0 * VE);
+            edge(v1 * VE, e1);
+        } else {
+            edge(e0, e1);
+        }
+    }
+    for (uint64_t v = v0 + g; v < v1; v += S * U) {
+        uint4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t vv = v + uint64_t(u) * S;
+            if (vv < v1) x[u] = ld16_cg<DT>(owner + vv * 16);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t vv = v + uint64_t(u) * S;
+            if (vv < v1) {
+                gfd::st16(local + vv * 16, x[u]);
+                unpack_vec<DT>(T, vv, x[u], inv);
+            }
+        }
+    }
+}
+
+template <int DT, int NT>
+__global__ void __launch_bounds__(kRingThreads)
+rsag_kernel(const __grid_constant__ RingArgs a, const __grid_constant__ StepTable T, float inv, int exit_barrier) {
+    constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
+    __shared__ int s_ok;
+    const uint64_t epoch = a.epochs[blockIdx.x];
+    if (threadIdx.x == 0) s_ok = 1;
+    const int n = NT > 0 ? NT : a.world;
+    const uint64_t S = uint64_t(gridDim.x) * blockDim.x;
+    const uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool tr = a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    if (tr) a.trace[0] = gfd::globaltimer_ns();
+    if (!cross_barrier(a, epoch + 1, &s_ok, false)) return;  // peers' pools are packed
+    if (tr) a.trace[1] = gfd::globaltimer_ns();
+    const char* src[NMAX];
+#pragma unroll
+    for (int t = 0; t < NMAX; ++t) src[t] = (t < n) ? a.bufs[a.ring[(a.pos + t) % n]] : nullptr;
+    for (int w = 0; w < a.nwin; ++w) {
+        uint64_t e0, e1;
+        segment(a, n, w, a.pos, e0, e1);
+        rs_pull_segment<DT, NT>(a, T, src, n, e0, e1, g, S, inv);
+    }
+    if (tr) a.trace[2] = gfd::globaltimer_ns();
+    if (!cross_barrier(a, epoch + 2, &s_ok, true)) return;  // my segment sums are visible
+    char* local = a.bufs[a.rank];
+    for (int w = 0; w < a.nwin; ++w) {
+        for (int j = 1; j < n; ++j) {  // next ring position first: owners differ across ranks
+            const int q = (a.pos + j) % n;
+            uint64_t e0, e1;
+            segment(a, n, w, q, e0, e1);
+            ag_pull_segment<DT>(T, a.bufs[a.ring[q]], local, e0, e1, g, S, inv);
+        }
+    }
+    uint64_t fin = epoch + 2;
+    if (exit_barrier) {  // the peers are done reading my pool (no write drain involved)
+        if (!cross_barrier(a, epoch + 3, &s_ok, false)) return;
+        fin = epoch + 3;
+    }
+    if (threadIdx.x == 0) a.epochs[blockIdx.x] = fin;
+    if (tr) a.trace[3] = gfd::globaltimer_ns();
+}
+
+template <int DT>
+void launch_rsag(const RingArgs& a, const StepTable& T, float inv, int exit_barrier, int grid, cudaStream_t s) {
+    switch (a.world) {
+        case 2: rsag_kernel<DT, 2><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier); break;
+        case 4: rsag_kernel<DT, 4><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier); break;
+        case 8: rsag_kernel<DT, 8><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier); break;
+        default: rsag_kernel<DT, 0><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier); break;
+    }
+}
+
+// tensor table in pool order; checks the tensors tile [off[0], hi) without overlap
+int build_table(const char* fn, const float* const* src, float* const* dst, const uint64_t* pool_off,
+                const uint64_t* count, int ntensors, StepTable& T, uint64_t& hi) {
+    std::vector<int> order(static_cast<size_t>(ntensors));
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int x, int y) { return pool_off[x] < pool_off[y]; });
+    std::memset(&T, 0, sizeof(T));
+    T.n = ntensors;
+    hi = 0;
+    for (int i = 0; i < ntensors; ++i) {
+        const int k = order[static_cast<size_t>(i)];
+        T.off[i] = pool_off[k];
+        T.cnt[i] = count[k];
+        T.src[i] = src ? src[k] : nullptr;
+        T.dst[i] = dst[k];
+        if ((src && !src[k]) || !dst[k]) return gfi::fail(GF_ERR_CONFIG, std::string(fn) + ": null tensor");
+        if (i > 0 && T.off[i] < T.off[i - 1] + T.cnt[i - 1])
+            return gfi::fail(GF_ERR_CONFIG, std::string(fn) + ": tensors overlap in the pool");
+        hi = std::max(hi, T.off[i] + T.cnt[i]);
+    }
+    return GF_OK;
+}
+
+// the tensors and the windows must tile the same pool range: every element is reduced and
+// unpacked exactly once
+int check_tiling(const char* fn, const StepTable& T, uint64_t hi, const uint64_t* win_start,
+                 const uint64_t* win_len, int nwin) {
+    for (int i = 0; i + 1 < T.n; ++i)
+        if (T.off[i] + T.cnt[i] != T.off[i + 1])
+            return gfi::fail(GF_ERR_CONFIG, std::string(fn) + ": tensors must tile the pool");
+    uint64_t cover = T.off[0];
+    for (int w = 0; w < nwin; ++w) {
+        if (win_start[w] != cover) return gfi::fail(GF_ERR_CONFIG, std::string(fn) + ": windows must tile the pool");
+        cover += win_len[w];
+    }
+    if (cover != hi) return gfi::fail(GF_ERR_CONFIG, std::string(fn) + ": windows must tile the pool");
+    return GF_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -272,41 +494,16 @@ int gf_sync_step_dense(gf_comm* c, int dtype, uint64_t pool_heap_off, const floa
         !count || nwin < 1 || !win_start || !win_len)
         return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense: bad arguments (1..256 tensors, >= 1 window)");
     const uint64_t es = gfi::esz(dtype);
-    std::vector<int> order(static_cast<size_t>(ntensors));  // tensor table in pool order
-    std::iota(order.begin(), order.end(), 0);
-    std::sort(order.begin(), order.end(), [&](int x, int y) { return pool_off[x] < pool_off[y]; });
     StepTable T;
-    std::memset(&T, 0, sizeof(T));
-    T.n = ntensors;
     uint64_t hi = 0;
-    for (int i = 0; i < ntensors; ++i) {
-        const int k = order[static_cast<size_t>(i)];
-        T.off[i] = pool_off[k];
-        T.cnt[i] = count[k];
-        T.src[i] = src[k];
-        T.dst[i] = dst[k];
-        if (!src[k] || !dst[k]) return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense: null tensor");
-        if (i > 0 && T.off[i] < T.off[i - 1] + T.cnt[i - 1])
-            return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense: tensors overlap in the pool");
-        hi = std::max(hi, T.off[i] + T.cnt[i]);
-    }
+    if (int rc = build_table("gf_sync_step_dense", src, dst, pool_off, count, ntensors, T, hi)) return rc;
     if (pool_heap_off + hi * es > c->heap_bytes)
         return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense: pool outside the symmetric heap");
     DeviceGuard guard(c->device);
     if (c->world == 1)  // no collective: pack and unpack in one streaming pass
         return gfi::pack_unpack_solo(dtype, c->alloc + kFlagBytes + pool_heap_off, src, dst, pool_off, count,
                                      ntensors, gfi::S(stream));
-    // the tensors and the windows must tile the same pool range: every element is packed,
-    // reduced and unpacked exactly once
-    for (int i = 0; i + 1 < ntensors; ++i)
-        if (T.off[i] + T.cnt[i] != T.off[i + 1])
-            return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense: tensors must tile the pool");
-    uint64_t cover = T.off[0];
-    for (int w = 0; w < nwin; ++w) {
-        if (win_start[w] != cover) return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense: windows must tile the pool");
-        cover += win_len[w];
-    }
-    if (cover != hi) return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense: windows must tile the pool");
+    if (int rc = check_tiling("gf_sync_step_dense", T, hi, win_start, win_len, nwin)) return rc;
     const float inv = 1.0f / static_cast<float>(c->world);
     for (int first = 0; first < nwin; first += kMaxW) {
         RingArgs a;
@@ -324,6 +521,47 @@ int gf_sync_step_dense(gf_comm* c, int dtype, uint64_t pool_heap_off, const floa
         else launch_step<GF_F32>(a, T, inv, grid, gfi::S(stream));
         gfi::count_launch();
         if (int rc = gfi::check_launch("gf_sync_step_dense")) return rc;
+    }
+    return GF_OK;
+}
+
+int gf_ring_allreduce_unpack(gf_comm* c, int dtype, uint64_t pool_heap_off, float* const* dst,
+                             const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                             const uint64_t* win_start, const uint64_t* win_len, int nwin, int flags,
+                             void* stream) {
+    static const char* fn = "gf_ring_allreduce_unpack";
+    if (int rc = comm_ready(c)) return rc;
+    if (!gfi::valid_dtype(dtype) || ntensors < 1 || ntensors > kStepMaxT || !dst || !pool_off || !count ||
+        nwin < 1 || !win_start || !win_len || (flags & ~GF_RSAG_NO_EXIT_BARRIER))
+        return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_unpack: bad arguments (1..256 tensors, >= 1 window)");
+    StepTable T;
+    uint64_t hi = 0;
+    if (int rc = build_table(fn, nullptr, dst, pool_off, count, ntensors, T, hi)) return rc;
+    const uint64_t es = gfi::esz(dtype);
+    if (pool_heap_off + hi * es > c->heap_bytes)
+        return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_unpack: pool outside the symmetric heap");
+    if (int rc = check_tiling(fn, T, hi, win_start, win_len, nwin)) return rc;
+    DeviceGuard guard(c->device);
+    if (c->world == 1)  // the collective is the identity (collectives.cpp:59)
+        return gf_unpack(dtype, c->alloc + kFlagBytes + pool_heap_off, dst, pool_off, count, ntensors, 1, stream);
+    const float inv = 1.0f / static_cast<float>(c->world);
+    const int exit_barrier = (flags & GF_RSAG_NO_EXIT_BARRIER) ? 0 : 1;
+    for (int first = 0; first < nwin; first += kMaxW) {
+        RingArgs a;
+        std::memset(&a, 0, sizeof(a));
+        a.nwin = std::min(kMaxW, nwin - first);
+        uint64_t max_seg = 0;
+        for (int w = 0; w < a.nwin; ++w) {
+            a.wstart[w] = win_start[first + w];
+            a.wlen[w] = win_len[first + w];
+            max_seg += (a.wlen[w] + c->world - 1) / c->world;
+        }
+        fill_common(c, a, pool_heap_off);
+        const int grid = gfr::ring_blocks(max_seg * es);
+        if (dtype == GF_F16) launch_rsag<GF_F16>(a, T, inv, exit_barrier, grid, gfi::S(stream));
+        else launch_rsag<GF_F32>(a, T, inv, exit_barrier, grid, gfi::S(stream));
+        gfi::count_launch();
+        if (int rc = gfi::check_launch(fn)) return rc;
     }
     return GF_OK;
 }

@@ -110,7 +110,7 @@ class GradSync:
 
     def __init__(self, sizes, rank=0, world=1, device=0, dtype=F16, theta=64 << 20,
                  chunk=32000, csc=False, final_sparsity=0.9, warmup_iters=0, momentum=0.9,
-                 lr=0.01, allgather=None, timeout_ms=30000):
+                 lr=0.01, allgather=None, timeout_ms=30000, dense_mode="pull"):
         self.layout = PoolLayout.build(sizes, chunk)
         self.rank, self.world, self.device, self.dtype = rank, world, device, dtype
         self.esz = 2 if dtype == F16 else 4
@@ -118,8 +118,18 @@ class GradSync:
         self.final_sparsity, self.warmup_iters = final_sparsity, warmup_iters
         self.momentum, self.lr = momentum, lr
         L = self.layout
+        if dense_mode not in ("pull", "push", "fused"):
+            raise capi.ConfigError(f"dense_mode {dense_mode!r}: pull, push or fused")
+        self.dense_mode = dense_mode
         self.pool_off = 0
         self.stage_off = _align(L.total * self.esz)
+        # dense pull mode at N>1: two pools used alternately, so a step never waits for the
+        # peers to finish reading the previous step's pool (GF_RSAG_NO_EXIT_BARRIER)
+        self._pull_pools = None
+        if dense_mode == "pull" and world > 1 and not csc:
+            self._pull_pools = [0, self.stage_off]
+            self.stage_off += _align(L.total * self.esz)
+        self._pull_flip = 0
         self.norms_off = self.stage_off + (_align(L.total * self.esz) if csc else 0)
         heap = self.norms_off + _align(L.num_chunks * 4)
         self.comm = C.c_void_p()
@@ -136,6 +146,7 @@ class GradSync:
         capi.call("gf_comm_heap", self.comm, C.byref(base), None)
         self.heap_base = base.value
         self.pool_ptr = self.heap_base + self.pool_off
+        self.last_pool_ptr = self.pool_ptr  # pool that holds the last dense step's sums
         self.stage_ptr = self.heap_base + self.stage_off
         self.norms_ptr = self.heap_base + self.norms_off
         ws, wl = dense_windows(L, self.esz, theta)
@@ -185,6 +196,25 @@ class GradSync:
                       self._win[2], stream)
             mark(None)
             return
+        if self.world > 1 and self.dense_mode == "fused" and not ring_only:
+            return self.fused_step(grad_ptrs, out_ptrs, stream=stream, mark=mark)
+        if self.world > 1 and self.dense_mode == "pull" and not ring_only:
+            # pack -> pull reduce-scatter + pull all-gather fused with the unpack
+            pool_off, flags = self.pool_off, 0
+            if self._pull_pools is not None:
+                pool_off = self._pull_pools[self._pull_flip]
+                self._pull_flip ^= 1
+                flags = capi.GF_RSAG_NO_EXIT_BARRIER
+            self.last_pool_ptr = self.heap_base + pool_off
+            mark("pack")
+            capi.call("gf_pack", self.dtype, self.last_pool_ptr, self._ptrs(grad_ptrs), self._offs,
+                      self._cnts, m, 1.0, stream)
+            mark("ring_unpack")
+            capi.call("gf_ring_allreduce_unpack", self.comm, self.dtype, pool_off, self._ptrs(out_ptrs),
+                      self._offs, self._cnts, m, self._win[0], self._win[1], self._win[2], flags, stream)
+            mark(None)
+            return
+        self.last_pool_ptr = self.pool_ptr
         if not ring_only:
             mark("pack")
             capi.call("gf_pack", self.dtype, self.pool_ptr, self._ptrs(grad_ptrs), self._offs,

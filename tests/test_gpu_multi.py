@@ -109,6 +109,58 @@ def _worker_ring(rank, world, port):
     dist.barrier()
 
 
+def _worker_rsag(rank, world, port):
+    """gf_ring_allreduce_unpack (pull RS + pull AG fused with the unpack): pools and g_avg
+    bit-exact vs the oracle ring + unpack, with and without the exit barrier."""
+    comm, base, capi, cudart, dist = _setup(rank, world, port)
+    import torch
+    from oracle.oracle import RESNET50, Oracle
+    o = Oracle()
+    rng = np.random.default_rng(11)
+    order = rng.permutation(world).astype(np.int32)
+    cases = [(RESNET50, F16, 1 << 20), (RESNET50, F16, capi.THETA_INF),
+             ([5, 97, 1, 4099, 3_000_001, 8, 77], F16, 4096), ([5, 97, 1, 4099, 300_001, 8, 77], F32, 1 << 16),
+             ([3], F16, capi.THETA_INF), ([1, 2], F32, capi.THETA_INF)]
+    it = 0
+    for ci, (sizes, dt, theta) in enumerate(cases):
+        esz = 2 if dt == F16 else 4
+        off, _, _ = o.pool_layout(sizes, 32000)
+        ws, wl = o.dense_windows(sizes, esz, theta)
+        total = int(sum(sizes))
+        pool_offs = [0, ((total * esz + 4095) // 4096) * 4096]
+        cur = order if ci % 2 else np.arange(world, dtype=np.int32)
+        capi.call("gf_comm_set_ring_order", comm, capi.int_array(cur))
+        for flags in (0, capi.GF_RSAG_NO_EXIT_BARRIER):
+            for rep in range(3):  # fresh data each time: pool reuse under both protocols
+                it += 1
+                grads = [o.gen_grads(100 * it + r, sizes) for r in range(world)]
+                for r in range(world):
+                    grads[r][::97] *= 3e4  # clamped / overflowing sums
+                pools = [o.pack(g, sizes, dtype=dt) for g in grads]
+                po = pool_offs[rep % 2] if flags else 0
+                _put(cudart, base, po, pools[rank])
+                # dst: one flat fp32 buffer cut at odd offsets (unaligned tensors take the scalar path)
+                flat = torch.full((total + 3,), float("nan"), device="cuda")
+                bounds = np.concatenate([[0], np.cumsum(sizes)])
+                shift = 1 if it % 2 else 0
+                dst = [flat[shift + int(bounds[i]):shift + int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
+                capi.call("gf_ring_allreduce_unpack", comm, dt, po, capi.ptr_array(dst), capi.u64_array(off),
+                          capi.u64_array(sizes), len(sizes), capi.u64_array(ws), capi.u64_array(wl), len(ws),
+                          flags, None)
+                torch.cuda.synchronize()
+                want = o.ring_allreduce([p.copy() for p in pools], dtype=dt, windows=(ws, wl), ring_order=cur)
+                got_pool = _get(cudart, base, po, pools[rank])
+                assert (_bits(got_pool) == _bits(want[rank])).all(), (sizes[:3], dt, theta, flags, rep)
+                g_avg = o.unpack(want[rank], world, dtype=dt)
+                h = flat.cpu().numpy()[shift:shift + total]
+                for i, sz in enumerate(sizes):
+                    a = h[int(bounds[i]):int(bounds[i + 1])]
+                    b = g_avg[int(off[i]):int(off[i]) + sz]
+                    assert (a.view(np.uint32) == b.view(np.uint32)).all(), ("g_avg", i, dt, flags)
+    capi.call("gf_comm_status", comm)
+    dist.barrier()
+
+
 def _worker_csc(rank, world, port):
     comm, base, capi, cudart, dist = _setup(rank, world, port)
     from oracle.oracle import Oracle
@@ -176,6 +228,11 @@ def test_p2p_ring_bit_exact():
 
 
 @pytest.mark.multigpu(2)
+def test_p2p_ring_allreduce_unpack_bit_exact():
+    _spawn(_worker_rsag, _world())
+
+
+@pytest.mark.multigpu(2)
 def test_p2p_csc_select_and_planned_ring():
     _spawn(_worker_csc, _world())
 
@@ -226,7 +283,8 @@ def test_inprocess_local_connect():
 
 
 def _worker_fused(rank, world, port):
-    """The fused dense step (pack + NVLink ring + unpack in one kernel) over several
+    """The engine's dense step in every mode — one fused kernel, pack + pull RS/AG with the
+    unpack fused in (alternating pools), pack + push-pull ring + unpack — over several
     iterations and theta values, bit-exact against the oracle's unfused path."""
     comm, base, capi, cudart, dist = _setup(rank, world, port)
     import torch
@@ -243,25 +301,31 @@ def _worker_fused(rank, world, port):
         dist.all_gather_object(out, b)
         return out
 
-    for theta in (64 << 20, 1 << 20, 0):
-        sync = GradSync(sizes, rank=rank, world=world, device=rank, theta=theta, allgather=ag)
+    for mode, theta in [(m, t) for m in ("fused", "pull", "push") for t in (64 << 20, 1 << 20, 0)]:
+        sync = GradSync(sizes, rank=rank, world=world, device=rank, theta=theta, allgather=ag,
+                        dense_mode=mode)
         for it in range(3):
             grads = [o.gen_grads(1000 * it + 17 * r + theta % 97, sizes) for r in range(world)]
             g = torch.from_numpy(grads[rank]).cuda()
             out = torch.empty_like(g)
             gp = [g[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
             op = [out[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
-            sync.fused_step(gp, op)
+            sync.dense_step(gp, op)
             torch.cuda.synchronize()
             sync.status()
             ws, wl = o.dense_windows(sizes, 2, theta)
             pools = o.ring_allreduce([o.pack(x, sizes) for x in grads], dtype=F16, windows=(ws, wl))
+            if mode != "fused":  # every rank's pool holds the sums, as after ring_allreduce
+                got_pool = np.empty_like(pools[rank])
+                cudart.memcpy(got_pool.ctypes.data, sync.last_pool_ptr, got_pool.nbytes)
+                cudart.sync_device()
+                assert (got_pool == pools[rank]).all(), (mode, theta, it)
             want_pool = o.unpack(pools[rank], world)
             got = out.cpu().numpy()
             for i, s in enumerate(sizes):
                 w = want_pool[int(off[i]):int(off[i]) + s]
                 assert (got[int(bounds[i]):int(bounds[i + 1])].view(np.uint32) == w.view(np.uint32)).all(), \
-                    (theta, it, i)
+                    (mode, theta, it, i)
         sync.close()
     dist.barrier()
 
