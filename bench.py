@@ -200,6 +200,12 @@ def main():
     ap.add_argument("--dense-mode", default="pull", choices=["pull", "push", "fused"],
                     help="dense N>1: pull (pack + pull RS/AG fused with unpack), push (pack + "
                          "push-pull ring + unpack) or fused (one kernel)")
+    ap.add_argument("--pull-parts", default=None,
+                    help="dense pull mode: piece cut points in 1/1024 of every segment, e.g. 0,256,1024 "
+                         "(piece k+1 is packed while piece k is exchanged)")
+    ap.add_argument("--csc-mode", default="pull", choices=["pull", "push"],
+                    help="CSC N>1 exchange: pull (pull RS/AG straight into the pool) or push "
+                         "(push-pull ring + fused write-back)")
     ap.add_argument("--fused", action="store_true",
                     help="dense: one fused pack+ring+unpack kernel per step (gf_sync_step_dense)")
     args = ap.parse_args()
@@ -237,7 +243,8 @@ def main():
         args.dense_mode = "fused"
     sync = GradSync(sizes, rank=rank, world=world, device=local, theta=wl["theta"], csc=csc,
                     final_sparsity=wl.get("sparsity", 0.9), allgather=allgather,
-                    dense_mode=args.dense_mode)
+                    dense_mode=args.dense_mode, csc_mode=args.csc_mode,
+                    pull_parts=[int(x) for x in args.pull_parts.split(",")] if args.pull_parts else None)
     L = sync.layout
     total = L.total
     esz = 2
@@ -376,13 +383,14 @@ def main():
     algo["ring"] = ring_bytes if world > 1 else None
     algo["ring_scatter"] = algo["ring"]  # CSC exchange with the write-back fused in
     algo["ring_unpack"] = algo["ring"]   # dense pull mode: RS + AG with the unpack fused in
+    algo["pull_step"] = algo["ring"]     # pull mode in pieces: packs overlap the exchanges
     if args.fused:  # its binding roofline: NVLink bus bytes at N>1, HBM bytes at N=1
         algo["fused_step"] = ring_bytes if world > 1 else total * 12
     dom = max(seg_ms, key=lambda k: seg_ms[k]) if seg_ms else None
     roof = None
     if dom is not None and algo.get(dom):
         t_s = seg_ms[dom] / 1e3
-        if dom in ("ring", "ring_scatter", "ring_unpack") or (dom == "fused_step" and world > 1):
+        if dom in ("ring", "ring_scatter", "ring_unpack", "pull_step") or (dom == "fused_step" and world > 1):
             ach = algo[dom] / t_s / 1e9
             roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": 900.0, "unit": "GB/s",
                     "frac": round(ach / 900.0, 3), "traffic": None, "kernel": "ring_kernel",
@@ -412,7 +420,7 @@ def main():
         d = {"ms": round(v, 4)}
         if algo.get(k):
             d["GBps"] = round(algo[k] / (v / 1e3) / 1e9, 1)
-            if k not in ("ring", "ring_scatter", "ring_unpack") and not (k == "fused_step" and world > 1):
+            if k not in ("ring", "ring_scatter", "ring_unpack", "pull_step") and not (k == "fused_step" and world > 1):
                 d["frac_hbm"] = round(d["GBps"] / hbm_peak, 3)
             else:
                 d["busbw_frac_900"] = round(d["GBps"] / 900, 3)
@@ -591,7 +599,7 @@ def main():
 
     if rank == 0:
         bus = None
-        rk = next((k for k in ("ring", "ring_unpack", "ring_scatter") if k in seg_ms), "ring")
+        rk = next((k for k in ("ring", "ring_unpack", "ring_scatter", "pull_step") if k in seg_ms), "ring")
         if world > 1 and rk in seg_ms:
             bus = round(ring_bytes / (seg_ms[rk] / 1e3) / 1e9, 1)
         elif world > 1 and "fused_step" in seg_ms:

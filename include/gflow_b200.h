@@ -39,6 +39,7 @@
  *                                   src/collectives.cpp:55-97, src/trainer.cpp:332-347
  *  gf_sync_step_dense               one dense iteration: write_tensor x m + FusionEngine windows +
  *                                   update read (src/trainer.cpp:297-347), fused into one kernel
+ *  gf_csc_exchange_pull             sparse_exchange ring + write-back (pull form) src/sparse.cpp:106-170
  *  gf_csc_select                    select_next_important (norm allreduce + top-k) src/sparse.cpp:172-204
  *  gf_ring_traffic                  TrafficStats record_send/recv of the ring include/gflow/transport.hpp:48-91, src/collectives.cpp:69-96
  *  gf_oracle_allreduce_ptrs         oracle_allreduce                         src/collectives.cpp:203-226
@@ -199,6 +200,14 @@ int gf_ring_allreduce_planned(gf_comm* comm, int dtype, uint64_t heap_off,
 int gf_ring_allreduce_planned_scatter(gf_comm* comm, int dtype, uint64_t stage_heap_off,
                                       const uint64_t* plan_dev, void* pool, uint64_t chunk,
                                       uint64_t nc, uint64_t* nacc, void* stream);
+/* The same exchange + write-back without pushes: the owner of each segment pulls it from all
+ * staging buffers (ring order), keeps the sum and writes it back; after one barrier every
+ * rank pulls the other segments from their owners straight into its pool (+ exact |x|
+ * units into nacc). Same results as gf_ring_allreduce_planned_scatter, bit for bit. The
+ * staging buffer must not be rewritten before the next collective on the communicator
+ * (gf_csc_select's barrier, in a CSC step). fp16, chunk % 8 == 0, nc <= 6144, world > 1. */
+int gf_csc_exchange_pull(gf_comm* comm, uint64_t stage_heap_off, const uint64_t* plan_dev, void* pool,
+                         uint64_t chunk, uint64_t nc, uint64_t* nacc, void* stream);
 /* One dense sync step as ONE kernel per rank: pack -> ring allreduce of the theta windows ->
  * unpack. Each CTA packs, reduces and unpacks one fixed strided set of pool vectors and only
  * synchronises with its peer CTAs (entry/exit barriers); at world 1 it is a single streaming
@@ -218,10 +227,24 @@ int gf_sync_step_dense(gf_comm* comm, int dtype, uint64_t pool_heap_off, const f
  * caller must then not rewrite this pool before its next collective on the communicator
  * (alternate two pools: the next collective's entry barrier orders the reuse). */
 #define GF_RSAG_NO_EXIT_BARRIER 1
+#define GF_PART_ONE 1024
 int gf_ring_allreduce_unpack(gf_comm* comm, int dtype, uint64_t pool_heap_off, float* const* dst,
                              const uint64_t* pool_off, const uint64_t* count, int ntensors,
                              const uint64_t* win_start, const uint64_t* win_len, int nwin, int flags,
                              void* stream);
+/* The same restricted to piece [part_lo, part_hi) (units of 1/GF_PART_ONE) of EVERY segment of
+ * every window. Pieces do not change any element's summation order, so a step can pack piece
+ * k+1 (gf_pack over gf_part_ranges) while piece k is exchanged; pieces of one step must be
+ * launched in the same order on every rank. */
+int gf_ring_allreduce_unpack_part(gf_comm* comm, int dtype, uint64_t pool_heap_off, float* const* dst,
+                                  const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                                  const uint64_t* win_start, const uint64_t* win_len, int nwin,
+                                  uint32_t part_lo, uint32_t part_hi, int flags, void* stream);
+/* Pool element ranges [lo[i], hi[i]) of piece [part_lo, part_hi) of every segment of the windows
+ * at `world` ranks, in pool order (empty ranges dropped). Returns the count (or -1 if it
+ * exceeds cap). Host-only, no GPU. */
+int gf_part_ranges(const uint64_t* win_start, const uint64_t* win_len, int nwin, int world,
+                   uint32_t part_lo, uint32_t part_hi, uint64_t* lo, uint64_t* hi, int cap);
 /* Emulation of `world` ranks whose buffers all live on the current device (no waits). */
 int gf_ring_allreduce_colocated(int dtype, void* const* bufs, int world, const int* ring_order,
                                 const uint64_t* win_start, const uint64_t* win_len, int nwin,

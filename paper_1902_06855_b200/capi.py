@@ -22,6 +22,7 @@ GF_F32, GF_F16 = 0, 1
 GF_MAX_RANKS = 16
 GF_IPC_HANDLE_BYTES = 64
 GF_RSAG_NO_EXIT_BARRIER = 1
+GF_PART_ONE = 1024
 THETA_INF = (1 << 64) - 1
 
 
@@ -55,6 +56,7 @@ _EXC = {GF_ERR_CONFIG: ConfigError, GF_ERR_PROTOCOL: ProtocolError,
         GF_ERR_TRANSPORT: TransportError, GF_ERR_TRAINING: TrainingError, GF_ERR_CUDA: CudaError}
 
 _vp, _u64, _i, _f = C.c_void_p, C.c_uint64, C.c_int, C.c_float
+_u32 = C.c_uint32
 _u64p = C.POINTER(C.c_uint64)
 
 # name -> argtypes (restype int unless listed in _RET)
@@ -90,9 +92,11 @@ SIGNATURES = {
     "gf_ring_allreduce": [_vp, _i, _u64, _vp, _vp, _i, _vp],
     "gf_ring_allreduce_planned": [_vp, _i, _u64, _vp, _vp],
     "gf_ring_allreduce_planned_scatter": [_vp, _i, _u64, _vp, _vp, _u64, _u64, _vp, _vp],
+    "gf_csc_exchange_pull": [_vp, _u64, _vp, _vp, _u64, _u64, _vp, _vp],
     "gf_ring_allreduce_ptrs": [_vp, _i, _vp, _vp, _vp, _i, _vp],
     "gf_sync_step_dense": [_vp, _i, _u64, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _vp],
     "gf_ring_allreduce_unpack": [_vp, _i, _u64, _vp, _vp, _vp, _i, _vp, _vp, _i, _i, _vp],
+    "gf_ring_allreduce_unpack_part": [_vp, _i, _u64, _vp, _vp, _vp, _i, _vp, _vp, _i, _u32, _u32, _i, _vp],
     "gf_ipc_export": [_vp, _vp, _u64p],
     "gf_ipc_open": [_vp, _vp, C.POINTER(_vp)],
     "gf_ipc_close": [_vp, _vp],
@@ -105,6 +109,7 @@ SIGNATURES = {
     "gf_oracle_allreduce_ptrs": [_i, _vp, _i, _u64, _vp],
     "gf_broadcast_ptrs": [_vp, _i, _i, _u64, _vp],
     "gf_ring_reduce_ptrs": [_i, _vp, _i, _i, _u64, _vp],
+    "gf_part_ranges": [_vp, _vp, _i, _i, _u32, _u32, _vp, _vp, _i],
     "gf_abi_version": [],
     "gf_last_error": [],
     "gf_kernel_launches": [],
@@ -157,6 +162,19 @@ def ptr(t) -> int:
     if hasattr(t, "ctypes"):
         return t.ctypes.data
     raise TypeError(type(t))
+
+
+def part_ranges(win_start, win_len, world, part_lo, part_hi):
+    """Pool element ranges of one piece of every segment (gf_part_ranges), as numpy arrays."""
+    import numpy as np
+    n = len(win_start)
+    cap = n * world + 1
+    lo, hi = (C.c_uint64 * cap)(), (C.c_uint64 * cap)()
+    k = lib().gf_part_ranges(u64_array(win_start), u64_array(win_len), n, world, part_lo, part_hi,
+                             lo, hi, cap)
+    if k < 0:
+        check(GF_ERR_CONFIG)
+    return np.array(lo[:k], dtype=np.uint64), np.array(hi[:k], dtype=np.uint64)
 
 
 def u64_array(vals):

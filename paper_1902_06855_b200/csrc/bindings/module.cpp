@@ -23,6 +23,7 @@
 #include "gflow/half.hpp"
 #include "gflow/inproc.hpp"
 #include "gflow/sparse.hpp"
+#include "gflow/tcp.hpp"
 #include "gflow/trainer.hpp"
 
 namespace py = pybind11;
@@ -329,7 +330,32 @@ PYBIND11_MODULE(gflowpy, m) {
         .def("barrier", &Transport::barrier, release())
         .def("stats", [](Transport& t) { return stats_dict(t.stats()); })
         .def("total_payload_sent", [](Transport& t) { return t.stats().total().payload_bytes_sent; })
-        .def("set_timeout_ms", [](Transport& t, int ms) { t.set_timeout(std::chrono::milliseconds(ms)); });
+        .def("set_timeout_ms", [](Transport& t, int ms) { t.set_timeout(std::chrono::milliseconds(ms)); })
+        .def("send", [](Transport& t, int dst, std::uint32_t tag, const py::bytes& data, const std::string& phase) {
+            const std::string s = data;
+            const auto* p = reinterpret_cast<const std::byte*>(s.data());
+            py::gil_scoped_release nogil;
+            t.send(dst, tag, std::span<const std::byte>(p, s.size()), phase);
+        }, py::arg("dst"), py::arg("tag"), py::arg("data"), py::arg("phase") = "data")
+        .def("recv", [](Transport& t, int src, std::uint32_t tag, const std::string& phase) {
+            std::vector<std::byte> v;
+            {
+                py::gil_scoped_release nogil;
+                v = t.recv(src, tag, phase);
+            }
+            return py::bytes(reinterpret_cast<const char*>(v.data()), v.size());
+        }, py::arg("src"), py::arg("tag"), py::arg("phase") = "data");
+    // Multi-process control plane (reference: include/gflow/tcp.hpp:18-47): GFL1 over TCP.
+    m.def("make_tcp_transport", [](int rank, int world_size, const std::vector<std::string>& peers) {
+        std::shared_ptr<Transport> t;
+        {
+            py::gil_scoped_release nogil;
+            t = std::make_shared<TcpTransport>(rank, world_size, peers);
+        }
+        return t;
+    }, py::arg("rank"), py::arg("world_size"), py::arg("peers"));
+    m.def("tcp_loopback_addresses", &TcpTransport::loopback_addresses, py::arg("world_size"),
+          py::arg("port_base"));
     m.def("make_inproc_world", [](int n) {
         std::vector<std::shared_ptr<Transport>> out;
         for (auto& t : make_inproc_world(n)) out.emplace_back(t.release());

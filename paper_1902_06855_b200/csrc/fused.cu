@@ -410,7 +410,7 @@ rsag_kernel(const __grid_constant__ RingArgs a, const __grid_constant__ StepTabl
     for (int w = 0; w < a.nwin; ++w) {
         uint64_t e0, e1;
         segment(a, n, w, a.pos, e0, e1);
-        rs_pull_segment<DT, NT>(a, T, src, n, e0, e1, g, S, inv);
+        rs_pull_segment<DT, NT>(a, T, src, n, part_cut(e0, e1, a.part_lo), part_cut(e0, e1, a.part_hi), g, S, inv);
     }
     if (tr) a.trace[2] = gfd::globaltimer_ns();
     if (!cross_barrier(a, epoch + 2, &s_ok, true)) return;  // my segment sums are visible
@@ -420,7 +420,8 @@ rsag_kernel(const __grid_constant__ RingArgs a, const __grid_constant__ StepTabl
             const int q = (a.pos + j) % n;
             uint64_t e0, e1;
             segment(a, n, w, q, e0, e1);
-            ag_pull_segment<DT>(T, a.bufs[a.ring[q]], local, e0, e1, g, S, inv);
+            ag_pull_segment<DT>(T, a.bufs[a.ring[q]], local, part_cut(e0, e1, a.part_lo),
+                                part_cut(e0, e1, a.part_hi), g, S, inv);
         }
     }
     uint64_t fin = epoch + 2;
@@ -525,11 +526,13 @@ int gf_sync_step_dense(gf_comm* c, int dtype, uint64_t pool_heap_off, const floa
     return GF_OK;
 }
 
-int gf_ring_allreduce_unpack(gf_comm* c, int dtype, uint64_t pool_heap_off, float* const* dst,
-                             const uint64_t* pool_off, const uint64_t* count, int ntensors,
-                             const uint64_t* win_start, const uint64_t* win_len, int nwin, int flags,
-                             void* stream) {
+int gf_ring_allreduce_unpack_part(gf_comm* c, int dtype, uint64_t pool_heap_off, float* const* dst,
+                                  const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                                  const uint64_t* win_start, const uint64_t* win_len, int nwin,
+                                  uint32_t part_lo, uint32_t part_hi, int flags, void* stream) {
     static const char* fn = "gf_ring_allreduce_unpack";
+    if (part_lo >= part_hi || part_hi > GF_PART_ONE)
+        return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_unpack_part: need 0 <= part_lo < part_hi <= GF_PART_ONE");
     if (int rc = comm_ready(c)) return rc;
     if (!gfi::valid_dtype(dtype) || ntensors < 1 || ntensors > kStepMaxT || !dst || !pool_off || !count ||
         nwin < 1 || !win_start || !win_len || (flags & ~GF_RSAG_NO_EXIT_BARRIER))
@@ -542,8 +545,11 @@ int gf_ring_allreduce_unpack(gf_comm* c, int dtype, uint64_t pool_heap_off, floa
         return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_unpack: pool outside the symmetric heap");
     if (int rc = check_tiling(fn, T, hi, win_start, win_len, nwin)) return rc;
     DeviceGuard guard(c->device);
-    if (c->world == 1)  // the collective is the identity (collectives.cpp:59)
+    if (c->world == 1) {  // the collective is the identity (collectives.cpp:59)
+        if (part_lo != 0 || part_hi != GF_PART_ONE)
+            return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_unpack_part: pieces need world > 1");
         return gf_unpack(dtype, c->alloc + kFlagBytes + pool_heap_off, dst, pool_off, count, ntensors, 1, stream);
+    }
     const float inv = 1.0f / static_cast<float>(c->world);
     const int exit_barrier = (flags & GF_RSAG_NO_EXIT_BARRIER) ? 0 : 1;
     for (int first = 0; first < nwin; first += kMaxW) {
@@ -557,13 +563,51 @@ int gf_ring_allreduce_unpack(gf_comm* c, int dtype, uint64_t pool_heap_off, floa
             max_seg += (a.wlen[w] + c->world - 1) / c->world;
         }
         fill_common(c, a, pool_heap_off);
-        const int grid = gfr::ring_blocks(max_seg * es);
+        a.part_lo = part_lo;
+        a.part_hi = part_hi;
+        const uint64_t part_seg = std::max<uint64_t>(1, max_seg * (part_hi - part_lo) / GF_PART_ONE);
+        const int grid = gfr::ring_blocks(part_seg * es);
         if (dtype == GF_F16) launch_rsag<GF_F16>(a, T, inv, exit_barrier, grid, gfi::S(stream));
         else launch_rsag<GF_F32>(a, T, inv, exit_barrier, grid, gfi::S(stream));
         gfi::count_launch();
         if (int rc = gfi::check_launch(fn)) return rc;
     }
     return GF_OK;
+}
+
+int gf_ring_allreduce_unpack(gf_comm* c, int dtype, uint64_t pool_heap_off, float* const* dst,
+                             const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                             const uint64_t* win_start, const uint64_t* win_len, int nwin, int flags,
+                             void* stream) {
+    return gf_ring_allreduce_unpack_part(c, dtype, pool_heap_off, dst, pool_off, count, ntensors, win_start,
+                                         win_len, nwin, 0, GF_PART_ONE, flags, stream);
+}
+
+int gf_part_ranges(const uint64_t* win_start, const uint64_t* win_len, int nwin, int world,
+                   uint32_t part_lo, uint32_t part_hi, uint64_t* lo, uint64_t* hi, int cap) {
+    if (!win_start || !win_len || nwin < 0 || world < 1 || world > GF_MAX_RANKS || part_lo > part_hi ||
+        part_hi > GF_PART_ONE || (cap > 0 && (!lo || !hi)))
+        return gfi::fail(GF_ERR_CONFIG, "gf_part_ranges: bad arguments"), -1;
+    int k = 0;
+    const uint64_t n = uint64_t(world);
+    for (int w = 0; w < nwin; ++w) {
+        const uint64_t base = win_len[w] / n, rem = win_len[w] % n;
+        for (uint64_t j = 0; j < n; ++j) {  // segment_of (collectives.cpp:47-53)
+            const uint64_t e0 = win_start[w] + j * base + std::min(j, rem);
+            const uint64_t e1 = e0 + base + (j < rem ? 1 : 0);
+            const uint64_t a = part_cut(e0, e1, part_lo), b = part_cut(e0, e1, part_hi);
+            if (a >= b) continue;
+            if (k > 0 && hi[k - 1] == a) {  // adjacent: merge
+                hi[k - 1] = b;
+                continue;
+            }
+            if (k >= cap) return -1;
+            lo[k] = a;
+            hi[k] = b;
+            ++k;
+        }
+    }
+    return k;
 }
 
 }  // extern "C"

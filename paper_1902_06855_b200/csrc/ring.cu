@@ -153,6 +153,150 @@ __device__ void wb_segment(const RingArgs& a, const uint64_t* list, uint64_t k, 
     }
 }
 
+// ---- CSC exchange, pull form (gf_csc_exchange_pull) ------------------------------------
+// The planned windows over the staging buffers, without any push: the rank at ring position
+// p sums segment p of every window by pulling it from all N staging buffers in ring order
+// (bit-identical to the ring), keeps the sum in its own staging buffer and writes it back
+// into its pool (+ exact |x| units, the norms of the important chunks); after one barrier
+// with its peer CTAs it pulls every other segment from the owner's staging buffer straight
+// into its pool. The write-back's address math and atomics overlap the NVLink loads; no
+// barrier waits for posted writes to drain. The caller's next write of its staging buffer
+// must come after a later collective's barrier (gf_csc_select's, in the CSC step).
+__device__ __forceinline__ void wb_scalar(const RingArgs& a, const uint64_t* list, uint64_t k, uint64_t i,
+                                          uint16_t h) {
+    uint64_t c;
+    const uint64_t d = wb_target(a, list, k, i, c);
+    reinterpret_cast<uint16_t*>(a.wb_pool)[d] = h;
+    if ((h & 0x7C00u) == 0x7C00u)
+        atomicOr(reinterpret_cast<unsigned long long*>(a.wb_nacc + c), (unsigned long long)kNaccNaN);
+    else if (half_units(h))
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.wb_nacc + c), (unsigned long long)half_units(h));
+}
+
+// RS (OWN = true: sum from all N in ring order, keep in the local staging) or AG (OWN =
+// false: src[0] is the owner's staging) of staging range [e0, e1), written back to the pool.
+template <int NT, bool OWN>
+__device__ void csc_pull_range(const RingArgs& a, const char* const* src, int n, const uint64_t* list,
+                               uint64_t k, uint64_t e0, uint64_t e1, uint64_t gtid, uint64_t T) {
+    constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
+    constexpr int NS = OWN ? NMAX : 1;
+    constexpr int U = OWN ? (NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1)) : 8;
+    uint16_t* local = reinterpret_cast<uint16_t*>(a.bufs[a.rank]);
+    uint64_t v0 = (e0 + 7) / 8, v1 = e1 / 8;
+    if (v0 >= v1) v0 = v1 = e1 / 8 + 1;  // no aligned vector inside: all scalar
+    if (blockIdx.x == 0) {
+        auto edge = [&](uint64_t lo, uint64_t hi) {
+            for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+                uint16_t h;
+                if (OWN) {
+                    h = reinterpret_cast<const uint16_t*>(src[0])[i];
+                    for (int t = 1; t < n; ++t) h = gfd::acc16(reinterpret_cast<const uint16_t*>(src[t])[i], h);
+                    local[i] = h;
+                } else {
+                    h = reinterpret_cast<const volatile uint16_t*>(src[0])[i];
+                }
+                wb_scalar(a, list, k, i, h);
+            }
+        };
+        if (v0 < v1) {
+            edge(e0, v0 * 8);
+            edge(v1 * 8, e1);
+        } else {
+            edge(e0, e1);
+        }
+    }
+    // whole-warp iterations (the units aggregation shuffles need every lane)
+    const uint64_t lane = gtid & 31;
+    for (uint64_t base = v0 + gtid - lane; base < v1; base += T * U) {
+        uint4 x[U][NS];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t vv = base + uint64_t(u) * T + lane;
+            if (vv < v1) {
+#pragma unroll
+                for (int t = 0; t < NS; ++t) {
+                    if (OWN) {
+                        if (t < n) x[u][t] = gfd::ld16(src[t] + vv * 16);
+                    } else {
+                        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"  // the owner wrote it
+                                     : "=r"(x[u][t].x), "=r"(x[u][t].y), "=r"(x[u][t].z), "=r"(x[u][t].w)
+                                     : "l"(src[0] + vv * 16));
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (base + uint64_t(u) * T >= v1) break;  // warp-uniform
+            const uint64_t vv = base + uint64_t(u) * T + lane;
+            const bool act = vv < v1;
+            uint64_t c = 0, un = 0;
+            bool nan = false;
+            if (act) {
+                uint4 acc = x[u][0];
+                if (OWN) {
+#pragma unroll
+                    for (int t = 1; t < NS; ++t)
+                        if (t < n) acc = gfd::acc16x8(x[u][t], acc);
+                    gfd::st16_keep(local + vv * 8, acc);  // the peers pull it next
+                }
+                const uint64_t d = wb_target(a, list, k, vv * 8, c);
+                gfd::st16(reinterpret_cast<uint16_t*>(a.wb_pool) + d, acc);
+                nan = gfd::any_special(acc);
+                if (!nan) un = gfd::units8(acc);
+            }
+            wb_nacc_add(a.wb_nacc, c, un, nan, act);
+        }
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kRingThreads) csc_pull_kernel(const __grid_constant__ RingArgs a) {
+    constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
+    extern __shared__ uint64_t wb_list[];  // the plan's important chunks (plan[1] <= nc)
+    __shared__ int s_ok;
+    const uint64_t epoch = a.epochs[blockIdx.x];
+    if (threadIdx.x == 0) s_ok = 1;
+    const int n = NT > 0 ? NT : a.world;
+    const uint64_t k = a.plan[1];
+    for (uint64_t q = threadIdx.x; q < k; q += blockDim.x) wb_list[q] = a.plan[4 + q];
+    const bool tr = a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    if (tr) a.trace[0] = gfd::globaltimer_ns();
+    if (!cross_barrier(a, epoch + 1, &s_ok, false)) return;  // peers' staging buffers are packed
+    if (tr) a.trace[1] = gfd::globaltimer_ns();
+    const uint64_t staged = a.plan[0], stride = a.plan[3];
+    const int nwin = int(a.plan[2]);
+    const uint64_t T = uint64_t(gridDim.x) * blockDim.x;
+    const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const char* src[NMAX];
+#pragma unroll
+    for (int t = 0; t < NMAX; ++t) src[t] = (t < n) ? a.bufs[a.ring[(a.pos + t) % n]] : nullptr;
+    auto seg = [&](int w, int j, uint64_t& e0, uint64_t& e1) {  // segment_of (collectives.cpp:47-53)
+        const uint64_t ws = uint64_t(w) * stride, wl = (w == nwin - 1) ? staged - ws : stride;
+        const uint64_t base = wl / uint64_t(n), rem = wl % uint64_t(n), uj = uint64_t(j);
+        e0 = ws + uj * base + min(uj, rem);
+        e1 = e0 + base + (uj < rem ? 1 : 0);
+    };
+    for (int w = 0; w < nwin; ++w) {
+        uint64_t e0, e1;
+        seg(w, a.pos, e0, e1);
+        csc_pull_range<NT, true>(a, src, n, wb_list, k, e0, e1, gtid, T);
+    }
+    if (tr) a.trace[2] = gfd::globaltimer_ns();
+    if (!cross_barrier(a, epoch + 2, &s_ok, true)) return;  // my segment sums are visible
+    for (int w = 0; w < nwin; ++w) {
+        for (int j = 1; j < n; ++j) {
+            const int q = (a.pos + j) % n;
+            uint64_t e0, e1;
+            seg(w, q, e0, e1);
+            const char* owner[1] = {a.bufs[a.ring[q]]};
+            csc_pull_range<NT, false>(a, owner, n, wb_list, k, e0, e1, gtid, T);
+        }
+    }
+    if (threadIdx.x == 0) a.epochs[blockIdx.x] = epoch + 2;
+    if (tr) a.trace[3] = gfd::globaltimer_ns();
+}
+
 template <int DT, int NT, bool P2P>
 __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constant__ RingArgs a) {
     constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
@@ -638,6 +782,38 @@ int gf_ring_allreduce_planned_scatter(gf_comm* c, int dtype, uint64_t stage_heap
     launch_ring(dtype, true, a, dim3(gfr::ring_blocks(bound)), gfi::S(stream), size_t(nc) * 8);
     gfi::count_launch();
     return gfi::check_launch("gf_ring_allreduce_planned_scatter");
+}
+
+int gf_csc_exchange_pull(gf_comm* c, uint64_t stage_heap_off, const uint64_t* plan_dev, void* pool,
+                         uint64_t chunk, uint64_t nc, uint64_t* nacc, void* stream) {
+    if (int rc = comm_ready(c)) return rc;
+    if (!plan_dev || !pool || !nacc || chunk == 0 || chunk % 8 != 0 || nc == 0 || nc > 6144 ||
+        (reinterpret_cast<uintptr_t>(pool) & 15u) != 0)
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_exchange_pull: fp16 pool (16-B aligned), chunk % 8 == 0, "
+                                        "nc <= 6144 (chunk list in shared memory), nacc required");
+    if (c->world == 1) return gfi::fail(GF_ERR_CONFIG, "gf_csc_exchange_pull: world 1 has no exchange");
+    DeviceGuard g(c->device);
+    RingArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.nwin = -1;
+    a.plan = plan_dev;
+    fill_common(c, a, stage_heap_off);
+    a.wb_pool = static_cast<char*>(pool);
+    a.wb_nacc = nacc;
+    a.wb_chunk = chunk;
+    a.wb_nc = nc;
+    const uint64_t bound = c->heap_bytes > stage_heap_off ? (c->heap_bytes - stage_heap_off) / c->world : 0;
+    const dim3 grid(gfr::ring_blocks(bound));
+    const size_t smem = size_t(nc) * 8;
+    cudaStream_t s = gfi::S(stream);
+    switch (c->world) {
+        case 2: csc_pull_kernel<2><<<grid, kRingThreads, smem, s>>>(a); break;
+        case 4: csc_pull_kernel<4><<<grid, kRingThreads, smem, s>>>(a); break;
+        case 8: csc_pull_kernel<8><<<grid, kRingThreads, smem, s>>>(a); break;
+        default: csc_pull_kernel<0><<<grid, kRingThreads, smem, s>>>(a); break;
+    }
+    gfi::count_launch();
+    return gfi::check_launch("gf_csc_exchange_pull");
 }
 
 int gf_ring_allreduce_colocated(int dtype, void* const* bufs, int world, const int* ring_order,

@@ -18,6 +18,7 @@ struct RingArgs {
     char* bufs[GF_MAX_RANKS];            // buffer base of each RANK (peer-mapped)
     int ring[GF_MAX_RANKS];              // rank at each ring position
     int world, rank, pos;
+    uint32_t part_lo, part_hi;           // gf_ring_allreduce_unpack_part: piece of every segment
     int nwin;                            // >= 0 explicit windows; -1: read plan
     uint64_t* flags_local;
     uint64_t* flags_peer[GF_MAX_RANKS];  // by rank
@@ -37,6 +38,16 @@ struct RingArgs {
     uint64_t wstart[kMaxW];
     uint64_t wlen[kMaxW];
 };
+
+// Piece [q_lo, q_hi) (units of 1/GF_PART_ONE) of segment [e0, e1): cut points are rounded
+// down to a multiple of 8 elements (16-byte vectors for fp16) and clamped to the segment.
+// Shared by the kernels and the host (gf_part_ranges), so both see the same element ranges.
+__host__ __device__ inline uint64_t part_cut(uint64_t e0, uint64_t e1, uint32_t q) {
+    if (q == 0) return e0;
+    if (q >= GF_PART_ONE) return e1;
+    uint64_t c = ((e0 + (e1 - e0) * q / GF_PART_ONE) / 8) * 8;
+    return c < e0 ? e0 : (c > e1 ? e1 : c);
+}
 
 // ---- cross-GPU barrier (CTA b <-> CTA b of every peer) ------------------------
 // release_writes: the CTA's earlier global stores (incl. pushes into peers) must be visible

@@ -110,7 +110,8 @@ class GradSync:
 
     def __init__(self, sizes, rank=0, world=1, device=0, dtype=F16, theta=64 << 20,
                  chunk=32000, csc=False, final_sparsity=0.9, warmup_iters=0, momentum=0.9,
-                 lr=0.01, allgather=None, timeout_ms=30000, dense_mode="pull"):
+                 lr=0.01, allgather=None, timeout_ms=30000, dense_mode="pull", pull_parts=None,
+                 csc_mode="pull"):
         self.layout = PoolLayout.build(sizes, chunk)
         self.rank, self.world, self.device, self.dtype = rank, world, device, dtype
         self.esz = 2 if dtype == F16 else 4
@@ -121,6 +122,9 @@ class GradSync:
         if dense_mode not in ("pull", "push", "fused"):
             raise capi.ConfigError(f"dense_mode {dense_mode!r}: pull, push or fused")
         self.dense_mode = dense_mode
+        if csc_mode not in ("pull", "push"):
+            raise capi.ConfigError(f"csc_mode {csc_mode!r}: pull or push")
+        self.csc_mode = csc_mode
         self.pool_off = 0
         self.stage_off = _align(L.total * self.esz)
         # dense pull mode at N>1: two pools used alternately, so a step never waits for the
@@ -130,6 +134,15 @@ class GradSync:
             self._pull_pools = [0, self.stage_off]
             self.stage_off += _align(L.total * self.esz)
         self._pull_flip = 0
+        # pull mode pieces (units of 1/GF_PART_ONE of every segment): piece k+1 is packed on a
+        # side stream while piece k is exchanged; one piece = pack then exchange, serially
+        parts = tuple(pull_parts) if pull_parts else (0, capi.GF_PART_ONE)
+        if parts[0] != 0 or parts[-1] != capi.GF_PART_ONE or any(a >= b for a, b in zip(parts, parts[1:])):
+            raise capi.ConfigError(f"pull_parts {parts!r}: increasing from 0 to {capi.GF_PART_ONE}")
+        self.pull_parts = parts
+        self._piece_tabs = None
+        self._piece_cache = {}
+        self._pieces_s = None
         self.norms_off = self.stage_off + (_align(L.total * self.esz) if csc else 0)
         heap = self.norms_off + _align(L.num_chunks * 4)
         self.comm = C.c_void_p()
@@ -206,6 +219,9 @@ class GradSync:
                 self._pull_flip ^= 1
                 flags = capi.GF_RSAG_NO_EXIT_BARRIER
             self.last_pool_ptr = self.heap_base + pool_off
+            if len(self.pull_parts) > 2:
+                self._pull_pieces(grad_ptrs, out_ptrs, pool_off, flags, stream, mark)
+                return
             mark("pack")
             capi.call("gf_pack", self.dtype, self.last_pool_ptr, self._ptrs(grad_ptrs), self._offs,
                       self._cnts, m, 1.0, stream)
@@ -227,6 +243,76 @@ class GradSync:
             mark("unpack")
             capi.call("gf_unpack", self.dtype, self.pool_ptr, self._ptrs(out_ptrs), self._offs,
                       self._cnts, m, self.world, stream)
+        mark(None)
+
+    def _piece_tables(self):
+        """Per piece: (tensor index, element offset in the tensor, pool offset, count) of the
+        pool ranges the piece covers (gf_part_ranges), cut at tensor boundaries."""
+        if self._piece_tabs is None:
+            import numpy as np
+            L = self.layout
+            offs = np.asarray(L.offsets, dtype=np.uint64)
+            sizes = np.asarray(L.sizes, dtype=np.uint64)
+            ws = [int(x) for x in self._win[0]]
+            wl = [int(x) for x in self._win[1]]
+            tabs = []
+            for lo_q, hi_q in zip(self.pull_parts, self.pull_parts[1:]):
+                lo, hi = capi.part_ranges(ws, wl, self.world, lo_q, hi_q)
+                ent = []
+                for a, b in zip(lo.tolist(), hi.tolist()):
+                    for i in np.nonzero((offs < b) & (offs + sizes > a))[0].tolist():
+                        s0, s1 = max(a, int(offs[i])), min(b, int(offs[i] + sizes[i]))
+                        ent.append((i, s0 - int(offs[i]), s0, s1 - s0))
+                tabs.append(np.array(ent, dtype=np.int64).reshape(-1, 4))
+            self._piece_tabs = tabs
+        return self._piece_tabs
+
+    def _piece_args(self, grad_ptrs):
+        """gf_pack tables of every piece for one gradient pointer table (cached per table)."""
+        key = id(grad_ptrs) if isinstance(grad_ptrs, C.Array) else tuple(grad_ptrs)
+        hit = self._piece_cache.get(key)
+        if hit is not None and hit[0] is grad_ptrs:
+            return hit[1]
+        import numpy as np
+        base = np.array([int(p) for p in grad_ptrs], dtype=np.uint64)
+        out = []
+        for t in self._piece_tables():
+            src = base[t[:, 0]] + 4 * t[:, 1].astype(np.uint64)
+            out.append(((C.c_void_p * len(t))(*src.tolist()), capi.u64_array(t[:, 2]),
+                        capi.u64_array(t[:, 3]), len(t)))
+        if len(self._piece_cache) > 64:
+            self._piece_cache.clear()
+        self._piece_cache[key] = (grad_ptrs, out)
+        return out
+
+    def _pull_pieces(self, grad_ptrs, out_ptrs, pool_off, flags, stream, mark):
+        """Pull-mode step in pieces: piece 0 is packed and exchanged on `stream` while pieces
+        1.. are packed on a side stream; piece k's exchange waits for its pack. Every rank
+        launches the pieces' exchanges in the same order (their CTA-pair barriers pair up)."""
+        import numpy as np  # noqa: F401
+        m = len(self.layout.sizes)
+        args = self._piece_args(grad_ptrs)
+        if self._pieces_s is None:
+            cudart.set_device(self.device)
+            self._pieces_s = (cudart.stream_create(), cudart.event_create(),
+                              [cudart.event_create() for _ in args])
+        side, ev_fork, ev_packed = self._pieces_s
+        pool = self.heap_base + pool_off
+        outp = self._ptrs(out_ptrs)
+        mark("pull_step")
+        for k, (src, po, cnt, n) in enumerate(args):
+            capi.call("gf_pack", self.dtype, pool, src, po, cnt, n, 1.0, stream if k == 0 else side)
+            if k == 0:  # the side stream packs the later pieces once piece 0 is packed
+                cudart.event_record(ev_fork, stream)
+                cudart.stream_wait(side, ev_fork)
+            else:
+                cudart.event_record(ev_packed[k], side)
+        for k in range(len(args)):
+            if k > 0:
+                cudart.stream_wait(stream, ev_packed[k])
+            capi.call("gf_ring_allreduce_unpack_part", self.comm, self.dtype, pool_off, outp, self._offs,
+                      self._cnts, m, self._win[0], self._win[1], self._win[2], self.pull_parts[k],
+                      self.pull_parts[k + 1], flags, stream)
         mark(None)
 
     def fused_step(self, grad_ptrs, out_ptrs, stream=None, mark=None):
@@ -328,7 +414,13 @@ class GradSync:
         k_cur = L.num_chunks if self.iteration == 0 else selection_count(
             sparsity_at(self.iteration, self.warmup_iters, self.final_sparsity), L.num_chunks)
         fused_wb = not solo and nacc is not None and L.chunk % 8 == 0 and L.num_chunks <= 6144
-        if fused_wb:  # exchange + write-back + exact L1 of the exchanged chunks, one launch
+        if fused_wb and self.csc_mode == "pull":
+            # pull RS + pull AG straight into the pool (+ exact L1); the staging buffer is next
+            # rewritten after gf_csc_select's barrier, so no exit barrier is needed
+            mark("ring_scatter")
+            capi.call("gf_csc_exchange_pull", self.comm, self.stage_off, b["plan"][cur], self.pool_ptr,
+                      L.chunk, L.num_chunks, nacc, stream)
+        elif fused_wb:  # exchange + write-back + exact L1 of the exchanged chunks, one launch
             mark("ring_scatter")
             capi.call("gf_ring_allreduce_planned_scatter", self.comm, self.dtype, self.stage_off,
                       b["plan"][cur], self.pool_ptr, L.chunk, L.num_chunks, nacc, stream)

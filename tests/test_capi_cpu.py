@@ -51,3 +51,33 @@ def test_config_errors_map_to_exceptions():
         capi.call("gf_ring_allreduce_colocated", 1, None, 0, None, None, None, 0, None)
     with pytest.raises(capi.ConfigError):
         capi.call("gf_comm_create", 4, 7, 0, 1024, C.byref(C.c_void_p()))
+
+
+def test_part_ranges_tile_every_segment():
+    """gf_part_ranges (host-only): the pieces of a pull-mode step are disjoint, tile every
+    window exactly, and cut segments at multiples of 8 elements (16-byte fp16 vectors)."""
+    import numpy as np
+    rng = np.random.default_rng(3)
+    for world in (2, 3, 4, 8):
+        for _ in range(20):
+            nwin = int(rng.integers(1, 6))
+            wl = rng.integers(1, 200_000, nwin).tolist()
+            ws = np.concatenate([[0], np.cumsum(wl)[:-1]]).tolist()
+            cuts = sorted(set([0, 1024] + rng.integers(1, 1024, int(rng.integers(0, 4))).tolist()))
+            cover = np.zeros(sum(wl), np.int32)
+            for lo_q, hi_q in zip(cuts, cuts[1:]):
+                lo, hi = capi.part_ranges(ws, wl, world, lo_q, hi_q)
+                assert (lo < hi).all() and (lo[1:] >= hi[:-1]).all()
+                for a, b in zip(lo.tolist(), hi.tolist()):
+                    cover[a:b] += 1
+                    # a cut point inside a segment is 8-aligned
+                    seg_edges = set()
+                    for s0, l in zip(ws, wl):
+                        base, rem = divmod(l, world)
+                        for j in range(world + 1):
+                            seg_edges.add(s0 + j * base + min(j, rem))
+                    assert a in seg_edges or a % 8 == 0
+                    assert b in seg_edges or b % 8 == 0
+            assert (cover == 1).all()
+    with pytest.raises(capi.ConfigError):
+        capi.part_ranges([0], [10], 2, 5, 4)

@@ -307,12 +307,15 @@ def test_csc_correct_and_fused(gf, oracle, G, dtype):
 
 def test_select_topk_and_plan(gf, oracle, G):
     rng = np.random.default_rng(8)
-    for nc, k in ((4, 2), (1909, 191), (799, 80), (5000, 1), (3000, 3000), (2048, 1024)):
-        for kind in ("random", "ties", "zeros"):
+    for nc, k in ((4, 2), (3, 1), (1909, 191), (799, 80), (5000, 1), (3000, 3000), (2048, 1024),
+                  (4096, 409), (4097, 409), (6000, 2999)):
+        for kind in ("random", "ties", "zeros", "signed_zero_inf"):
             if kind == "random":
                 norms = rng.uniform(0, 10, nc).astype(np.float32)
             elif kind == "ties":
                 norms = rng.integers(0, 4, nc).astype(np.float32)
+            elif kind == "signed_zero_inf":
+                norms = rng.choice(np.array([0.0, -0.0, 1.5, np.inf, 3e38], np.float32), nc)
             else:
                 norms = np.zeros(nc, np.float32)
             want = oracle.select_topk(norms, k)

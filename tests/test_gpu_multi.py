@@ -301,9 +301,11 @@ def _worker_fused(rank, world, port):
         dist.all_gather_object(out, b)
         return out
 
-    for mode, theta in [(m, t) for m in ("fused", "pull", "push") for t in (64 << 20, 1 << 20, 0)]:
+    modes = [("fused", None), ("pull", None), ("pull", (0, 256, 1024)), ("pull", (0, 100, 101, 700, 1024)),
+             ("push", None)]
+    for (mode, parts), theta in [(m, t) for m in modes for t in (64 << 20, 1 << 20, 0)]:
         sync = GradSync(sizes, rank=rank, world=world, device=rank, theta=theta, allgather=ag,
-                        dense_mode=mode)
+                        dense_mode=mode, pull_parts=parts)
         for it in range(3):
             grads = [o.gen_grads(1000 * it + 17 * r + theta % 97, sizes) for r in range(world)]
             g = torch.from_numpy(grads[rank]).cuda()
@@ -319,13 +321,13 @@ def _worker_fused(rank, world, port):
                 got_pool = np.empty_like(pools[rank])
                 cudart.memcpy(got_pool.ctypes.data, sync.last_pool_ptr, got_pool.nbytes)
                 cudart.sync_device()
-                assert (got_pool == pools[rank]).all(), (mode, theta, it)
+                assert (got_pool == pools[rank]).all(), (mode, parts, theta, it)
             want_pool = o.unpack(pools[rank], world)
             got = out.cpu().numpy()
             for i, s in enumerate(sizes):
                 w = want_pool[int(off[i]):int(off[i]) + s]
                 assert (got[int(bounds[i]):int(bounds[i + 1])].view(np.uint32) == w.view(np.uint32)).all(), \
-                    (mode, theta, it, i)
+                    (mode, parts, theta, it, i)
         sync.close()
     dist.barrier()
 
@@ -357,7 +359,7 @@ def _worker_engine_csc(rank, world, port):
 
     g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "csc_run.npz"))
     ran = 0
-    for ci in range(int(g["csc_cases"][0])):
+    for ci, mode in [(c, m) for c in range(int(g["csc_cases"][0])) for m in ("pull", "push")]:
         p = f"c{ci}_"
         n, dt, theta, chunk, T = (int(x) for x in g[p + "meta"])
         if n != world:
@@ -367,7 +369,7 @@ def _worker_engine_csc(rank, world, port):
         total = sum(sizes)
         sync = GradSync(sizes, rank=rank, world=world, device=rank, dtype=dt, theta=theta, chunk=chunk,
                         csc=True, final_sparsity=0.75, warmup_iters=2, momentum=0.9, lr=0.01,
-                        allgather=ag)
+                        allgather=ag, csc_mode=mode)
         nc = sync.layout.num_chunks
         dev = torch.device("cuda", rank)
         hg = torch.zeros(total, device=dev)
@@ -391,7 +393,7 @@ def _worker_engine_csc(rank, world, port):
             cudart.memcpy(pool.ctypes.data, sync.pool_ptr, pool.nbytes)
             cudart.sync_device()
             want_pool = np.ascontiguousarray(g[p + "pool_x"][t][rank])
-            assert (pool == want_pool.view(np.uint8)).all(), (ci, t)
+            assert (pool == want_pool.view(np.uint8)).all(), (ci, mode, t)
             assert (hg.cpu().numpy().view(np.uint32) == g[p + "hg"][t][rank].view(np.uint32)).all(), (ci, t)
             assert (imp[(t + 1) & 1].cpu().numpy() == g[p + "next_imp"][t][rank]).all(), (ci, t)
             assert (hu.cpu().numpy().view(np.uint32) == g[p + "hu"][t][rank].view(np.uint32)).all(), (ci, t)
@@ -461,3 +463,50 @@ def _worker_overlap(rank, world, port):
 @pytest.mark.multigpu(2)
 def test_p2p_overlapped_windows_bit_exact():
     _spawn(_worker_overlap, _world())
+
+
+def _worker_tcp_cpp_api(rank, world, port):
+    """The reference's C++ API across PROCESSES: TcpTransport (GFL1 over TCP) as the control
+    plane, Communicator -> DeviceContext in IPC mode (one GPU per process), ring_allreduce /
+    broadcast / FusionEngine over NVLink peer memory — bit-exact vs the oracle, payload
+    accounting as the reference's ring (2(N-1) segment_of transfers)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_1902_06855_b200.gflowpy as g
+    from oracle.oracle import Oracle
+    o = Oracle()
+    g.set_device(rank)
+    t = g.make_tcp_transport(rank, world, g.tcp_loopback_addresses(world, port))
+    comm = g.Communicator(t)
+    assert comm.device_mode() == "ipc-p2p", comm.device_mode()
+    assert comm.device() == rank
+    for it, (L, dt) in enumerate([(1, 1), (97, 1), (1 << 20, 1), (4099, 0), (300_001, 0)]):
+        vals = []
+        for r in range(world):
+            x = np.random.default_rng(500 + 10 * it + r).uniform(-8, 8, L).astype(np.float32)
+            vals.append(o.f2h(x) if dt == 1 else x)
+        buf = vals[rank].copy()
+        before = t.stats().get("ring", {}).get("payload_bytes_sent", 0)
+        g.ring_allreduce(comm, buf)
+        want = o.ring_allreduce([v.copy() for v in vals], dtype=dt)
+        assert (_bits(buf) == _bits(want[rank])).all(), (L, dt)
+        sent = t.stats()["ring"]["payload_bytes_sent"] - before
+        esz = 2 if dt == 1 else 4
+        base, rem = divmod(L, world)
+        segs = [base + (1 if j < rem else 0) for j in range(world)]
+        p = comm.ring_order.index(rank)
+        # RS sends segments p-s, AG sends p+1-s (collectives.cpp:69-96)
+        want_sent = sum(segs[(p - s) % world] for s in range(world - 1)) + \
+            sum(segs[(p + 1 - s) % world] for s in range(world - 1))
+        assert sent == want_sent * esz, (L, sent, want_sent * esz)
+    root = world - 1
+    b = np.random.default_rng(rank).uniform(-1, 1, 12345).astype(np.float32)
+    want_b = np.random.default_rng(root).uniform(-1, 1, 12345).astype(np.float32)
+    g.broadcast(comm, b, root)
+    assert (b.view(np.uint32) == want_b.view(np.uint32)).all()
+    t.barrier()
+
+
+@pytest.mark.multigpu(2)
+def test_tcp_transport_cpp_api_across_processes():
+    _spawn(_worker_tcp_cpp_api, _world())
