@@ -197,13 +197,13 @@ def main():
                     help="also measure the dense sync overlapped with a synthetic backward of "
                          "this many ms (bf16 GEMMs; tensors complete in descending id, theta "
                          "windows launch as they close: the reference's lazy allreduce)")
-    ap.add_argument("--dense-mode", default="pull", choices=["pull", "push", "fused"],
+    ap.add_argument("--dense-mode", default="auto", choices=["auto", "pull", "push", "fused"],
                     help="dense N>1: pull (pack + pull RS/AG fused with unpack), push (pack + "
-                         "push-pull ring + unpack) or fused (one kernel)")
+                         "push-pull ring + unpack), fused (one kernel); auto = pull at N=2, else push")
     ap.add_argument("--pull-parts", default=None,
                     help="dense pull mode: piece cut points in 1/1024 of every segment, e.g. 0,256,1024 "
                          "(piece k+1 is packed while piece k is exchanged)")
-    ap.add_argument("--csc-mode", default="pull", choices=["pull", "push"],
+    ap.add_argument("--csc-mode", default="push", choices=["pull", "push"],
                     help="CSC N>1 exchange: pull (pull RS/AG straight into the pool) or push "
                          "(push-pull ring + fused write-back)")
     ap.add_argument("--fused", action="store_true",
@@ -609,6 +609,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
             "data": "synthetic", "config": dict(config_of(args, wl, world),
+                                                exchange=("none (N=1)" if world == 1 else
+                                                          (sync.csc_mode if csc else sync.dense_mode)),
                                                 l2=f"{n_sets} rotating input sets of {in_bytes >> 20} MiB "
                                                    f"(> 126 MB L2)"),
             "bus_gbs": bus, "kernels": kernels, "kernel_timing": kernel_timing, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
