@@ -98,7 +98,7 @@ __device__ __forceinline__ void wb_nacc_add(uint64_t* nacc, uint64_t c, uint64_t
 // This CTA's staging vectors of segment [e0, e1) (the reduce pattern: every segment's, since
 // the exit barrier covered the pushes of CTA b on every rank) -> pool, + units.
 __device__ void wb_segment(const RingArgs& a, const uint64_t* list, uint64_t k, uint64_t e0, uint64_t e1,
-                           uint64_t gtid, uint64_t T) {
+                           uint64_t gtid, uint64_t T, int edge_cta = 0) {
     const uint16_t* stg = reinterpret_cast<const uint16_t*>(a.bufs[a.rank]);
     uint16_t* pool = reinterpret_cast<uint16_t*>(a.wb_pool);
     const uint64_t v0 = (e0 + 7) / 8, v1 = e1 / 8;
@@ -115,10 +115,10 @@ __device__ void wb_segment(const RingArgs& a, const uint64_t* list, uint64_t k, 
         }
     };
     if (v0 >= v1) {
-        if (blockIdx.x == 0) scalar(e0, e1);
+        if (int(blockIdx.x) == edge_cta) scalar(e0, e1);
         return;
     }
-    if (blockIdx.x == 0) {
+    if (int(blockIdx.x) == edge_cta) {
         scalar(e0, v0 * 8);
         scalar(v1 * 8, e1);
     }
@@ -177,14 +177,15 @@ __device__ __forceinline__ void wb_scalar(const RingArgs& a, const uint64_t* lis
 // false: src[0] is the owner's staging) of staging range [e0, e1), written back to the pool.
 template <int NT, bool OWN>
 __device__ void csc_pull_range(const RingArgs& a, const char* const* src, int n, const uint64_t* list,
-                               uint64_t k, uint64_t e0, uint64_t e1, uint64_t gtid, uint64_t T) {
+                               uint64_t k, uint64_t e0, uint64_t e1, uint64_t gtid, uint64_t T,
+                               int edge_cta) {
     constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
     constexpr int NS = OWN ? NMAX : 1;
     constexpr int U = OWN ? (NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1)) : 8;
     uint16_t* local = reinterpret_cast<uint16_t*>(a.bufs[a.rank]);
     uint64_t v0 = (e0 + 7) / 8, v1 = e1 / 8;
     if (v0 >= v1) v0 = v1 = e1 / 8 + 1;  // no aligned vector inside: all scalar
-    if (blockIdx.x == 0) {
+    if (int(blockIdx.x) == edge_cta) {
         auto edge = [&](uint64_t lo, uint64_t hi) {
             for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
                 uint16_t h;
@@ -266,8 +267,6 @@ __global__ void __launch_bounds__(kRingThreads) csc_pull_kernel(const __grid_con
     if (tr) a.trace[1] = gfd::globaltimer_ns();
     const uint64_t staged = a.plan[0], stride = a.plan[3];
     const int nwin = int(a.plan[2]);
-    const uint64_t T = uint64_t(gridDim.x) * blockDim.x;
-    const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const char* src[NMAX];
 #pragma unroll
     for (int t = 0; t < NMAX; ++t) src[t] = (t < n) ? a.bufs[a.ring[(a.pos + t) % n]] : nullptr;
@@ -277,20 +276,21 @@ __global__ void __launch_bounds__(kRingThreads) csc_pull_kernel(const __grid_con
         e0 = ws + uj * base + min(uj, rem);
         e1 = e0 + base + (uj < rem ? 1 : 0);
     };
-    for (int w = 0; w < nwin; ++w) {
+    const WinGroups wg(nwin, true);  // CTA groups sweep the windows concurrently
+    for (int w = wg.first; w < nwin; w += wg.step) {
         uint64_t e0, e1;
         seg(w, a.pos, e0, e1);
-        csc_pull_range<NT, true>(a, src, n, wb_list, k, e0, e1, gtid, T);
+        csc_pull_range<NT, true>(a, src, n, wb_list, k, e0, e1, wg.lg, wg.LT, wg.edge_cta);
     }
     if (tr) a.trace[2] = gfd::globaltimer_ns();
     if (!cross_barrier(a, epoch + 2, &s_ok, true)) return;  // my segment sums are visible
-    for (int w = 0; w < nwin; ++w) {
+    for (int w = wg.first; w < nwin; w += wg.step) {
         for (int j = 1; j < n; ++j) {
             const int q = (a.pos + j) % n;
             uint64_t e0, e1;
             seg(w, q, e0, e1);
             const char* owner[1] = {a.bufs[a.ring[q]]};
-            csc_pull_range<NT, false>(a, owner, n, wb_list, k, e0, e1, gtid, T);
+            csc_pull_range<NT, false>(a, owner, n, wb_list, k, e0, e1, wg.lg, wg.LT, wg.edge_cta);
         }
     }
     if (threadIdx.x == 0) a.epochs[blockIdx.x] = epoch + 2;
@@ -325,7 +325,8 @@ __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constan
         nwin = int(a.plan[2]);
         stride = a.plan[3];
     }
-    for (int w = 0; w < nwin; ++w) {
+    const WinGroups wg(nwin, a.nwin < 0);  // planned windows: CTA groups sweep them concurrently
+    for (int w = wg.first; w < nwin; w += wg.step) {
         uint64_t ws, wl;
         if (a.nwin >= 0) {
             ws = a.wstart[w];
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constan
         // owned segment: segment_of(wl, n, p) (collectives.cpp:47-53)
         const uint64_t base = wl / uint64_t(n), rem = wl % uint64_t(n), up = uint64_t(p);
         const uint64_t e0 = ws + up * base + min(up, rem);
-        reduce_segment<DT, NT>(a, src, n, e0, e0 + base + (up < rem ? 1 : 0), gtid, T);
+        reduce_segment<DT, NT>(a, src, n, e0, e0 + base + (up < rem ? 1 : 0), wg.lg, wg.LT, wg.edge_cta);
     }
     if (tr) a.trace[2] = gfd::globaltimer_ns();
     if (P2P && !cross_barrier(a, epoch + 2, &s_ok, true)) return;
@@ -348,12 +349,12 @@ __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constan
         const uint64_t k = a.plan[1];
         for (uint64_t q = threadIdx.x; q < k; q += blockDim.x) wb_list[q] = a.plan[4 + q];
         __syncthreads();
-        for (int w = 0; w < nwin; ++w) {
+        for (int w = wg.first; w < nwin; w += wg.step) {  // the vectors my group reduced
             const uint64_t ws = uint64_t(w) * stride, wl = (w == nwin - 1) ? staged - ws : stride;
             const uint64_t base = wl / uint64_t(n), rem = wl % uint64_t(n);
             for (int j = 0; j < n; ++j) {
                 const uint64_t uj = uint64_t(j), e0 = ws + uj * base + min(uj, rem);
-                wb_segment(a, wb_list, k, e0, e0 + base + (uj < rem ? 1 : 0), gtid, T);
+                wb_segment(a, wb_list, k, e0, e0 + base + (uj < rem ? 1 : 0), wg.lg, wg.LT, wg.edge_cta);
             }
         }
     }

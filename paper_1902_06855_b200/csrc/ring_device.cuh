@@ -105,23 +105,26 @@ struct Vec<GF_F32> {
     }
 };
 
-// Reduction of one window's owned segment: the grid sweeps its 16-byte vectors in
-// lockstep (thread g takes vectors g, g+T, g+2T, ... with T = all threads of the grid), so
+// Reduction of one window's owned segment: the grid (or the CTA group given the window)
+// sweeps its 16-byte vectors in lockstep (thread g takes vectors g, g+T, g+2T, ... with T =
+// all threads sweeping it), so
 // every thread gets the same number of vectors (+-1) and all CTAs of a rank finish
 // together; U vectors x N sources of loads are in flight per thread.
 template <int DT, int NT>
 __device__ __forceinline__ void reduce_segment(const RingArgs& a, const char* const* src, int n,
-                                               uint64_t e0, uint64_t e1, uint64_t gtid, uint64_t T) {
+                                               uint64_t e0, uint64_t e1, uint64_t gtid, uint64_t T,
+                                               int edge_cta = 0) {
     constexpr int VE = Vec<DT>::kElems;
     constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
     constexpr int U = NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1);
     const uint64_t v0 = (e0 + VE - 1) / VE, v1 = e1 / VE;
-    if (v0 >= v1) {  // no aligned vector inside: all scalar, CTA 0
-        if (blockIdx.x == 0)
+    const bool edge = int(blockIdx.x) == edge_cta;  // this CTA takes the unaligned edges
+    if (v0 >= v1) {  // no aligned vector inside: all scalar, the edge CTA
+        if (edge)
             for (uint64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
         return;
     }
-    if (blockIdx.x == 0) {
+    if (edge) {
         for (uint64_t e = e0 + threadIdx.x; e < v0 * VE; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
         for (uint64_t e = v1 * VE + threadIdx.x; e < e1; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
     }
@@ -171,6 +174,32 @@ inline void fill_common(gf_comm* c, RingArgs& a, uint64_t heap_off) {
     a.err = c->err_dev;
     a.trace = c->trace ? reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(c->err_dev) + 64) : nullptr;
 }
+
+// Planned (CSC) windows are all of one length except the last. With several of them the grid
+// is cut into `groups` CTA groups of c CTAs; group g sweeps windows g, g + groups, ... so the
+// windows' NVLink round trips overlap instead of following one another. Depends only on
+// (nwin, grid), so CTA b covers the same vectors on every rank (the barriers pair CTA b only).
+struct WinGroups {
+    int first, step, edge_cta;  // windows first, first+step, ...; edge handler of my group
+    uint64_t lg, LT;            // my thread index within the group, the group's threads
+    __device__ WinGroups(int nwin, bool grouped) {
+        const int G = int(gridDim.x);
+        if (!grouped || nwin <= 1) {
+            first = 0;
+            step = 1;
+            edge_cta = 0;
+            lg = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+            LT = uint64_t(G) * blockDim.x;
+            return;
+        }
+        const int c = max(1, G / nwin), groups = G / c, grp = int(blockIdx.x) / c;
+        first = grp < groups ? grp : nwin;  // CTAs past the last full group sit out
+        step = groups;
+        edge_cta = grp * c;
+        lg = uint64_t(int(blockIdx.x) % c) * blockDim.x + threadIdx.x;
+        LT = uint64_t(c) * blockDim.x;
+    }
+};
 
 }  // namespace
 

@@ -161,6 +161,63 @@ def _worker_rsag(rank, world, port):
     dist.barrier()
 
 
+def _worker_csc_windows(rank, world, port):
+    """The CSC exchange with its write-back over MANY planned windows (theta = 0: one window
+    per selected chunk), push form (gf_ring_allreduce_planned_scatter) and pull form
+    (gf_csc_exchange_pull): pool bits and exact L1 units of the received chunks vs the oracle."""
+    comm, base, capi, cudart, dist = _setup(rank, world, port)
+    import torch
+    from oracle.oracle import Oracle
+    o = Oracle()
+    chunk, nc = 1000, 700
+    total = nc * chunk - 1000 + 1377  # longer last chunk
+    soff = 0
+    rng = np.random.default_rng(5)
+    for theta in (0, 2 * chunk * 2 + 1, 77 * chunk * 2, capi.THETA_INF):
+        for form in ("push", "pull"):
+            imp = (rng.random(nc) < 0.3).astype(np.uint8)
+            imp[-1] = 1
+            impd = torch.from_numpy(imp).cuda()
+            coff = torch.zeros(nc, dtype=torch.int64, device="cuda")
+            plan = torch.zeros(4 + nc, dtype=torch.int64, device="cuda")
+            capi.call("gf_csc_plan", impd.data_ptr(), total, chunk, nc, F16, theta, coff.data_ptr(),
+                      plan.data_ptr(), None)
+            torch.cuda.synchronize()
+            staged = int(plan[0].item())
+            stg = [o.f2h(np.random.default_rng(1000 * theta % 997 + 10 * r + (form == "pull")).uniform(-2, 2, staged)
+                         .astype(np.float32)) for r in range(world)]
+            pool0 = o.f2h(np.random.default_rng(77 + rank).uniform(-1, 1, total).astype(np.float32))
+            _put(cudart, base, soff, stg[rank])
+            pool = torch.from_numpy(pool0.view(np.int16).copy()).cuda()
+            nacc = torch.zeros(nc, dtype=torch.int64, device="cuda")
+            if form == "push":
+                capi.call("gf_ring_allreduce_planned_scatter", comm, F16, soff, plan.data_ptr(), pool.data_ptr(),
+                          chunk, nc, nacc.data_ptr(), None)
+            else:
+                capi.call("gf_csc_exchange_pull", comm, soff, plan.data_ptr(), pool.data_ptr(), chunk, nc,
+                          nacc.data_ptr(), None)
+            torch.cuda.synchronize()
+            capi.call("gf_comm_status", comm)
+            ws, wl = o.csc_windows(imp, total, chunk, 2, theta)
+            assert int(plan[2].item()) == len(ws)
+            red = o.ring_allreduce([x.copy() for x in stg], dtype=F16, windows=(ws, wl))[rank]
+            want = pool0.copy()
+            lens = np.where(np.arange(nc) == nc - 1, total - (nc - 1) * chunk, chunk)
+            s0 = 0
+            want_units = np.zeros(nc, np.int64)
+            for c in np.nonzero(imp)[0]:
+                L = int(lens[c])
+                want[c * chunk:c * chunk + L] = red[s0:s0 + L]
+                f = np.abs(o.h2f(red[s0:s0 + L]).astype(np.float64))
+                want_units[c] = int((f * 2.0 ** 24).sum())
+                s0 += L
+            got = pool.cpu().numpy().view(np.uint16)
+            assert (got == want).all(), (theta, form)
+            assert (nacc.cpu().numpy()[imp == 1] == want_units[imp == 1]).all(), (theta, form)
+            dist.barrier()
+    dist.barrier()
+
+
 def _worker_csc(rank, world, port):
     comm, base, capi, cudart, dist = _setup(rank, world, port)
     from oracle.oracle import Oracle
@@ -230,6 +287,11 @@ def test_p2p_ring_bit_exact():
 @pytest.mark.multigpu(2)
 def test_p2p_ring_allreduce_unpack_bit_exact():
     _spawn(_worker_rsag, _world())
+
+
+@pytest.mark.multigpu(2)
+def test_p2p_csc_exchange_many_windows():
+    _spawn(_worker_csc_windows, _world())
 
 
 @pytest.mark.multigpu(2)
