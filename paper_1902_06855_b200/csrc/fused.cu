@@ -281,111 +281,91 @@ __device__ __forceinline__ uint4 ld16_cg(const void* p) {  // L2 only: a peer wr
     return v;
 }
 
-template <int DT, int NT>
-__device__ void rs_pull_segment(const RingArgs& a, const StepTable& T, const char* const* src, int n,
-                                uint64_t e0, uint64_t e1, uint64_t g, uint64_t S, float inv) {
-    constexpr int VE = Vec<DT>::kElems;
-    constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
-    constexpr int U = NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1);
-    char* local = const_cast<char*>(src[0]);  // ring[pos] == rank
-    uint64_t v0 = (e0 + VE - 1) / VE, v1 = e1 / VE;
-    if (v0 >= v1) v0 = v1 = e1 / VE + 1;  // no aligned vector inside: all scalar
-    if (blockIdx.x == 0) {  // unaligned edges (or the whole segment), scalar, CTA 0
-        auto edge = [&](uint64_t lo, uint64_t hi) {
-            for (uint64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-                float xv;
-                if (DT == GF_F16) {
-                    uint16_t acc = reinterpret_cast<const uint16_t*>(src[0])[e];
-                    for (int t = 1; t < n; ++t) acc = gfd::acc16(reinterpret_cast<const uint16_t*>(src[t])[e], acc);
-                    reinterpret_cast<uint16_t*>(local)[e] = acc;
-                    xv = gfd::dec(acc);
-                } else {
-                    float acc = reinterpret_cast<const float*>(src[0])[e];
-                    for (int t = 1; t < n; ++t) acc = gfd::add(reinterpret_cast<const float*>(src[t])[e], acc);
-                    reinterpret_cast<float*>(local)[e] = acc;
-                    xv = acc;
-                }
-                const int t = tensor_at(T, e);
-                T.dst[t][e - T.off[t]] = gfd::mul(xv, inv);
-            }
-        };
-        if (v0 < v1) {
-            edge(e0, v0 * VE);
-            edge(v1 * VE, e1);
+// Scalar reduce (or copy) + unpack of pool element e by the edge CTA.
+template <int DT, bool OWN>
+__device__ __forceinline__ void pull_elem(const StepTable& T, const char* const* src, int n, char* local,
+                                          uint64_t e, float inv) {
+    float xv;
+    if (DT == GF_F16) {
+        uint16_t h;
+        if (OWN) {
+            h = reinterpret_cast<const uint16_t*>(src[0])[e];
+            for (int t = 1; t < n; ++t) h = gfd::acc16(reinterpret_cast<const uint16_t*>(src[t])[e], h);
         } else {
-            edge(e0, e1);
+            h = reinterpret_cast<const volatile uint16_t*>(src[0])[e];
         }
+        reinterpret_cast<uint16_t*>(local)[e] = h;
+        xv = gfd::dec(h);
+    } else {
+        float acc;
+        if (OWN) {
+            acc = reinterpret_cast<const float*>(src[0])[e];
+            for (int t = 1; t < n; ++t) acc = gfd::add(reinterpret_cast<const float*>(src[t])[e], acc);
+        } else {
+            acc = reinterpret_cast<const volatile float*>(src[0])[e];
+        }
+        reinterpret_cast<float*>(local)[e] = acc;
+        xv = acc;
     }
-    for (uint64_t v = v0 + g; v < v1; v += S * U) {
-        uint4 x[U][NMAX];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t vv = v + uint64_t(u) * S;
-            if (vv < v1) {
-#pragma unroll
-                for (int t = 0; t < NMAX; ++t)
-                    if (t < n) x[u][t] = gfd::ld16(src[t] + vv * 16);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t vv = v + uint64_t(u) * S;
-            if (vv < v1) {
-                uint4 acc = x[u][0];
-#pragma unroll
-                for (int t = 1; t < NMAX; ++t)
-                    if (t < n) acc = Vec<DT>::acc(x[u][t], acc);
-                gfd::st16_keep(local + vv * 16, acc);  // the peers pull it next
-                unpack_vec<DT>(T, vv, acc, inv);
-            }
-        }
-    }
+    const int t = tensor_at(T, e);
+    T.dst[t][e - T.off[t]] = gfd::mul(xv, inv);
 }
 
-template <int DT>
-__device__ void ag_pull_segment(const StepTable& T, const char* owner, char* local, uint64_t e0, uint64_t e1,
-                                uint64_t g, uint64_t S, float inv) {
+// OWN: reduce-scatter of my segment of every window (sum of all N pools in ring order, kept
+// in my pool); else all-gather of segment q from its owner (src[0]) into my pool. Both unpack
+// every value from registers. f is the flattened vector space of that segment over the
+// windows (FlatWins): the owner's RS and every rank's AG of segment q map flat vector x to the
+// same CTA, so the middle barrier (CTA b <-> CTA b) orders exactly the vectors it needs.
+template <int DT, int NT, bool OWN>
+__device__ void pull_flat(const RingArgs& a, const StepTable& T, const char* const* src, int n, char* local,
+                          const FlatWins& f, uint64_t g, uint64_t S, float inv) {
     constexpr int VE = Vec<DT>::kElems;
-    constexpr int U = 8;
-    uint64_t v0 = (e0 + VE - 1) / VE, v1 = e1 / VE;
-    if (v0 >= v1) v0 = v1 = e1 / VE + 1;
-    if (blockIdx.x == 0) {
-        auto edge = [&](uint64_t lo, uint64_t hi) {
-            for (uint64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-                float xv;
-                if (DT == GF_F16) {
-                    const uint16_t h = reinterpret_cast<const volatile uint16_t*>(owner)[e];
-                    reinterpret_cast<uint16_t*>(local)[e] = h;
-                    xv = gfd::dec(h);
-                } else {
-                    xv = reinterpret_cast<const volatile float*>(owner)[e];
-                    reinterpret_cast<float*>(local)[e] = xv;
-                }
-                const int t = tensor_at(T, e);
-                T.dst[t][e - T.off[t]] = gfd::mul(xv, inv);
-            }
-        };
-        if (v0 < v1) {
-            edge(e0, v0 * VE);
-            edge(v1 * VE, e1);
-        } else {
-            edge(e0, e1);
-        }
+    constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
+    constexpr int NS = OWN ? NMAX : 1;
+    constexpr int U = OWN ? (NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1)) : 8;
+    // unaligned edges, scalar: window w's by CTA w mod grid (the same CTA in RS and AG)
+    for (int w = int(blockIdx.x); w < a.nwin; w += int(gridDim.x)) {
+        const uint64_t e0 = f.e0[w], e1 = f.e1[w], v0 = f.v0[w], v1 = v0 + (f.pre[w + 1] - f.pre[w]);
+        const uint64_t h0 = v1 > v0 ? min(e1, v0 * VE) : e1;
+        for (uint64_t e = e0 + threadIdx.x; e < h0; e += blockDim.x) pull_elem<DT, OWN>(T, src, n, local, e, inv);
+        if (v1 > v0)
+            for (uint64_t e = v1 * VE + threadIdx.x; e < e1; e += blockDim.x)
+                pull_elem<DT, OWN>(T, src, n, local, e, inv);
     }
-    for (uint64_t v = v0 + g; v < v1; v += S * U) {
-        uint4 x[U];
+    const uint64_t total = f.pre[a.nwin];
+    for (uint64_t x = g; x < total; x += S * U) {
+        uint4 v[U][NS];
+        uint64_t vv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t vv = v + uint64_t(u) * S;
-            if (vv < v1) x[u] = ld16_cg<DT>(owner + vv * 16);
+            const uint64_t xu = x + uint64_t(u) * S;
+            vv[u] = ~0ull;
+            if (xu < total) {
+                const int w = flat_window(f, a.nwin, xu);
+                vv[u] = f.v0[w] + (xu - f.pre[w]);
+#pragma unroll
+                for (int t = 0; t < NS; ++t) {
+                    if (OWN) {
+                        if (t < n) v[u][t] = gfd::ld16(src[t] + vv[u] * 16);
+                    } else {
+                        v[u][t] = ld16_cg<DT>(src[0] + vv[u] * 16);
+                    }
+                }
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t vv = v + uint64_t(u) * S;
-            if (vv < v1) {
-                gfd::st16(local + vv * 16, x[u]);
-                unpack_vec<DT>(T, vv, x[u], inv);
+            if (vv[u] == ~0ull) continue;
+            uint4 acc = v[u][0];
+            if (OWN) {
+#pragma unroll
+                for (int t = 1; t < NS; ++t)
+                    if (t < n) acc = Vec<DT>::acc(v[u][t], acc);
+                gfd::st16_keep(local + vv[u] * 16, acc);  // the peers pull it next
+            } else {
+                gfd::st16(local + vv[u] * 16, acc);
             }
+            unpack_vec<DT>(T, vv[u], acc, inv);
         }
     }
 }
@@ -402,27 +382,23 @@ rsag_kernel(const __grid_constant__ RingArgs a, const __grid_constant__ StepTabl
     const uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool tr = a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
     if (tr) a.trace[0] = gfd::globaltimer_ns();
+    constexpr int VE = Vec<DT>::kElems;
+    __shared__ FlatWins flat;
+    flat_build<VE>(a, n, a.pos, flat, true);  // my segment of every window (this piece)
     if (!cross_barrier(a, epoch + 1, &s_ok, false)) return;  // peers' pools are packed
     if (tr) a.trace[1] = gfd::globaltimer_ns();
     const char* src[NMAX];
 #pragma unroll
     for (int t = 0; t < NMAX; ++t) src[t] = (t < n) ? a.bufs[a.ring[(a.pos + t) % n]] : nullptr;
-    for (int w = 0; w < a.nwin; ++w) {
-        uint64_t e0, e1;
-        segment(a, n, w, a.pos, e0, e1);
-        rs_pull_segment<DT, NT>(a, T, src, n, part_cut(e0, e1, a.part_lo), part_cut(e0, e1, a.part_hi), g, S, inv);
-    }
+    char* local = a.bufs[a.rank];
+    pull_flat<DT, NT, true>(a, T, src, n, local, flat, g, S, inv);
     if (tr) a.trace[2] = gfd::globaltimer_ns();
     if (!cross_barrier(a, epoch + 2, &s_ok, true)) return;  // my segment sums are visible
-    char* local = a.bufs[a.rank];
-    for (int w = 0; w < a.nwin; ++w) {
-        for (int j = 1; j < n; ++j) {  // next ring position first: owners differ across ranks
-            const int q = (a.pos + j) % n;
-            uint64_t e0, e1;
-            segment(a, n, w, q, e0, e1);
-            ag_pull_segment<DT>(T, a.bufs[a.ring[q]], local, part_cut(e0, e1, a.part_lo),
-                                part_cut(e0, e1, a.part_hi), g, S, inv);
-        }
+    for (int j = 1; j < n; ++j) {  // next ring position first: owners differ across ranks
+        const int q = (a.pos + j) % n;
+        flat_build<VE>(a, n, q, flat, true);
+        const char* owner[1] = {a.bufs[a.ring[q]]};
+        pull_flat<DT, NT, false>(a, T, owner, n, local, flat, g, S, inv);
     }
     uint64_t fin = epoch + 2;
     if (exit_barrier) {  // the peers are done reading my pool (no write drain involved)

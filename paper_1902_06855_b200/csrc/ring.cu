@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kRingThreads) csc_pull_kernel(const __grid_con
 }
 
 template <int DT, int NT, bool P2P>
-__global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constant__ RingArgs a) {
+__global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(const __grid_constant__ RingArgs a) {
     constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
     __shared__ int s_ok;
     uint64_t epoch = 0;
@@ -308,6 +308,9 @@ __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constan
     const int p = P2P ? a.pos : int(blockIdx.y);
     const bool tr = P2P && a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
     if (tr) a.trace[0] = gfd::globaltimer_ns();
+    __shared__ FlatWins flat;  // explicit windows, several: one flattened sweep
+    const bool use_flat = a.nwin > 1;
+    if (use_flat) flat_build<Vec<DT>::kElems>(a, n, p, flat);
     if (P2P && !cross_barrier(a, epoch + 1, &s_ok, false)) return;
     if (tr) a.trace[1] = gfd::globaltimer_ns();
 
@@ -326,7 +329,8 @@ __global__ void __launch_bounds__(kRingThreads) ring_kernel(const __grid_constan
         stride = a.plan[3];
     }
     const WinGroups wg(nwin, a.nwin < 0);  // planned windows: CTA groups sweep them concurrently
-    for (int w = wg.first; w < nwin; w += wg.step) {
+    if (use_flat) reduce_flat<DT, NT>(a, src, n, flat, gtid, T);
+    for (int w = use_flat ? nwin : wg.first; w < nwin; w += wg.step) {
         uint64_t ws, wl;
         if (a.nwin >= 0) {
             ws = a.wstart[w];

@@ -175,6 +175,117 @@ inline void fill_common(gf_comm* c, RingArgs& a, uint64_t heap_off) {
     a.trace = c->trace ? reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(c->err_dev) + 64) : nullptr;
 }
 
+// Explicit windows (FusionEngine theta windows, <= kMaxW per launch, lengths as they fall):
+// the owned segments of all windows form ONE vector space that the grid sweeps in lockstep,
+// so a launch over many small windows costs one NVLink round trip, not one per window.
+// FlatWins::build runs before the entry barrier (it only reads the launch arguments).
+struct FlatWins {
+    uint64_t pre[kMaxW + 1];  // vectors of the owned segments of windows < w
+    uint64_t v0[kMaxW];       // first aligned vector of window w's owned segment
+    uint64_t e0[kMaxW], e1[kMaxW];
+};
+
+template <int VE>
+__device__ __forceinline__ void flat_build(const RingArgs& a, int n, int p, FlatWins& f, bool parts = false) {
+    __shared__ uint64_t warp_tot[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();  // f may still be read by a sweep over the previous segment
+    for (int w0 = 0; w0 < a.nwin; w0 += blockDim.x) {  // one pass for <= blockDim windows
+        const int w = w0 + threadIdx.x;
+        uint64_t cnt = 0;
+        if (w < a.nwin) {
+            const uint64_t wl = a.wlen[w], base = wl / uint64_t(n), rem = wl % uint64_t(n), up = uint64_t(p);
+            uint64_t e0 = a.wstart[w] + up * base + min(up, rem);  // segment_of (collectives.cpp:47-53)
+            uint64_t e1 = e0 + base + (up < rem ? 1 : 0);
+            if (parts) {
+                const uint64_t s0 = e0, s1 = e1;
+                e0 = part_cut(s0, s1, a.part_lo);
+                e1 = part_cut(s0, s1, a.part_hi);
+            }
+            const uint64_t v0 = (e0 + VE - 1) / VE, v1 = e1 / VE;
+            f.e0[w] = e0;
+            f.e1[w] = e1;
+            f.v0[w] = v0;
+            cnt = v1 > v0 ? v1 - v0 : 0;
+        }
+        uint64_t x = cnt;  // block-wide inclusive scan: warps, then warp totals
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_tot[warp] = x;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t run = w0 == 0 ? 0 : f.pre[w0];
+            for (int q = 0; q < int(blockDim.x >> 5); ++q) {
+                const uint64_t t = warp_tot[q];
+                warp_tot[q] = run;
+                run += t;
+            }
+            if (w0 == 0) f.pre[0] = 0;
+        }
+        __syncthreads();
+        if (w < a.nwin) f.pre[w + 1] = warp_tot[warp] + x;
+        __syncthreads();
+    }
+}
+
+// window holding flat vector x: the last w with pre[w] <= x
+__device__ __forceinline__ int flat_window(const FlatWins& f, int nwin, uint64_t x) {
+    int lo = 0, hi = nwin;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (f.pre[mid] <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+template <int DT, int NT>
+__device__ __forceinline__ void reduce_flat(const RingArgs& a, const char* const* src, int n, const FlatWins& f,
+                                            uint64_t gtid, uint64_t T) {
+    constexpr int VE = Vec<DT>::kElems;
+    constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
+    constexpr int U = NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1);
+    for (int w = int(blockIdx.x); w < a.nwin; w += int(gridDim.x)) {  // unaligned edges, scalar
+        const uint64_t e0 = f.e0[w], e1 = f.e1[w], v0 = f.v0[w], v1 = v0 + (f.pre[w + 1] - f.pre[w]);
+        if (v1 == v0) {
+            for (uint64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
+        } else {
+            for (uint64_t e = e0 + threadIdx.x; e < v0 * VE; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
+            for (uint64_t e = v1 * VE + threadIdx.x; e < e1; e += blockDim.x) Vec<DT>::scalar(a, src, n, e);
+        }
+    }
+    const uint64_t total = f.pre[a.nwin];
+    for (uint64_t x = gtid; x < total; x += T * U) {
+        uint4 v[U][NMAX];
+        uint64_t vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t xu = x + uint64_t(u) * T;
+            vv[u] = ~0ull;
+            if (xu < total) {
+                const int w = flat_window(f, a.nwin, xu);
+                vv[u] = f.v0[w] + (xu - f.pre[w]);
+#pragma unroll
+                for (int t = 0; t < NMAX; ++t)
+                    if (t < n) v[u][t] = gfd::ld16(src[t] + vv[u] * 16);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (vv[u] == ~0ull) continue;
+            uint4 acc = v[u][0];
+#pragma unroll
+            for (int t = 1; t < NMAX; ++t)
+                if (t < n) acc = Vec<DT>::acc(v[u][t], acc);
+#pragma unroll
+            for (int t = 0; t < NMAX; ++t)
+                if (t < n) gfd::st16(const_cast<char*>(src[(t + 1) % n]) + vv[u] * 16, acc);
+        }
+    }
+}
+
 // Planned (CSC) windows are all of one length except the last. With several of them the grid
 // is cut into `groups` CTA groups of c CTAs; group g sweeps windows g, g + groups, ... so the
 // windows' NVLink round trips overlap instead of following one another. Depends only on
