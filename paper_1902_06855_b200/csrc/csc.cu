@@ -185,6 +185,112 @@ __device__ __forceinline__ void nacc_add(uint64_t* nacc, uint64_t c, uint64_t u,
     }
 }
 
+// One 16-byte pool vector of K2: g (8 fp32) packed, corrected with hg (8 fp32) into the new
+// pool halves ov and the new residual hn (write_tensor + csc_correct, sparse.hpp:35-40). The
+// packed fast path runs when no half is special; otherwise the exact per-element path. nan:
+// the vector holds a NaN (the pool holds no inf, so special == NaN).
+__device__ __forceinline__ void correct8(const gfd::F8& gv, const float* hp, bool im, float mom, float hn[8],
+                                         uint4& ov, bool& nan) {
+    const uint4 h1 = gfd::enc8(gv.lo, gv.hi);  // pack (write_tensor)
+    bool slow = gfd::any_special(h1);
+    if (!slow) {
+        const uint32_t hw[4] = {h1.x, h1.y, h1.z, h1.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float2 g1 = gfd::h2f2(hw[k]);
+            const float a0 = __fadd_rn(g1.x, hp[2 * k]);
+            const float a1 = __fadd_rn(g1.y, hp[2 * k + 1]);
+            hn[2 * k] = im ? 0.0f : __fmul_rn(mom, a0);
+            hn[2 * k + 1] = im ? 0.0f : __fmul_rn(mom, a1);
+            o[k] = gfd::f22h2(a0, a1);
+        }
+        ov = make_uint4(o[0], o[1], o[2], o[3]);
+        slow = gfd::any_special(ov);  // non-finite or clamped sum: exact slow path
+    }
+    nan = false;
+    if (slow) {
+        const float g[8] = {gv.lo.x, gv.lo.y, gv.lo.z, gv.lo.w, gv.hi.x, gv.hi.y, gv.hi.z, gv.hi.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) hn[k] = hp[k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint16_t lo = gfd::enc(correct_elem(gfd::dec(gfd::enc(g[2 * k])), &hn[2 * k], im, mom));
+            const uint16_t hi = gfd::enc(correct_elem(gfd::dec(gfd::enc(g[2 * k + 1])), &hn[2 * k + 1], im, mom));
+            o[k] = uint32_t(lo) | (uint32_t(hi) << 16);
+        }
+        ov = make_uint4(o[0], o[1], o[2], o[3]);
+        nan = gfd::any_special(ov);
+    }
+}
+
+// K2 over one 8192-element tile of tensor table entry (tile index `tile`), by NTH threads.
+template <int DT, int NTH>
+__device__ __forceinline__ void pack_correct_tile(const TensorTable& T, uint64_t tile, void* __restrict__ pool,
+                                                  float* __restrict__ hg, void* __restrict__ staging,
+                                                  const uint8_t* __restrict__ imp, const uint64_t* __restrict__ coff,
+                                                  uint64_t chunk, uint64_t nc, float mom, uint64_t* __restrict__ nacc) {
+    const int t = find_tensor(T, tile);
+    const uint64_t base = (tile - T.tiles[t]) * kTile;
+    const uint64_t len = min(kTile, T.cnt[t] - base);
+    const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
+    const uint64_t po = T.off[t] + base;
+    uint64_t done = 0;
+    if (DT == GF_F16 && (reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0 && po % 8 == 0 &&
+        chunk % 8 == 0 && (reinterpret_cast<uintptr_t>(hg) & 31u) == 0 &&
+        (reinterpret_cast<uintptr_t>(pool) & 15u) == 0 &&
+        (reinterpret_cast<uintptr_t>(staging) & 15u) == 0) {
+        // 8 consecutive pool elements never straddle a chunk boundary here.
+        uint16_t* __restrict__ d = static_cast<uint16_t*>(pool) + po;
+        uint16_t* __restrict__ stg = static_cast<uint16_t*>(staging);
+        const int nvec = int(len / 8);
+        for (int v0 = 0; v0 < nvec; v0 += NTH) {
+            const int v = v0 + threadIdx.x;
+            const bool act = v < nvec;
+            uint64_t c = 0, units = 0;
+            bool im = true, nan = false;
+            if (act) {
+                const uint64_t pi = po + 8 * uint64_t(v);
+                c = min(pi / chunk, nc - 1);
+                im = imp[c] != 0;
+                const gfd::F8 gv = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
+                const gfd::F8 hv = gfd::ld32f(hg + pi);
+                float hn[8];
+                uint4 ov;
+                correct8(gv, reinterpret_cast<const float*>(&hv), im, mom, hn, ov, nan);
+                gfd::st32f(hg + pi, make_float4(hn[0], hn[1], hn[2], hn[3]),
+                           make_float4(hn[4], hn[5], hn[6], hn[7]));
+                gfd::st16(d + 8 * v, ov);
+                if (im && stg) gfd::st16(stg + coff[c] + (pi - c * chunk), ov);
+                if ((!im || !stg) && nacc) units = units8(nan ? make_uint4(0, 0, 0, 0) : ov);
+            }
+            if (nacc) nacc_add(nacc, c, units, nan, act && (!im || !stg));
+        }
+        done = uint64_t(nvec) * 8;
+    }
+    for (uint64_t i = done + threadIdx.x; i < len; i += NTH) {
+        const uint64_t pi = po + i;
+        const uint64_t c = min(pi / chunk, nc - 1);
+        const bool im = imp[c] != 0;
+        if (DT == GF_F16) {
+            const uint16_t w = gfd::enc(correct_elem(gfd::dec(gfd::enc(s[i])), hg + pi, im, mom));
+            static_cast<uint16_t*>(pool)[pi] = w;
+            if (im && staging) static_cast<uint16_t*>(staging)[coff[c] + (pi - c * chunk)] = w;
+            if ((!im || !staging) && nacc) {
+                if ((w & 0x7C00u) == 0x7C00u)
+                    atomicOr(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)kNaccNaN);
+                else if (half_units(w))
+                    atomicAdd(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)half_units(w));
+            }
+        } else {
+            const float w = correct_elem(s[i], hg + pi, im, mom);
+            static_cast<float*>(pool)[pi] = w;
+            if (im && staging) static_cast<float*>(staging)[coff[c] + (pi - c * chunk)] = w;
+        }
+    }
+}
+
 // K2: fused pack + correction + compaction (+ exact norms of the unimportant chunks; of
 // every chunk when staging is null: world 1, where the pool already holds the exchanged sums).
 // 4 CTAs per SM (64 registers): measured best (AlexNet CSC: 154 us; 168 us at 78 registers
@@ -196,97 +302,8 @@ pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ po
                     const uint8_t* __restrict__ imp, const uint64_t* __restrict__ coff,
                     uint64_t chunk, uint64_t nc, float mom, uint64_t total_tiles,
                     uint64_t* __restrict__ nacc) {
-    for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const int t = find_tensor(T, tile);
-        const uint64_t base = (tile - T.tiles[t]) * kTile;
-        const uint64_t len = min(kTile, T.cnt[t] - base);
-        const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
-        const uint64_t po = T.off[t] + base;
-        uint64_t done = 0;
-        if (DT == GF_F16 && (reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0 && po % 8 == 0 &&
-            chunk % 8 == 0 && (reinterpret_cast<uintptr_t>(hg) & 31u) == 0 &&
-            (reinterpret_cast<uintptr_t>(pool) & 15u) == 0 &&
-            (reinterpret_cast<uintptr_t>(staging) & 15u) == 0) {
-            // 8 consecutive pool elements never straddle a chunk boundary here.
-            uint16_t* __restrict__ d = static_cast<uint16_t*>(pool) + po;
-            uint16_t* __restrict__ stg = static_cast<uint16_t*>(staging);
-            const int nvec = int(len / 8);
-            for (int v0 = 0; v0 < nvec; v0 += kThreads) {
-                const int v = v0 + threadIdx.x;
-                const bool act = v < nvec;
-                uint64_t c = 0, units = 0;
-                bool im = true, nan = false;
-                if (act) {
-                    const uint64_t pi = po + 8 * uint64_t(v);
-                    c = min(pi / chunk, nc - 1);
-                    im = imp[c] != 0;
-                    const gfd::F8 gv = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
-                    gfd::F8 hv = gfd::ld32f(hg + pi);
-                    float* hp = reinterpret_cast<float*>(&hv);
-                    const uint4 h1 = gfd::enc8(gv.lo, gv.hi);  // pack (write_tensor)
-                    uint4 ov;
-                    bool slow = gfd::any_special(h1);
-                    float hn[8];
-                    if (!slow) {
-                        const uint32_t hw[4] = {h1.x, h1.y, h1.z, h1.w};
-                        uint32_t o[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const float2 g1 = gfd::h2f2(hw[k]);
-                            const float a0 = __fadd_rn(g1.x, hp[2 * k]);
-                            const float a1 = __fadd_rn(g1.y, hp[2 * k + 1]);
-                            hn[2 * k] = im ? 0.0f : __fmul_rn(mom, a0);
-                            hn[2 * k + 1] = im ? 0.0f : __fmul_rn(mom, a1);
-                            o[k] = gfd::f22h2(a0, a1);
-                        }
-                        ov = make_uint4(o[0], o[1], o[2], o[3]);
-                        slow = gfd::any_special(ov);  // non-finite or clamped sum: exact slow path
-                    }
-                    if (slow) {
-                        const float g[8] = {gv.lo.x, gv.lo.y, gv.lo.z, gv.lo.w, gv.hi.x, gv.hi.y, gv.hi.z, gv.hi.w};
-                        uint32_t o[4];
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) hn[k] = hp[k];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const uint16_t lo = gfd::enc(correct_elem(gfd::dec(gfd::enc(g[2 * k])), &hn[2 * k], im, mom));
-                            const uint16_t hi = gfd::enc(correct_elem(gfd::dec(gfd::enc(g[2 * k + 1])), &hn[2 * k + 1], im, mom));
-                            o[k] = uint32_t(lo) | (uint32_t(hi) << 16);
-                        }
-                        ov = make_uint4(o[0], o[1], o[2], o[3]);
-                        nan = gfd::any_special(ov);  // the pool holds no inf, so special == NaN
-                    }
-                    gfd::st32f(hg + pi, make_float4(hn[0], hn[1], hn[2], hn[3]),
-                               make_float4(hn[4], hn[5], hn[6], hn[7]));
-                    gfd::st16(d + 8 * v, ov);
-                    if (im && stg) gfd::st16(stg + coff[c] + (pi - c * chunk), ov);
-                    if ((!im || !stg) && nacc) units = units8(nan ? make_uint4(0, 0, 0, 0) : ov);
-                }
-                if (nacc) nacc_add(nacc, c, units, nan, act && (!im || !stg));
-            }
-            done = uint64_t(nvec) * 8;
-        }
-        for (uint64_t i = done + threadIdx.x; i < len; i += kThreads) {
-            const uint64_t pi = po + i;
-            const uint64_t c = min(pi / chunk, nc - 1);
-            const bool im = imp[c] != 0;
-            if (DT == GF_F16) {
-                const uint16_t w = gfd::enc(correct_elem(gfd::dec(gfd::enc(s[i])), hg + pi, im, mom));
-                static_cast<uint16_t*>(pool)[pi] = w;
-                if (im && staging) static_cast<uint16_t*>(staging)[coff[c] + (pi - c * chunk)] = w;
-                if ((!im || !staging) && nacc) {
-                    if ((w & 0x7C00u) == 0x7C00u)
-                        atomicOr(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)kNaccNaN);
-                    else if (half_units(w))
-                        atomicAdd(reinterpret_cast<unsigned long long*>(nacc + c), (unsigned long long)half_units(w));
-                }
-            } else {
-                const float w = correct_elem(s[i], hg + pi, im, mom);
-                static_cast<float*>(pool)[pi] = w;
-                if (im && staging) static_cast<float*>(staging)[coff[c] + (pi - c * chunk)] = w;
-            }
-        }
-    }
+    for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x)
+        pack_correct_tile<DT, kThreads>(T, tile, pool, hg, staging, imp, coff, chunk, nc, mom, nacc);
 }
 
 // Staging pack (dir=0) / write-back (dir=1) over the important chunks listed in the plan
