@@ -293,7 +293,6 @@ class GradSync:
         """Pull-mode step in pieces: piece 0 is packed and exchanged on `stream` while pieces
         1.. are packed on a side stream; piece k's exchange waits for its pack. Every rank
         launches the pieces' exchanges in the same order (their CTA-pair barriers pair up)."""
-        import numpy as np  # noqa: F401
         m = len(self.layout.sizes)
         args = self._piece_args(grad_ptrs)
         if self._pieces_s is None:

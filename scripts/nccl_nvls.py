@@ -1,4 +1,4 @@
-import os, torch, torch.distributed as dist
+import torch, torch.distributed as dist
 dist.init_process_group("nccl")
 r = dist.get_rank(); torch.cuda.set_device(r)
 x = torch.ones(1 << 26, dtype=torch.float16, device="cuda")

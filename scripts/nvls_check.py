@@ -1,5 +1,5 @@
 # Does this box expose NVLink SHARP multicast (NVLS)? Device attribute + NCCL's own log.
-import ctypes, os, sys
+import ctypes
 import torch
 cuda = ctypes.CDLL("libcuda.so.1")
 cuda.cuInit(0)
