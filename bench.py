@@ -435,16 +435,21 @@ def main():
             barrier()
             step(i)
             torch.cuda.synchronize()
-            t = (_C.c_uint64 * 4)()
-            capi.call("gf_comm_trace", sync.comm, t)
-            rec.append([t[1] - t[0], t[2] - t[1], t[3] - t[2]])
+            t = (_C.c_uint64 * 11)()
+            capi.call("gf_comm_trace_n", sync.comm, t, 11)
+            rec.append([t[1] - t[0], t[2] - t[1], t[3] - t[2]] +
+                       ([t[5] - t[4], t[6] - t[5], t[7] - t[6], t[8] - t[7], t[9] - t[8], t[10] - t[9]]
+                        if csc else []))
         capi.call("gf_comm_set_trace", sync.comm, 0)
-        med = [statistics.median(r[j] for r in rec) / 1e3 for j in range(3)]
+        med = [statistics.median(r[j] for r in rec) / 1e3 for j in range(3)]  # ring CTA 0
         ring_trace = {"entry_wait_us": round(allmax(med[0]), 2), "body_us": round(allmax(med[1]), 2),
                       "exit_wait_us": round(allmax(med[2]), 2)}
         per_rank = [None] * world
         dist.all_gather_object(per_rank, [round(m, 2) for m in med])
         ring_trace["per_rank_entry_body_exit_us"] = per_rank
+        if csc:  # gf_csc_select phases (thread 0): finalize, entry wait, ring-order sums, exit wait, top-k, plan
+            ring_trace["select_phases_us"] = [round(allmax(statistics.median(r[j] for r in rec) / 1e3), 2)
+                                              for j in range(3, 9)]
 
     # ---- overlap with backward (fusion.cpp:72-123) -----------------------------
     overlap = None

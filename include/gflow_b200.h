@@ -170,6 +170,10 @@ int gf_comm_status(gf_comm* comm);
  * gf_comm_trace copies the latest record (call after the launch completed). */
 int gf_comm_set_trace(gf_comm* comm, int on);
 int gf_comm_trace(gf_comm* comm, uint64_t* out4);
+/* Words 0..n-1 (n <= 16) of the trace area: [0,4) the last collective kernel's CTA 0
+ * [start, entered, exit begin, end]; [4,11) gf_csc_select's [start, norms finalized, entry
+ * barrier passed, ring-order sums done, exit barrier passed, top-k done, end] (globaltimer ns). */
+int gf_comm_trace_n(gf_comm* comm, uint64_t* out, int n);
 int gf_comm_rank(gf_comm* comm);
 int gf_comm_world(gf_comm* comm);
 
@@ -258,6 +262,13 @@ int gf_ring_allreduce_colocated_planned(int dtype, void* const* bufs, int world,
  * norms, top-k selected -> flags (device, nc bytes); then coff/plan as gf_csc_plan. */
 /* With nacc != NULL the local norms are first finalized from the exact accumulators
  * (float(sum), x1/N where imp_cur[c]) and nacc is zeroed for the next iteration. */
+/* Switches this communicator's gf_csc_select to the push-inbox norm exchange: every rank
+ * writes its finalized norms into slot `rank` of each peer's inbox (world x nc floats at
+ * inbox_heap_off in the symmetric heap, same offset on every rank), so the selection needs one
+ * cross-GPU barrier instead of two and reads only local memory. Same results. All ranks must
+ * switch together; UINT64_MAX switches back. The caller must not rewrite its norms or
+ * inbox before its next exchange (the CSC step order guarantees it). */
+int gf_comm_set_select_inbox(gf_comm* comm, uint64_t inbox_heap_off);
 int gf_csc_select(gf_comm* comm, uint64_t norms_off, uint64_t nc, uint64_t k,
                   uint8_t* flags, uint64_t total, uint64_t chunk, int dtype, uint64_t theta,
                   uint64_t* coff, uint64_t* plan, uint64_t* nacc, const void* pool,

@@ -37,6 +37,7 @@ struct gf_comm {
     bool trace = false;
     uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;  // transport.hpp:25 kDefaultTimeout
     bool connected = false;
+    uint64_t sel_inbox_off = UINT64_MAX;  // gf_comm_set_select_inbox (UINT64_MAX: pull protocol)
 };
 
 namespace {

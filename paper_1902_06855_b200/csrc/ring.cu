@@ -57,6 +57,10 @@ struct SelArgs {
     uint64_t timeout_ns;
     int* err;
     uint64_t* trace;
+    // push-inbox norm exchange (gf_comm_set_select_inbox): rank r's finalized norms go to
+    // slot r of every peer's inbox before the one barrier; the sums then read local memory only
+    float* inbox_local;                  // world x nc floats: slot r = rank r's norms
+    float* inbox_peer[GF_MAX_RANKS];     // each rank's inbox as mapped here
 };
 
 // ---- CSC write-back fused into the planned ring (staging -> pool + exact chunk L1) -------
@@ -372,6 +376,8 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
     if (threadIdx.x == 0) s_ok = 1;
     const int n = a.world;
     const uint64_t epoch = a.p2p ? a.epochs[0] : 0;
+    const bool tr = a.trace != nullptr && threadIdx.x == 0;  // [start, finalized, entered, summed, exited, top-k, end]
+    if (tr) a.trace[0] = gfd::globaltimer_ns();
     // Finalize this iteration's local norms from the exact accumulators written by
     // pack_correct (unimportant chunks) and scatter (important chunks): chunk_l1 +
     // x1/N (sparse.cpp:176-184), then re-arm the accumulators for the next iteration.
@@ -398,7 +404,20 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
         }
         __syncthreads();
     }
+    const bool inbox = a.p2p && a.inbox_local != nullptr;
+    if (inbox) {  // push my norms into slot `rank` of every peer's inbox (posted NVLink writes)
+        for (uint64_t i = threadIdx.x; i < a.nc; i += gfs::kSelThreads) {
+            const float v = a.norms[a.rank][i];
+            for (int q = 0; q < n; ++q)
+                if (q != a.rank) a.inbox_peer[q][uint64_t(a.rank) * a.nc + i] = v;
+        }
+    }
+    if (tr) a.trace[1] = gfd::globaltimer_ns();
+    // entry: peers' norms are final (and, with the inbox, have landed here: the fence before
+    // each flag release makes the CTA's pushes visible first)
     if (a.p2p && !cross_barrier(a, epoch + 1, &s_ok)) return;
+    if (inbox && threadIdx.x == 0) a.epochs[0] = epoch + 1;
+    if (tr) a.trace[2] = gfd::globaltimer_ns();
     const uint64_t base = a.nc / uint64_t(n), rem = a.nc % uint64_t(n);
     for (uint64_t i = threadIdx.x; i < a.nc; i += gfs::kSelThreads) {
         // segment index of element i under segment_of(nc, n, .) (collectives.cpp:47-53)
@@ -407,18 +426,27 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
         // issue every rank's load before the first add: one NVLink round trip, not n
         float v[GF_MAX_RANKS];
 #pragma unroll
-        for (int t = 0; t < GF_MAX_RANKS; ++t)
-            if (t < n) v[t] = a.norms[a.ring[(j + t) % n]][i];
+        for (int t = 0; t < GF_MAX_RANKS; ++t) {
+            if (t < n) {
+                const int src = a.ring[(j + t) % n];
+                v[t] = (inbox && src != a.rank) ? a.inbox_local[uint64_t(src) * a.nc + i] : a.norms[src][i];
+            }
+        }
         float acc = v[0];
 #pragma unroll
         for (int t = 1; t < GF_MAX_RANKS; ++t)
             if (t < n) acc = gfd::add(v[t], acc);
         red[i] = acc;
     }
-    if (a.p2p) {
+    if (tr) a.trace[3] = gfd::globaltimer_ns();
+    // exit: without the inbox, peers may still be loading my norms, which are overwritten with
+    // the sums below. With it nobody reads my norms buffer; my inbox slots are next written by
+    // the peers' next selection, which follows the next exchange's entry barrier with me.
+    if (a.p2p && !inbox) {
         if (!cross_barrier(a, epoch + 2, &s_ok)) return;
         if (threadIdx.x == 0) a.epochs[0] = epoch + 2;
     }
+    if (tr) a.trace[4] = gfd::globaltimer_ns();
     __syncthreads();
     for (uint64_t i = threadIdx.x; i < a.nc; i += gfs::kSelThreads) {
         if (a.p2p) {
@@ -428,7 +456,9 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
         }
     }
     gfs::block_topk(red, a.nc, a.k, a.flags, sh);
+    if (tr) a.trace[5] = gfd::globaltimer_ns();
     if (a.coff && a.plan) gfs::block_plan(a.flags, a.total, a.chunk, a.nc, a.esz, a.theta, a.coff, a.plan, sh);
+    if (tr) a.trace[6] = gfd::globaltimer_ns();
 }
 
 template <int DT, bool P2P>
@@ -501,9 +531,9 @@ int gf_comm_create(int world, int rank, int device, uint64_t heap_bytes, gf_comm
     c->pos = rank;
     cudaError_t e = cudaMalloc(&c->alloc, kFlagBytes + c->heap_bytes);
     if (e == cudaSuccess) e = cudaMemset(c->alloc, 0, kFlagBytes);
-    if (e == cudaSuccess) e = cudaHostAlloc(&c->err_host, 128, cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostAlloc(&c->err_host, 256, cudaHostAllocMapped);
     if (e == cudaSuccess) {
-        std::memset(c->err_host, 0, 128);
+        std::memset(c->err_host, 0, 256);
         e = cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0);
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -635,6 +665,22 @@ int gf_comm_trace(gf_comm* c, uint64_t* out4) {
     const volatile uint64_t* t =
         reinterpret_cast<const volatile uint64_t*>(reinterpret_cast<char*>(c->err_host) + 64);
     for (int i = 0; i < 4; ++i) out4[i] = t[i];
+    return GF_OK;
+}
+
+int gf_comm_set_select_inbox(gf_comm* c, uint64_t inbox_heap_off) {
+    if (!c) return gfi::fail(GF_ERR_CONFIG, "null communicator");
+    if (inbox_heap_off != UINT64_MAX && (inbox_heap_off % 16 != 0 || inbox_heap_off >= c->heap_bytes))
+        return gfi::fail(GF_ERR_CONFIG, "gf_comm_set_select_inbox: offset outside the heap or not 16-B aligned");
+    c->sel_inbox_off = inbox_heap_off;
+    return GF_OK;
+}
+
+int gf_comm_trace_n(gf_comm* c, uint64_t* out, int n) {
+    if (!c || !out || n < 0 || n > 16) return gfi::fail(GF_ERR_CONFIG, "gf_comm_trace_n: bad arguments");
+    const volatile uint64_t* t =
+        reinterpret_cast<const volatile uint64_t*>(reinterpret_cast<char*>(c->err_host) + 64);
+    for (int i = 0; i < n; ++i) out[i] = t[i];
     return GF_OK;
 }
 
@@ -916,8 +962,16 @@ int gf_csc_select(gf_comm* c, uint64_t norms_off, uint64_t nc, uint64_t k, uint8
     a.imp_cur = imp_cur;
     a.flags_local = reinterpret_cast<uint64_t*>(c->alloc);
     a.epochs = a.flags_local + kFlagWords;
+    a.trace = c->trace ? reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(c->err_dev) + 64) + 4 : nullptr;
     a.timeout_ns = c->timeout_ns;
     a.err = c->err_dev;
+    if (c->world > 1 && c->sel_inbox_off != UINT64_MAX) {
+        if (c->sel_inbox_off + uint64_t(c->world) * nc * 4 > c->heap_bytes)
+            return gfi::fail(GF_ERR_CONFIG, "gf_csc_select: the select inbox (world x nc floats) is outside the heap");
+        a.inbox_local = reinterpret_cast<float*>(c->alloc + kFlagBytes + c->sel_inbox_off);
+        for (int r = 0; r < c->world; ++r)
+            a.inbox_peer[r] = reinterpret_cast<float*>(c->peer_alloc[r] + kFlagBytes + c->sel_inbox_off);
+    }
     return select_launch(a, gfi::S(stream));
 }
 

@@ -148,7 +148,9 @@ class GradSync:
         self._piece_cache = {}
         self._pieces_s = None
         self.norms_off = self.stage_off + (_align(L.total * self.esz) if csc else 0)
-        heap = self.norms_off + _align(L.num_chunks * 4)
+        # CSC at N>1: the select's push-inbox (world x nc norms), one barrier instead of two
+        self.inbox_off = self.norms_off + _align(L.num_chunks * 4)
+        heap = self.inbox_off + (_align(world * L.num_chunks * 4) if csc and world > 1 else 0)
         self.comm = C.c_void_p()
         capi.call("gf_comm_create", world, rank, device, heap, C.byref(self.comm))
         if world > 1:
@@ -159,6 +161,8 @@ class GradSync:
             handles = allgather(bytes(h))
             capi.call("gf_comm_connect_ipc", self.comm, b"".join(handles))
         capi.call("gf_comm_set_timeout_ms", self.comm, timeout_ms)
+        if csc and world > 1:
+            capi.call("gf_comm_set_select_inbox", self.comm, self.inbox_off)
         base = C.c_void_p()
         capi.call("gf_comm_heap", self.comm, C.byref(base), None)
         self.heap_base = base.value

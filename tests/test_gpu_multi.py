@@ -252,6 +252,23 @@ def _worker_csc(rank, world, port):
     wantr = o.ring_allreduce([s.copy() for s in stg], dtype=F16)
     assert (got == wantr[rank]).all()
     dist.barrier()
+    # push-inbox norm exchange (one barrier): same sums and set, several rounds
+    capi.call("gf_comm_set_select_inbox", comm, 2 << 20)
+    for it in range(4):
+        norms = [np.random.default_rng(100 * it + r).uniform(0, 5, nc).astype(np.float32) for r in range(world)]
+        for r in range(world):
+            norms[r][: 16 * (it + 1)] = 1.25  # ties
+        _put(cudart, base, noff, norms[rank])
+        capi.call("gf_csc_select", comm, noff, nc, k + it, flags.data_ptr(), total, 32000, F16,
+                  capi.THETA_INF, coff.data_ptr(), plan.data_ptr(), None, None, None, None)
+        torch.cuda.synchronize()
+        capi.call("gf_comm_status", comm)
+        want_sum = o.ring_allreduce([x.copy() for x in norms], dtype=F32)
+        assert (_bits(_get(cudart, base, noff, norms[rank])) == _bits(want_sum[rank])).all(), it
+        assert (flags.cpu().numpy() == o.select_topk(want_sum[0], k + it)).all(), it
+        dist.barrier()  # the next round's pushes follow every rank's reads (the exchange's role)
+    capi.call("gf_comm_set_select_inbox", comm, (1 << 64) - 1)
+    dist.barrier()
 
 
 def _worker_timeout(rank, world, port):
