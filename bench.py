@@ -196,7 +196,7 @@ def main():
                     help="also measure the dense sync overlapped with a synthetic backward of "
                          "this many ms (bf16 GEMMs; tensors complete in descending id, theta "
                          "windows launch as they close: the reference's lazy allreduce)")
-    ap.add_argument("--dense-mode", default="auto", choices=["auto", "pull", "push", "fused"],
+    ap.add_argument("--dense-mode", default="auto", choices=["auto", "pull", "push", "fused", "rspush"],
                     help="dense N>1: pull (pack + pull RS/AG fused with unpack), push (pack + "
                          "push-pull ring + unpack), fused (one kernel); auto = pull at N=2, else push")
     ap.add_argument("--pull-parts", default=None,
@@ -383,13 +383,14 @@ def main():
     algo["ring_scatter"] = algo["ring"]  # CSC exchange with the write-back fused in
     algo["ring_unpack"] = algo["ring"]   # dense pull mode: RS + AG with the unpack fused in
     algo["pull_step"] = algo["ring"]     # pull mode in pieces: packs overlap the exchanges
+    algo["push_step"] = algo["ring"]     # rspush: pack (with the RS pushes) + reduce/AG + unpack
     if args.fused:  # its binding roofline: NVLink bus bytes at N>1, HBM bytes at N=1
         algo["fused_step"] = ring_bytes if world > 1 else total * 12
     dom = max(seg_ms, key=lambda k: seg_ms[k]) if seg_ms else None
     roof = None
     if dom is not None and algo.get(dom):
         t_s = seg_ms[dom] / 1e3
-        if dom in ("ring", "ring_scatter", "ring_unpack", "pull_step") or (dom == "fused_step" and world > 1):
+        if dom in ("ring", "ring_scatter", "ring_unpack", "pull_step", "push_step") or (dom == "fused_step" and world > 1):
             ach = algo[dom] / t_s / 1e9
             roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": 900.0, "unit": "GB/s",
                     "frac": round(ach / 900.0, 3), "traffic": None, "kernel": "ring_kernel",
@@ -419,7 +420,7 @@ def main():
         d = {"ms": round(v, 4)}
         if algo.get(k):
             d["GBps"] = round(algo[k] / (v / 1e3) / 1e9, 1)
-            if k not in ("ring", "ring_scatter", "ring_unpack", "pull_step") and not (k == "fused_step" and world > 1):
+            if k not in ("ring", "ring_scatter", "ring_unpack", "pull_step", "push_step") and not (k == "fused_step" and world > 1):
                 d["frac_hbm"] = round(d["GBps"] / hbm_peak, 3)
             else:
                 d["busbw_frac_900"] = round(d["GBps"] / 900, 3)
@@ -603,7 +604,7 @@ def main():
 
     if rank == 0:
         bus = None
-        rk = next((k for k in ("ring", "ring_unpack", "ring_scatter", "pull_step") if k in seg_ms), "ring")
+        rk = next((k for k in ("ring", "ring_unpack", "ring_scatter", "pull_step", "push_step") if k in seg_ms), "ring")
         if world > 1 and rk in seg_ms:
             bus = round(ring_bytes / (seg_ms[rk] / 1e3) / 1e9, 1)
         elif world > 1 and "fused_step" in seg_ms:

@@ -37,6 +37,8 @@
  *  gf_ring_allreduce_colocated      same, all ranks' buffers on one device   src/collectives.cpp:55-97
  *  gf_ring_allreduce_unpack         ring_allreduce of the windows + the update read g = get(i)*(1/N)
  *                                   src/collectives.cpp:55-97, src/trainer.cpp:332-347
+ *  gf_sync_step_dense_push          the same with the reduce-scatter pushed by the pack (write_tensor
+ *                                   src/gradient_pool.cpp:78-105 + ring_allreduce_on src/collectives.cpp:55-97)
  *  gf_sync_step_dense               one dense iteration: write_tensor x m + FusionEngine windows +
  *                                   update read (src/trainer.cpp:297-347), fused into one kernel
  *  gf_csc_exchange_pull             sparse_exchange ring + write-back (pull form) src/sparse.cpp:106-170
@@ -249,6 +251,17 @@ int gf_ring_allreduce_unpack_part(gf_comm* comm, int dtype, uint64_t pool_heap_o
  * exceeds cap). Host-only, no GPU. */
 int gf_part_ranges(const uint64_t* win_start, const uint64_t* win_len, int nwin, int world,
                    uint32_t part_lo, uint32_t part_hi, uint64_t* lo, uint64_t* hi, int cap);
+/* One dense sync step with the reduce-scatter's traffic riding on the pack (push form): the
+ * pack stores each packed vector straight into the owner of its segment (my pool, or my slot
+ * of the owner's inbox over NVLink); one kernel then sums every owned segment from local
+ * memory in ring order and pushes the sums into all pools; then unpack. Same results as
+ * gf_pack + gf_ring_allreduce + gf_unpack, bit for bit. fp16; the inbox (world-1 slots of
+ * the pool span, at inbox_heap_off, same offset on every rank) lives in the symmetric heap.
+ * src/dst/pool_off/count are HOST arrays (<= 256 tensors, covering the windows). */
+int gf_sync_step_dense_push(gf_comm* comm, int dtype, uint64_t pool_heap_off, uint64_t inbox_heap_off,
+                            const float* const* src, float* const* dst, const uint64_t* pool_off,
+                            const uint64_t* count, int ntensors, const uint64_t* win_start,
+                            const uint64_t* win_len, int nwin, void* stream);
 /* Emulation of `world` ranks whose buffers all live on the current device (no waits). */
 int gf_ring_allreduce_colocated(int dtype, void* const* bufs, int world, const int* ring_order,
                                 const uint64_t* win_start, const uint64_t* win_len, int nwin,

@@ -97,6 +97,7 @@ SIGNATURES = {
     "gf_csc_exchange_pull": [_vp, _u64, _vp, _vp, _u64, _u64, _vp, _vp],
     "gf_ring_allreduce_ptrs": [_vp, _i, _vp, _vp, _vp, _i, _vp],
     "gf_sync_step_dense": [_vp, _i, _u64, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _vp],
+    "gf_sync_step_dense_push": [_vp, _i, _u64, _u64, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _vp],
     "gf_ring_allreduce_unpack": [_vp, _i, _u64, _vp, _vp, _vp, _i, _vp, _vp, _i, _i, _vp],
     "gf_ring_allreduce_unpack_part": [_vp, _i, _u64, _vp, _vp, _vp, _i, _vp, _vp, _i, _u32, _u32, _i, _vp],
     "gf_ipc_export": [_vp, _vp, _u64p],

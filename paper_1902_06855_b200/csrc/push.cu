@@ -1,0 +1,271 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// The dense step in push form (gf_sync_step_dense_push): the reduce-scatter's traffic rides
+// on the pack.
+//
+//   1. pack_push   fp32 tensors -> fp16, and every packed vector is STORED where the ring will
+//                  reduce it: the rank at ring position j owns segment j of every window
+//                  (segment_of, src/collectives.cpp:47-53), so a vector of segment j goes to my
+//                  own pool when j is my position, else into my slot of rank ring[j]'s inbox
+//                  over NVLink. The pack's HBM reads and the scatter's NVLink writes overlap.
+//   2. rsp_kernel  after the entry barrier every operand of my segments is LOCAL (my pool + my
+//                  inbox slots): the sums, in ring order from my position (the reference's
+//                  arrival order, bit-identical), are pushed into every rank's pool (the
+//                  all-gather as posted writes), then the exit barrier.
+//   3. unpack      (K6) g_avg = dec(pool) * 1/N.
+//
+// Per rank and direction the NVLink bytes are the ring's 2(N-1)/N * K: (N-1)/N * K pushed by
+// the pack and (N-1)/N * K by the all-gather. Inbox slot s of the owner at position j holds
+// the contribution of the rank at position j + 1 + s (mod N), laid out like the pool.
+
+#include <algorithm>
+#include <cstring>
+
+#include "ring_device.cuh"
+#include "tensor_table.cuh"
+
+namespace {
+
+struct SegMap {  // routing of pool elements to their owners (explicit windows)
+    int nwin, world, pos, pad;
+    uint64_t slot_elems;                 // elements per inbox slot (the pool span)
+    char* pool_local;                    // my pool (fp16)
+    char* inbox_by_pos[GF_MAX_RANKS];    // owner at ring position j: its inbox as mapped here
+    uint64_t wstart[kMaxW];
+    uint64_t wlen[kMaxW];
+};
+
+// owner position and the end of its segment for pool element e (e inside the windows)
+__device__ __forceinline__ int seg_owner(const SegMap& m, uint64_t e, uint64_t& seg_end) {
+    int lo = 0, hi = m.nwin;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (m.wstart[mid] <= e) lo = mid; else hi = mid;
+    }
+    const uint64_t n = uint64_t(m.world), L = m.wlen[lo], x = e - m.wstart[lo];
+    const uint64_t base = L / n, rem = L % n, big = rem * (base + 1);
+    uint64_t j, j0;
+    if (x < big) {
+        j = x / (base + 1);
+        j0 = j * (base + 1);
+        seg_end = m.wstart[lo] + j0 + base + 1;
+    } else {
+        j = rem + (x - big) / base;
+        j0 = big + (j - rem) * base;
+        seg_end = m.wstart[lo] + j0 + base;
+    }
+    return int(j);
+}
+
+// where a packed element of segment owned by position j goes
+__device__ __forceinline__ uint16_t* route(const SegMap& m, int j, uint64_t e) {
+    if (j == m.pos) return reinterpret_cast<uint16_t*>(m.pool_local) + e;
+    const int slot = (m.pos - j - 1 + m.world) % m.world;
+    return reinterpret_cast<uint16_t*>(m.inbox_by_pos[j]) + uint64_t(slot) * m.slot_elems + e;
+}
+
+__device__ __forceinline__ void put_elem(const SegMap& m, uint64_t e, uint16_t h) {
+    uint64_t end;
+    *route(m, seg_owner(m, e, end), e) = h;
+}
+
+__global__ void __launch_bounds__(kThreads)
+pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ SegMap M, uint64_t total_tiles) {
+    for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const int t = find_tensor(T, tile);
+        const uint64_t base = (tile - T.tiles[t]) * kTile;
+        const uint64_t len = min(kTile, T.cnt[t] - base);
+        const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
+        const uint64_t po = T.off[t] + base;
+        uint64_t done = 0;
+        if ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0 && po % 8 == 0) {
+            const int nvec = int(len / 8);
+            float4 a[kVecPerThread], b[kVecPerThread];
+#pragma unroll
+            for (int k = 0; k < kVecPerThread; ++k) {
+                const int v = threadIdx.x + k * kThreads;
+                if (v < nvec) {
+                    const gfd::F8 f = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
+                    a[k] = f.lo;
+                    b[k] = f.hi;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kVecPerThread; ++k) {
+                const int v = threadIdx.x + k * kThreads;
+                if (v < nvec) {
+                    const uint4 h = gfd::enc8(a[k], b[k]);
+                    const uint64_t e = po + 8 * uint64_t(v);
+                    uint64_t end;
+                    const int j = seg_owner(M, e, end);
+                    if (e + 8 <= end) {  // the whole vector belongs to one owner
+                        gfd::st16(route(M, j, e), h);
+                    } else {             // a segment boundary inside the vector
+                        const uint32_t w[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            put_elem(M, e + q, uint16_t((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu));
+                    }
+                }
+            }
+            done = uint64_t(nvec) * 8;
+        }
+        for (uint64_t i = done + threadIdx.x; i < len; i += kThreads) put_elem(M, po + i, gfd::enc(s[i]));
+    }
+    // the CTA's NVLink stores are performed before the kernel ends (bar.sync makes the
+    // fence cumulative over the CTA, as in cross_barrier); the next kernel's flag follows
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+}
+
+// All-local reduce of my segments (pool + inbox slots, ring order) pushed to every pool.
+template <int NT>
+__global__ void __launch_bounds__(kRingThreads, 1)
+rsp_kernel(const __grid_constant__ RingArgs a, const char* __restrict__ inbox_local, uint64_t slot_bytes) {
+    constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
+    constexpr int U = NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1);
+    __shared__ int s_ok;
+    __shared__ FlatWins flat;
+    const uint64_t epoch = a.epochs[blockIdx.x];
+    if (threadIdx.x == 0) s_ok = 1;
+    const int n = NT > 0 ? NT : a.world;
+    flat_build<8>(a, n, a.pos, flat);
+    const bool tr = a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    if (tr) a.trace[0] = gfd::globaltimer_ns();
+    if (!cross_barrier(a, epoch + 1, &s_ok, false)) return;  // every peer's pack (and its pushes) is done
+    if (tr) a.trace[1] = gfd::globaltimer_ns();
+    const char* src[NMAX];  // ring order from my position: me, then the slots
+    char* dst[NMAX];        // every rank's pool, the next one on the ring first
+#pragma unroll
+    for (int t = 0; t < NMAX; ++t) {
+        src[t] = t == 0 ? a.bufs[a.rank] : (t < n ? inbox_local + uint64_t(t - 1) * slot_bytes : nullptr);
+        dst[t] = t < n ? a.bufs[a.ring[(a.pos + 1 + t) % n]] : nullptr;
+    }
+    // unaligned edges of window w: CTA w mod grid, scalar
+    for (int w = int(blockIdx.x); w < a.nwin; w += int(gridDim.x)) {
+        const uint64_t e0 = flat.e0[w], e1 = flat.e1[w], v0 = flat.v0[w], v1 = v0 + (flat.pre[w + 1] - flat.pre[w]);
+        auto edge = [&](uint64_t lo, uint64_t hi) {
+            for (uint64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+                uint16_t acc = reinterpret_cast<const uint16_t*>(src[0])[e];
+                for (int t = 1; t < n; ++t) acc = gfd::acc16(reinterpret_cast<const uint16_t*>(src[t])[e], acc);
+                for (int t = 0; t < n; ++t) reinterpret_cast<uint16_t*>(dst[t])[e] = acc;
+            }
+        };
+        if (v1 > v0) {
+            edge(e0, v0 * 8);
+            edge(v1 * 8, e1);
+        } else {
+            edge(e0, e1);
+        }
+    }
+    const uint64_t total = flat.pre[a.nwin];
+    const uint64_t T = uint64_t(gridDim.x) * blockDim.x, g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (uint64_t x = g; x < total; x += T * U) {
+        uint4 v[U][NMAX];
+        uint64_t vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t xu = x + uint64_t(u) * T;
+            vv[u] = ~0ull;
+            if (xu < total) {
+                const int w = flat_window(flat, a.nwin, xu);
+                vv[u] = flat.v0[w] + (xu - flat.pre[w]);
+#pragma unroll
+                for (int t = 0; t < NMAX; ++t)
+                    if (t < n) v[u][t] = gfd::ld16(src[t] + vv[u] * 16);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (vv[u] == ~0ull) continue;
+            uint4 acc = v[u][0];
+#pragma unroll
+            for (int t = 1; t < NMAX; ++t)
+                if (t < n) acc = gfd::acc16x8(v[u][t], acc);
+#pragma unroll
+            for (int t = 0; t < NMAX; ++t)
+                if (t < n) gfd::st16(dst[t] + vv[u] * 16, acc);
+        }
+    }
+    if (tr) a.trace[2] = gfd::globaltimer_ns();
+    if (!cross_barrier(a, epoch + 2, &s_ok, true)) return;  // every push into my pool landed
+    if (threadIdx.x == 0) a.epochs[blockIdx.x] = epoch + 2;
+    if (tr) a.trace[3] = gfd::globaltimer_ns();
+}
+
+}  // namespace
+
+extern "C" {
+
+int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint64_t inbox_heap_off,
+                            const float* const* src, float* const* dst, const uint64_t* pool_off,
+                            const uint64_t* count, int ntensors, const uint64_t* win_start,
+                            const uint64_t* win_len, int nwin, void* stream) {
+    if (int rc = comm_ready(c)) return rc;
+    if (dtype != GF_F16 || ntensors < 1 || ntensors > kMaxT || !src || !dst || !pool_off || !count || nwin < 1 ||
+        nwin > kMaxW || !win_start || !win_len)
+        return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense_push: fp16, 1..256 tensors, 1..256 windows");
+    if (c->world == 1)  // no collective: the one-pass pack + unpack
+        return gf_sync_step_dense(c, dtype, pool_heap_off, src, dst, pool_off, count, ntensors, win_start, win_len,
+                                  nwin, stream);
+    uint64_t lo = UINT64_MAX, hi = 0, cover = win_start[0];
+    for (int i = 0; i < ntensors; ++i) {
+        lo = std::min(lo, pool_off[i]);
+        hi = std::max(hi, pool_off[i] + count[i]);
+    }
+    for (int w = 0; w < nwin; ++w) {
+        if (win_start[w] != cover) return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense_push: windows must be contiguous");
+        cover += win_len[w];
+    }
+    if (lo != win_start[0] || hi != cover)
+        return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense_push: tensors and windows must cover the same pool range");
+    const uint64_t slot_elems = hi;  // an inbox slot mirrors pool indices [0, hi)
+    if (pool_heap_off + hi * 2 > c->heap_bytes ||
+        inbox_heap_off + uint64_t(c->world - 1) * slot_elems * 2 > c->heap_bytes || inbox_heap_off % 16 != 0)
+        return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense_push: pool or inbox outside the symmetric heap");
+    DeviceGuard guard(c->device);
+    cudaStream_t s = gfi::S(stream);
+    // 1. pack, routed to the owners
+    SegMap M;
+    std::memset(&M, 0, sizeof(M));
+    M.nwin = nwin;
+    M.world = c->world;
+    M.pos = c->pos;
+    M.slot_elems = slot_elems;
+    M.pool_local = c->alloc + kFlagBytes + pool_heap_off;
+    for (int j = 0; j < c->world; ++j) M.inbox_by_pos[j] = c->peer_alloc[c->ring[j]] + kFlagBytes + inbox_heap_off;
+    for (int w = 0; w < nwin; ++w) {
+        M.wstart[w] = win_start[w];
+        M.wlen[w] = win_len[w];
+    }
+    if (int rc = for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
+                                [&](const TensorTable& T, uint64_t tiles, int grid) {
+                                    pack_push_kernel<<<grid, kThreads, 0, s>>>(T, M, tiles);
+                                }))
+        return rc;
+    // 2. local reduce + all-gather push
+    RingArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.nwin = nwin;
+    uint64_t max_seg = 0;
+    for (int w = 0; w < nwin; ++w) {
+        a.wstart[w] = win_start[w];
+        a.wlen[w] = win_len[w];
+        max_seg += (win_len[w] + c->world - 1) / c->world;
+    }
+    fill_common(c, a, pool_heap_off);
+    const char* inbox_local = c->alloc + kFlagBytes + inbox_heap_off;
+    const int grid = gfr::ring_blocks(max_seg * 2);
+    switch (c->world) {
+        case 2: rsp_kernel<2><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
+        case 4: rsp_kernel<4><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
+        case 8: rsp_kernel<8><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
+        default: rsp_kernel<0><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
+    }
+    gfi::count_launch();
+    if (int rc = gfi::check_launch("gf_sync_step_dense_push")) return rc;
+    // 3. unpack
+    return gf_unpack(dtype, c->alloc + kFlagBytes + pool_heap_off, dst, pool_off, count, ntensors, c->world, stream);
+}
+
+}  // extern "C"

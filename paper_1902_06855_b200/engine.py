@@ -119,8 +119,8 @@ class GradSync:
         self.final_sparsity, self.warmup_iters = final_sparsity, warmup_iters
         self.momentum, self.lr = momentum, lr
         L = self.layout
-        if dense_mode not in ("auto", "pull", "push", "fused"):
-            raise capi.ConfigError(f"dense_mode {dense_mode!r}: auto, pull, push or fused")
+        if dense_mode not in ("auto", "pull", "push", "fused", "rspush"):
+            raise capi.ConfigError(f"dense_mode {dense_mode!r}: auto, pull, push, rspush or fused")
         if dense_mode == "auto":
             # measured: pull is ahead at 2 ranks (AlexNet -6 %, ResNet-50 even),
             # push-pull at 4 (-1 to -2 %)
@@ -138,6 +138,11 @@ class GradSync:
             self._pull_pools = [0, self.stage_off]
             self.stage_off += _align(L.total * self.esz)
         self._pull_flip = 0
+        # rspush: the pack pushes the reduce-scatter operands into the owners' inboxes
+        self._push_inbox = None
+        if dense_mode == "rspush" and world > 1 and not csc and self.dtype == F16:
+            self._push_inbox = self.stage_off
+            self.stage_off += _align((world - 1) * L.total * self.esz)
         # pull mode pieces (units of 1/GF_PART_ONE of every segment): piece k+1 is packed on a
         # side stream while piece k is exchanged; one piece = pack then exchange, serially
         parts = tuple(pull_parts) if pull_parts else (0, capi.GF_PART_ONE)
@@ -219,6 +224,14 @@ class GradSync:
             return
         if self.world > 1 and self.dense_mode == "fused" and not ring_only:
             return self.fused_step(grad_ptrs, out_ptrs, stream=stream, mark=mark)
+        if self._push_inbox is not None and not ring_only:
+            self.last_pool_ptr = self.pool_ptr
+            mark("push_step")
+            capi.call("gf_sync_step_dense_push", self.comm, self.dtype, self.pool_off, self._push_inbox,
+                      self._ptrs(grad_ptrs), self._ptrs(out_ptrs), self._offs, self._cnts, m, self._win[0],
+                      self._win[1], self._win[2], stream)
+            mark(None)
+            return
         if self.world > 1 and self.dense_mode == "pull" and not ring_only:
             # pack -> pull reduce-scatter + pull all-gather fused with the unpack
             pool_off, flags = self.pool_off, 0

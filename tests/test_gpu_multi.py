@@ -381,7 +381,7 @@ def _worker_fused(rank, world, port):
         return out
 
     modes = [("fused", None), ("pull", None), ("pull", (0, 256, 1024)), ("pull", (0, 100, 101, 700, 1024)),
-             ("push", None)]
+             ("push", None), ("rspush", None)]
     for (mode, parts), theta in [(m, t) for m in modes for t in (64 << 20, 1 << 20, 0)]:
         sync = GradSync(sizes, rank=rank, world=world, device=rank, theta=theta, allgather=ag,
                         dense_mode=mode, pull_parts=parts)
