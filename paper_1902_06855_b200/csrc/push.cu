@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <numeric>
 
 #include "ring_device.cuh"
 #include "tensor_table.cuh"
@@ -70,8 +71,13 @@ __device__ __forceinline__ void put_elem(const SegMap& m, uint64_t e, uint16_t h
 }
 
 __global__ void __launch_bounds__(kThreads)
-pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ SegMap M, uint64_t total_tiles) {
-    for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ SegMap M, uint64_t total_tiles,
+                 uint64_t spread) {
+    // CTA i packs tile (i * spread) mod tiles (spread coprime with tiles, ~tiles/N): consecutive
+    // CTAs hit different segments, so every rank keeps all its peers' links busy at once
+    // instead of streaming one owner's segment after another
+    for (uint64_t i = blockIdx.x; i < total_tiles; i += gridDim.x) {
+        const uint64_t tile = (i * spread) % total_tiles;
         const int t = find_tensor(T, tile);
         const uint64_t base = (tile - T.tiles[t]) * kTile;
         const uint64_t len = min(kTile, T.cnt[t] - base);
@@ -240,7 +246,9 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
     }
     if (int rc = for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
                                 [&](const TensorTable& T, uint64_t tiles, int grid) {
-                                    pack_push_kernel<<<grid, kThreads, 0, s>>>(T, M, tiles);
+                                    uint64_t spread = std::max<uint64_t>(1, tiles / uint64_t(c->world));
+                                    while (std::gcd(spread, tiles) != 1) ++spread;
+                                    pack_push_kernel<<<grid, kThreads, 0, s>>>(T, M, tiles, spread);
                                 }))
         return rc;
     // 2. local reduce + all-gather push
