@@ -70,7 +70,7 @@ __device__ __forceinline__ void put_elem(const SegMap& m, uint64_t e, uint16_t h
     *route(m, seg_owner(m, e, end), e) = h;
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ SegMap M, uint64_t total_tiles,
                  uint64_t spread) {
     // CTA i packs tile (i * spread) mod tiles (spread coprime with tiles, ~tiles/N): consecutive
