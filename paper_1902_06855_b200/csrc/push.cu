@@ -118,10 +118,9 @@ pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ 
         }
         for (uint64_t i = done + threadIdx.x; i < len; i += kThreads) put_elem(M, po + i, gfd::enc(s[i]));
     }
-    // the CTA's NVLink stores are performed before the kernel ends (bar.sync makes the
-    // fence cumulative over the CTA, as in cross_barrier); the next kernel's flag follows
-    __syncthreads();
-    if (threadIdx.x == 0) __threadfence_system();
+    // No fence: CTAs retire with their NVLink stores in flight. The kernel boundary orders
+    // all of them before rsp_kernel, whose release of the entry flag publishes them (the
+    // same ordering the ring relies on for the pack's local stores).
 }
 
 // All-local reduce of my segments (pool + inbox slots, ring order) pushed to every pool.
