@@ -197,8 +197,9 @@ def main():
                          "this many ms (bf16 GEMMs; tensors complete in descending id, theta "
                          "windows launch as they close: the reference's lazy allreduce)")
     ap.add_argument("--dense-mode", default="auto", choices=["auto", "pull", "push", "fused", "rspush"],
-                    help="dense N>1: pull (pack + pull RS/AG fused with unpack), push (pack + "
-                         "push-pull ring + unpack), fused (one kernel); auto = pull at N=2, else push")
+                    help="dense N>1: rspush (pack pushes the reduce-scatter operands to their owners, "
+                         "local reduce + all-gather push, unpack), pull (pack + pull RS/AG fused with "
+                         "unpack), push (pack + push-pull ring + unpack), fused (one kernel); auto = rspush")
     ap.add_argument("--pull-parts", default=None,
                     help="dense pull mode: piece cut points in 1/1024 of every segment, e.g. 0,256,1024 "
                          "(piece k+1 is packed while piece k is exchanged)")

@@ -122,9 +122,9 @@ class GradSync:
         if dense_mode not in ("auto", "pull", "push", "fused", "rspush"):
             raise capi.ConfigError(f"dense_mode {dense_mode!r}: auto, pull, push, rspush or fused")
         if dense_mode == "auto":
-            # measured: pull is ahead at 2 ranks (AlexNet -6 %, ResNet-50 even),
-            # push-pull at 4 (-1 to -2 %)
-            dense_mode = "pull" if world == 2 else "push"
+            # measured: the reduce-scatter pushed by the pack is ahead of pull and
+            # push-pull at 2 and 4 ranks (ResNet-50 -9 / -8 %, AlexNet -6 / -5 %); fp16 pools only
+            dense_mode = "rspush" if dtype == F16 and not csc else ("pull" if world == 2 else "push")
         self.dense_mode = dense_mode
         if csc_mode not in ("pull", "push"):
             raise capi.ConfigError(f"csc_mode {csc_mode!r}: pull or push")
