@@ -19,6 +19,7 @@
 // the contribution of the rank at position j + 1 + s (mod N), laid out like the pool.
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -70,7 +71,8 @@ __device__ __forceinline__ void put_elem(const SegMap& m, uint64_t e, uint16_t h
     *route(m, seg_owner(m, e, end), e) = h;
 }
 
-__global__ void __launch_bounds__(kThreads, 4)
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
 pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ SegMap M, uint64_t total_tiles,
                  uint64_t spread) {
     // CTA i packs tile (i * spread) mod tiles (spread coprime with tiles, ~tiles/N): consecutive
@@ -121,6 +123,17 @@ pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ 
     // No fence: CTAs retire with their NVLink stores in flight. The kernel boundary orders
     // all of them before rsp_kernel, whose release of the entry flag publishes them (the
     // same ordering the ring relies on for the pack's local stores).
+}
+
+// CTAs per SM the routed pack is compiled for (register cap 65536 / (256 * MINB)); 4 measured
+// best so far. GF_PUSH_MINB (4, 6 or 8) is a tuning override.
+int push_minb() {
+    static const int v = [] {
+        const char* e = std::getenv("GF_PUSH_MINB");
+        const int x = e ? std::atoi(e) : 4;
+        return (x == 6 || x == 8) ? x : 4;
+    }();
+    return v;
 }
 
 // All-local reduce of my segments (pool + inbox slots, ring order) pushed to every pool.
@@ -247,7 +260,11 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
                                 [&](const TensorTable& T, uint64_t tiles, int grid) {
                                     uint64_t spread = std::max<uint64_t>(1, tiles / uint64_t(c->world));
                                     while (std::gcd(spread, tiles) != 1) ++spread;
-                                    pack_push_kernel<<<grid, kThreads, 0, s>>>(T, M, tiles, spread);
+                                    switch (push_minb()) {
+                                        case 6: pack_push_kernel<6><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
+                                        case 8: pack_push_kernel<8><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
+                                        default: pack_push_kernel<4><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
+                                    }
                                 }))
         return rc;
     // 2. local reduce + all-gather push
