@@ -191,23 +191,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--trace", action="store_true", help="report ring CTA-0 timestamps (diagnostic)")
-    ap.add_argument("--ring-only", action="store_true", help="diagnostic: time the collective alone")
     ap.add_argument("--overlap", type=float, default=0.0, metavar="BACKWARD_MS",
                     help="also measure the dense sync overlapped with a synthetic backward of "
                          "this many ms (bf16 GEMMs; tensors complete in descending id, theta "
                          "windows launch as they close: the reference's lazy allreduce)")
-    ap.add_argument("--dense-mode", default="auto", choices=["auto", "pull", "push", "fused", "rspush"],
+    ap.add_argument("--dense-mode", default="auto", choices=["auto", "pull", "push", "rspush"],
                     help="dense N>1: rspush (pack pushes the reduce-scatter operands to their owners, "
                          "local reduce + all-gather push, unpack), pull (pack + pull RS/AG fused with "
-                         "unpack), push (pack + push-pull ring + unpack), fused (one kernel); auto = rspush")
-    ap.add_argument("--pull-parts", default=None,
-                    help="dense pull mode: piece cut points in 1/1024 of every segment, e.g. 0,256,1024 "
-                         "(piece k+1 is packed while piece k is exchanged)")
+                         "unpack), push (pack + push-pull ring + unpack); auto = rspush")
     ap.add_argument("--csc-mode", default="push", choices=["pull", "push"],
                     help="CSC N>1 exchange: pull (pull RS/AG straight into the pool) or push "
                          "(push-pull ring + fused write-back)")
-    ap.add_argument("--fused", action="store_true",
-                    help="dense: one fused pack+ring+unpack kernel per step (gf_sync_step_dense)")
     args = ap.parse_args()
 
     wl = dict(WORKLOADS[args.workload])
@@ -239,12 +233,9 @@ def main():
 
     sizes = wl["sizes"]
     csc = wl["csc"]
-    if args.fused:
-        args.dense_mode = "fused"
     sync = GradSync(sizes, rank=rank, world=world, device=local, theta=wl["theta"], csc=csc,
                     final_sparsity=wl.get("sparsity", 0.9), allgather=allgather,
-                    dense_mode=args.dense_mode, csc_mode=args.csc_mode,
-                    pull_parts=[int(x) for x in args.pull_parts.split(",")] if args.pull_parts else None)
+                    dense_mode=args.dense_mode, csc_mode=args.csc_mode)
     L = sync.layout
     total = L.total
     esz = 2
@@ -268,40 +259,11 @@ def main():
     in_ptrs = [(C.c_void_p * len(sizes))(*views(x)) for x in inputs]  # prebuilt launch tables
     outs = [torch.empty(total, device=dev) for _ in range(2)]
     out_ptrs = [(C.c_void_p * len(sizes))(*views(x)) for x in outs]
-    if csc:
-        nc = L.num_chunks
-        hg = torch.zeros(total, device=dev)
-        imp = [torch.ones(nc, dtype=torch.uint8, device=dev), torch.zeros(nc, dtype=torch.uint8, device=dev)]
-        coff = [torch.zeros(nc, dtype=torch.int64, device=dev) for _ in range(2)]
-        plan = [torch.zeros(4 + nc, dtype=torch.int64, device=dev) for _ in range(2)]
-        hu = torch.zeros(total, device=dev)
-        w = torch.zeros(total, device=dev)
-        nacc = torch.zeros(nc, dtype=torch.int64, device=dev)
-        sync.attach_csc_state(hg.data_ptr(), [t.data_ptr() for t in imp], [t.data_ptr() for t in coff],
-                              [t.data_ptr() for t in plan], hu.data_ptr(), w.data_ptr(),
-                              nacc=nacc.data_ptr())
-        sync.init_csc_plan(sp)
-
-    marks = []
-
-    def mark_factory(record):
-        def mark(name):
-            if record:
-                e = torch.cuda.Event(enable_timing=True)
-                e.record(stream)
-                marks.append((name, e))
-        return mark
-
-    def step(i, record=False):
-        m = mark_factory(record) if record else None  # None: the production schedule
+    def step(i):
         if csc:
-            sync.csc_step(in_ptrs[i % n_sets], stream=sp, mark=m)
+            sync.csc_step(in_ptrs[i % n_sets], stream=sp)
         else:
-            if args.fused:
-                sync.fused_step(in_ptrs[i % n_sets], out_ptrs[i % 2], stream=sp, mark=m)
-            else:
-                sync.dense_step(in_ptrs[i % n_sets], out_ptrs[i % 2], stream=sp, mark=m,
-                                ring_only=args.ring_only)
+            sync.dense_step(in_ptrs[i % n_sets], out_ptrs[i % 2], stream=sp)
 
     def barrier():
         if world > 1:
@@ -333,16 +295,14 @@ def main():
     # per-kernel durations: the same K steps again, with CUDA events on the launching stream
     # between the kernels. Kept out of the headline pass: an event between two kernels costs
     # the step ~3-4 us of GPU time (scripts/hbm_probe.py), so `kernels` is slightly pessimistic.
+    sync.set_marks(True)
     for i in range(args.steps):
-        step(warm + args.steps + i, record=True)
+        step(warm + args.steps + i)
     torch.cuda.synchronize()
+    seg_ms = sync.marks()
+    sync.set_marks(False)
     barrier()
     sync.status()
-    seg = {}
-    for (name, e0), (_, e1) in zip(marks, marks[1:]):
-        if name is not None:
-            seg.setdefault(name, []).append(e0.elapsed_time(e1))
-    seg_ms = {k: sum(v) / len(v) for k, v in seg.items()}
 
     def allmax(x):
         if world == 1:
@@ -366,13 +326,15 @@ def main():
     algo = {  # algorithmic bytes per launch
         "pack": total * 6, "unpack": total * 6, "pack_correct": total * 14,
         "pack_unpack": total * 10,  # N=1: g in (4), pool out (2), g_avg out (4)
-        "fused_step": None,
         "norms": total * 2, "scatter": None, "select": None, "sgd_update": None,
         "ring": None,
     }
     if csc:
         # staged elements of the last timed (sparse) iteration, read back after timing
-        staged = int(plan[(sync.iteration - 1) & 1][0].item())
+        pc = np.zeros(1, np.uint64)
+        cudart.memcpy(pc.ctypes.data, sync.state("plan_cur")[0], 8)
+        cudart.sync_device()
+        staged = int(pc[0])
         # g, hg in; pool, hg out; + the staging copy at N>1 (N=1 has no exchange, no staging)
         algo["pack_correct"] = total * 14 + (staged * 2 if world > 1 else 0)
         algo["scatter"] = staged * 4                      # staging in, pool out (+ exact L1)
@@ -383,24 +345,21 @@ def main():
     algo["ring"] = ring_bytes if world > 1 else None
     algo["ring_scatter"] = algo["ring"]  # CSC exchange with the write-back fused in
     algo["ring_unpack"] = algo["ring"]   # dense pull mode: RS + AG with the unpack fused in
-    algo["pull_step"] = algo["ring"]     # pull mode in pieces: packs overlap the exchanges
-    algo["push_step"] = algo["ring"]     # rspush: pack (with the RS pushes) + reduce/AG + unpack
-    if args.fused:  # its binding roofline: NVLink bus bytes at N>1, HBM bytes at N=1
-        algo["fused_step"] = ring_bytes if world > 1 else total * 12
+    algo["rsp"] = algo["ring"]           # rspush: local reduce + all-gather push (the NVLink kernel)
+    algo["pack_push"] = total * 6        # rspush: the routed pack (HBM 6 B/el; its NVLink stores ride on it)
     dom = max(seg_ms, key=lambda k: seg_ms[k]) if seg_ms else None
     roof = None
     if dom is not None and algo.get(dom):
         t_s = seg_ms[dom] / 1e3
-        if dom in ("ring", "ring_scatter", "ring_unpack", "pull_step", "push_step") or (dom == "fused_step" and world > 1):
+        if dom in ("ring", "ring_scatter", "ring_unpack", "rsp"):
             ach = algo[dom] / t_s / 1e9
             roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": 900.0, "unit": "GB/s",
                     "frac": round(ach / 900.0, 3), "traffic": None,
                     "kernel": "ring_kernel" if dom == "ring" else dom,
                     "peak_src": "NVLink 5 nominal 900 GB/s/direction (measured peer copy 770)",
                     "frac_of_measured_770": round(ach / 770.0, 3)}
-            if dom in ("push_step", "pull_step", "ring_unpack", "fused_step"):
-                roof["note"] = ("one launch sequence timed whole: the pack/unpack HBM passes sit inside "
-                                "the time the NVLink bus bytes are divided by")
+            if dom == "ring_unpack":
+                roof["note"] = "the unpack HBM pass sits inside the time the NVLink bus bytes are divided by"
         else:
             ach = algo[dom] / t_s / 1e9
             roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
@@ -413,7 +372,7 @@ def main():
                 tr = json.load(f)
             kname = {"pack": "pack_kernel", "pack_unpack": "pack_kernel", "unpack": "unpack_kernel", "pack_correct": "pack_correct_kernel",
                      "sgd_update": "csc_sgd_kernel", "scatter": "compact_kernel",
-                     "select": "select_kernel"}.get(dom)
+                     "select": "select_kernel", "pack_push": "pack_push_kernel", "rsp": "rsp_kernel"}.get(dom)
             ent = tr.get(args.workload, {}).get(kname or "", {})
             if ent:
                 roof["traffic"] = ent["dram_bytes_per_launch"]
@@ -425,7 +384,7 @@ def main():
         d = {"ms": round(v, 4)}
         if algo.get(k):
             d["GBps"] = round(algo[k] / (v / 1e3) / 1e9, 1)
-            if k not in ("ring", "ring_scatter", "ring_unpack", "pull_step", "push_step") and not (k == "fused_step" and world > 1):
+            if k not in ("ring", "ring_scatter", "ring_unpack", "rsp"):
                 d["frac_hbm"] = round(d["GBps"] / hbm_peak, 3)
             else:
                 d["busbw_frac_900"] = round(d["GBps"] / 900, 3)
@@ -549,8 +508,7 @@ def main():
         d2h = total * 4
         s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
 
-        def result(slot):
-            return outs[slot] if not csc else w
+        wptr = sync.state("w")[0] if csc else None
 
         def run_e2e(k):
             ev_in = [torch.cuda.Event() for _ in range(k)]
@@ -569,8 +527,11 @@ def main():
                 step(slot)
                 ev_comp[i].record(stream)
                 s_out.wait_event(ev_comp[i])
-                with torch.cuda.stream(s_out):
-                    h_out[slot].copy_(result(slot), non_blocking=True)
+                if csc:  # the updated weights w (engine-owned) leave the device
+                    cudart.memcpy(h_out[slot].data_ptr(), wptr, d2h, s_out.cuda_stream)
+                else:
+                    with torch.cuda.stream(s_out):
+                        h_out[slot].copy_(outs[slot], non_blocking=True)
                 ev_out[i].record(s_out)
             return ev_out[-1]
 
@@ -609,11 +570,9 @@ def main():
 
     if rank == 0:
         bus = None
-        rk = next((k for k in ("ring", "ring_unpack", "ring_scatter", "pull_step", "push_step") if k in seg_ms), "ring")
+        rk = next((k for k in ("ring", "ring_unpack", "ring_scatter", "rsp") if k in seg_ms), "ring")
         if world > 1 and rk in seg_ms:
             bus = round(ring_bytes / (seg_ms[rk] / 1e3) / 1e9, 1)
-        elif world > 1 and "fused_step" in seg_ms:
-            bus = round(ring_bytes / (seg_ms["fused_step"] / 1e3) / 1e9, 1)
         line = {
             "metric": "grad-sync ms/step", "value": round(ms, 4), "unit": "ms", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),

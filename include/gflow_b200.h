@@ -40,7 +40,10 @@
  *  gf_sync_step_dense_push          the same with the reduce-scatter pushed by the pack (write_tensor
  *                                   src/gradient_pool.cpp:78-105 + ring_allreduce_on src/collectives.cpp:55-97)
  *  gf_sync_step_dense               one dense iteration: write_tensor x m + FusionEngine windows +
- *                                   update read (src/trainer.cpp:297-347), fused into one kernel
+ *                                   update read (src/trainer.cpp:297-347); one pass at world 1
+ *  gf_engine_*                      one rank's whole iteration: train_worker's sync half
+ *                                   (src/trainer.cpp:297-347), FusionEngine (src/fusion.cpp:25-123),
+ *                                   SparseState (src/sparse.cpp:57-224)
  *  gf_csc_exchange_pull             sparse_exchange ring + write-back (pull form) src/sparse.cpp:106-170
  *  gf_csc_select                    select_next_important (norm allreduce + top-k) src/sparse.cpp:172-204
  *  gf_ring_traffic                  TrafficStats record_send/recv of the ring include/gflow/transport.hpp:48-91, src/collectives.cpp:69-96
@@ -162,6 +165,14 @@ int gf_comm_export_handle(gf_comm* comm, void* handle_out);
 int gf_comm_connect_ipc(gf_comm* comm, const void* all_handles);
 /* In-process bootstrap: comms[r] for every rank r, each on a distinct device. */
 int gf_comm_connect_local(gf_comm* const* comms, int world);
+/* Emulated world on ONE device: comms[r] for every rank r, all created on the same device.
+ * Every kernel runs exactly as across GPUs (same instantiations, same cross-rank flags and
+ * barriers, "peer" memory = the other ranks' allocations on this device); each rank must
+ * launch on its own non-blocking stream. Grids are capped so that all ranks' barrier-waiting
+ * CTAs are resident at once. Used to prove the multi-GPU kernels on a single B200. Requires
+ * CUDA_MODULE_LOADING=EAGER (and, for worlds with more than 8 active streams,
+ * CUDA_DEVICE_MAX_CONNECTIONS >= their count) in the environment before CUDA initialises. */
+int gf_comm_connect_colocated(gf_comm* const* comms, int world);
 /* Ring order (collectives.hpp:37-38): a permutation of ranks, identical on all ranks. */
 int gf_comm_set_ring_order(gf_comm* comm, const int* order);
 int gf_comm_set_timeout_ms(gf_comm* comm, uint64_t ms);
@@ -214,12 +225,12 @@ int gf_ring_allreduce_planned_scatter(gf_comm* comm, int dtype, uint64_t stage_h
  * (gf_csc_select's barrier, in a CSC step). fp16, chunk % 8 == 0, nc <= 6144, world > 1. */
 int gf_csc_exchange_pull(gf_comm* comm, uint64_t stage_heap_off, const uint64_t* plan_dev, void* pool,
                          uint64_t chunk, uint64_t nc, uint64_t* nacc, void* stream);
-/* One dense sync step as ONE kernel per rank: pack -> ring allreduce of the theta windows ->
- * unpack. Each CTA packs, reduces and unpacks one fixed strided set of pool vectors and only
- * synchronises with its peer CTAs (entry/exit barriers); at world 1 it is a single streaming
- * pass. Result-identical to gf_pack + gf_ring_allreduce + gf_unpack (bit for bit). The
- * fp16/fp32 pool lives at pool_heap_off in the symmetric heap; src/dst/pool_off/count are
- * HOST arrays (<= 256 tensors, tiling the windows) of device pointers / sizes. */
+/* One dense sync step (pack -> ring allreduce of the theta windows -> unpack), bit-identical to
+ * gf_pack + gf_ring_allreduce + gf_unpack. At world 1 the collective is the identity
+ * (collectives.cpp:59) and the step is ONE streaming pass (pack_kernel<DstTable>: each value
+ * is encoded, stored to the pool and decoded to g_avg from registers). The fp16/fp32 pool
+ * lives at pool_heap_off in the symmetric heap; src/dst/pool_off/count are HOST arrays of
+ * device pointers / sizes (any number of tensors, tiling the windows). */
 int gf_sync_step_dense(gf_comm* comm, int dtype, uint64_t pool_heap_off, const float* const* src,
                        float* const* dst, const uint64_t* pool_off, const uint64_t* count,
                        int ntensors, const uint64_t* win_start, const uint64_t* win_len, int nwin,
@@ -233,31 +244,19 @@ int gf_sync_step_dense(gf_comm* comm, int dtype, uint64_t pool_heap_off, const f
  * caller must then not rewrite this pool before its next collective on the communicator
  * (alternate two pools: the next collective's entry barrier orders the reuse). */
 #define GF_RSAG_NO_EXIT_BARRIER 1
-#define GF_PART_ONE 1024
 int gf_ring_allreduce_unpack(gf_comm* comm, int dtype, uint64_t pool_heap_off, float* const* dst,
                              const uint64_t* pool_off, const uint64_t* count, int ntensors,
                              const uint64_t* win_start, const uint64_t* win_len, int nwin, int flags,
                              void* stream);
-/* The same restricted to piece [part_lo, part_hi) (units of 1/GF_PART_ONE) of EVERY segment of
- * every window. Pieces do not change any element's summation order, so a step can pack piece
- * k+1 (gf_pack over gf_part_ranges) while piece k is exchanged; pieces of one step must be
- * launched in the same order on every rank. */
-int gf_ring_allreduce_unpack_part(gf_comm* comm, int dtype, uint64_t pool_heap_off, float* const* dst,
-                                  const uint64_t* pool_off, const uint64_t* count, int ntensors,
-                                  const uint64_t* win_start, const uint64_t* win_len, int nwin,
-                                  uint32_t part_lo, uint32_t part_hi, int flags, void* stream);
-/* Pool element ranges [lo[i], hi[i]) of piece [part_lo, part_hi) of every segment of the windows
- * at `world` ranks, in pool order (empty ranges dropped). Returns the count (or -1 if it
- * exceeds cap). Host-only, no GPU. */
-int gf_part_ranges(const uint64_t* win_start, const uint64_t* win_len, int nwin, int world,
-                   uint32_t part_lo, uint32_t part_hi, uint64_t* lo, uint64_t* hi, int cap);
 /* One dense sync step with the reduce-scatter's traffic riding on the pack (push form): the
  * pack stores each packed vector straight into the owner of its segment (my pool, or my slot
  * of the owner's inbox over NVLink); one kernel then sums every owned segment from local
  * memory in ring order and pushes the sums into all pools; then unpack. Same results as
  * gf_pack + gf_ring_allreduce + gf_unpack, bit for bit. fp16; the inbox (world-1 slots of
- * the pool span, at inbox_heap_off, same offset on every rank) lives in the symmetric heap.
- * src/dst/pool_off/count are HOST arrays (<= 256 tensors, covering the windows). */
+ * round_up(pool span, 8) elements each, at inbox_heap_off, same offset on every rank) lives in
+ * the symmetric heap; pool and inbox offsets are 16-byte aligned and must not overlap.
+ * src/dst/pool_off/count are HOST arrays (any number of tensors, covering the windows; more
+ * than GF_MAX_WINDOWS_PER_LAUNCH windows run as several launch pairs). */
 int gf_sync_step_dense_push(gf_comm* comm, int dtype, uint64_t pool_heap_off, uint64_t inbox_heap_off,
                             const float* const* src, float* const* dst, const uint64_t* pool_off,
                             const uint64_t* count, int ntensors, const uint64_t* win_start,
@@ -309,6 +308,74 @@ int gf_ring_reduce_ptrs(int dtype, void* const* bufs, int n, int root_pos, uint6
  * position `position` (collectives.cpp:69-96): 2(N-1) sends of segment_of sizes. */
 int gf_ring_traffic(uint64_t len, int world, int position, int dtype, uint64_t* bytes_sent,
                     uint64_t* bytes_received, uint64_t* frames_sent);
+
+
+/* ---- synthetic inputs (harness) --------------------------------------------------------------
+ * The benchmark's seeded gradient sets (extends bench_allreduce's stream,
+ * src/harness.cpp:280-283): std::mt19937_64(1234 + rank + 7919*step), tensors in ascending id,
+ * uniform_real_distribution<float>(-1,1) * 2^-(id mod 7). out: HOST buffer of sum(sizes) floats,
+ * ascending id. Host-only, no GPU. */
+int gf_synth_grads(int rank, int step, const uint64_t* sizes, int ntensors, float* out);
+
+/* ---- engine: one rank's whole gradient-sync step ---------------------------------------------
+ * The launch sequence a data-parallel trainer runs per iteration (trainer.cpp:297-347 with
+ * FusionEngine fusion.cpp:72-109 and SparseState sparse.cpp:57-224), device-resident and
+ * asynchronous on the caller's stream: no host synchronisation inside a step, so a step can be
+ * captured into a CUDA graph. Gradient/output tables are HOST arrays of per-tensor DEVICE
+ * pointers in ascending tensor id (id 1 first), as the reference's write_tensor(id, span). */
+typedef struct gf_engine gf_engine;
+enum { GF_DENSE_AUTO = 0, GF_DENSE_RSPUSH = 1, GF_DENSE_PULL = 2, GF_DENSE_PUSH = 3 };
+enum { GF_CSC_PUSH = 0, GF_CSC_PULL = 1 };
+typedef struct {
+    int world, rank, device, dtype;
+    uint64_t theta_bytes;     /* FusionConfig::threshold_bytes (fusion.hpp:27-30) */
+    uint64_t chunk;           /* GradientPool chunk size (gradient_pool.hpp:16) */
+    int csc;                  /* 0: dense lazy allreduce; 1: CSC (TrainOptions::csc) */
+    int dense_mode;           /* GF_DENSE_*: N>1 dense exchange (AUTO = RSPUSH for fp16) */
+    int csc_mode;             /* GF_CSC_*: N>1 CSC exchange form */
+    double final_sparsity;    /* SparseConfig (sparse.hpp:21-26) */
+    uint64_t warmup_iters;
+    double momentum, learning_rate;
+    uint64_t timeout_ms;      /* device-side barrier timeout (transport.hpp:25) */
+} gf_engine_config;
+typedef struct {
+    uint64_t total, num_chunks, heap_bytes;
+    int nwin;                 /* dense theta windows per iteration */
+    int dense_mode;           /* resolved GF_DENSE_* */
+    uint64_t iteration;       /* CSC iterations run */
+} gf_engine_info;
+enum { GF_STATE_POOL = 0, GF_STATE_HG, GF_STATE_HU, GF_STATE_W, GF_STATE_IMP_NEXT, GF_STATE_NORMS,
+       GF_STATE_NACC, GF_STATE_PLAN_NEXT, GF_STATE_IMP_CUR, GF_STATE_PLAN_CUR };
+/* Defaults: world 1, fp16, theta 64 MiB, chunk 32000, dense, AUTO, momentum 0.9, lr 0.01,
+ * final_sparsity 0.9, timeout 30 s (trainer.hpp / fusion.hpp / sparse.hpp defaults). */
+void gf_engine_config_init(gf_engine_config* cfg);
+int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int ntensors, gf_engine** out);
+int gf_engine_destroy(gf_engine* e);
+/* The engine's communicator: bootstrap with gf_comm_export_handle + gf_engine_connect_ipc. */
+gf_comm* gf_engine_comm(gf_engine* e);
+int gf_engine_connect_ipc(gf_engine* e, const void* all_handles);
+int gf_engine_connect_local(gf_engine* const* engines, int world);
+int gf_engine_connect_colocated(gf_engine* const* engines, int world);
+int gf_engine_info_get(gf_engine* e, gf_engine_info* out);
+/* Device buffers the engine owns (GF_STATE_*): pool (the one holding the last dense step's
+ * sums), CSC residual hg, momentum hu, weights w (zero-initialised), the next important set,
+ * the chunk norms, the exact-L1 accumulators, the next plan, the current set. */
+int gf_engine_state(gf_engine* e, int which, void** ptr, uint64_t* bytes);
+/* Dense iteration: out[t] = g_avg of tensor t (sum over ranks x 1/N, via the fp16/fp32 pool). */
+int gf_engine_dense_step(gf_engine* e, const float* const* grads, float* const* out, void* stream);
+/* CSC iteration (Algorithm 1): pack+correct+compact, exchange + write-back + exact L1, norm
+ * exchange + top-k of the next set, momentum update of the important chunks of w. */
+int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream);
+/* Overlap with backward (fusion.cpp:72-123): tensors become final in descending id; each theta
+ * window is launched on a communication stream when it closes; finalize makes `stream` wait. */
+int gf_engine_begin_iteration(gf_engine* e, const float* const* grads, float* const* out, void* stream);
+int gf_engine_tensor_complete(gf_engine* e, int tensor_id);
+int gf_engine_finalize_iteration(gf_engine* e);
+/* Per-kernel timing: with marks on, every step records an event before each kernel phase;
+ * gf_engine_marks synchronises and returns the mean ms per phase ("name" strings separated by
+ * ';' in names) over the steps since the last call, then clears. Returns the phase count. */
+int gf_engine_set_marks(gf_engine* e, int on);
+int gf_engine_marks(gf_engine* e, char* names, int names_cap, float* ms, int cap);
 
 #ifdef __cplusplus
 }

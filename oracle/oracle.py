@@ -46,7 +46,7 @@ def np_ptr(a: np.ndarray):
 
 
 def ptr_array(arrs):
-    return (_vp * len(arrs))(*[a.ctypes.data for a in arrs])
+    return (_vp * len(arrs))(*[None if a is None else a.ctypes.data for a in arrs])
 
 
 def u64(a):
@@ -365,15 +365,24 @@ class Reference:
         return pools, gavg, wb[: int(nw[0])].copy(), sent
 
     def csc_run(self, grads_steps, sizes, chunk, dtype=1, theta=THETA_INF, final_sparsity=0.9,
-                warmup=0, momentum=0.9, lr=0.01, weights0=None):
-        """grads_steps[t][r] flat ascending. Returns dict of per-step per-rank arrays."""
+                warmup=0, momentum=0.9, lr=0.01, weights0=None, keep=None):
+        """grads_steps[t][r] flat ascending. Returns dict of per-step per-rank arrays.
+        keep(key, t, r) -> bool selects which outputs to materialise (full-size runs: the
+        others are passed as NULL and come back as None); default: all."""
         T, n = len(grads_steps), len(grads_steps[0])
         s = u64(sizes)
         total = int(s.sum())
         _, nc, _ = self.pool_layout(sizes, chunk)
         dt = np.uint16 if dtype == 1 else np.float32
         K = T * n
-        mk = lambda shape, d: [np.zeros(shape, d) for _ in range(K)]
+        if keep is None:
+            mk = lambda shape, d: [np.zeros(shape, d) for _ in range(K)]
+        else:
+            names = iter(["pool_corr", "hg", "pool_x", "norms_loc", "norms_sum", "imp", "next_imp", "hu", "w"])
+
+            def mk(shape, d):
+                key = next(names)
+                return [np.zeros(shape, d) if keep(key, k // n, k % n) else None for k in range(K)]
         out = dict(pool_corr=mk(total, dt), hg=mk(total, np.float32), pool_x=mk(total, dt),
                    norms_loc=mk(nc, np.float32), norms_sum=mk(nc, np.float32),
                    imp=mk(nc, np.uint8), next_imp=mk(nc, np.uint8), hu=mk(total, np.float32),

@@ -22,7 +22,10 @@ GF_F32, GF_F16 = 0, 1
 GF_MAX_RANKS = 16
 GF_IPC_HANDLE_BYTES = 64
 GF_RSAG_NO_EXIT_BARRIER = 1
-GF_PART_ONE = 1024
+GF_DENSE_AUTO, GF_DENSE_RSPUSH, GF_DENSE_PULL, GF_DENSE_PUSH = range(4)
+GF_CSC_PUSH, GF_CSC_PULL = range(2)
+(GF_STATE_POOL, GF_STATE_HG, GF_STATE_HU, GF_STATE_W, GF_STATE_IMP_NEXT, GF_STATE_NORMS, GF_STATE_NACC,
+ GF_STATE_PLAN_NEXT, GF_STATE_IMP_CUR, GF_STATE_PLAN_CUR) = range(10)
 THETA_INF = (1 << 64) - 1
 
 
@@ -99,7 +102,6 @@ SIGNATURES = {
     "gf_sync_step_dense": [_vp, _i, _u64, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _vp],
     "gf_sync_step_dense_push": [_vp, _i, _u64, _u64, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _vp],
     "gf_ring_allreduce_unpack": [_vp, _i, _u64, _vp, _vp, _vp, _i, _vp, _vp, _i, _i, _vp],
-    "gf_ring_allreduce_unpack_part": [_vp, _i, _u64, _vp, _vp, _vp, _i, _vp, _vp, _i, _u32, _u32, _i, _vp],
     "gf_ipc_export": [_vp, _vp, _u64p],
     "gf_ipc_open": [_vp, _vp, C.POINTER(_vp)],
     "gf_ipc_close": [_vp, _vp],
@@ -112,18 +114,52 @@ SIGNATURES = {
     "gf_oracle_allreduce_ptrs": [_i, _vp, _i, _u64, _vp],
     "gf_broadcast_ptrs": [_vp, _i, _i, _u64, _vp],
     "gf_ring_reduce_ptrs": [_i, _vp, _i, _i, _u64, _vp],
-    "gf_part_ranges": [_vp, _vp, _i, _i, _u32, _u32, _vp, _vp, _i],
+    "gf_comm_connect_colocated": [_vp, _i],
+    "gf_synth_grads": [_i, _i, _vp, _i, _vp],
+    "gf_engine_config_init": [_vp],
+    "gf_engine_create": [_vp, _vp, _i, C.POINTER(_vp)],
+    "gf_engine_destroy": [_vp],
+    "gf_engine_comm": [_vp],
+    "gf_engine_connect_ipc": [_vp, _vp],
+    "gf_engine_connect_local": [_vp, _i],
+    "gf_engine_connect_colocated": [_vp, _i],
+    "gf_engine_info_get": [_vp, _vp],
+    "gf_engine_state": [_vp, _i, C.POINTER(_vp), _u64p],
+    "gf_engine_dense_step": [_vp, _vp, _vp, _vp],
+    "gf_engine_csc_step": [_vp, _vp, _vp],
+    "gf_engine_begin_iteration": [_vp, _vp, _vp, _vp],
+    "gf_engine_tensor_complete": [_vp, _i],
+    "gf_engine_finalize_iteration": [_vp],
+    "gf_engine_set_marks": [_vp, _i],
+    "gf_engine_marks": [_vp, _vp, _i, _vp, _i],
     "gf_abi_version": [],
     "gf_last_error": [],
     "gf_kernel_launches": [],
 }
-_RET = {"gf_last_error": C.c_char_p, "gf_kernel_launches": C.c_uint64}
+_RET = {"gf_last_error": C.c_char_p, "gf_kernel_launches": C.c_uint64, "gf_engine_config_init": None,
+        "gf_engine_comm": C.c_void_p}
+
+
+class EngineConfig(C.Structure):
+    """gf_engine_config (include/gflow_b200.h)."""
+    _fields_ = [("world", C.c_int), ("rank", C.c_int), ("device", C.c_int), ("dtype", C.c_int),
+                ("theta_bytes", C.c_uint64), ("chunk", C.c_uint64), ("csc", C.c_int),
+                ("dense_mode", C.c_int), ("csc_mode", C.c_int), ("final_sparsity", C.c_double),
+                ("warmup_iters", C.c_uint64), ("momentum", C.c_double), ("learning_rate", C.c_double),
+                ("timeout_ms", C.c_uint64)]
+
+
+class EngineInfo(C.Structure):
+    """gf_engine_info (include/gflow_b200.h)."""
+    _fields_ = [("total", C.c_uint64), ("num_chunks", C.c_uint64), ("heap_bytes", C.c_uint64),
+                ("nwin", C.c_int), ("dense_mode", C.c_int), ("iteration", C.c_uint64)]
 
 
 def header_symbols() -> list[str]:
     """Every function the public header declares."""
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^(?:int|const char\*|uint64_t)\s+(gf_[a-z0-9_]+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^(?:int|const char\*|uint64_t|void|gf_comm\*)\s+(gf_[a-z0-9_]+)\s*\(", txt,
+                                 re.M)))
 
 
 _lib = None
@@ -167,22 +203,17 @@ def ptr(t) -> int:
     raise TypeError(type(t))
 
 
-def part_ranges(win_start, win_len, world, part_lo, part_hi):
-    """Pool element ranges of one piece of every segment (gf_part_ranges), as numpy arrays."""
-    import numpy as np
-    n = len(win_start)
-    cap = n * world + 1
-    lo, hi = (C.c_uint64 * cap)(), (C.c_uint64 * cap)()
-    k = lib().gf_part_ranges(u64_array(win_start), u64_array(win_len), n, world, part_lo, part_hi,
-                             lo, hi, cap)
-    if k < 0:
-        check(GF_ERR_CONFIG)
-    return np.array(lo[:k], dtype=np.uint64), np.array(hi[:k], dtype=np.uint64)
-
-
 def u64_array(vals):
     arr = (C.c_uint64 * len(vals))(*[int(v) for v in vals])
     return arr
+
+
+def synth_grads(rank, step, sizes):
+    """SURVEY §8(d) seeded gradients (gf_synth_grads) as a flat ascending-id float32 array."""
+    import numpy as np
+    out = np.empty(int(sum(int(s) for s in sizes)), dtype=np.float32)
+    call("gf_synth_grads", int(rank), int(step), u64_array(sizes), len(sizes), out.ctypes.data)
+    return out
 
 
 def ptr_array(ptrs):

@@ -11,6 +11,8 @@
 
 namespace {
 thread_local std::string g_last_error;
+thread_local gfi::PhaseHook g_phase_hook = nullptr;
+thread_local void* g_phase_ctx = nullptr;
 std::atomic<uint64_t> g_launches{0};
 std::mutex g_sm_mu;
 int g_sm_count[64] = {};
@@ -42,6 +44,15 @@ int sm_count() {
         g_sm_count[dev] = n;
     }
     return g_sm_count[dev];
+}
+
+void set_phase_hook(PhaseHook hook, void* ctx) {
+    g_phase_hook = hook;
+    g_phase_ctx = ctx;
+}
+
+void phase(const char* name, cudaStream_t s) {
+    if (g_phase_hook) g_phase_hook(g_phase_ctx, name, s);
 }
 
 int check_launch(const char* what) {

@@ -37,6 +37,11 @@ struct gf_comm {
     bool trace = false;
     uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;  // transport.hpp:25 kDefaultTimeout
     bool connected = false;
+    // gf_comm_connect_colocated: every rank of the world lives on this device (emulation of an
+    // N-GPU world on one B200, the same kernels and barriers); grids are capped so all ranks'
+    // barrier-waiting CTAs fit on the SMs at once
+    bool colocated = false;
+    int grid_cap = 0;
     uint64_t sel_inbox_off = UINT64_MAX;  // gf_comm_set_select_inbox (UINT64_MAX: pull protocol)
 };
 

@@ -20,6 +20,12 @@ void count_launch(uint64_t n = 1);
 int sm_count();              // SMs of the current device (cached per device)
 int check_launch(const char* what);  // cudaGetLastError -> status
 
+// Phase marks between the launches of a multi-kernel entry point (per calling thread): the
+// engine's per-kernel timing records an event on the launching stream at each mark.
+using PhaseHook = void (*)(void* ctx, const char* name, cudaStream_t s);
+void set_phase_hook(PhaseHook hook, void* ctx);
+void phase(const char* name, cudaStream_t s);
+
 // world == 1 dense step (pack.cu): pack and unpack in one pass (the collective is the identity)
 int pack_unpack_solo(int dtype, void* pool, const float* const* src, float* const* dst,
                      const uint64_t* pool_off, const uint64_t* count, int ntensors, cudaStream_t stream);

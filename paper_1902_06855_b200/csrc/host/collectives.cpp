@@ -11,7 +11,10 @@ namespace gflow {
 
 namespace {
 
-constexpr std::uint8_t kPhaseDevice = 9;  // control-plane tag phase of the device layer
+// control-plane tag phase of the device layer; the rooted handshake's two messages add the
+// disjoint bits kReady / kRelease, so no sub-phase tag can alias another
+constexpr std::uint8_t kPhaseDevice = 0x10;
+constexpr std::uint32_t kReady = 0x40u, kRelease = 0x80u;
 
 std::uint32_t device_tag(Communicator& comm) {
     return (comm.acquire_collective_id() << 8) | kPhaseDevice;
@@ -58,15 +61,15 @@ void rooted(Communicator& comm, ScalarBuffer dev, int root, F&& launch) {
     const std::vector<std::byte> token(1);
     if (comm.rank() == root) {
         for (int r = 0; r < comm.world_size(); ++r)
-            if (r != root) tp.control_recv(r, tag | 0x40u);
+            if (r != root) tp.control_recv(r, tag | kReady);
         ctx.activate();
         launch(ptrs);
         if (cudaDeviceSynchronize() != cudaSuccess) throw TransportError("rooted collective failed");
         for (int r = 0; r < comm.world_size(); ++r)
-            if (r != root) tp.control_send(r, tag | 0x41u, token);
+            if (r != root) tp.control_send(r, tag | kRelease, token);
     } else {
-        tp.control_send(root, tag | 0x40u, token);
-        tp.control_recv(root, tag | 0x41u);
+        tp.control_send(root, tag | kReady, token);
+        tp.control_recv(root, tag | kRelease);
     }
 }
 

@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <vector>
 
 #include "ring_device.cuh"
 #include "tensor_table.cuh"
@@ -220,9 +221,8 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
                             const uint64_t* count, int ntensors, const uint64_t* win_start,
                             const uint64_t* win_len, int nwin, void* stream) {
     if (int rc = comm_ready(c)) return rc;
-    if (dtype != GF_F16 || ntensors < 1 || ntensors > kMaxT || !src || !dst || !pool_off || !count || nwin < 1 ||
-        nwin > kMaxW || !win_start || !win_len)
-        return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense_push: fp16, 1..256 tensors, 1..256 windows");
+    if (dtype != GF_F16 || ntensors < 1 || !src || !dst || !pool_off || !count || nwin < 1 || !win_start || !win_len)
+        return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense_push: fp16 pool, >= 1 tensor, >= 1 window");
     if (c->world == 1)  // no collective: the one-pass pack + unpack
         return gf_sync_step_dense(c, dtype, pool_heap_off, src, dst, pool_off, count, ntensors, win_start, win_len,
                                   nwin, stream);
@@ -237,58 +237,86 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
     }
     if (lo != win_start[0] || hi != cover)
         return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense_push: tensors and windows must cover the same pool range");
-    const uint64_t slot_elems = hi;  // an inbox slot mirrors pool indices [0, hi)
-    if (pool_heap_off + hi * 2 > c->heap_bytes ||
-        inbox_heap_off + uint64_t(c->world - 1) * slot_elems * 2 > c->heap_bytes || inbox_heap_off % 16 != 0)
+    // an inbox slot mirrors pool indices [0, hi); its stride is rounded up to 8 elements so every
+    // slot base stays 16-byte aligned for the vector stores and loads
+    const uint64_t slot_elems = (hi + 7) & ~uint64_t(7);
+    const uint64_t pool_end = pool_heap_off + hi * 2, inbox_end = inbox_heap_off + uint64_t(c->world - 1) * slot_elems * 2;
+    if (pool_end > c->heap_bytes || inbox_end > c->heap_bytes)
         return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense_push: pool or inbox outside the symmetric heap");
+    if (pool_heap_off % 16 != 0 || inbox_heap_off % 16 != 0)
+        return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense_push: pool and inbox offsets must be 16-byte aligned");
+    if (pool_heap_off < inbox_end && inbox_heap_off < pool_end)
+        return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense_push: pool and inbox ranges overlap");
     DeviceGuard guard(c->device);
     cudaStream_t s = gfi::S(stream);
-    // 1. pack, routed to the owners
-    SegMap M;
-    std::memset(&M, 0, sizeof(M));
-    M.nwin = nwin;
-    M.world = c->world;
-    M.pos = c->pos;
-    M.slot_elems = slot_elems;
-    M.pool_local = c->alloc + kFlagBytes + pool_heap_off;
-    for (int j = 0; j < c->world; ++j) M.inbox_by_pos[j] = c->peer_alloc[c->ring[j]] + kFlagBytes + inbox_heap_off;
-    for (int w = 0; w < nwin; ++w) {
-        M.wstart[w] = win_start[w];
-        M.wlen[w] = win_len[w];
+    // Windows go in groups of <= kMaxW per launch pair; windows are cut at tensor boundaries,
+    // so every tensor belongs to exactly one group.
+    std::vector<const void*> gsrc;
+    std::vector<uint64_t> goff, gcnt;
+    for (int first = 0; first < nwin; first += kMaxW) {
+        const int nw = std::min(kMaxW, nwin - first);
+        const uint64_t g0 = win_start[first], g1 = win_start[first + nw - 1] + win_len[first + nw - 1];
+        gsrc.clear();
+        goff.clear();
+        gcnt.clear();
+        for (int i = 0; i < ntensors; ++i) {
+            if (pool_off[i] < g0 || pool_off[i] >= g1) continue;
+            if (pool_off[i] + count[i] > g1)
+                return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense_push: a tensor straddles a window boundary");
+            gsrc.push_back(src[i]);
+            goff.push_back(pool_off[i]);
+            gcnt.push_back(count[i]);
+        }
+        // 1. pack, routed to the owners
+        gfi::phase("pack_push", s);
+        SegMap M;
+        std::memset(&M, 0, sizeof(M));
+        M.nwin = nw;
+        M.world = c->world;
+        M.pos = c->pos;
+        M.slot_elems = slot_elems;
+        M.pool_local = c->alloc + kFlagBytes + pool_heap_off;
+        for (int j = 0; j < c->world; ++j) M.inbox_by_pos[j] = c->peer_alloc[c->ring[j]] + kFlagBytes + inbox_heap_off;
+        for (int w = 0; w < nw; ++w) {
+            M.wstart[w] = win_start[first + w];
+            M.wlen[w] = win_len[first + w];
+        }
+        if (int rc = for_each_table(gsrc.data(), goff.data(), gcnt.data(), int(gsrc.size()),
+                                    [&](const TensorTable& T, uint64_t tiles, int grid) {
+                                        uint64_t spread = std::max<uint64_t>(1, tiles / uint64_t(c->world));
+                                        while (std::gcd(spread, tiles) != 1) ++spread;
+                                        switch (push_minb()) {
+                                            case 6: pack_push_kernel<6><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
+                                            case 8: pack_push_kernel<8><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
+                                            default: pack_push_kernel<4><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
+                                        }
+                                    }))
+            return rc;
+        // 2. local reduce + all-gather push
+        RingArgs a;
+        std::memset(&a, 0, sizeof(a));
+        a.nwin = nw;
+        uint64_t max_seg = 0;
+        for (int w = 0; w < nw; ++w) {
+            a.wstart[w] = win_start[first + w];
+            a.wlen[w] = win_len[first + w];
+            max_seg += (a.wlen[w] + c->world - 1) / c->world;
+        }
+        fill_common(c, a, pool_heap_off);
+        const char* inbox_local = c->alloc + kFlagBytes + inbox_heap_off;
+        const int grid = gfr::comm_blocks(c, max_seg * 2);
+        gfi::phase("rsp", s);
+        switch (c->world) {
+            case 2: rsp_kernel<2><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
+            case 4: rsp_kernel<4><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
+            case 8: rsp_kernel<8><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
+            default: rsp_kernel<0><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
+        }
+        gfi::count_launch();
+        if (int rc = gfi::check_launch("gf_sync_step_dense_push")) return rc;
     }
-    if (int rc = for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
-                                [&](const TensorTable& T, uint64_t tiles, int grid) {
-                                    uint64_t spread = std::max<uint64_t>(1, tiles / uint64_t(c->world));
-                                    while (std::gcd(spread, tiles) != 1) ++spread;
-                                    switch (push_minb()) {
-                                        case 6: pack_push_kernel<6><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
-                                        case 8: pack_push_kernel<8><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
-                                        default: pack_push_kernel<4><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
-                                    }
-                                }))
-        return rc;
-    // 2. local reduce + all-gather push
-    RingArgs a;
-    std::memset(&a, 0, sizeof(a));
-    a.nwin = nwin;
-    uint64_t max_seg = 0;
-    for (int w = 0; w < nwin; ++w) {
-        a.wstart[w] = win_start[w];
-        a.wlen[w] = win_len[w];
-        max_seg += (win_len[w] + c->world - 1) / c->world;
-    }
-    fill_common(c, a, pool_heap_off);
-    const char* inbox_local = c->alloc + kFlagBytes + inbox_heap_off;
-    const int grid = gfr::ring_blocks(max_seg * 2);
-    switch (c->world) {
-        case 2: rsp_kernel<2><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
-        case 4: rsp_kernel<4><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
-        case 8: rsp_kernel<8><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
-        default: rsp_kernel<0><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
-    }
-    gfi::count_launch();
-    if (int rc = gfi::check_launch("gf_sync_step_dense_push")) return rc;
     // 3. unpack
+    gfi::phase("unpack", s);
     return gf_unpack(dtype, c->alloc + kFlagBytes + pool_heap_off, dst, pool_off, count, ntensors, c->world, stream);
 }
 

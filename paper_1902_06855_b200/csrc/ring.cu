@@ -499,6 +499,24 @@ int ring_blocks_impl(uint64_t max_seg_bytes) {
     return int(std::max<uint64_t>(1, std::min(want, cap)));
 }
 
+// CUDA 12 loads kernels lazily by default (CUDA_MODULE_LOADING=LAZY). Loading a kernel while
+// another kernel of the same context spins at a cross-rank barrier was measured to stall the
+// colocated world (the barrier never observes the peer): colocated worlds require EAGER loading.
+bool lazy_module_loading() {
+    using fn_t = CUresult (*)(CUmoduleLoadingMode*);
+    static fn_t fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuModuleGetLoadingMode", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<fn_t>(f);
+    }();
+    CUmoduleLoadingMode m = CU_MODULE_EAGER_LOADING;
+    if (!fn || fn(&m) != CUDA_SUCCESS) return false;
+    return m == CU_MODULE_LAZY_LOADING;
+}
+
 bool valid_ring(const int* order, int world) {
     bool seen[GF_MAX_RANKS] = {};
     for (int i = 0; i < world; ++i) {
@@ -630,6 +648,33 @@ int gf_comm_connect_local(gf_comm* const* comms, int world) {
     return GF_OK;
 }
 
+int gf_comm_connect_colocated(gf_comm* const* comms, int world) {
+    if (!comms || world < 1 || world > GF_MAX_RANKS) return gfi::fail(GF_ERR_CONFIG, "gf_comm_connect_colocated: bad arguments");
+    if (world > 1 && lazy_module_loading())
+        return gfi::fail(GF_ERR_CONFIG,
+                         "gf_comm_connect_colocated: needs CUDA_MODULE_LOADING=EAGER in the environment before CUDA "
+                         "initialises (a kernel loaded lazily while another rank's kernel waits at a barrier on the "
+                         "same device can stall both)");
+    for (int r = 0; r < world; ++r) {
+        if (!comms[r] || comms[r]->world != world || comms[r]->rank != r)
+            return gfi::fail(GF_ERR_CONFIG, "gf_comm_connect_colocated: comms[r] must be rank r of this world");
+        if (comms[r]->device != comms[0]->device)
+            return gfi::fail(GF_ERR_CONFIG, "gf_comm_connect_colocated: every rank must use the same device");
+        if (comms[r]->connected && world > 1)
+            return gfi::fail(GF_ERR_CONFIG, "gf_comm_connect_colocated: communicator already connected");
+    }
+    // every rank's barrier-waiting CTAs (one per SM at most) must be resident at once, with
+    // SMs left over for the ranks' non-waiting kernels: world x cap <= SMs / 2
+    const int cap = std::max(1, gfi::sm_count() / (2 * world));
+    for (int r = 0; r < world; ++r) {
+        for (int q = 0; q < world; ++q) comms[r]->peer_alloc[q] = comms[q]->alloc;
+        comms[r]->colocated = true;
+        comms[r]->grid_cap = cap;
+        comms[r]->connected = true;
+    }
+    return GF_OK;
+}
+
 int gf_comm_set_ring_order(gf_comm* c, const int* order) {
     if (!c || !order) return gfi::fail(GF_ERR_CONFIG, "gf_comm_set_ring_order: null argument");
     if (!valid_ring(order, c->world)) return gfi::fail(GF_ERR_CONFIG, "ring order is not a permutation of ranks");
@@ -709,7 +754,7 @@ int gf_ring_allreduce(gf_comm* c, int dtype, uint64_t heap_off, const uint64_t* 
             max_seg += (a.wlen[w] + c->world - 1) / c->world;
         }
         fill_common(c, a, heap_off);
-        launch_ring(dtype, true, a, dim3(gfr::ring_blocks(max_seg * es)), gfi::S(stream));
+        launch_ring(dtype, true, a, dim3(gfr::comm_blocks(c, max_seg * es)), gfi::S(stream));
         gfi::count_launch();
         if (int rc = gfi::check_launch("gf_ring_allreduce")) return rc;
     }
@@ -741,7 +786,7 @@ int gf_ring_allreduce_ptrs(gf_comm* c, int dtype, void* const* rank_bufs, const 
         }
         fill_common(c, a, 0);
         for (int r = 0; r < c->world; ++r) a.bufs[r] = static_cast<char*>(rank_bufs[r]);
-        launch_ring(dtype, true, a, dim3(gfr::ring_blocks(max_seg * es)), gfi::S(stream));
+        launch_ring(dtype, true, a, dim3(gfr::comm_blocks(c, max_seg * es)), gfi::S(stream));
         gfi::count_launch();
         if (int rc = gfi::check_launch("gf_ring_allreduce_ptrs")) return rc;
     }
@@ -806,7 +851,7 @@ int gf_ring_allreduce_planned(gf_comm* c, int dtype, uint64_t heap_off, const ui
     a.plan = plan_dev;
     fill_common(c, a, heap_off);
     const uint64_t bound = c->heap_bytes > heap_off ? (c->heap_bytes - heap_off) / c->world : 0;
-    launch_ring(dtype, true, a, dim3(gfr::ring_blocks(bound)), gfi::S(stream));
+    launch_ring(dtype, true, a, dim3(gfr::comm_blocks(c, bound)), gfi::S(stream));
     gfi::count_launch();
     return gfi::check_launch("gf_ring_allreduce_planned");
 }
@@ -830,7 +875,7 @@ int gf_ring_allreduce_planned_scatter(gf_comm* c, int dtype, uint64_t stage_heap
     a.wb_chunk = chunk;
     a.wb_nc = nc;
     const uint64_t bound = c->heap_bytes > stage_heap_off ? (c->heap_bytes - stage_heap_off) / c->world : 0;
-    launch_ring(dtype, true, a, dim3(gfr::ring_blocks(bound)), gfi::S(stream), size_t(nc) * 8);
+    launch_ring(dtype, true, a, dim3(gfr::comm_blocks(c, bound)), gfi::S(stream), size_t(nc) * 8);
     gfi::count_launch();
     return gfi::check_launch("gf_ring_allreduce_planned_scatter");
 }
@@ -854,7 +899,7 @@ int gf_csc_exchange_pull(gf_comm* c, uint64_t stage_heap_off, const uint64_t* pl
     a.wb_chunk = chunk;
     a.wb_nc = nc;
     const uint64_t bound = c->heap_bytes > stage_heap_off ? (c->heap_bytes - stage_heap_off) / c->world : 0;
-    const dim3 grid(gfr::ring_blocks(bound));
+    const dim3 grid(gfr::comm_blocks(c, bound));
     const size_t smem = size_t(nc) * 8;
     cudaStream_t s = gfi::S(stream);
     switch (c->world) {
@@ -1034,4 +1079,8 @@ int gf_ring_traffic(uint64_t len, int world, int position, int dtype, uint64_t* 
 
 namespace gfr {
 int ring_blocks(uint64_t max_seg_bytes) { return ring_blocks_impl(max_seg_bytes); }
+int comm_blocks(const gf_comm* c, uint64_t max_seg_bytes) {
+    const int g = ring_blocks_impl(max_seg_bytes);
+    return c->grid_cap > 0 ? std::min(g, c->grid_cap) : g;
+}
 }  // namespace gfr

@@ -39,6 +39,7 @@ def rt():
         _rt.cudaEventCreateWithFlags.argtypes = [C.POINTER(C.c_void_p), C.c_uint]
         _rt.cudaEventRecord.argtypes = [C.c_void_p, C.c_void_p]
         _rt.cudaStreamWaitEvent.argtypes = [C.c_void_p, C.c_void_p, C.c_uint]
+        _rt.cudaStreamDestroy.argtypes = [C.c_void_p]
     return _rt
 
 
@@ -62,6 +63,14 @@ def stream_create() -> int:
     h = C.c_void_p()
     _chk(rt().cudaStreamCreateWithFlags(C.byref(h), 1), "cudaStreamCreateWithFlags")
     return h.value
+
+
+def stream_destroy(s: int) -> None:
+    _chk(rt().cudaStreamDestroy(C.c_void_p(s)), "cudaStreamDestroy")
+
+
+def stream_sync(s: int | None) -> None:
+    _chk(rt().cudaStreamSynchronize(C.c_void_p(s or 0)), "cudaStreamSynchronize")
 
 
 def event_create() -> int:

@@ -5,6 +5,14 @@ import sys
 import numpy as np
 import pytest
 
+# Colocated worlds (tests/colo.py) run every rank's kernels concurrently on one device, each rank on
+# its own streams: give each stream its own hardware queue so no rank's barrier-waiting kernel can
+# sit in front of another rank's work (set before CUDA initialises in this process).
+# Kernels must also be loaded eagerly: a kernel loaded lazily while another rank's kernel spins at
+# a barrier on the same device stalls the world (gf_comm_connect_colocated refuses lazy loading).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

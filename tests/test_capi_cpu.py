@@ -53,31 +53,29 @@ def test_config_errors_map_to_exceptions():
         capi.call("gf_comm_create", 4, 7, 0, 1024, C.byref(C.c_void_p()))
 
 
-def test_part_ranges_tile_every_segment():
-    """gf_part_ranges (host-only): the pieces of a pull-mode step are disjoint, tile every
-    window exactly, and cut segments at multiples of 8 elements (16-byte fp16 vectors)."""
-    import numpy as np
-    rng = np.random.default_rng(3)
-    for world in (2, 3, 4, 8):
-        for _ in range(20):
-            nwin = int(rng.integers(1, 6))
-            wl = rng.integers(1, 200_000, nwin).tolist()
-            ws = np.concatenate([[0], np.cumsum(wl)[:-1]]).tolist()
-            cuts = sorted(set([0, 1024] + rng.integers(1, 1024, int(rng.integers(0, 4))).tolist()))
-            cover = np.zeros(sum(wl), np.int32)
-            for lo_q, hi_q in zip(cuts, cuts[1:]):
-                lo, hi = capi.part_ranges(ws, wl, world, lo_q, hi_q)
-                assert (lo < hi).all() and (lo[1:] >= hi[:-1]).all()
-                for a, b in zip(lo.tolist(), hi.tolist()):
-                    cover[a:b] += 1
-                    # a cut point inside a segment is 8-aligned
-                    seg_edges = set()
-                    for s0, l in zip(ws, wl):
-                        base, rem = divmod(l, world)
-                        for j in range(world + 1):
-                            seg_edges.add(s0 + j * base + min(j, rem))
-                    assert a in seg_edges or a % 8 == 0
-                    assert b in seg_edges or b % 8 == 0
-            assert (cover == 1).all()
+def test_engine_config_defaults():
+    """gf_engine_config_init: the reference's defaults (fusion.hpp:27-30 theta 64 MiB,
+    gradient_pool.hpp:16 chunk 32000, sparse.hpp:21-26 momentum 0.9 / lr 0.01, transport.hpp:25
+    timeout 30 s); host-only."""
+    cfg = capi.EngineConfig()
+    capi.lib().gf_engine_config_init(C.byref(cfg))
+    assert (cfg.world, cfg.rank, cfg.dtype, cfg.theta_bytes, cfg.chunk) == (1, 0, capi.GF_F16, 64 << 20, 32000)
+    assert (cfg.csc, cfg.dense_mode, cfg.csc_mode) == (0, capi.GF_DENSE_AUTO, capi.GF_CSC_PUSH)
+    assert (cfg.momentum, cfg.learning_rate, cfg.timeout_ms) == (0.9, 0.01, 30000)
     with pytest.raises(capi.ConfigError):
-        capi.part_ranges([0], [10], 2, 5, 4)
+        capi.call("gf_engine_create", C.byref(cfg), capi.u64_array([]), 0, C.byref(C.c_void_p()))
+    cfg.chunk = 0
+    with pytest.raises(capi.ConfigError):
+        capi.call("gf_engine_create", C.byref(cfg), capi.u64_array([5]), 1, C.byref(C.c_void_p()))
+
+
+def test_synth_grads_match_reference_stream(reference):
+    """gf_synth_grads (host) is the reference's seeded generator (the stream
+    oracle/ref_driver.cpp draws with the reference build): bit-identical values, so bench.py's
+    GPU arm and its CPU reference arm sync the same gradients."""
+    import numpy as np
+    sizes = [23232, 64, 307200, 192, 7, 1000]
+    for r, t in ((0, 0), (3, 1), (7, 5)):
+        a = capi.synth_grads(r, t, sizes)
+        b = reference.gen_grads(r, t, sizes)
+        assert (a.view(np.uint32) == b.view(np.uint32)).all(), (r, t)

@@ -471,30 +471,6 @@ def test_csc_multistep_colocated_vs_reference_golden(gf, golden, oracle, G, fuse
             imp, coff, plan = nxt, nxt_coff, nxt_plan
 
 
-def test_fused_step_single_rank(gf, oracle, G):
-    """world == 1: the fused kernel's pack/unpack path (no peers) vs the oracle."""
-    import torch
-    from paper_1902_06855_b200.engine import GradSync
-    sizes = RESNET50[:40] + [13, 7]  # includes two tensors with unaligned pool offsets
-    off, _, _ = oracle.pool_layout(sizes, 32000)
-    bounds = np.concatenate([[0], np.cumsum(sizes)])
-    sync = GradSync(sizes, theta=1 << 16)
-    for it in range(3):
-        flat = oracle.gen_grads(40 + it, sizes) * np.float32(1 + it)
-        g = torch.from_numpy(flat).cuda()
-        out = torch.empty_like(g)
-        gp = [g[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
-        op = [out[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))]
-        sync.fused_step(gp, op)
-        torch.cuda.synchronize()
-        want = oracle.unpack(oracle.pack(flat, sizes), 1)
-        got = out.cpu().numpy()
-        for i, s in enumerate(sizes):
-            assert (got[int(bounds[i]):int(bounds[i + 1])].view(np.uint32) ==
-                    want[int(off[i]):int(off[i]) + s].view(np.uint32)).all(), (it, i)
-    sync.close()
-
-
 @pytest.mark.parametrize("dtype", [F16, F32])
 @pytest.mark.parametrize("aligned", [True, False])
 def test_sync_step_world1_one_pass(gf, oracle, G, dtype, aligned):
@@ -545,17 +521,18 @@ def test_engine_csc_world1_vs_oracle(gf, oracle, G, dtype, theta):
     sync = GradSync(sizes, dtype=dtype, theta=theta, chunk=chunk, csc=True, final_sparsity=0.75,
                     warmup_iters=2, momentum=0.9, lr=0.01)
     nc = sync.layout.num_chunks
-    hg = torch.zeros(total, device="cuda")
-    imp = [torch.ones(nc, dtype=torch.uint8, device="cuda"), torch.zeros(nc, dtype=torch.uint8, device="cuda")]
-    coff = [torch.zeros(nc, dtype=torch.int64, device="cuda") for _ in range(2)]
-    plan = [torch.zeros(4 + nc, dtype=torch.int64, device="cuda") for _ in range(2)]
     rng = np.random.default_rng(5 + dtype)
     w0 = rng.uniform(-1, 1, total).astype(np.float32)
-    hu, w = torch.zeros(total, device="cuda"), torch.from_numpy(w0.copy()).cuda()
-    nacc = torch.zeros(nc, dtype=torch.int64, device="cuda")
-    sync.attach_csc_state(hg.data_ptr(), [t.data_ptr() for t in imp], [t.data_ptr() for t in coff],
-                          [t.data_ptr() for t in plan], hu.data_ptr(), w.data_ptr(), nacc=nacc.data_ptr())
-    sync.init_csc_plan()
+    wp, _ = sync.state("w")
+    cudart.memcpy(wp, w0.ctypes.data, w0.nbytes)
+    cudart.sync_device()
+
+    def st(name, dt):
+        p, n = sync.state(name)
+        out = np.empty(n // np.dtype(dt).itemsize, dt)
+        cudart.memcpy(out.ctypes.data, p, out.nbytes)
+        cudart.sync_device()
+        return out
     bounds = np.concatenate([[0], np.cumsum(sizes)])
     o_hg, o_hu, o_w = [np.zeros(total, np.float32)], np.zeros(total, np.float32), w0.copy()
     o_imp = np.ones(nc, np.uint8)
@@ -570,14 +547,11 @@ def test_engine_csc_world1_vs_oracle(gf, oracle, G, dtype, theta):
                                                 dtype=dtype)
         oracle.csc_sgd_update(pools[0], o_imp, chunk, 1, np.float32(0.9), np.float32(0.01), o_hu, o_w,
                               dtype=dtype)
-        pool = np.empty(total * esz, np.uint8)
-        cudart.memcpy(pool.ctypes.data, sync.pool_ptr, pool.nbytes)
-        cudart.sync_device()
-        assert (pool == pools[0].view(np.uint8)).all(), t
-        assert (G.bits(hg.cpu().numpy()) == G.bits(o_hg[0])).all(), t
-        assert (imp[(t + 1) & 1].cpu().numpy() == nxt).all(), t
-        assert (G.bits(hu.cpu().numpy()) == G.bits(o_hu)).all(), t
-        assert (G.bits(w.cpu().numpy()) == G.bits(o_w)).all(), t
+        assert (st("pool", np.uint8) == pools[0].view(np.uint8)).all(), t
+        assert (G.bits(st("hg", np.float32)) == G.bits(o_hg[0])).all(), t
+        assert (st("imp_next", np.uint8) == nxt).all(), t
+        assert (G.bits(st("hu", np.float32)) == G.bits(o_hu)).all(), t
+        assert (G.bits(st("w", np.float32)) == G.bits(o_w)).all(), t
         o_imp = nxt
     sync.close()
 

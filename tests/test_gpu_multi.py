@@ -362,9 +362,9 @@ def test_inprocess_local_connect():
 
 
 def _worker_fused(rank, world, port):
-    """The engine's dense step in every mode — one fused kernel, pack + pull RS/AG with the
-    unpack fused in (alternating pools), pack + push-pull ring + unpack — over several
-    iterations and theta values, bit-exact against the oracle's unfused path."""
+    """The engine's dense step in every mode — the routed pack + local reduce + push all-gather
+    (rspush), pack + pull RS/AG with the unpack fused in (alternating pools), pack + push-pull
+    ring + unpack — over several iterations and theta values, bit-exact vs the oracle."""
     comm, base, capi, cudart, dist = _setup(rank, world, port)
     import torch
     from oracle.oracle import RESNET50, Oracle
@@ -380,11 +380,8 @@ def _worker_fused(rank, world, port):
         dist.all_gather_object(out, b)
         return out
 
-    modes = [("fused", None), ("pull", None), ("pull", (0, 256, 1024)), ("pull", (0, 100, 101, 700, 1024)),
-             ("push", None), ("rspush", None)]
-    for (mode, parts), theta in [(m, t) for m in modes for t in (64 << 20, 1 << 20, 0)]:
-        sync = GradSync(sizes, rank=rank, world=world, device=rank, theta=theta, allgather=ag,
-                        dense_mode=mode, pull_parts=parts)
+    for mode, theta in [(m, t) for m in ("pull", "push", "rspush") for t in (64 << 20, 1 << 20, 0)]:
+        sync = GradSync(sizes, rank=rank, world=world, device=rank, theta=theta, allgather=ag, dense_mode=mode)
         for it in range(3):
             grads = [o.gen_grads(1000 * it + 17 * r + theta % 97, sizes) for r in range(world)]
             g = torch.from_numpy(grads[rank]).cuda()
@@ -396,23 +393,22 @@ def _worker_fused(rank, world, port):
             sync.status()
             ws, wl = o.dense_windows(sizes, 2, theta)
             pools = o.ring_allreduce([o.pack(x, sizes) for x in grads], dtype=F16, windows=(ws, wl))
-            if mode != "fused":  # every rank's pool holds the sums, as after ring_allreduce
-                got_pool = np.empty_like(pools[rank])
-                cudart.memcpy(got_pool.ctypes.data, sync.last_pool_ptr, got_pool.nbytes)
-                cudart.sync_device()
-                assert (got_pool == pools[rank]).all(), (mode, parts, theta, it)
+            got_pool = np.empty_like(pools[rank])  # every rank's pool holds the sums
+            cudart.memcpy(got_pool.ctypes.data, sync.last_pool_ptr, got_pool.nbytes)
+            cudart.sync_device()
+            assert (got_pool == pools[rank]).all(), (mode, theta, it)
             want_pool = o.unpack(pools[rank], world)
             got = out.cpu().numpy()
             for i, s in enumerate(sizes):
                 w = want_pool[int(off[i]):int(off[i]) + s]
                 assert (got[int(bounds[i]):int(bounds[i + 1])].view(np.uint32) == w.view(np.uint32)).all(), \
-                    (mode, parts, theta, it, i)
+                    (mode, theta, it, i)
         sync.close()
     dist.barrier()
 
 
 @pytest.mark.multigpu(2)
-def test_p2p_fused_step_bit_exact():
+def test_p2p_engine_dense_modes_bit_exact():
     _spawn(_worker_fused, _world())
 
 
@@ -449,18 +445,18 @@ def _worker_engine_csc(rank, world, port):
         sync = GradSync(sizes, rank=rank, world=world, device=rank, dtype=dt, theta=theta, chunk=chunk,
                         csc=True, final_sparsity=0.75, warmup_iters=2, momentum=0.9, lr=0.01,
                         allgather=ag, csc_mode=mode)
-        nc = sync.layout.num_chunks
         dev = torch.device("cuda", rank)
-        hg = torch.zeros(total, device=dev)
-        imp = [torch.ones(nc, dtype=torch.uint8, device=dev), torch.zeros(nc, dtype=torch.uint8, device=dev)]
-        coff = [torch.zeros(nc, dtype=torch.int64, device=dev) for _ in range(2)]
-        plan = [torch.zeros(4 + nc, dtype=torch.int64, device=dev) for _ in range(2)]
-        hu = torch.zeros(total, device=dev)
-        w = torch.from_numpy(g[p + "w0"]).to(dev)
-        nacc = torch.zeros(nc, dtype=torch.int64, device=dev)
-        sync.attach_csc_state(hg.data_ptr(), [t.data_ptr() for t in imp], [t.data_ptr() for t in coff],
-                              [t.data_ptr() for t in plan], hu.data_ptr(), w.data_ptr(), nacc=nacc.data_ptr())
-        sync.init_csc_plan()
+
+        def st(name, d):
+            ptr, nb = sync.state(name)
+            out = np.empty(nb // np.dtype(d).itemsize, d)
+            cudart.memcpy(out.ctypes.data, ptr, out.nbytes)
+            cudart.sync_device()
+            return out
+
+        w0 = np.ascontiguousarray(g[p + "w0"])
+        cudart.memcpy(sync.state("w")[0], w0.ctypes.data, w0.nbytes)
+        cudart.sync_device()
         bounds = np.concatenate([[0], np.cumsum(sizes)])
         esz = 2 if dt == F16 else 4
         for t in range(T):
@@ -468,15 +464,12 @@ def _worker_engine_csc(rank, world, port):
             sync.csc_step([x[int(bounds[i]):int(bounds[i + 1])].data_ptr() for i in range(len(sizes))])
             torch.cuda.synchronize()
             sync.status()
-            pool = np.empty(total * esz, np.uint8)
-            cudart.memcpy(pool.ctypes.data, sync.pool_ptr, pool.nbytes)
-            cudart.sync_device()
             want_pool = np.ascontiguousarray(g[p + "pool_x"][t][rank])
-            assert (pool == want_pool.view(np.uint8)).all(), (ci, mode, t)
-            assert (hg.cpu().numpy().view(np.uint32) == g[p + "hg"][t][rank].view(np.uint32)).all(), (ci, t)
-            assert (imp[(t + 1) & 1].cpu().numpy() == g[p + "next_imp"][t][rank]).all(), (ci, t)
-            assert (hu.cpu().numpy().view(np.uint32) == g[p + "hu"][t][rank].view(np.uint32)).all(), (ci, t)
-            assert (w.cpu().numpy().view(np.uint32) == g[p + "w"][t][rank].view(np.uint32)).all(), (ci, t)
+            assert (st("pool", np.uint8) == want_pool.view(np.uint8)).all(), (ci, mode, t)
+            assert (st("hg", np.uint32) == g[p + "hg"][t][rank].view(np.uint32)).all(), (ci, t)
+            assert (st("imp_next", np.uint8) == g[p + "next_imp"][t][rank]).all(), (ci, t)
+            assert (st("hu", np.uint32) == g[p + "hu"][t][rank].view(np.uint32)).all(), (ci, t)
+            assert (st("w", np.uint32) == g[p + "w"][t][rank].view(np.uint32)).all(), (ci, t)
         sync.close()
     assert ran > 0 or world not in (2, 4)
     dist.barrier()
