@@ -370,6 +370,8 @@ class Run:
         out.update(self.roofline(seg_ms))
         if e2e and not args.no_e2e:
             out["e2e"] = self.e2e()
+            if self.world == 1:
+                out["e2e_api"] = self.e2e_api()
         if self.world == 1 and self.rank == 0 and cpu_leg and not args.no_cpu_baseline:
             out.update(self.cpu_leg())
         else:
@@ -502,6 +504,22 @@ class Run:
                 "d2h_bytes_per_step": d2h,
                 "path": "C-ABI gf_engine_* with pinned host grads in / results out, double-buffered: "
                         "H2D of step i+1 overlaps D2H of step i"}
+
+    def e2e_api(self):
+        """The same workload through the reference-shaped C++ API (gflow::GradientPool /
+        FusionEngine / SparseState, what a drop-in user of the reference calls): a train_worker
+        sync loop with pinned host gradients (write_tensor per tensor) and the update read
+        (read_averaged: unpack + D2H) or the CSC calls; wall clock, N=1 (gflowpy.bench_api)."""
+        try:
+            import paper_1902_06855_b200.gflowpy as gp
+            r = gp.bench_api(self.sizes, steps=self.args.steps, warmup=max(self.args.warmup, 1),
+                             theta=self.wl["theta"], csc=self.csc, final_sparsity=self.wl.get("sparsity", 0.9))
+            return {"value": round(r["ms_per_step"], 4), "unit": "ms", "h2d_bytes_per_step": r["h2d_bytes_per_step"],
+                    "d2h_bytes_per_step": r["d2h_bytes_per_step"],
+                    "path": "gflow:: C++ API (GradientPool.write_tensor per tensor from pinned host memory, "
+                            "FusionEngine windows, wait_all, read_averaged / SparseState calls), wall clock"}
+        except Exception as e:  # pragma: no cover
+            return {"error": str(e)[:200]}
 
     def cpu_leg(self):
         """N=1, rank 0: the reference library (oracle/_ref) as the checker of the recorded steps
@@ -714,6 +732,7 @@ def main():
             "parity": res["parity"], "parity_detail": res.get("parity_detail"),
             "bus_gbs": res["bus_gbs"], "kernels": res["kernels"], "kernel_timing": res["kernel_timing"],
             "roofline": res["roofline"], "cpu_baseline": res.get("cpu_baseline"), "e2e": res.get("e2e"),
+            "e2e_api": res.get("e2e_api"),
             "nccl_allreduce": nccl, "gpu_launches": res["launches"], "clocks": clk,
             "host_enqueue_ms_per_step": res["host_enqueue_ms_per_step"], "csc": csc_sub,
         }

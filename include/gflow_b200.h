@@ -128,6 +128,14 @@ int gf_csc_pack_correct(int dtype, void* pool, float* hg, void* staging,
                         uint64_t chunk, uint64_t nc, const float* const* src,
                         const uint64_t* pool_off, const uint64_t* count, int ntensors,
                         float momentum, uint64_t* nacc, void* stream);
+/* The same restricted to a part of the chunks: part 0 all, 1 the important chunks only (every
+ * staged chunk), 2 the unimportant ones only. A CSC step runs part 1, starts the exchange of the
+ * staging buffer, and runs part 2 beside it (they touch disjoint pool/hg/nacc elements). */
+int gf_csc_pack_correct_part(int dtype, void* pool, float* hg, void* staging,
+                             const uint8_t* important, const uint64_t* coff, uint64_t total,
+                             uint64_t chunk, uint64_t nc, const float* const* src,
+                             const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                             float momentum, uint64_t* nacc, int part, void* stream);
 /* Staging pack / write-back over the important chunks listed in `plan` (see gf_csc_plan):
  * staging[coff[c] + i] <-> pool[c*chunk + i]. max_chunks bounds plan[1] (launch size; nc is safe). */
 int gf_csc_compact(int dtype, const void* pool, void* staging, const uint64_t* plan,
@@ -176,6 +184,10 @@ int gf_comm_connect_colocated(gf_comm* const* comms, int world);
 /* Ring order (collectives.hpp:37-38): a permutation of ranks, identical on all ranks. */
 int gf_comm_set_ring_order(gf_comm* comm, const int* order);
 int gf_comm_set_timeout_ms(gf_comm* comm, uint64_t ms);
+/* Upper bound on the CTAs per rank of this communicator's NVLink kernels (0: automatic). Must be
+ * the same on every rank (CTA b pairs with CTA b). A CSC step caps its exchange so the rest of
+ * the SMs keep packing beside it. */
+int gf_comm_set_max_blocks(gf_comm* comm, int max_blocks);
 /* GF_OK, or GF_ERR_TRANSPORT once a device-side wait timed out (comm is then poisoned). */
 int gf_comm_status(gf_comm* comm);
 /* Tracing: when on, CTA 0 of every NVLink ring launch stamps %globaltimer (ns) into a
@@ -250,13 +262,14 @@ int gf_ring_allreduce_unpack(gf_comm* comm, int dtype, uint64_t pool_heap_off, f
                              void* stream);
 /* One dense sync step with the reduce-scatter's traffic riding on the pack (push form): the
  * pack stores each packed vector straight into the owner of its segment (my pool, or my slot
- * of the owner's inbox over NVLink); one kernel then sums every owned segment from local
- * memory in ring order and pushes the sums into all pools; then unpack. Same results as
- * gf_pack + gf_ring_allreduce + gf_unpack, bit for bit. fp16; the inbox (world-1 slots of
- * round_up(pool span, 8) elements each, at inbox_heap_off, same offset on every rank) lives in
- * the symmetric heap; pool and inbox offsets are 16-byte aligned and must not overlap.
- * src/dst/pool_off/count are HOST arrays (any number of tensors, covering the windows; more
- * than GF_MAX_WINDOWS_PER_LAUNCH windows run as several launch pairs). */
+ * of the owner's inbox over NVLink); then one kernel sums every owned segment from LOCAL memory
+ * (pool + inbox slots, ring order from the owner: bit-identical), pushes the sums into every
+ * rank's pool and unpacks them from registers, and after its exit barrier unpacks the segments
+ * the peers pushed to it. Same results as gf_pack + gf_ring_allreduce + gf_unpack, bit for bit.
+ * fp16; the inbox (world-1 slots of round_up(pool span, 8) elements each, at inbox_heap_off,
+ * same offset on every rank) lives in the symmetric heap; pool and inbox offsets are 16-byte
+ * aligned and must not overlap. src/dst/pool_off/count are HOST arrays. Beyond 256 tensors or
+ * windows (or with GF_FUSE_UNPACK=0) a separate unpack launch follows. */
 int gf_sync_step_dense_push(gf_comm* comm, int dtype, uint64_t pool_heap_off, uint64_t inbox_heap_off,
                             const float* const* src, float* const* dst, const uint64_t* pool_off,
                             const uint64_t* count, int ntensors, const uint64_t* win_start,

@@ -21,6 +21,7 @@
 #include "gflow/fusion.hpp"
 #include "gflow/gradient_pool.hpp"
 #include "gflow/half.hpp"
+#include "gflow/harness.hpp"
 #include "gflow/inproc.hpp"
 #include "gflow/sparse.hpp"
 #include "gflow/tcp.hpp"
@@ -73,23 +74,14 @@ py::dict pool_info(const std::vector<std::size_t>& sizes, std::size_t chunk_size
     return out;
 }
 
-// harness.cpp:132-159 (analytic payload; dense 2(N-1)/N * pool bytes, CSC over the k
-// selected chunks plus the fp32 norm vector; the reference uses ceil for the chunk count here)
-py::dict predict_traffic(std::uint64_t pool_elements, std::size_t element_bytes, int ranks, double sparsity,
+// harness.cpp:132-159 (gflow::predict_traffic, host/harness.cpp)
+py::dict py_predict_traffic(std::uint64_t pool_elements, std::size_t element_bytes, int ranks, double sparsity,
                          std::size_t chunk_size, bool csc) {
-    const double n = ranks, factor = ranks > 1 ? 2.0 * (n - 1.0) / n : 0.0;
-    const double pool_bytes = static_cast<double>(pool_elements) * static_cast<double>(element_bytes);
-    double grad = factor * pool_bytes, norm = 0.0;
-    if (csc) {
-        const std::size_t nc = (pool_elements + chunk_size - 1) / chunk_size;
-        const std::size_t k = selection_count(sparsity, nc);
-        grad = factor * std::min(pool_bytes, static_cast<double>(k) * chunk_size * element_bytes);
-        norm = factor * static_cast<double>(nc) * 4.0;
-    }
+    const TrafficPrediction p = gflow::predict_traffic(pool_elements, element_bytes, ranks, sparsity, chunk_size, csc);
     py::dict out;
-    out["grad_bytes"] = grad;
-    out["norm_bytes"] = norm;
-    out["total_bytes"] = grad + norm;
+    out["grad_bytes"] = p.grad_bytes;
+    out["norm_bytes"] = p.norm_bytes;
+    out["total_bytes"] = p.total();
     return out;
 }
 
@@ -102,12 +94,6 @@ int device_count() {
     return n;
 }
 
-// Rank r's GPU when ranks are threads: its own GPU if there are enough, else all share GPU 0.
-int rank_device(int rank, int ranks) {
-    const int n = device_count();
-    return n >= ranks ? rank : 0;
-}
-
 template <typename F>
 void run_ranks(int ranks, F body) {
     auto world = make_inproc_world(ranks);
@@ -116,7 +102,7 @@ void run_ranks(int ranks, F body) {
     for (int r = 0; r < ranks; ++r) {
         ts.emplace_back([&, r] {
             try {
-                cudaSetDevice(rank_device(r, ranks));
+                cudaSetDevice(gflow::thread_rank_device(r, ranks));
                 body(r, *world[static_cast<std::size_t>(r)]);
             } catch (...) {
                 errors[static_cast<std::size_t>(r)] = std::current_exception();
@@ -128,62 +114,22 @@ void run_ranks(int ranks, F body) {
         if (e) std::rethrow_exception(e);
 }
 
-// harness.cpp:245-339 semantics, ranks as threads, the allreduce on the GPU.
-py::dict bench_allreduce(int ranks, std::uint64_t bytes, const std::string& algo, int group_size,
+// harness.cpp:245-339 (gflow::bench_allreduce, host/harness.cpp): ranks as threads, the
+// allreduce on the GPU.
+py::dict py_bench_allreduce(int ranks, std::uint64_t bytes, const std::string& algo, int group_size,
                          const std::string& precision) {
     const Algo a = algo_from_name(algo);
     const ElementType et = precision_from_name(precision);
-    if (ranks < 1) throw ConfigError("ranks must be >= 1");
-    const std::size_t esz = element_size(et), n = bytes / esz;
-    if (n == 0) throw ConfigError("buffer too small for element type");
-    if (a == Algo::kHierarchical && (group_size < 1 || ranks % group_size != 0))
-        throw ConfigError("group size " + std::to_string(group_size) + " must divide world " + std::to_string(ranks));
-    std::uint64_t sent0 = 0, phase2 = 0;
-    std::vector<std::vector<float>> got(static_cast<std::size_t>(ranks)), want(static_cast<std::size_t>(ranks));
+    BenchResult r;
     {
         py::gil_scoped_release nogil;
-        run_ranks(ranks, [&](int r, Transport& tp) {
-            Communicator comm(tp, group_size);
-            std::mt19937_64 rng(1234 + static_cast<std::uint64_t>(r));
-            std::uniform_real_distribution<float> uni(-1.0f, 1.0f);
-            std::vector<float> v(n);
-            for (auto& x : v) x = uni(rng);
-            auto buf = OwnedBuffer::from_floats(et, v);
-            auto ref = OwnedBuffer::from_floats(et, v);
-            switch (a) {
-                case Algo::kRing: ring_allreduce(comm, buf.view()); break;
-                case Algo::kHierarchical: hierarchical_allreduce(comm, buf.view()); break;
-                case Algo::kOracle: oracle_allreduce(comm, buf.view()); break;
-            }
-            oracle_allreduce(comm, ref.view());
-            got[static_cast<std::size_t>(r)] = buf.to_floats();
-            want[static_cast<std::size_t>(r)] = ref.to_floats();
-            if (r == 0) {
-                for (const auto& [label, c] : tp.stats().snapshot())
-                    if (label != "oracle") sent0 += c.payload_bytes_sent;
-                const auto segs = comm.phase2_segment_bytes();
-                phase2 = segs.empty() ? 0 : segs.front();
-            }
-        });
+        r = gflow::bench_allreduce(ranks, bytes, a, group_size, "inproc", et);
     }
-    std::uint64_t predicted = 0;
-    if (a == Algo::kRing && ranks > 1) {
-        for (int s = 0; s < ranks - 1; ++s) {
-            predicted += (detail::segment_of(n, ranks, (ranks - s) % ranks).length +
-                          detail::segment_of(n, ranks, (1 - s + ranks) % ranks).length) * esz;
-        }
-    }
-    double max_rel = 0.0;
-    for (int r = 0; r < ranks; ++r)
-        for (std::size_t i = 0; i < n; ++i) {
-            const double w = want[static_cast<std::size_t>(r)][i], g = got[static_cast<std::size_t>(r)][i];
-            max_rel = std::max(max_rel, std::fabs(g - w) / std::max(1.0, std::fabs(w)));
-        }
     py::dict out;
-    out["per_rank_payload_sent"] = sent0;
-    out["predicted_payload"] = predicted;
-    out["phase2_segment_bytes"] = phase2;
-    out["matches_oracle"] = max_rel <= (et == ElementType::kF32 ? 1e-6 : 1e-2);
+    out["per_rank_payload_sent"] = r.per_rank_payload_sent;
+    out["predicted_payload"] = r.predicted_payload;
+    out["phase2_segment_bytes"] = r.phase2_segment_bytes;
+    out["matches_oracle"] = r.matches_oracle;
     return out;
 }
 
@@ -303,9 +249,27 @@ PYBIND11_MODULE(gflowpy, m) {
     m.def("pool_info", &pool_info, py::arg("tensor_sizes"), py::arg("chunk_size") = 32000);
     m.def("sparsity_at", &sparsity_at, py::arg("iteration"), py::arg("warmup_iters"), py::arg("final_sparsity"));
     m.def("selection_count", &selection_count, py::arg("sparsity"), py::arg("num_chunks"));
-    m.def("predict_traffic", &predict_traffic, py::arg("pool_elements"), py::arg("element_bytes"),
+    m.def("predict_traffic", &py_predict_traffic, py::arg("pool_elements"), py::arg("element_bytes"),
           py::arg("ranks"), py::arg("sparsity") = 0.0, py::arg("chunk_size") = 32000, py::arg("csc") = false);
-    m.def("bench_allreduce", &bench_allreduce, py::arg("ranks"), py::arg("bytes"), py::arg("algo") = "ring",
+    m.def(
+        "bench_api",
+        [](const std::vector<std::size_t>& sizes, int steps, int warmup, std::uint64_t theta, bool csc,
+           double final_sparsity) {
+            ApiBenchResult r;
+            {
+                py::gil_scoped_release nogil;
+                r = gflow::bench_api_sync(sizes, steps, warmup, theta, csc, final_sparsity);
+            }
+            py::dict d;
+            d["ms_per_step"] = r.ms_per_step;
+            d["h2d_bytes_per_step"] = r.h2d_bytes_per_step;
+            d["d2h_bytes_per_step"] = r.d2h_bytes_per_step;
+            d["steps"] = r.steps;
+            return d;
+        },
+        py::arg("sizes"), py::arg("steps") = 20, py::arg("warmup") = 3, py::arg("theta") = 64ull << 20,
+        py::arg("csc") = false, py::arg("final_sparsity") = 0.9);
+    m.def("bench_allreduce", &py_bench_allreduce, py::arg("ranks"), py::arg("bytes"), py::arg("algo") = "ring",
           py::arg("group_size") = 1, py::arg("precision") = "fp32");
     m.def("train", &train, py::arg("ranks") = 2, py::arg("model_dims") = std::vector<std::size_t>{64, 32, 1},
           py::arg("task") = "linear", py::arg("iterations") = 50, py::arg("n_examples") = 1024,
@@ -418,7 +382,7 @@ PYBIND11_MODULE(gflowpy, m) {
         })
         .def("chunk_begin", &GradientPool::chunk_begin)
         .def("chunk_length", &GradientPool::chunk_length)
-        .def("begin_iteration", &GradientPool::begin_iteration)
+        .def("begin_iteration", &GradientPool::begin_iteration, release())
         .def("write_tensor", [](GradientPool& p, int id, py::object values) {
             Span s = as_float_span(values);
             py::gil_scoped_release nogil;
@@ -426,11 +390,16 @@ PYBIND11_MODULE(gflowpy, m) {
         })
         .def_property_readonly("written_elements", &GradientPool::written_elements)
         .def("iteration_complete", &GradientPool::iteration_complete)
-        .def("get", &GradientPool::get)
-        .def("set", &GradientPool::set)
+        .def("get", &GradientPool::get, release())
+        .def("set", &GradientPool::set, release())
+        .def("synchronize", &GradientPool::synchronize, release())
         .def("chunk_l1", &GradientPool::chunk_l1, release())
         .def("device_ptr", [](GradientPool& p) { return reinterpret_cast<std::uintptr_t>(p.device_data()); })
         .def("to_numpy", [](GradientPool& p) {
+            {
+                py::gil_scoped_release nogil;
+                p.synchronize();  // the pool's queued packs / collectives / corrections
+            }
             const std::size_t n = p.total_elements();
             if (p.element_type() == ElementType::kF16) {
                 py::array_t<std::uint16_t> a(n);
@@ -459,12 +428,22 @@ PYBIND11_MODULE(gflowpy, m) {
              py::arg("pool"), py::arg("comm"), py::arg("threshold_bytes") = 64ull << 20,
              py::arg("algorithm") = Algo::kRing, py::keep_alive<1, 2>(), py::keep_alive<1, 3>())
         .def("begin_iteration", &FusionEngine::begin_iteration)
-        .def("on_tensor_complete", [](FusionEngine& e, int id) { return Handles{e.on_tensor_complete(id)}; })
+        // a window launch may bootstrap the device context (a collective): no GIL while in C++
+        .def("on_tensor_complete", [](FusionEngine& e, int id) { return Handles{e.on_tensor_complete(id)}; },
+             release())
         .def("finalize_iteration", [](FusionEngine& e) {
             Handles h;
             if (auto f = e.finalize_iteration()) h.h.push_back(std::move(*f));
             return h;
-        })
+        }, release())
+        .def("enqueue_collective", [](FusionEngine& e, GradientPool& p, std::size_t first, std::size_t count) {
+            if (first + count > p.total_elements()) throw ConfigError("enqueue_collective: range outside the pool");
+            const std::size_t es = element_size(p.element_type());
+            Handles h;
+            h.h.push_back(e.enqueue_collective(
+                ScalarBuffer{p.element_type(), p.device_data() + first * es, count, Residency::kDevice}));
+            return h;
+        }, release())
         .def("window_bytes", [](const FusionEngine& e) { return e.last_log().window_bytes; })
         .def("log_csv_line", &FusionEngine::log_csv_line);
 
@@ -474,8 +453,8 @@ PYBIND11_MODULE(gflowpy, m) {
              }),
              py::arg("pool"), py::arg("momentum") = 0.9, py::arg("learning_rate") = 0.01,
              py::arg("final_sparsity") = 0.0, py::arg("warmup_iters") = 0, py::keep_alive<1, 2>())
-        .def("begin_iteration", &SparseState::begin_iteration)
-        .def("correction_pre_allreduce", &SparseState::correction_pre_allreduce)
+        .def("begin_iteration", &SparseState::begin_iteration, release())
+        .def("correction_pre_allreduce", &SparseState::correction_pre_allreduce, release())
         .def("sparse_exchange", &SparseState::sparse_exchange, release())
         .def("select_next_important", &SparseState::select_next_important, release())
         .def("sgd_update", [](SparseState& s, py::object w, int world) {
@@ -484,8 +463,10 @@ PYBIND11_MODULE(gflowpy, m) {
             s.sgd_update(std::span<float>(sp.ptr, sp.n), world);
         })
         .def_property_readonly("important", &SparseState::important)
-        .def("hg", [](const SparseState& s) { auto v = s.hg(); return std::vector<float>(v.begin(), v.end()); })
-        .def("hu", [](const SparseState& s) { auto v = s.hu(); return std::vector<float>(v.begin(), v.end()); })
+        .def("hg", [](const SparseState& s) { auto v = s.hg(); return std::vector<float>(v.begin(), v.end()); },
+             release())
+        .def("hu", [](const SparseState& s) { auto v = s.hu(); return std::vector<float>(v.begin(), v.end()); },
+             release())
         .def("selected_chunks", &SparseState::selected_chunks)
         .def("selected_payload_bytes", &SparseState::selected_payload_bytes)
         .def_property_readonly("current_sparsity", &SparseState::current_sparsity)

@@ -42,6 +42,7 @@ struct gf_comm {
     // barrier-waiting CTAs fit on the SMs at once
     bool colocated = false;
     int grid_cap = 0;
+    int max_blocks = 0;  // gf_comm_set_max_blocks (0: automatic)
     uint64_t sel_inbox_off = UINT64_MAX;  // gf_comm_set_select_inbox (UINT64_MAX: pull protocol)
 };
 

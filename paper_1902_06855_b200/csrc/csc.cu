@@ -226,16 +226,25 @@ __device__ __forceinline__ void correct8(const gfd::F8& gv, const float* hp, boo
 }
 
 // K2 over one 8192-element tile of tensor table entry (tile index `tile`), by NTH threads.
+// part: 0 every chunk, 1 the important chunks only, 2 the unimportant ones only (the CSC step
+// runs part 1 first, so the exchange of the staged chunks overlaps part 2).
 template <int DT, int NTH>
 __device__ __forceinline__ void pack_correct_tile(const TensorTable& T, uint64_t tile, void* __restrict__ pool,
                                                   float* __restrict__ hg, void* __restrict__ staging,
                                                   const uint8_t* __restrict__ imp, const uint64_t* __restrict__ coff,
-                                                  uint64_t chunk, uint64_t nc, float mom, uint64_t* __restrict__ nacc) {
+                                                  uint64_t chunk, uint64_t nc, float mom, uint64_t* __restrict__ nacc,
+                                                  int part) {
     const int t = find_tensor(T, tile);
     const uint64_t base = (tile - T.tiles[t]) * kTile;
     const uint64_t len = min(kTile, T.cnt[t] - base);
     const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
     const uint64_t po = T.off[t] + base;
+    if (part != 0) {  // a tile with no chunk of this part is skipped whole (block-uniform)
+        const uint64_t c0 = min(po / chunk, nc - 1), c1 = min((po + len - 1) / chunk, nc - 1);
+        bool any = c1 - c0 > 8;  // many small chunks: no shortcut
+        for (uint64_t c = c0; !any && c <= c1; ++c) any = (imp[c] != 0) == (part == 1);
+        if (!any) return;
+    }
     uint64_t done = 0;
     if (DT == GF_F16 && (reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0 && po % 8 == 0 &&
         chunk % 8 == 0 && (reinterpret_cast<uintptr_t>(hg) & 31u) == 0 &&
@@ -251,9 +260,12 @@ __device__ __forceinline__ void pack_correct_tile(const TensorTable& T, uint64_t
             uint64_t c = 0, units = 0;
             bool im = true, nan = false;
             if (act) {
-                const uint64_t pi = po + 8 * uint64_t(v);
-                c = min(pi / chunk, nc - 1);
+                c = min((po + 8 * uint64_t(v)) / chunk, nc - 1);
                 im = imp[c] != 0;
+            }
+            const bool mine = act && (part == 0 || (part == 1) == im);
+            if (mine) {
+                const uint64_t pi = po + 8 * uint64_t(v);
                 const gfd::F8 gv = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
                 const gfd::F8 hv = gfd::ld32f(hg + pi);
                 float hn[8];
@@ -265,7 +277,7 @@ __device__ __forceinline__ void pack_correct_tile(const TensorTable& T, uint64_t
                 if (im && stg) gfd::st16(stg + coff[c] + (pi - c * chunk), ov);
                 if ((!im || !stg) && nacc) units = units8(nan ? make_uint4(0, 0, 0, 0) : ov);
             }
-            if (nacc) nacc_add(nacc, c, units, nan, act && (!im || !stg));
+            if (nacc) nacc_add(nacc, c, units, nan, mine && (!im || !stg));
         }
         done = uint64_t(nvec) * 8;
     }
@@ -273,6 +285,7 @@ __device__ __forceinline__ void pack_correct_tile(const TensorTable& T, uint64_t
         const uint64_t pi = po + i;
         const uint64_t c = min(pi / chunk, nc - 1);
         const bool im = imp[c] != 0;
+        if (part != 0 && (part == 1) != im) continue;
         if (DT == GF_F16) {
             const uint16_t w = gfd::enc(correct_elem(gfd::dec(gfd::enc(s[i])), hg + pi, im, mom));
             static_cast<uint16_t*>(pool)[pi] = w;
@@ -301,9 +314,9 @@ pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ po
                     float* __restrict__ hg, void* __restrict__ staging,
                     const uint8_t* __restrict__ imp, const uint64_t* __restrict__ coff,
                     uint64_t chunk, uint64_t nc, float mom, uint64_t total_tiles,
-                    uint64_t* __restrict__ nacc) {
+                    uint64_t* __restrict__ nacc, int part) {
     for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x)
-        pack_correct_tile<DT, kThreads>(T, tile, pool, hg, staging, imp, coff, chunk, nc, mom, nacc);
+        pack_correct_tile<DT, kThreads>(T, tile, pool, hg, staging, imp, coff, chunk, nc, mom, nacc, part);
 }
 
 // Staging pack (dir=0) / write-back (dir=1) over the important chunks listed in the plan
@@ -504,6 +517,16 @@ int gf_csc_pack_correct(int dtype, void* pool, float* hg, void* staging,
                         uint64_t chunk, uint64_t nc, const float* const* src,
                         const uint64_t* pool_off, const uint64_t* count, int ntensors,
                         float momentum, uint64_t* nacc, void* stream) {
+    return gf_csc_pack_correct_part(dtype, pool, hg, staging, important, coff, total, chunk, nc, src, pool_off,
+                                    count, ntensors, momentum, nacc, 0, stream);
+}
+
+int gf_csc_pack_correct_part(int dtype, void* pool, float* hg, void* staging,
+                             const uint8_t* important, const uint64_t* coff, uint64_t total,
+                             uint64_t chunk, uint64_t nc, const float* const* src,
+                             const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                             float momentum, uint64_t* nacc, int part, void* stream) {
+    if (part < 0 || part > 2) return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct_part: part is 0, 1 or 2");
     if (!gfi::valid_dtype(dtype) || chunk == 0 || nc == 0 || !pool || !hg || !important)
         return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct: bad arguments");
     if (nacc && dtype != GF_F16) return gfi::fail(GF_ERR_CONFIG, "exact norm accumulation needs an fp16 pool");
@@ -513,10 +536,10 @@ int gf_csc_pack_correct(int dtype, void* pool, float* hg, void* staging,
                           [&](const TensorTable& T, uint64_t tiles, int grid) {
                               if (dtype == GF_F16)
                                   pack_correct_kernel<GF_F16><<<grid, kThreads, 0, gfi::S(stream)>>>(
-                                      T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc);
+                                      T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc, part);
                               else
                                   pack_correct_kernel<GF_F32><<<grid, kThreads, 0, gfi::S(stream)>>>(
-                                      T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc);
+                                      T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc, part);
                           });
 }
 

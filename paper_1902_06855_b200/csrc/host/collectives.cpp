@@ -113,13 +113,20 @@ void ring_allreduce_windows(Communicator& comm, ScalarBuffer buf,
     DeviceContext& ctx = comm.device();
     const std::uint32_t tag = device_tag(comm);
     with_device_view(ctx, buf, [&](ScalarBuffer dev) { ctx.ring_allreduce(dev, comm.ring_order(), windows, tag); });
-    // Payload accounting of the reference ring (collectives.cpp:69-96): what this rank's
-    // peer stores/loads moved, counted as the 2(N-1) segment transfers per window.
+    record_ring_payload(comm, buf.type, windows, label);
+}
+
+void record_ring_payload(Communicator& comm, ElementType type,
+                         const std::vector<std::pair<std::size_t, std::size_t>>& windows, const std::string& label) {
+    const int n = comm.world_size();
+    if (n == 1) return;
+    // what this rank's peer stores/loads moved, counted as the reference ring's 2(N-1)
+    // segment transfers per window (collectives.cpp:69-96)
     const auto& ring = comm.ring_order();
     const int pos = static_cast<int>(std::find(ring.begin(), ring.end(), comm.rank()) - ring.begin());
     for (auto& w : windows) {
         std::uint64_t sent = 0, recvd = 0, frames = 0;
-        check(gf_ring_traffic(w.second, n, pos, static_cast<int>(buf.type), &sent, &recvd, &frames), "traffic");
+        check(gf_ring_traffic(w.second, n, pos, static_cast<int>(type), &sent, &recvd, &frames), "traffic");
         comm.transport().stats().record_send(label, sent, frames);
         comm.transport().stats().record_recv(label, recvd);
     }

@@ -151,6 +151,14 @@ DeviceContext::DeviceContext(Transport& tp, int device) : tp_(tp), rank_(tp.rank
                           "process) all share one GPU");
     }
     DeviceGuard g(device_);
+    cudaStream_t st = nullptr;
+    cuda_ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreateWithFlags");
+    stream_ = st;
+    cudaEvent_t e1 = nullptr, e2 = nullptr;
+    cuda_ok(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming), "event");
+    cuda_ok(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming), "event");
+    ev_client_ = e1;
+    ev_done_ = e2;
     if (mode_ == Mode::kColocated) {
         std::uintptr_t key = 0;
         if (rank_ == 0) {
@@ -193,6 +201,9 @@ DeviceContext::~DeviceContext() {
     for (auto& [k, base] : ipc_cache_) gf_ipc_close(comm_, base);
     for (auto& s : scratch_) cudaFree(s.first);
     if (comm_) gf_comm_destroy(comm_);
+    if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
+    if (ev_client_) cudaEventDestroy(static_cast<cudaEvent_t>(ev_client_));
+    if (ev_done_) cudaEventDestroy(static_cast<cudaEvent_t>(ev_done_));
     if (group_) {
         std::lock_guard lk(g_groups_mu);
         for (auto it = g_groups.begin(); it != g_groups.end(); ++it) {
@@ -272,6 +283,7 @@ void DeviceContext::ring_allreduce(ScalarBuffer buf, const std::vector<int>& rin
                                    std::uint32_t tag) {
     if (world_ == 1 || windows.empty()) return;
     DeviceGuard g(device_);
+    const auto st = static_cast<cudaStream_t>(stream_);
     const std::size_t es = element_size(buf.type);
     // Peers' buffers must share this buffer's 16-byte misalignment so one aligned base plus
     // shifted windows describes every rank; otherwise the collective runs in aligned scratch.
@@ -294,7 +306,7 @@ void DeviceContext::ring_allreduce(ScalarBuffer buf, const std::vector<int>& rin
         }
     } else {
         staged = static_cast<std::byte*>(scratch((hi - lo) * es, 1));
-        cuda_ok(cudaMemcpy(staged, buf.data + lo * es, (hi - lo) * es, cudaMemcpyDefault), "stage");
+        cuda_ok(cudaMemcpyAsync(staged, buf.data + lo * es, (hi - lo) * es, cudaMemcpyDefault, st), "stage");
         ptrs = exchange(staged, tag | 0x80u);
         for (auto& w : windows) {
             ws.push_back(w.first - lo);
@@ -306,19 +318,49 @@ void DeviceContext::ring_allreduce(ScalarBuffer buf, const std::vector<int>& rin
         group_->run(rank_, ptrs[static_cast<std::size_t>(rank_)], tp_.timeout(), [&](std::vector<void*>& slots) {
             std::vector<void*> b = slots;  // each rank's own view of its buffer (same device)
             check(gf_ring_allreduce_colocated(dt, b.data(), world_, ring.data(), ws.data(), wl.data(),
-                                              static_cast<int>(ws.size()), nullptr),
+                                              static_cast<int>(ws.size()), st),
                   "gf_ring_allreduce_colocated");
-            cuda_ok(cudaStreamSynchronize(nullptr), "colocated ring");
+            cuda_ok(cudaStreamSynchronize(st), "colocated ring");
         });
     } else {
         check(gf_comm_set_ring_order(comm_, ring.data()), "ring order");
-        check(gf_ring_allreduce_ptrs(comm_, dt, ptrs.data(), ws.data(), wl.data(), static_cast<int>(ws.size()),
-                                     nullptr),
+        check(gf_ring_allreduce_ptrs(comm_, dt, ptrs.data(), ws.data(), wl.data(), static_cast<int>(ws.size()), st),
               "gf_ring_allreduce_ptrs");
-        cuda_ok(cudaStreamSynchronize(nullptr), "ring allreduce");
+        cuda_ok(cudaStreamSynchronize(st), "ring allreduce");
         check(gf_comm_status(comm_), "ring allreduce");
     }
-    if (staged) cuda_ok(cudaMemcpy(buf.data + lo * es, staged, (hi - lo) * es, cudaMemcpyDefault), "unstage");
+    if (staged) {
+        cuda_ok(cudaMemcpyAsync(buf.data + lo * es, staged, (hi - lo) * es, cudaMemcpyDefault, st), "unstage");
+        cuda_ok(cudaStreamSynchronize(st), "unstage");
+    }
+}
+
+void DeviceContext::ring_allreduce_async(ElementType type, const std::vector<void*>& rank_bufs,
+                                         const std::vector<int>& ring,
+                                         const std::vector<std::pair<std::size_t, std::size_t>>& windows,
+                                         void* client) {
+    if (world_ == 1 || windows.empty()) return;
+    if (!async_collectives()) throw ConfigError("ring_allreduce_async needs peer-mapped ranks on distinct GPUs");
+    DeviceGuard g(device_);
+    const auto cs = static_cast<cudaStream_t>(stream_);
+    if (client) {
+        cuda_ok(cudaEventRecord(static_cast<cudaEvent_t>(ev_client_), static_cast<cudaStream_t>(client)), "event");
+        cuda_ok(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(ev_client_), 0), "wait");
+    }
+    std::vector<std::uint64_t> ws, wl;
+    for (auto& w : windows) {
+        ws.push_back(w.first);
+        wl.push_back(w.second);
+    }
+    check(gf_comm_set_ring_order(comm_, ring.data()), "ring order");
+    std::vector<void*> b = rank_bufs;
+    check(gf_ring_allreduce_ptrs(comm_, static_cast<int>(type), b.data(), ws.data(), wl.data(),
+                                 static_cast<int>(ws.size()), stream_),
+          "gf_ring_allreduce_ptrs");
+    if (client) {
+        cuda_ok(cudaEventRecord(static_cast<cudaEvent_t>(ev_done_), cs), "event");
+        cuda_ok(cudaStreamWaitEvent(static_cast<cudaStream_t>(client), static_cast<cudaEvent_t>(ev_done_), 0), "wait");
+    }
 }
 
 }  // namespace gflow

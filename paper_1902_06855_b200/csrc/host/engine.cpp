@@ -8,7 +8,8 @@
 //   dense, world 1   gf_sync_step_dense: one streaming pass (the collective is the identity,
 //                    collectives.cpp:59)
 //   dense, world > 1 RSPUSH  gf_sync_step_dense_push: the pack routes every vector to the owner of
-//                            its segment (NVLink stores), local reduce + all-gather push, unpack
+//                            its segment (NVLink stores); local reduce + all-gather push with
+//                            the unpack fused in
 //                    PULL    gf_pack -> gf_ring_allreduce_unpack (two pools used alternately)
 //                    PUSH    gf_pack -> gf_ring_allreduce -> gf_unpack
 //   CSC              gf_csc_pack_correct -> exchange + write-back + exact L1 (pull or push form)
@@ -23,6 +24,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -91,9 +93,11 @@ struct gf_engine {
     uint64_t* plan[2] = {};
     uint64_t* nacc = nullptr;
     uint64_t iteration = 0;
+    int xblocks = 0;  // CTAs of the CSC exchange (the packing of the other chunks runs beside it)
     // streams / events (created on the engine's device, non-blocking)
     cudaStream_t side = nullptr, comm_s = nullptr;
-    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_ready = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_ready = nullptr, ev_done = nullptr, ev_sel = nullptr,
+                ev_rest = nullptr;
     // overlap state
     bool ov_on = false;
     std::vector<const float*> ov_grad;
@@ -154,7 +158,7 @@ void dense_windows(gf_engine* e) {
 int create_streams(gf_engine* e) {
     GF_ENG_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
     GF_ENG_CUDA(cudaStreamCreateWithFlags(&e->comm_s, cudaStreamNonBlocking));
-    for (cudaEvent_t* ev : {&e->ev_a, &e->ev_b, &e->ev_ready, &e->ev_done})
+    for (cudaEvent_t* ev : {&e->ev_a, &e->ev_b, &e->ev_ready, &e->ev_done, &e->ev_sel, &e->ev_rest})
         GF_ENG_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     return GF_OK;
 }
@@ -278,6 +282,8 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
     if (mode == GF_DENSE_PULL && ntensors > GF_MAX_WINDOWS_PER_LAUNCH) mode = GF_DENSE_PUSH;  // 256-tensor table
     e->dense_mode = mode;
     dense_windows(e);
+    if (const char* xb = std::getenv("GF_CSC_XBLOCKS")) e->xblocks = std::max(0, std::atoi(xb));
+    else e->xblocks = 64;
     // symmetric heap: [pool | (pull: 2nd pool) | (rspush: N-1 inbox slots) | (CSC: staging) | norms | (CSC N>1: select inbox)]
     const uint64_t pool_bytes = align_up(e->total * e->esz);
     e->pool_off = 0;
@@ -321,7 +327,7 @@ int gf_engine_destroy(gf_engine* e) {
     DevGuard g(e->cfg.device);
     if (e->side) cudaStreamSynchronize(e->side);
     if (e->comm_s) cudaStreamSynchronize(e->comm_s);
-    for (cudaEvent_t ev : {e->ev_a, e->ev_b, e->ev_ready, e->ev_done})
+    for (cudaEvent_t ev : {e->ev_a, e->ev_b, e->ev_ready, e->ev_done, e->ev_sel, e->ev_rest})
         if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
     if (e->side) cudaStreamDestroy(e->side);
@@ -458,30 +464,61 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
     char* stage = e->heap_base + e->stage_off;
     e->last_pool = pool;
     const bool solo = W == 1;  // the exchange is the identity: no staging, no scatter
-    mark(e, "pack_correct", s);
-    GF_ENG_OK(gf_csc_pack_correct(dt, pool, e->hg, solo ? nullptr : stage, e->imp[cur], e->coff[cur], T, chunk, nc,
-                                  grads, e->offs.data(), e->sizes.data(), e->m, static_cast<float>(C.momentum),
-                                  e->nacc, s));
     // chunks selected for this iteration (iteration 0 is dense, sparse.cpp:45-51)
     const uint64_t k_cur = e->iteration == 0
                                ? nc
                                : gflow::selection_count(gflow::sparsity_at(e->iteration, C.warmup_iters, C.final_sparsity),
                                                         nc);
     const bool fused_wb = !solo && e->nacc && chunk % 8 == 0 && nc <= 6144;
-    if (fused_wb && C.csc_mode == GF_CSC_PULL) {
-        // pull RS + pull AG straight into the pool (+ exact L1); the staging buffer is next
-        // rewritten after gf_csc_select's barrier, so no exit barrier is needed
-        mark(e, "ring_scatter", s);
-        GF_ENG_OK(gf_csc_exchange_pull(e->comm, e->stage_off, e->plan[cur], pool, chunk, nc, e->nacc, s));
-    } else if (fused_wb) {  // exchange + write-back + exact L1 of the exchanged chunks, one launch
-        mark(e, "ring_scatter", s);
-        GF_ENG_OK(gf_ring_allreduce_planned_scatter(e->comm, dt, e->stage_off, e->plan[cur], pool, chunk, nc, e->nacc,
-                                                    s));
-    } else if (!solo) {
+    auto exchange = [&]() -> int {
+        if (fused_wb && C.csc_mode == GF_CSC_PULL) {
+            // pull RS + pull AG straight into the pool (+ exact L1); the staging buffer is next
+            // rewritten after gf_csc_select's barrier, so no exit barrier is needed
+            mark(e, "ring_scatter", s);
+            return gf_csc_exchange_pull(e->comm, e->stage_off, e->plan[cur], pool, chunk, nc, e->nacc, s);
+        }
+        if (fused_wb) {  // exchange + write-back + exact L1 of the exchanged chunks, one launch
+            mark(e, "ring_scatter", s);
+            return gf_ring_allreduce_planned_scatter(e->comm, dt, e->stage_off, e->plan[cur], pool, chunk, nc,
+                                                     e->nacc, s);
+        }
         mark(e, "ring", s);
         GF_ENG_OK(gf_ring_allreduce_planned(e->comm, dt, e->stage_off, e->plan[cur], s));
         mark(e, "scatter", s);
-        GF_ENG_OK(gf_csc_scatter(dt, pool, stage, e->plan[cur], e->coff[cur], T, chunk, nc, k_cur, e->nacc, s));
+        return gf_csc_scatter(dt, pool, stage, e->plan[cur], e->coff[cur], T, chunk, nc, k_cur, e->nacc, s);
+    };
+    auto pack_correct = [&](int part, cudaStream_t st) {
+        return gf_csc_pack_correct_part(dt, pool, e->hg, solo ? nullptr : stage, e->imp[cur], e->coff[cur], T, chunk,
+                                        nc, grads, e->offs.data(), e->sizes.data(), e->m,
+                                        static_cast<float>(C.momentum), e->nacc, part, st);
+    };
+    if (solo) {
+        mark(e, "pack_correct", s);
+        GF_ENG_OK(pack_correct(0, s));
+    } else {
+        // the staged (important) chunks first; their exchange then runs beside the correction
+        // of the other chunks (disjoint pool / hg / nacc elements), its grid capped so that the
+        // packing CTAs keep the rest of the SMs
+        mark(e, "pack_correct_sel", s);
+        GF_ENG_OK(pack_correct(1, s));
+        if (e->marks_on) {
+            GF_ENG_OK(gf_comm_set_max_blocks(e->comm, e->xblocks));
+            const int rc = exchange();
+            gf_comm_set_max_blocks(e->comm, 0);
+            GF_ENG_OK(rc);
+            mark(e, "pack_correct_rest", s);
+            GF_ENG_OK(pack_correct(2, s));
+        } else {
+            GF_ENG_CUDA(cudaEventRecord(e->ev_sel, s));
+            GF_ENG_CUDA(cudaStreamWaitEvent(e->side, e->ev_sel, 0));
+            GF_ENG_OK(pack_correct(2, e->side));
+            GF_ENG_CUDA(cudaEventRecord(e->ev_rest, e->side));
+            GF_ENG_OK(gf_comm_set_max_blocks(e->comm, e->xblocks));
+            const int rc = exchange();
+            gf_comm_set_max_blocks(e->comm, 0);
+            GF_ENG_OK(rc);
+            GF_ENG_CUDA(cudaStreamWaitEvent(s, e->ev_rest, 0));
+        }
     }
     if (!e->nacc) {  // fp32 pool: separate norm pass (sequential fp64, as the reference)
         mark(e, "norms", s);

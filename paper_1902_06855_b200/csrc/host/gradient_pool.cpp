@@ -1,6 +1,9 @@
 // SPDX-License-Identifier: Apache-2.0
 // GradientPool on the GPU (reference: src/gradient_pool.cpp — layout :11-41, chunking
 // :55-70, write_tensor :78-105, chunk_l1 :107-116, dump_snapshot :118-128).
+// Device work is ordered on the pool's own stream (no device-wide synchronisation): host
+// gradients are DMA'd on a copy stream into a per-tensor fp32 staging slot and packed on the
+// pool stream; host reads wait for the pool stream only.
 #include "gflow/gradient_pool.hpp"
 
 #include <cuda_runtime.h>
@@ -19,13 +22,16 @@ void cuda_ok(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw TransportError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-bool is_device_ptr(const void* p) {
+enum class Where { kPageable, kPinned, kDevice };
+
+Where locate(const void* p) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
-        return false;
+        return Where::kPageable;
     }
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return Where::kDevice;
+    return a.type == cudaMemoryTypeHost ? Where::kPinned : Where::kPageable;
 }
 
 struct OnDevice {
@@ -40,6 +46,59 @@ struct OnDevice {
 };
 
 }  // namespace
+
+// Device-side state: the pool, its stream (packs, windows, readbacks in FIFO order), a copy
+// stream for host gradients, and the fp32 staging they land in.
+struct GradientPool::Device {
+    int device;
+    std::byte* data = nullptr;
+    cudaStream_t stream = nullptr, copy = nullptr;
+    cudaEvent_t ev_copy = nullptr, ev_input = nullptr;
+    cudaEvent_t ev_packed[2] = {nullptr, nullptr};  // an iteration's packs done (per staging buffer)
+    bool packed_recorded[2] = {false, false};
+    int parity = 0;             // staging buffer of the current iteration (double-buffered)
+    float* stage[2] = {nullptr, nullptr};  // fp32, one slot per tensor (pool offsets)
+    float* avg = nullptr;       // fp32 g_avg for read_averaged
+    float* norm_out = nullptr;
+    float* norm_host = nullptr;  // pinned
+    bool fresh_iteration = true;
+
+    Device(int dev, std::size_t bytes) : device(dev) {
+        cuda_ok(cudaMalloc(&data, std::max<std::size_t>(bytes, 16)), "cudaMalloc pool");
+        cuda_ok(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "pool stream");
+        cuda_ok(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "copy stream");
+        cuda_ok(cudaEventCreateWithFlags(&ev_copy, cudaEventDisableTiming), "event");
+        cuda_ok(cudaEventCreateWithFlags(&ev_input, cudaEventDisableTiming), "event");
+        for (auto& ev : ev_packed) cuda_ok(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        cuda_ok(cudaMemsetAsync(data, 0, bytes, stream), "cudaMemset pool");
+        cuda_ok(cudaMalloc(&norm_out, sizeof(float)), "cudaMalloc");
+        cuda_ok(cudaMallocHost(&norm_host, sizeof(float)), "cudaMallocHost");
+        cuda_ok(cudaStreamSynchronize(stream), "pool init");
+    }
+    ~Device() {
+        OnDevice g(device);
+        cudaStreamSynchronize(copy);
+        cudaStreamSynchronize(stream);
+        for (void* p : {static_cast<void*>(data), static_cast<void*>(stage[0]), static_cast<void*>(stage[1]),
+                        static_cast<void*>(avg), static_cast<void*>(norm_out)})
+            if (p) cudaFree(p);
+        for (auto& ev : ev_packed) cudaEventDestroy(ev);
+        if (norm_host) cudaFreeHost(norm_host);
+        cudaEventDestroy(ev_copy);
+        cudaEventDestroy(ev_input);
+        cudaStreamDestroy(copy);
+        cudaStreamDestroy(stream);
+    }
+    float* staging(std::size_t n) {
+        float*& b = stage[parity];
+        if (!b) cuda_ok(cudaMalloc(&b, std::max<std::size_t>(n * 4, 16)), "cudaMalloc staging");
+        return b;
+    }
+    float* averaged(std::size_t n) {
+        if (!avg) cuda_ok(cudaMalloc(&avg, std::max<std::size_t>(n * 4, 16)), "cudaMalloc g_avg");
+        return avg;
+    }
+};
 
 GradientPool::GradientPool(const std::vector<std::size_t>& sizes, std::size_t chunk_size, ElementType type)
     : chunk_size_(chunk_size), element_type_(type) {
@@ -59,32 +118,22 @@ GradientPool::GradientPool(const std::vector<std::size_t>& sizes, std::size_t ch
         1, static_cast<std::size_t>(std::llround(static_cast<double>(off) / static_cast<double>(chunk_size))));
     next_expected_id_ = m;
     cuda_ok(cudaGetDevice(&device_), "cudaGetDevice");
-    const std::size_t bytes = total_elements_ * element_size(type);
-    cuda_ok(cudaMalloc(&data_, std::max<std::size_t>(bytes, 16)), "cudaMalloc pool");
-    cuda_ok(cudaMemset(data_, 0, bytes), "cudaMemset pool");
-    cuda_ok(cudaMalloc(&norm_out_, sizeof(float)), "cudaMalloc");
-    host_.assign(bytes, std::byte{0});
+    dev_ = std::make_unique<Device>(device_, total_elements_ * element_size(type));
+    data_ = dev_->data;
+    host_.assign(total_elements_ * element_size(type), std::byte{0});
     host_valid_ = true;
 }
 
-GradientPool::GradientPool(GradientPool&& o) noexcept
-    : descs_(std::move(o.descs_)), total_elements_(o.total_elements_), chunk_size_(o.chunk_size_),
-      num_chunks_(o.num_chunks_), element_type_(o.element_type_), device_(o.device_), data_(o.data_),
-      stage_(o.stage_), stage_elems_(o.stage_elems_), norm_out_(o.norm_out_), host_(std::move(o.host_)),
-      host_valid_(o.host_valid_), watermark_(o.watermark_), chunks_reported_(o.chunks_reported_),
-      next_expected_id_(o.next_expected_id_) {
-    o.data_ = nullptr;
-    o.stage_ = nullptr;
-    o.norm_out_ = nullptr;
-}
+GradientPool::GradientPool(GradientPool&& o) noexcept = default;
 
-GradientPool::~GradientPool() {
-    if (!data_ && !stage_ && !norm_out_) return;
+GradientPool::~GradientPool() = default;
+
+void* GradientPool::stream() const { return dev_->stream; }
+
+void GradientPool::synchronize() {
+    run_pending_work();
     OnDevice g(device_);
-    cudaDeviceSynchronize();
-    cudaFree(data_);
-    cudaFree(stage_);
-    cudaFree(norm_out_);
+    cuda_ok(cudaStreamSynchronize(dev_->stream), "pool stream");
 }
 
 const TensorDesc& GradientPool::desc(int tensor_id) const {
@@ -94,6 +143,7 @@ const TensorDesc& GradientPool::desc(int tensor_id) const {
 }
 
 ScalarBuffer GradientPool::view() {
+    synchronize();
     host_valid_ = false;  // the caller may write through the view
     return {element_type_, data_, total_elements_, Residency::kDevice};
 }
@@ -118,6 +168,14 @@ ScalarBuffer GradientPool::chunk_view(std::size_t c) {
 }
 
 void GradientPool::begin_iteration() {
+    Device& D = *dev_;
+    if (!D.fresh_iteration) {  // an abandoned iteration: retire its staging buffer like a full one
+        OnDevice g(device_);
+        cuda_ok(cudaEventRecord(D.ev_packed[D.parity], D.stream), "event");
+        D.packed_recorded[D.parity] = true;
+        D.parity ^= 1;
+    }
+    D.fresh_iteration = true;
     watermark_ = 0;
     chunks_reported_ = 0;
     next_expected_id_ = num_tensors();
@@ -134,22 +192,43 @@ std::vector<std::size_t> GradientPool::write_tensor(int tensor_id, std::span<con
         throw ConfigError("tensor " + std::to_string(tensor_id) + " length mismatch: " +
                           std::to_string(values.size()) + " vs " + std::to_string(d.element_count));
     OnDevice g(device_);
+    Device& D = *dev_;
     const float* src = values.data();
-    if (!is_device_ptr(src)) {  // host gradients: one H2D copy into the staging buffer
-        if (stage_elems_ < values.size()) {
-            cudaFree(stage_);
-            stage_ = nullptr;
-            cuda_ok(cudaMalloc(&stage_, values.size() * sizeof(float)), "cudaMalloc stage");
-            stage_elems_ = values.size();
+    const std::size_t bytes = values.size() * sizeof(float);
+    const Where where = locate(src);
+    if (where == Where::kDevice) {
+        // produced on the legacy default stream (the reference's synchronous model): order after it
+        cuda_ok(cudaEventRecord(D.ev_input, cudaStreamLegacy), "event");
+        cuda_ok(cudaStreamWaitEvent(D.stream, D.ev_input, 0), "wait");
+    } else {
+        // host gradients: H2D on the copy stream into this tensor's slot of the fp32 staging
+        // (one slot per tensor: no reuse within an iteration); the pack waits for the copy
+        if (D.fresh_iteration) {
+            // double-buffered staging: this buffer was last read by the packs of the iteration
+            // before the previous one, so the H2D copies overlap the previous iteration's tail
+            if (D.packed_recorded[D.parity]) cuda_ok(cudaStreamWaitEvent(D.copy, D.ev_packed[D.parity], 0), "wait");
+            D.fresh_iteration = false;
         }
-        cuda_ok(cudaMemcpy(stage_, src, values.size() * sizeof(float), cudaMemcpyHostToDevice), "H2D");
-        src = stage_;
+        float* slot = D.staging(total_elements_) + d.pool_offset;
+        cuda_ok(cudaMemcpyAsync(slot, src, bytes, cudaMemcpyHostToDevice, D.copy), "H2D gradients");
+        cuda_ok(cudaEventRecord(D.ev_copy, D.copy), "event");
+        cuda_ok(cudaStreamWaitEvent(D.stream, D.ev_copy, 0), "wait");
+        // the span is the caller's again when we return: wait for a pinned DMA (pageable
+        // sources were staged by the driver before cudaMemcpyAsync returned)
+        if (where == Where::kPinned && !async_host_input_) cuda_ok(cudaEventSynchronize(D.ev_copy), "H2D");
+        src = slot;
     }
     const std::uint64_t off = d.pool_offset, cnt = d.element_count;
-    check(gf_pack(static_cast<int>(element_type_), data_, &src, &off, &cnt, 1, 1.0f, nullptr), "write_tensor");
+    check(gf_pack(static_cast<int>(element_type_), data_, &src, &off, &cnt, 1, 1.0f, D.stream), "write_tensor");
     host_valid_ = false;
     next_expected_id_ = tensor_id - 1;
     watermark_ = d.pool_offset + d.element_count;
+    if (next_expected_id_ == 0) {  // the iteration's last tensor: its staging buffer is free once packed
+        cuda_ok(cudaEventRecord(D.ev_packed[D.parity], D.stream), "event");
+        D.packed_recorded[D.parity] = true;
+        D.parity ^= 1;
+        D.fresh_iteration = true;
+    }
     std::vector<std::size_t> done;
     while (chunks_reported_ < num_chunks_ &&
            chunk_begin(chunks_reported_) + chunk_length(chunks_reported_) <= watermark_) {
@@ -158,10 +237,25 @@ std::vector<std::size_t> GradientPool::write_tensor(int tensor_id, std::span<con
     return done;
 }
 
+void GradientPool::read_averaged(std::span<float> out, int world, bool wait) {
+    if (out.size() != total_elements_) throw ConfigError("read_averaged: output does not match the pool layout");
+    if (world < 1) throw ConfigError("read_averaged: world must be >= 1");
+    run_pending_work();
+    OnDevice g(device_);
+    Device& D = *dev_;
+    float* avg = D.averaged(total_elements_);
+    const std::uint64_t off = 0, cnt = total_elements_;
+    check(gf_unpack(static_cast<int>(element_type_), data_, &avg, &off, &cnt, 1, world, D.stream), "read_averaged");
+    cuda_ok(cudaMemcpyAsync(out.data(), avg, total_elements_ * 4, cudaMemcpyDeviceToHost, D.stream), "D2H g_avg");
+    if (wait || locate(out.data()) != Where::kPinned) cuda_ok(cudaStreamSynchronize(D.stream), "read_averaged");
+}
+
 void GradientPool::sync_host() {
     if (host_valid_) return;
+    synchronize();
     OnDevice g(device_);
-    cuda_ok(cudaMemcpy(host_.data(), data_, host_.size(), cudaMemcpyDeviceToHost), "pool D2H");
+    cuda_ok(cudaMemcpyAsync(host_.data(), data_, host_.size(), cudaMemcpyDeviceToHost, dev_->stream), "pool D2H");
+    cuda_ok(cudaStreamSynchronize(dev_->stream), "pool D2H");
     host_valid_ = true;
 }
 
@@ -177,19 +271,23 @@ void GradientPool::set(std::size_t i, float v) {
     h.set(i, v);
     const std::size_t es = element_size(element_type_);
     OnDevice g(device_);
-    cuda_ok(cudaMemcpy(data_ + i * es, host_.data() + i * es, es, cudaMemcpyHostToDevice), "pool set");
+    cuda_ok(cudaMemcpyAsync(data_ + i * es, host_.data() + i * es, es, cudaMemcpyHostToDevice, dev_->stream),
+            "pool set");
+    cuda_ok(cudaStreamSynchronize(dev_->stream), "pool set");
 }
 
 float GradientPool::chunk_l1(std::size_t c) {
     const std::size_t b = chunk_begin(c), len = chunk_length(c);
+    run_pending_work();
     OnDevice g(device_);
+    Device& D = *dev_;
     // one-chunk launch of K3 (exact; bit-identical to the reference's fp64 loop)
     check(gf_chunk_norms(static_cast<int>(element_type_), data_ + b * element_size(element_type_), len, len, 1,
-                         nullptr, 1, norm_out_, nullptr),
+                         nullptr, 1, D.norm_out, D.stream),
           "chunk_l1");
-    float out = 0.0f;
-    cuda_ok(cudaMemcpy(&out, norm_out_, sizeof(float), cudaMemcpyDeviceToHost), "chunk_l1 D2H");
-    return out;
+    cuda_ok(cudaMemcpyAsync(D.norm_host, D.norm_out, sizeof(float), cudaMemcpyDeviceToHost, D.stream), "D2H");
+    cuda_ok(cudaStreamSynchronize(D.stream), "chunk_l1");
+    return *D.norm_host;
 }
 
 void GradientPool::dump_snapshot(std::ostream& os) {

@@ -1,5 +1,6 @@
 // SPDX-License-Identifier: Apache-2.0
-// Coarse-grained sparse communication on the GPU (reference: src/sparse.cpp).
+// Coarse-grained sparse communication on the GPU (reference: src/sparse.cpp). Device work is
+// ordered on the pool's stream; see gflow/sparse.hpp for where the host waits.
 #include "gflow/sparse.hpp"
 
 #include <cuda_runtime.h>
@@ -18,10 +19,10 @@ void cuda_ok(cudaError_t e, const char* what) {
 }
 
 template <typename T>
-T* dalloc(std::size_t n) {
+T* dalloc(std::size_t n, cudaStream_t s) {
     T* p = nullptr;
     cuda_ok(cudaMalloc(&p, std::max<std::size_t>(n * sizeof(T), 16)), "cudaMalloc");
-    cuda_ok(cudaMemset(p, 0, std::max<std::size_t>(n * sizeof(T), 16)), "cudaMemset");
+    cuda_ok(cudaMemsetAsync(p, 0, std::max<std::size_t>(n * sizeof(T), 16), s), "cudaMemset");
     return p;
 }
 
@@ -67,27 +68,62 @@ SparseState::SparseState(GradientPool& pool, SparseConfig config) : pool_(pool),
     next_important_.assign(nc, 1);
     corrected_.assign(nc, 0);
     OnDevice g(pool_.device());
-    d_hg_ = dalloc<float>(total);
-    d_hu_ = dalloc<float>(total);
-    d_imp_ = dalloc<std::uint8_t>(nc);
-    d_coff_ = dalloc<std::uint64_t>(nc);
-    d_plan_ = dalloc<std::uint64_t>(4 + nc);
-    d_staging_ = dalloc<std::byte>(total * element_size(pool_.element_type()));
-    d_norms_ = dalloc<float>(nc);
+    const auto ps = static_cast<cudaStream_t>(pool_.stream());
+    d_hg_ = dalloc<float>(total, ps);
+    d_hu_ = dalloc<float>(total, ps);
+    d_imp_ = dalloc<std::uint8_t>(nc, ps);
+    d_coff_ = dalloc<std::uint64_t>(nc, ps);
+    d_plan_ = dalloc<std::uint64_t>(4 + nc, ps);
+    d_staging_ = dalloc<std::byte>(total * element_size(pool_.element_type()), ps);
+    d_norms_ = dalloc<float>(nc, ps);
+    cuda_ok(cudaMallocHost(&h_imp_, nc), "cudaMallocHost");
+    cuda_ok(cudaMallocHost(&h_coff_, nc * 8), "cudaMallocHost");
+    cuda_ok(cudaMallocHost(&h_plan_, (4 + nc) * 8), "cudaMallocHost");
+    cuda_ok(cudaStreamSynchronize(ps), "sparse state init");
+    pool_.set_pending_work([this] { flush_corrections(); });
 }
 
 SparseState::~SparseState() {
+    pool_.set_pending_work(nullptr);
     OnDevice g(pool_.device());
-    cudaDeviceSynchronize();
+    cudaStreamSynchronize(static_cast<cudaStream_t>(pool_.stream()));
     for (void* p : {static_cast<void*>(d_hg_), static_cast<void*>(d_hu_), static_cast<void*>(d_imp_),
                     static_cast<void*>(d_coff_), static_cast<void*>(d_plan_), static_cast<void*>(d_staging_),
                     static_cast<void*>(d_norms_), static_cast<void*>(d_w_)})
-        cudaFree(p);
+        if (p) cudaFree(p);
+    for (void* p : {static_cast<void*>(h_imp_), static_cast<void*>(h_coff_), static_cast<void*>(h_plan_)})
+        if (p) cudaFreeHost(p);
 }
 
+// The pinned control arrays are reused every iteration: earlier copies out of them have
+// completed by the time they are rewritten (the iteration's host-visible results synchronise
+// the pool stream), and a stream sync guards the rare early reuse.
 void SparseState::upload_important() {
     OnDevice g(pool_.device());
-    cuda_ok(cudaMemcpy(d_imp_, important_.data(), important_.size(), cudaMemcpyHostToDevice), "H2D flags");
+    const auto ps = static_cast<cudaStream_t>(pool_.stream());
+    cuda_ok(cudaStreamSynchronize(ps), "pool stream");
+    std::memcpy(h_imp_, important_.data(), important_.size());
+    cuda_ok(cudaMemcpyAsync(d_imp_, h_imp_, important_.size(), cudaMemcpyHostToDevice, ps), "H2D flags");
+}
+
+// plan[0] staged elements, plan[1] chunk count, plan[4..] the chunks in the given (queue)
+// order; coff[c] = staging offset of chunk c (sparse.cpp:129-140)
+void SparseState::upload_plan(const std::vector<std::size_t>& chunks, bool with_coff) {
+    const std::size_t nc = pool_.num_chunks();
+    OnDevice g(pool_.device());
+    const auto ps = static_cast<cudaStream_t>(pool_.stream());
+    cuda_ok(cudaStreamSynchronize(ps), "pool stream");
+    std::uint64_t staged = 0;
+    for (std::size_t j = 0; j < chunks.size(); ++j) {
+        if (with_coff) h_coff_[chunks[j]] = staged;
+        h_plan_[4 + j] = chunks[j];
+        staged += pool_.chunk_length(chunks[j]);
+    }
+    h_plan_[0] = staged;
+    h_plan_[1] = chunks.size();
+    h_plan_[2] = h_plan_[3] = 0;
+    cuda_ok(cudaMemcpyAsync(d_plan_, h_plan_, (4 + chunks.size()) * 8, cudaMemcpyHostToDevice, ps), "H2D plan");
+    if (with_coff) cuda_ok(cudaMemcpyAsync(d_coff_, h_coff_, nc * 8, cudaMemcpyHostToDevice, ps), "H2D coff");
 }
 
 void SparseState::begin_iteration(std::uint64_t t) {
@@ -97,8 +133,19 @@ void SparseState::begin_iteration(std::uint64_t t) {
     else std::fill(important_.begin(), important_.end(), 1);  // iteration 0 is dense
     queued_.clear();
     std::fill(corrected_.begin(), corrected_.end(), 0);
+    run_lo_ = run_hi_ = 0;
     exchanged_ = false;
     upload_important();
+}
+
+void SparseState::flush_corrections() {
+    if (run_hi_ == run_lo_) return;
+    OnDevice g(pool_.device());
+    check(gf_csc_correct(static_cast<int>(pool_.element_type()), pool_.device_data(), d_hg_, d_imp_,
+                         pool_.total_elements(), pool_.chunk_size(), pool_.num_chunks(), run_lo_, run_hi_ - run_lo_,
+                         static_cast<float>(config_.momentum), pool_.stream()),
+          "correction_pre_allreduce");
+    run_lo_ = run_hi_ = 0;
 }
 
 void SparseState::correction_pre_allreduce(std::size_t c) {
@@ -108,11 +155,14 @@ void SparseState::correction_pre_allreduce(std::size_t c) {
         throw ConfigError("correction on incomplete chunk " + std::to_string(c));
     if (corrected_[c]) throw ConfigError("chunk " + std::to_string(c) + " corrected twice");
     corrected_[c] = 1;
-    OnDevice g(pool_.device());
-    check(gf_csc_correct(static_cast<int>(pool_.element_type()), pool_.device_data(), d_hg_, d_imp_,
-                         pool_.total_elements(), pool_.chunk_size(), pool_.num_chunks(), c, 1,
-                         static_cast<float>(config_.momentum), nullptr),
-          "correction_pre_allreduce");
+    // consecutive chunks (the watermark's order) join one pending K2 launch
+    if (run_hi_ > run_lo_ && c == run_hi_) {
+        ++run_hi_;
+    } else {
+        flush_corrections();
+        run_lo_ = c;
+        run_hi_ = c + 1;
+    }
     pool_.invalidate_host();
     if (important_[c]) queued_.push_back(c);
 }
@@ -137,6 +187,19 @@ std::uint64_t SparseState::checksum() const {
     return h;
 }
 
+void SparseState::device_allreduce(Communicator& comm, std::vector<void*>& ranks, std::byte* buf, ElementType type,
+                                   std::size_t length, const std::vector<std::pair<std::size_t, std::size_t>>& windows,
+                                   std::uint32_t phase) {
+    DeviceContext& ctx = comm.device();
+    if (ranks.empty()) {  // first use: every rank registers this buffer at the same call
+        pool_.synchronize();
+        ranks = ctx.exchange(buf, (comm.acquire_collective_id() << 8) | phase);
+    }
+    (void)length;
+    ctx.ring_allreduce_async(type, ranks, comm.ring_order(), windows, pool_.stream());
+    detail::record_ring_payload(comm, type, windows, "ring");
+}
+
 void SparseState::sparse_exchange(Communicator& comm, FusionEngine& engine) {
     if (exchanged_) throw ConfigError("sparse_exchange called twice in one iteration");
     // every rank must hold the same important set before gradients move (sparse.cpp:109-127)
@@ -156,45 +219,43 @@ void SparseState::sparse_exchange(Communicator& comm, FusionEngine& engine) {
                 throw ProtocolError("important-set divergence at rank " + std::to_string(comm.rank()));
         }
     }
-    // staging layout: queued chunks in queue order (sparse.cpp:129-140)
+    flush_corrections();
     const std::size_t nc = pool_.num_chunks(), esz = element_size(pool_.element_type());
-    std::vector<std::uint64_t> coff(nc, 0), plan(4 + nc, 0);
-    std::uint64_t total = 0;
-    for (std::size_t j = 0; j < queued_.size(); ++j) {
-        coff[queued_[j]] = total;
-        plan[4 + j] = queued_[j];
-        total += pool_.chunk_length(queued_[j]);
-    }
-    plan[0] = total;
-    plan[1] = queued_.size();
-    OnDevice g(pool_.device());
-    cuda_ok(cudaMemcpy(d_coff_, coff.data(), nc * 8, cudaMemcpyHostToDevice), "H2D coff");
-    cuda_ok(cudaMemcpy(d_plan_, plan.data(), (4 + nc) * 8, cudaMemcpyHostToDevice), "H2D plan");
     const int dt = static_cast<int>(pool_.element_type());
+    OnDevice g(pool_.device());
+    // staging layout: the queued chunks in queue order (sparse.cpp:129-140)
+    upload_plan(queued_, true);
     check(gf_csc_compact(dt, pool_.device_data(), d_staging_, d_plan_, d_coff_, pool_.total_elements(),
-                         pool_.chunk_size(), nc, queued_.size(), nullptr),
+                         pool_.chunk_size(), nc, queued_.size(), pool_.stream()),
           "sparse_exchange compact");
-    cuda_ok(cudaDeviceSynchronize(), "compact");
-    // theta windows over the staging buffer (sparse.cpp:142-158)
-    ScalarBuffer stage{pool_.element_type(), d_staging_, total, Residency::kDevice};
+    // theta windows over the staging buffer (sparse.cpp:142-158), all reduced in one launch
     const std::uint64_t theta = engine.config().threshold_bytes;
-    std::vector<FusedHandle> handles;
+    std::vector<std::pair<std::size_t, std::size_t>> windows;
     std::size_t ws = 0, pos = 0;
     for (std::size_t c : queued_) {
         pos += pool_.chunk_length(c);
         if (theta != kThetaInfinite && (pos - ws) * esz >= theta) {
-            handles.push_back(engine.enqueue_collective(stage.subspan(ws, pos - ws)));
+            windows.emplace_back(ws, pos - ws);
             ws = pos;
         }
     }
-    if (pos > ws) handles.push_back(engine.enqueue_collective(stage.subspan(ws, pos - ws)));
-    last_exchange_windows_ = handles.size();
-    FusionEngine::wait_all(handles);
+    if (pos > ws) windows.emplace_back(ws, pos - ws);
+    last_exchange_windows_ = windows.size();
+    if (comm.world_size() > 1 && !windows.empty()) {
+        if (engine.config().algorithm == Algo::kRing && comm.device().async_collectives()) {
+            device_allreduce(comm, stage_ranks_, d_staging_, pool_.element_type(), pos, windows, 0x21u);
+        } else {  // colocated ranks / rooted algorithms: the engine's synchronous collectives
+            pool_.synchronize();
+            ScalarBuffer stage{pool_.element_type(), d_staging_, pos, Residency::kDevice};
+            std::vector<FusedHandle> handles;
+            for (auto& w : windows) handles.push_back(engine.enqueue_collective(stage.subspan(w.first, w.second)));
+            FusionEngine::wait_all(handles);
+        }
+    }
     // global sums back into the pool (sparse.cpp:162-168)
     check(gf_csc_scatter(dt, pool_.device_data(), d_staging_, d_plan_, d_coff_, pool_.total_elements(),
-                         pool_.chunk_size(), nc, queued_.size(), nullptr, nullptr),
+                         pool_.chunk_size(), nc, queued_.size(), nullptr, pool_.stream()),
           "sparse_exchange write-back");
-    cuda_ok(cudaDeviceSynchronize(), "write-back");
     pool_.invalidate_host();
     exchanged_ = true;
 }
@@ -203,17 +264,28 @@ const std::vector<std::uint8_t>& SparseState::select_next_important(Communicator
     if (!exchanged_) throw ConfigError("select_next_important before sparse_exchange");
     const std::size_t nc = pool_.num_chunks();
     OnDevice g(pool_.device());
+    const auto ps = static_cast<cudaStream_t>(pool_.stream());
     // exact chunk L1 (K3), x1/N on important chunks (sparse.cpp:176-184)
     check(gf_chunk_norms(static_cast<int>(pool_.element_type()), pool_.device_data(), pool_.total_elements(),
-                         pool_.chunk_size(), nc, d_imp_, comm.world_size(), d_norms_, nullptr),
+                         pool_.chunk_size(), nc, d_imp_, comm.world_size(), d_norms_, ps),
           "chunk norms");
-    cuda_ok(cudaDeviceSynchronize(), "chunk norms");
     // fp32 ring allreduce of the norms (sparse.cpp:185-187), on the NVLink ring
-    ring_allreduce(comm, ScalarBuffer{ElementType::kF32, reinterpret_cast<std::byte*>(d_norms_), nc,
-                                      Residency::kDevice});
+    if (comm.world_size() > 1) {
+        if (comm.device().async_collectives()) {
+            device_allreduce(comm, norm_ranks_, reinterpret_cast<std::byte*>(d_norms_), ElementType::kF32, nc,
+                             {{0, nc}}, 0x22u);
+        } else {
+            pool_.synchronize();
+            ring_allreduce(comm, ScalarBuffer{ElementType::kF32, reinterpret_cast<std::byte*>(d_norms_), nc,
+                                              Residency::kDevice});
+        }
+    }
     const std::size_t k = selection_count(sparsity_at(t + 1, config_.warmup_iters, config_.final_sparsity), nc);
-    check(gf_select_topk(d_norms_, nc, k, d_imp_, nullptr), "select");  // d_imp_ reloaded next iteration
-    cuda_ok(cudaMemcpy(next_important_.data(), d_imp_, nc, cudaMemcpyDeviceToHost), "D2H selection");
+    check(gf_select_topk(d_norms_, nc, k, d_imp_, ps), "select");  // d_imp_ reloaded below
+    cuda_ok(cudaMemcpyAsync(h_imp_, d_imp_, nc, cudaMemcpyDeviceToHost, ps), "D2H selection");
+    cuda_ok(cudaStreamSynchronize(ps), "select");
+    if (comm.world_size() > 1 && comm.device().comm()) check(gf_comm_status(comm.device().comm()), "select");
+    next_important_.assign(h_imp_, h_imp_ + nc);
     upload_important();  // d_imp_ keeps THIS iteration's set for sgd_update
     has_selection_ = true;
     return next_important_;
@@ -221,41 +293,58 @@ const std::vector<std::uint8_t>& SparseState::select_next_important(Communicator
 
 void SparseState::sgd_update(std::span<float> weights, int world_size) {
     if (weights.size() != pool_.total_elements()) throw ConfigError("weight vector does not match pool layout");
-    const std::size_t nc = pool_.num_chunks(), total = pool_.total_elements();
+    flush_corrections();
+    const std::size_t nc = pool_.num_chunks(), total = pool_.total_elements(), chunk = pool_.chunk_size();
     OnDevice g(pool_.device());
-    // plan of the current important set (all of its chunks, ascending)
-    std::vector<std::uint64_t> plan(4 + nc, 0);
-    std::uint64_t k = 0;
+    const auto ps = static_cast<cudaStream_t>(pool_.stream());
+    std::vector<std::size_t> imp;  // the current important set, ascending
     for (std::size_t c = 0; c < nc; ++c)
-        if (important_[c]) plan[4 + k++] = c;
-    plan[1] = k;
-    cuda_ok(cudaMemcpy(d_plan_, plan.data(), (4 + nc) * 8, cudaMemcpyHostToDevice), "H2D plan");
+        if (important_[c]) imp.push_back(c);
+    upload_plan(imp, false);
     float* w = weights.data();
     const bool host = !is_device_ptr(w);
+    // runs of consecutive important chunks: the only part of w the update touches
+    std::vector<std::pair<std::size_t, std::size_t>> runs;
+    for (std::size_t c : imp) {
+        const std::size_t b = c * chunk, e = b + pool_.chunk_length(c);
+        if (!runs.empty() && runs.back().second == b) runs.back().second = e;
+        else runs.emplace_back(b, e);
+    }
     if (host) {
-        if (!d_w_) d_w_ = dalloc<float>(total);
-        cuda_ok(cudaMemcpy(d_w_, w, total * 4, cudaMemcpyHostToDevice), "H2D weights");
+        if (!d_w_) d_w_ = dalloc<float>(total, ps);
+        for (auto& r : runs)
+            cuda_ok(cudaMemcpyAsync(d_w_ + r.first, w + r.first, (r.second - r.first) * 4, cudaMemcpyHostToDevice, ps),
+                    "H2D weights");
         w = d_w_;
     }
-    check(gf_csc_sgd_update(static_cast<int>(pool_.element_type()), pool_.device_data(), d_plan_, total,
-                            pool_.chunk_size(), nc, k, world_size, static_cast<float>(config_.momentum),
-                            static_cast<float>(config_.learning_rate), d_hu_, w, nullptr),
+    check(gf_csc_sgd_update(static_cast<int>(pool_.element_type()), pool_.device_data(), d_plan_, total, chunk, nc,
+                            imp.size(), world_size, static_cast<float>(config_.momentum),
+                            static_cast<float>(config_.learning_rate), d_hu_, w, ps),
           "sgd_update");
-    if (host) cuda_ok(cudaMemcpy(weights.data(), d_w_, total * 4, cudaMemcpyDeviceToHost), "D2H weights");
-    else cuda_ok(cudaDeviceSynchronize(), "sgd_update");
+    if (host)
+        for (auto& r : runs)
+            cuda_ok(cudaMemcpyAsync(weights.data() + r.first, d_w_ + r.first, (r.second - r.first) * 4,
+                                    cudaMemcpyDeviceToHost, ps),
+                    "D2H weights");
+    cuda_ok(cudaStreamSynchronize(ps), "sgd_update");
 }
 
 std::span<const float> SparseState::hg() const {
+    const_cast<SparseState*>(this)->flush_corrections();
     OnDevice g(pool_.device());
+    const auto ps = static_cast<cudaStream_t>(pool_.stream());
     hg_host_.resize(pool_.total_elements());
-    cuda_ok(cudaMemcpy(hg_host_.data(), d_hg_, hg_host_.size() * 4, cudaMemcpyDeviceToHost), "D2H hg");
+    cuda_ok(cudaMemcpyAsync(hg_host_.data(), d_hg_, hg_host_.size() * 4, cudaMemcpyDeviceToHost, ps), "D2H hg");
+    cuda_ok(cudaStreamSynchronize(ps), "D2H hg");
     return hg_host_;
 }
 
 std::span<const float> SparseState::hu() const {
     OnDevice g(pool_.device());
+    const auto ps = static_cast<cudaStream_t>(pool_.stream());
     hu_host_.resize(pool_.total_elements());
-    cuda_ok(cudaMemcpy(hu_host_.data(), d_hu_, hu_host_.size() * 4, cudaMemcpyDeviceToHost), "D2H hu");
+    cuda_ok(cudaMemcpyAsync(hu_host_.data(), d_hu_, hu_host_.size() * 4, cudaMemcpyDeviceToHost, ps), "D2H hu");
+    cuda_ok(cudaStreamSynchronize(ps), "D2H hu");
     return hu_host_;
 }
 

@@ -80,6 +80,11 @@ Segment segment_of(std::size_t length, int n, int i);
 void ring_allreduce_windows(Communicator& comm, ScalarBuffer buf,
                             const std::vector<std::pair<std::size_t, std::size_t>>& windows,
                             const std::string& label = "ring");
+// TrafficStats of the reference ring for these windows (collectives.cpp:69-96): 2(N-1)
+// segment_of transfers per window at this rank's ring position.
+void record_ring_payload(Communicator& comm, ElementType type,
+                         const std::vector<std::pair<std::size_t, std::size_t>>& windows,
+                         const std::string& label = "ring");
 }  // namespace detail
 
 }  // namespace gflow

@@ -62,6 +62,21 @@ public:
     // Device scratch of at least `bytes` on this GPU (grown on demand, kept).
     void* scratch(std::size_t bytes, int slot = 0);
 
+    // The rank's collective stream (a cudaStream_t, non-blocking): every device collective of
+    // this context is enqueued on it, FIFO — the NVLink kernels' per-CTA epoch protocol needs
+    // one collective at a time per communicator.
+    void* stream() const { return stream_; }
+    // True when collectives can be enqueued without a host rendezvous (peer-mapped ranks on
+    // distinct GPUs); colocated ranks run each collective as one host-orchestrated launch.
+    bool async_collectives() const { return mode_ == Mode::kLocal || mode_ == Mode::kIpc; }
+    // Enqueue the ring allreduce of `windows` (element ranges) over rank_bufs (each rank's
+    // buffer as mapped here, 16-byte aligned, from exchange()) on stream(); no host wait.
+    // With `client` (a cudaStream_t) the collective is ordered after the client stream's queued
+    // work and the client stream after the collective (CUDA events both ways).
+    void ring_allreduce_async(ElementType type, const std::vector<void*>& rank_bufs, const std::vector<int>& ring,
+                              const std::vector<std::pair<std::size_t, std::size_t>>& windows,
+                              void* client = nullptr);
+
 private:
     Transport& tp_;
     int rank_, world_, device_ = 0;
@@ -70,6 +85,9 @@ private:
     std::shared_ptr<ColocatedGroup> group_;
     std::map<std::string, void*> ipc_cache_;  // peer handle bytes -> mapped base
     std::vector<std::pair<void*, std::size_t>> scratch_;
+    void* stream_ = nullptr;
+    void* ev_client_ = nullptr;  // client stream -> collective stream
+    void* ev_done_ = nullptr;    // collective stream -> client stream
     std::mutex mu_;
 };
 

@@ -22,61 +22,9 @@
 #include <vector>
 
 #include "ring_device.cuh"
+#include "step_table.cuh"
 
 namespace {
-
-constexpr int kStepMaxT = 256;
-struct StepTable {  // tensors sorted by pool offset
-    int n;
-    int pad;
-    uint64_t off[kStepMaxT];
-    uint64_t cnt[kStepMaxT];
-    const float* src[kStepMaxT];
-    float* dst[kStepMaxT];
-};
-
-// last tensor whose pool range starts at or before element e
-__device__ __forceinline__ int tensor_at(const StepTable& T, uint64_t e) {
-    int lo = 0, hi = T.n;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (T.off[mid] <= e) lo = mid; else hi = mid;
-    }
-    return lo;
-}
-
-// one 16-byte pool vector vv holding x -> fp32 g_avg = x * (1/N) in its tensor(s)
-template <int DT>
-__device__ __forceinline__ void unpack_vec(const StepTable& T, uint64_t vv, uint4 x, float inv) {
-    constexpr int VE = Vec<DT>::kElems;
-    const uint64_t e = vv * VE;
-    int t = tensor_at(T, e);
-    float* d = T.dst[t] + (e - T.off[t]);
-    const bool whole = e + VE <= T.off[t] + T.cnt[t];
-    if (DT == GF_F16 && whole && (reinterpret_cast<uintptr_t>(d) & 31u) == 0 && !gfd::any_special(x)) {
-        const float2 f0 = gfd::h2f2(x.x), f1 = gfd::h2f2(x.y);
-        const float2 f2 = gfd::h2f2(x.z), f3 = gfd::h2f2(x.w);
-        gfd::st32f_stream(d,  // STG.E.256; finite halves: x * (1/N) cannot produce NaN
-                          make_float4(__fmul_rn(f0.x, inv), __fmul_rn(f0.y, inv), __fmul_rn(f1.x, inv),
-                                      __fmul_rn(f1.y, inv)),
-                          make_float4(__fmul_rn(f2.x, inv), __fmul_rn(f2.y, inv), __fmul_rn(f3.x, inv),
-                                      __fmul_rn(f3.y, inv)));
-    } else if (DT == GF_F32 && whole && (reinterpret_cast<uintptr_t>(d) & 15u) == 0) {
-        const float4 f = *reinterpret_cast<const float4*>(&x);
-        __stcs(reinterpret_cast<float4*>(d), make_float4(gfd::mul(f.x, inv), gfd::mul(f.y, inv),
-                                                        gfd::mul(f.z, inv), gfd::mul(f.w, inv)));
-    } else {
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(&x);
-#pragma unroll
-        for (int k = 0; k < VE; ++k) {
-            const uint64_t ek = e + k;
-            while (t + 1 < T.n && T.off[t + 1] <= ek) ++t;
-            const float xv = DT == GF_F16 ? gfd::dec(uint16_t((w[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu))
-                                          : gfd::u2f(w[k]);
-            T.dst[t][ek - T.off[t]] = gfd::mul(xv, inv);
-        }
-    }
-}
 
 // ---- gf_ring_allreduce_unpack: pull reduce-scatter, then pull all-gather fused with unpack ----
 // The rank at ring position p sums segment p of every window from all N pools in ring order
@@ -85,15 +33,6 @@ __device__ __forceinline__ void unpack_vec(const StepTable& T, uint64_t vv, uint
 // segment from the rank that owns it, writes it into its pool (every pool ends holding the
 // sums, as after ring_allreduce) and unpacks it. Nothing is pushed, so no barrier waits for
 // posted NVLink writes to drain; and the separate unpack pass (re-reading the pool) is gone.
-template <int DT>
-__device__ __forceinline__ uint4 ld16_cg(const void* p) {  // L2 only: a peer wrote it this launch
-    uint4 v;
-    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
-    return v;
-}
-
 // Scalar reduce (or copy) + unpack of pool element e by the edge CTA.
 template <int DT, bool OWN>
 __device__ __forceinline__ void pull_elem(const StepTable& T, const char* const* src, int n, char* local,
@@ -185,7 +124,8 @@ __device__ void pull_flat(const RingArgs& a, const StepTable& T, const char* con
 
 template <int DT, int NT>
 __global__ void __launch_bounds__(kRingThreads)
-rsag_kernel(const __grid_constant__ RingArgs a, const __grid_constant__ StepTable T, float inv, int exit_barrier) {
+rsag_kernel(const __grid_constant__ RingArgs a, const __grid_constant__ StepTable T, float inv, int exit_barrier,
+            const char* __restrict__ inbox, uint64_t slot_bytes) {
     constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
     __shared__ int s_ok;
     const uint64_t epoch = a.epochs[blockIdx.x];
@@ -200,9 +140,16 @@ rsag_kernel(const __grid_constant__ RingArgs a, const __grid_constant__ StepTabl
     flat_build<VE>(a, n, a.pos, flat);  // my segment of every window
     if (!cross_barrier(a, epoch + 1, &s_ok, false)) return;  // peers' pools are packed
     if (tr) a.trace[1] = gfd::globaltimer_ns();
+    // reduce-scatter operands in ring order from my position: pulled from the peers' pools, or
+    // (inbox != null, the push form) my pool + my inbox slots, where the peers' routed packs
+    // stored them: slot s holds position pos+1+s (gf_sync_step_dense_push)
     const char* src[NMAX];
 #pragma unroll
-    for (int t = 0; t < NMAX; ++t) src[t] = (t < n) ? a.bufs[a.ring[(a.pos + t) % n]] : nullptr;
+    for (int t = 0; t < NMAX; ++t) {
+        if (t >= n) src[t] = nullptr;
+        else if (inbox) src[t] = t == 0 ? a.bufs[a.rank] : inbox + uint64_t(t - 1) * slot_bytes;
+        else src[t] = a.bufs[a.ring[(a.pos + t) % n]];
+    }
     char* local = a.bufs[a.rank];
     pull_flat<DT, NT, true>(a, T, src, n, local, flat, g, S, inv);
     if (tr) a.trace[2] = gfd::globaltimer_ns();
@@ -223,55 +170,62 @@ rsag_kernel(const __grid_constant__ RingArgs a, const __grid_constant__ StepTabl
 }
 
 template <int DT>
-void launch_rsag(const RingArgs& a, const StepTable& T, float inv, int exit_barrier, int grid, cudaStream_t s) {
+void launch_rsag(const RingArgs& a, const StepTable& T, float inv, int exit_barrier, const char* inbox,
+                 uint64_t slot_bytes, int grid, cudaStream_t s) {
     switch (a.world) {
-        case 2: rsag_kernel<DT, 2><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier); break;
-        case 4: rsag_kernel<DT, 4><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier); break;
-        case 8: rsag_kernel<DT, 8><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier); break;
-        default: rsag_kernel<DT, 0><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier); break;
+        case 2: rsag_kernel<DT, 2><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier, inbox, slot_bytes); break;
+        case 3: rsag_kernel<DT, 3><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier, inbox, slot_bytes); break;
+        case 4: rsag_kernel<DT, 4><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier, inbox, slot_bytes); break;
+        case 8: rsag_kernel<DT, 8><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier, inbox, slot_bytes); break;
+        default: rsag_kernel<DT, 0><<<grid, kRingThreads, 0, s>>>(a, T, inv, exit_barrier, inbox, slot_bytes); break;
     }
 }
 
 // tensor table in pool order; checks the tensors tile [off[0], hi) without overlap
-int build_table(const char* fn, const float* const* src, float* const* dst, const uint64_t* pool_off,
-                const uint64_t* count, int ntensors, StepTable& T, uint64_t& hi) {
-    std::vector<int> order(static_cast<size_t>(ntensors));
-    std::iota(order.begin(), order.end(), 0);
-    std::sort(order.begin(), order.end(), [&](int x, int y) { return pool_off[x] < pool_off[y]; });
-    std::memset(&T, 0, sizeof(T));
-    T.n = ntensors;
-    hi = 0;
-    for (int i = 0; i < ntensors; ++i) {
-        const int k = order[static_cast<size_t>(i)];
-        T.off[i] = pool_off[k];
-        T.cnt[i] = count[k];
-        T.src[i] = src ? src[k] : nullptr;
-        T.dst[i] = dst[k];
-        if ((src && !src[k]) || !dst[k]) return gfi::fail(GF_ERR_CONFIG, std::string(fn) + ": null tensor");
-        if (i > 0 && T.off[i] < T.off[i - 1] + T.cnt[i - 1])
-            return gfi::fail(GF_ERR_CONFIG, std::string(fn) + ": tensors overlap in the pool");
-        hi = std::max(hi, T.off[i] + T.cnt[i]);
-    }
-    return GF_OK;
-}
-
-// the tensors and the windows must tile the same pool range: every element is reduced and
-// unpacked exactly once
-int check_tiling(const char* fn, const StepTable& T, uint64_t hi, const uint64_t* win_start,
-                 const uint64_t* win_len, int nwin) {
-    for (int i = 0; i + 1 < T.n; ++i)
-        if (T.off[i] + T.cnt[i] != T.off[i + 1])
-            return gfi::fail(GF_ERR_CONFIG, std::string(fn) + ": tensors must tile the pool");
-    uint64_t cover = T.off[0];
-    for (int w = 0; w < nwin; ++w) {
-        if (win_start[w] != cover) return gfi::fail(GF_ERR_CONFIG, std::string(fn) + ": windows must tile the pool");
-        cover += win_len[w];
-    }
-    if (cover != hi) return gfi::fail(GF_ERR_CONFIG, std::string(fn) + ": windows must tile the pool");
-    return GF_OK;
-}
-
 }  // namespace
+
+namespace gfr {
+
+int rsag_launch(gf_comm* c, int dtype, uint64_t pool_heap_off, const char* inbox, uint64_t slot_bytes,
+                float* const* dst, const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                const uint64_t* win_start, const uint64_t* win_len, int nwin, int flags, void* stream,
+                const char* fn) {
+    if (!gfi::valid_dtype(dtype) || ntensors < 1 || ntensors > kStepMaxT || !dst || !pool_off || !count ||
+        nwin < 1 || !win_start || !win_len || (flags & ~GF_RSAG_NO_EXIT_BARRIER))
+        return gfi::fail(GF_ERR_CONFIG, std::string(fn) + ": bad arguments (1..256 tensors, >= 1 window)");
+    StepTable T;
+    uint64_t hi = 0;
+    if (int rc = build_table(fn, nullptr, dst, pool_off, count, ntensors, T, hi)) return rc;
+    const uint64_t es = gfi::esz(dtype);
+    if (pool_heap_off + hi * es > c->heap_bytes)
+        return gfi::fail(GF_ERR_CONFIG, std::string(fn) + ": pool outside the symmetric heap");
+    if (int rc = check_tiling(fn, T, hi, win_start, win_len, nwin)) return rc;
+    DeviceGuard guard(c->device);
+    if (c->world == 1)  // the collective is the identity (collectives.cpp:59)
+        return gf_unpack(dtype, c->alloc + kFlagBytes + pool_heap_off, dst, pool_off, count, ntensors, 1, stream);
+    const float inv = 1.0f / static_cast<float>(c->world);
+    const int exit_barrier = (flags & GF_RSAG_NO_EXIT_BARRIER) ? 0 : 1;
+    for (int first = 0; first < nwin; first += kMaxW) {
+        RingArgs a;
+        std::memset(&a, 0, sizeof(a));
+        a.nwin = std::min(kMaxW, nwin - first);
+        uint64_t max_seg = 0;
+        for (int w = 0; w < a.nwin; ++w) {
+            a.wstart[w] = win_start[first + w];
+            a.wlen[w] = win_len[first + w];
+            max_seg += (a.wlen[w] + c->world - 1) / c->world;
+        }
+        fill_common(c, a, pool_heap_off);
+        const int grid = gfr::comm_blocks(c, max_seg * es);
+        if (dtype == GF_F16) launch_rsag<GF_F16>(a, T, inv, exit_barrier, inbox, slot_bytes, grid, gfi::S(stream));
+        else launch_rsag<GF_F32>(a, T, inv, exit_barrier, inbox, slot_bytes, grid, gfi::S(stream));
+        gfi::count_launch();
+        if (int rc = gfi::check_launch(fn)) return rc;
+    }
+    return GF_OK;
+}
+
+}  // namespace gfr
 
 extern "C" {
 
@@ -301,41 +255,9 @@ int gf_ring_allreduce_unpack(gf_comm* c, int dtype, uint64_t pool_heap_off, floa
                              const uint64_t* pool_off, const uint64_t* count, int ntensors,
                              const uint64_t* win_start, const uint64_t* win_len, int nwin, int flags,
                              void* stream) {
-    static const char* fn = "gf_ring_allreduce_unpack";
     if (int rc = comm_ready(c)) return rc;
-    if (!gfi::valid_dtype(dtype) || ntensors < 1 || ntensors > kStepMaxT || !dst || !pool_off || !count ||
-        nwin < 1 || !win_start || !win_len || (flags & ~GF_RSAG_NO_EXIT_BARRIER))
-        return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_unpack: bad arguments (1..256 tensors, >= 1 window)");
-    StepTable T;
-    uint64_t hi = 0;
-    if (int rc = build_table(fn, nullptr, dst, pool_off, count, ntensors, T, hi)) return rc;
-    const uint64_t es = gfi::esz(dtype);
-    if (pool_heap_off + hi * es > c->heap_bytes)
-        return gfi::fail(GF_ERR_CONFIG, "gf_ring_allreduce_unpack: pool outside the symmetric heap");
-    if (int rc = check_tiling(fn, T, hi, win_start, win_len, nwin)) return rc;
-    DeviceGuard guard(c->device);
-    if (c->world == 1)  // the collective is the identity (collectives.cpp:59)
-        return gf_unpack(dtype, c->alloc + kFlagBytes + pool_heap_off, dst, pool_off, count, ntensors, 1, stream);
-    const float inv = 1.0f / static_cast<float>(c->world);
-    const int exit_barrier = (flags & GF_RSAG_NO_EXIT_BARRIER) ? 0 : 1;
-    for (int first = 0; first < nwin; first += kMaxW) {
-        RingArgs a;
-        std::memset(&a, 0, sizeof(a));
-        a.nwin = std::min(kMaxW, nwin - first);
-        uint64_t max_seg = 0;
-        for (int w = 0; w < a.nwin; ++w) {
-            a.wstart[w] = win_start[first + w];
-            a.wlen[w] = win_len[first + w];
-            max_seg += (a.wlen[w] + c->world - 1) / c->world;
-        }
-        fill_common(c, a, pool_heap_off);
-        const int grid = gfr::comm_blocks(c, max_seg * es);
-        if (dtype == GF_F16) launch_rsag<GF_F16>(a, T, inv, exit_barrier, grid, gfi::S(stream));
-        else launch_rsag<GF_F32>(a, T, inv, exit_barrier, grid, gfi::S(stream));
-        gfi::count_launch();
-        if (int rc = gfi::check_launch(fn)) return rc;
-    }
-    return GF_OK;
+    return gfr::rsag_launch(c, dtype, pool_heap_off, nullptr, 0, dst, pool_off, count, ntensors, win_start, win_len,
+                            nwin, flags, stream, "gf_ring_allreduce_unpack");
 }
 
 }  // extern "C"

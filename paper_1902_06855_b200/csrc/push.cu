@@ -25,12 +25,13 @@
 #include <vector>
 
 #include "ring_device.cuh"
+#include "step_table.cuh"
 #include "tensor_table.cuh"
 
 namespace {
 
 struct SegMap {  // routing of pool elements to their owners (explicit windows)
-    int nwin, world, pos, pad;
+    int nwin, world, pos, diag;  // diag: GF_PUSH_DIAG timing probe (1: every store local; results invalid)
     uint64_t slot_elems;                 // elements per inbox slot (the pool span)
     char* pool_local;                    // my pool (fp16)
     char* inbox_by_pos[GF_MAX_RANKS];    // owner at ring position j: its inbox as mapped here
@@ -62,7 +63,7 @@ __device__ __forceinline__ int seg_owner(const SegMap& m, uint64_t e, uint64_t& 
 
 // where a packed element of segment owned by position j goes
 __device__ __forceinline__ uint16_t* route(const SegMap& m, int j, uint64_t e) {
-    if (j == m.pos) return reinterpret_cast<uint16_t*>(m.pool_local) + e;
+    if (j == m.pos || m.diag == 1) return reinterpret_cast<uint16_t*>(m.pool_local) + e;
     const int slot = (m.pos - j - 1 + m.world) % m.world;
     return reinterpret_cast<uint16_t*>(m.inbox_by_pos[j]) + uint64_t(slot) * m.slot_elems + e;
 }
@@ -126,6 +127,113 @@ pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ 
     // same ordering the ring relies on for the pack's local stores).
 }
 
+// ---- the routed pack with its stores staged through shared memory and written by TMA -----------
+// Each CTA encodes a tile into a shared-memory stage; one elected thread then issues bulk copies
+// (cp.async.bulk.global.shared::cta) of the tile's pieces to their owners — my pool or a peer's
+// inbox over NVLink. The threads go straight on to the next tile's HBM loads while the copy
+// engine drains the stage, so the NVLink write latency no longer throttles the SM's stores.
+// A vector that straddles a segment boundary is stored element by element (as the register
+// kernel does); the bulk pieces cover the whole vectors of each owner.
+constexpr int kTmaStages = 3;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+pack_push_tma_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ SegMap M, uint64_t total_tiles,
+                     uint64_t spread) {
+    extern __shared__ __align__(128) unsigned char stage_mem[];  // kTmaStages x kTile fp16
+    int it = 0;
+    for (uint64_t i = blockIdx.x; i < total_tiles; i += gridDim.x, ++it) {
+        const uint64_t tile = (i * spread) % total_tiles;
+        const int t = find_tensor(T, tile);
+        const uint64_t base = (tile - T.tiles[t]) * kTile;
+        const uint64_t len = min(kTile, T.cnt[t] - base);
+        const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
+        const uint64_t po = T.off[t] + base;
+        uint16_t* buf = reinterpret_cast<uint16_t*>(stage_mem) + size_t(it % kTmaStages) * kTile;
+        uint64_t done = 0;
+        const bool vec = (reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0 && po % 8 == 0;
+        const int nvec = vec ? int(len / 8) : 0;
+        if (vec) {
+            float4 a[kVecPerThread], b[kVecPerThread];
+#pragma unroll
+            for (int k = 0; k < kVecPerThread; ++k) {
+                const int v = threadIdx.x + k * kThreads;
+                if (v < nvec) {
+                    const gfd::F8 f = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
+                    a[k] = f.lo;
+                    b[k] = f.hi;
+                }
+            }
+            // the stage this tile uses was last read by the bulk copies kTmaStages tiles ago
+            if (it >= kTmaStages && threadIdx.x == 0)
+                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaStages - 1) : "memory");
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < kVecPerThread; ++k) {
+                const int v = threadIdx.x + k * kThreads;
+                if (v < nvec) {
+                    const uint4 h = gfd::enc8(a[k], b[k]);
+                    const uint64_t e = po + 8 * uint64_t(v);
+                    uint64_t end;
+                    const int j = seg_owner(M, e, end);
+                    if (e + 8 <= end) {
+                        *reinterpret_cast<uint4*>(buf + 8 * v) = h;  // bulk-copied below
+                    } else {  // a segment boundary inside the vector: element stores
+                        const uint32_t w[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            put_elem(M, e + q, uint16_t((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu));
+                        (void)j;
+                    }
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                // pieces: maximal runs of whole vectors with one owner
+                const uint64_t hi = po + uint64_t(nvec) * 8;
+                uint64_t cur = po;
+                while (cur < hi) {
+                    uint64_t end;
+                    const int j = seg_owner(M, cur, end);
+                    if (cur + 8 > end) {  // straddling vector: already stored element-wise
+                        cur += 8;
+                        continue;
+                    }
+                    const uint64_t stop = min(hi, po + ((end - po) / 8) * 8);
+                    bulk_s2g(route(M, j, cur), buf + (cur - po), uint32_t((stop - cur) * 2));
+                    cur = stop;
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            done = uint64_t(nvec) * 8;
+        }
+        for (uint64_t q = done + threadIdx.x; q < len; q += kThreads) put_elem(M, po + q, gfd::enc(s[q]));
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // all bulk writes performed
+}
+
+// Routed-pack form: direct register stores (default) or TMA-staged stores (GF_PACK_TMA=1).
+// Measured at N=2 (ResNet-50): 61 us register vs 69 us TMA-staged, and the TMA form takes 64 us
+// even with every store local — its per-tile load -> stage -> bulk-copy sequence is latency-bound
+// at 2 CTAs per SM, where the register kernel keeps 4 CTAs' loads in flight.
+bool pack_tma() {
+    static const bool v = [] {
+        const char* e = std::getenv("GF_PACK_TMA");
+        return e && std::strcmp(e, "1") == 0;
+    }();
+    return v;
+}
+
 // CTAs per SM the routed pack is compiled for (register cap 65536 / (256 * MINB)); 4 measured
 // best so far. GF_PUSH_MINB (4, 6 or 8) is a tuning override.
 int push_minb() {
@@ -138,9 +246,14 @@ int push_minb() {
 }
 
 // All-local reduce of my segments (pool + inbox slots, ring order) pushed to every pool.
-template <int NT>
+// UNPACK: the step's unpack is fused in — my segments' g_avg straight from the sums in
+// registers while the pushes drain, and after the exit barrier the other segments from my pool:
+// CTA b unpacks exactly the vectors its peer CTAs b pushed to me (the same flat sweep on the
+// owner's segment), which is what its CTA-pair exit barrier covers.
+template <int NT, bool UNPACK>
 __global__ void __launch_bounds__(kRingThreads, 1)
-rsp_kernel(const __grid_constant__ RingArgs a, const char* __restrict__ inbox_local, uint64_t slot_bytes) {
+rsp_kernel(const __grid_constant__ RingArgs a, const char* __restrict__ inbox_local, uint64_t slot_bytes,
+           const __grid_constant__ StepTable TT, float inv) {
     constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
     constexpr int U = NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1);
     __shared__ int s_ok;
@@ -160,6 +273,10 @@ rsp_kernel(const __grid_constant__ RingArgs a, const char* __restrict__ inbox_lo
         src[t] = t == 0 ? a.bufs[a.rank] : (t < n ? inbox_local + uint64_t(t - 1) * slot_bytes : nullptr);
         dst[t] = t < n ? a.bufs[a.ring[(a.pos + 1 + t) % n]] : nullptr;
     }
+    auto unpack_elem = [&](uint64_t e, uint16_t h) {
+        const int t = tensor_at(TT, e);
+        TT.dst[t][e - TT.off[t]] = gfd::mul(gfd::dec(h), inv);
+    };
     // unaligned edges of window w: CTA w mod grid, scalar
     for (int w = int(blockIdx.x); w < a.nwin; w += int(gridDim.x)) {
         const uint64_t e0 = flat.e0[w], e1 = flat.e1[w], v0 = flat.v0[w], v1 = v0 + (flat.pre[w + 1] - flat.pre[w]);
@@ -168,6 +285,7 @@ rsp_kernel(const __grid_constant__ RingArgs a, const char* __restrict__ inbox_lo
                 uint16_t acc = reinterpret_cast<const uint16_t*>(src[0])[e];
                 for (int t = 1; t < n; ++t) acc = gfd::acc16(reinterpret_cast<const uint16_t*>(src[t])[e], acc);
                 for (int t = 0; t < n; ++t) reinterpret_cast<uint16_t*>(dst[t])[e] = acc;
+                if (UNPACK) unpack_elem(e, acc);
             }
         };
         if (v1 > v0) {
@@ -204,12 +322,114 @@ rsp_kernel(const __grid_constant__ RingArgs a, const char* __restrict__ inbox_lo
 #pragma unroll
             for (int t = 0; t < NMAX; ++t)
                 if (t < n) gfd::st16(dst[t] + vv[u] * 16, acc);
+            if (UNPACK) unpack_vec<GF_F16>(TT, vv[u], acc, inv);
         }
     }
     if (tr) a.trace[2] = gfd::globaltimer_ns();
     if (!cross_barrier(a, epoch + 2, &s_ok, true)) return;  // every push into my pool landed
     if (threadIdx.x == 0) a.epochs[blockIdx.x] = epoch + 2;
     if (tr) a.trace[3] = gfd::globaltimer_ns();
+    if (!UNPACK) return;
+    // the other owners' segments, as their CTA b pushed them
+    const uint16_t* pool = reinterpret_cast<const uint16_t*>(a.bufs[a.rank]);
+    for (int j = 1; j < n; ++j) {
+        const int q = (a.pos + j) % n;
+        flat_build<8>(a, n, q, flat);
+        for (int w = int(blockIdx.x); w < a.nwin; w += int(gridDim.x)) {
+            const uint64_t e0 = flat.e0[w], e1 = flat.e1[w], v0 = flat.v0[w],
+                           v1 = v0 + (flat.pre[w + 1] - flat.pre[w]);
+            const uint64_t h0 = v1 > v0 ? v0 * 8 : e1;
+            for (uint64_t e = e0 + threadIdx.x; e < h0; e += blockDim.x)
+                unpack_elem(e, reinterpret_cast<const volatile uint16_t*>(pool)[e]);
+            if (v1 > v0)
+                for (uint64_t e = v1 * 8 + threadIdx.x; e < e1; e += blockDim.x)
+                    unpack_elem(e, reinterpret_cast<const volatile uint16_t*>(pool)[e]);
+        }
+        const uint64_t tq = flat.pre[a.nwin];
+        for (uint64_t x = g; x < tq; x += T * 4) {
+            uint4 h[4];
+            uint64_t vq[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t xu = x + uint64_t(u) * T;
+                vq[u] = ~0ull;
+                if (xu < tq) {
+                    const int w = flat_window(flat, a.nwin, xu);
+                    vq[u] = flat.v0[w] + (xu - flat.pre[w]);
+                    h[u] = ld16_cg<GF_F16>(a.bufs[a.rank] + vq[u] * 16);  // pushed by a peer: skip L1
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (vq[u] != ~0ull) unpack_vec<GF_F16>(TT, vq[u], h[u], inv);
+        }
+    }
+    if (tr) a.trace[3] = gfd::globaltimer_ns();
+}
+
+// GF_PUSH_DIAG timing probes (results invalid by design): 1 every routed store local, 2 the
+// routed pack alone (no reduce / all-gather / unpack).
+int push_diag() {
+    static const int v = [] {
+        const char* e = std::getenv("GF_PUSH_DIAG");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+// The routed pack of one group of <= kMaxW windows (the tensors inside them).
+int routed_pack(gf_comm* c, cudaStream_t s, uint64_t pool_heap_off, uint64_t inbox_heap_off, uint64_t slot_elems,
+                const float* const* src, const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                const uint64_t* win_start, const uint64_t* win_len, int nwin) {
+    SegMap M;
+    std::memset(&M, 0, sizeof(M));
+    M.nwin = nwin;
+    M.world = c->world;
+    M.pos = c->pos;
+    M.slot_elems = slot_elems;
+    M.pool_local = c->alloc + kFlagBytes + pool_heap_off;
+    M.diag = push_diag();
+    for (int j = 0; j < c->world; ++j) M.inbox_by_pos[j] = c->peer_alloc[c->ring[j]] + kFlagBytes + inbox_heap_off;
+    for (int w = 0; w < nwin; ++w) {
+        M.wstart[w] = win_start[w];
+        M.wlen[w] = win_len[w];
+    }
+    const bool tma = pack_tma();
+    if (tma) {
+        static bool attr_set[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+            GF_CHECK_CUDA(cudaFuncSetAttribute(pack_push_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               int(kTmaStages * kTile * 2)));
+            attr_set[dev] = true;
+        }
+    }
+    return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
+                          [&](const TensorTable& T, uint64_t tiles, int grid) {
+                              uint64_t spread = std::max<uint64_t>(1, tiles / uint64_t(c->world));
+                              while (std::gcd(spread, tiles) != 1) ++spread;
+                              if (tma) {  // persistent: 2 CTAs per SM, each loops over its tiles
+                                  const int g = int(std::min<uint64_t>(tiles, uint64_t(gfi::sm_count()) * 2));
+                                  pack_push_tma_kernel<2><<<g, kThreads, kTmaStages * kTile * 2, s>>>(T, M, tiles,
+                                                                                                      spread);
+                                  return;
+                              }
+                              switch (push_minb()) {
+                                  case 6: pack_push_kernel<6><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
+                                  case 8: pack_push_kernel<8><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
+                                  default: pack_push_kernel<4><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
+                              }
+                          });
+}
+
+// The unpack fused into rsp_kernel (default) or a separate unpack launch (GF_FUSE_UNPACK=0).
+bool fuse_unpack() {
+    static const bool v = [] {
+        const char* e = std::getenv("GF_FUSE_UNPACK");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    return v;
 }
 
 }  // namespace
@@ -249,6 +469,17 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
         return gfi::fail(GF_ERR_CONFIG, "gf_sync_step_dense_push: pool and inbox ranges overlap");
     DeviceGuard guard(c->device);
     cudaStream_t s = gfi::S(stream);
+    const char* inbox_local = c->alloc + kFlagBytes + inbox_heap_off;
+    // the unpack rides in rsp_kernel when the tensors fit its table and one launch covers the
+    // windows (the usual case); otherwise a separate unpack follows
+    const bool fused = ntensors <= kStepMaxT && nwin <= kMaxW && fuse_unpack();
+    StepTable TT;
+    std::memset(&TT, 0, sizeof(TT));
+    if (fused) {
+        uint64_t hi2 = 0;
+        if (int rc = build_table("gf_sync_step_dense_push", nullptr, dst, pool_off, count, ntensors, TT, hi2)) return rc;
+    }
+    const float inv = 1.0f / static_cast<float>(c->world);
     // Windows go in groups of <= kMaxW per launch pair; windows are cut at tensor boundaries,
     // so every tensor belongs to exactly one group.
     std::vector<const void*> gsrc;
@@ -269,30 +500,12 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
         }
         // 1. pack, routed to the owners
         gfi::phase("pack_push", s);
-        SegMap M;
-        std::memset(&M, 0, sizeof(M));
-        M.nwin = nw;
-        M.world = c->world;
-        M.pos = c->pos;
-        M.slot_elems = slot_elems;
-        M.pool_local = c->alloc + kFlagBytes + pool_heap_off;
-        for (int j = 0; j < c->world; ++j) M.inbox_by_pos[j] = c->peer_alloc[c->ring[j]] + kFlagBytes + inbox_heap_off;
-        for (int w = 0; w < nw; ++w) {
-            M.wstart[w] = win_start[first + w];
-            M.wlen[w] = win_len[first + w];
-        }
-        if (int rc = for_each_table(gsrc.data(), goff.data(), gcnt.data(), int(gsrc.size()),
-                                    [&](const TensorTable& T, uint64_t tiles, int grid) {
-                                        uint64_t spread = std::max<uint64_t>(1, tiles / uint64_t(c->world));
-                                        while (std::gcd(spread, tiles) != 1) ++spread;
-                                        switch (push_minb()) {
-                                            case 6: pack_push_kernel<6><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
-                                            case 8: pack_push_kernel<8><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
-                                            default: pack_push_kernel<4><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
-                                        }
-                                    }))
+        if (int rc = routed_pack(c, s, pool_heap_off, inbox_heap_off, slot_elems,
+                                 reinterpret_cast<const float* const*>(gsrc.data()), goff.data(), gcnt.data(),
+                                 int(gsrc.size()), win_start + first, win_len + first, nw))
             return rc;
-        // 2. local reduce + all-gather push
+        if (push_diag() == 2) continue;  // timing probe: the routed pack alone (results invalid)
+        // 2. local reduce + all-gather push (+ the unpack when fused)
         RingArgs a;
         std::memset(&a, 0, sizeof(a));
         a.nwin = nw;
@@ -303,18 +516,23 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
             max_seg += (a.wlen[w] + c->world - 1) / c->world;
         }
         fill_common(c, a, pool_heap_off);
-        const char* inbox_local = c->alloc + kFlagBytes + inbox_heap_off;
         const int grid = gfr::comm_blocks(c, max_seg * 2);
         gfi::phase("rsp", s);
+        const uint64_t sb = slot_elems * 2;
+#define GF_RSP(NT_)                                                                                  \
+    if (fused) rsp_kernel<NT_, true><<<grid, kRingThreads, 0, s>>>(a, inbox_local, sb, TT, inv);     \
+    else rsp_kernel<NT_, false><<<grid, kRingThreads, 0, s>>>(a, inbox_local, sb, TT, inv);
         switch (c->world) {
-            case 2: rsp_kernel<2><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
-            case 4: rsp_kernel<4><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
-            case 8: rsp_kernel<8><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
-            default: rsp_kernel<0><<<grid, kRingThreads, 0, s>>>(a, inbox_local, slot_elems * 2); break;
+            case 2: GF_RSP(2) break;
+            case 4: GF_RSP(4) break;
+            case 8: GF_RSP(8) break;
+            default: GF_RSP(0) break;
         }
+#undef GF_RSP
         gfi::count_launch();
         if (int rc = gfi::check_launch("gf_sync_step_dense_push")) return rc;
     }
+    if (fused || push_diag() == 2) return GF_OK;
     // 3. unpack
     gfi::phase("unpack", s);
     return gf_unpack(dtype, c->alloc + kFlagBytes + pool_heap_off, dst, pool_off, count, ntensors, c->world, stream);

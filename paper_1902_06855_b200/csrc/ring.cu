@@ -691,6 +691,12 @@ int gf_comm_set_timeout_ms(gf_comm* c, uint64_t ms) {
     return GF_OK;
 }
 
+int gf_comm_set_max_blocks(gf_comm* c, int max_blocks) {
+    if (!c || max_blocks < 0) return gfi::fail(GF_ERR_CONFIG, "gf_comm_set_max_blocks: bad arguments");
+    c->max_blocks = std::min(max_blocks, kMaxBlocks);
+    return GF_OK;
+}
+
 int gf_comm_status(gf_comm* c) {
     if (!c) return gfi::fail(GF_ERR_CONFIG, "null communicator");
     if (c->err_host && *reinterpret_cast<volatile int*>(c->err_host) != 0)
@@ -1080,7 +1086,8 @@ int gf_ring_traffic(uint64_t len, int world, int position, int dtype, uint64_t* 
 namespace gfr {
 int ring_blocks(uint64_t max_seg_bytes) { return ring_blocks_impl(max_seg_bytes); }
 int comm_blocks(const gf_comm* c, uint64_t max_seg_bytes) {
-    const int g = ring_blocks_impl(max_seg_bytes);
+    int g = ring_blocks_impl(max_seg_bytes);
+    if (c->max_blocks > 0) g = std::min(g, c->max_blocks);
     return c->grid_cap > 0 ? std::min(g, c->grid_cap) : g;
 }
 }  // namespace gfr

@@ -303,4 +303,10 @@ namespace gfr {
 int ring_blocks(uint64_t max_seg_bytes);
 // The same capped by the communicator (colocated ranks share one device's SMs).
 int comm_blocks(const gf_comm* c, uint64_t max_seg_bytes);
+// pull.cu: reduce-scatter (pulled from the peers' pools, or from my pool + my inbox slots when
+// inbox != null) then pull all-gather, both unpacking from registers (<= 256 tensors).
+int rsag_launch(gf_comm* c, int dtype, uint64_t pool_heap_off, const char* inbox, uint64_t slot_bytes,
+                float* const* dst, const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                const uint64_t* win_start, const uint64_t* win_len, int nwin, int flags, void* stream,
+                const char* fn);
 }  // namespace gfr
