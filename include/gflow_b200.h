@@ -130,10 +130,12 @@ int gf_csc_pack_correct(int dtype, void* pool, float* hg, void* staging,
                         float momentum, uint64_t* nacc, void* stream);
 /* The same restricted to a part of the chunks: part 0 all, 1 the important chunks only (every
  * staged chunk), 2 the unimportant ones only. A CSC step runs part 1, starts the exchange of the
- * staging buffer, and runs part 2 beside it (they touch disjoint pool/hg/nacc elements). */
+ * staging buffer, and runs part 2 beside it (they touch disjoint pool/hg/nacc elements). With
+ * `plan` (device, gf_csc_plan of the same set; nullable) and the tensors in ascending id, part 1
+ * walks only the planned chunks. */
 int gf_csc_pack_correct_part(int dtype, void* pool, float* hg, void* staging,
-                             const uint8_t* important, const uint64_t* coff, uint64_t total,
-                             uint64_t chunk, uint64_t nc, const float* const* src,
+                             const uint8_t* important, const uint64_t* coff, const uint64_t* plan,
+                             uint64_t total, uint64_t chunk, uint64_t nc, const float* const* src,
                              const uint64_t* pool_off, const uint64_t* count, int ntensors,
                              float momentum, uint64_t* nacc, int part, void* stream);
 /* Staging pack / write-back over the important chunks listed in `plan` (see gf_csc_plan):

@@ -319,6 +319,70 @@ pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ po
         pack_correct_tile<DT, kThreads>(T, tile, pool, hg, staging, imp, coff, chunk, nc, mom, nacc, part);
 }
 
+// K2 part 1 driven by the plan: only the important chunks (plan[4 .. 4+plan[1])), each cut into
+// kTile-element pieces walked by a persistent grid — its work is proportional to the staged data,
+// where the tile-driven kernel visits (and skips) every tile of the gradient set. The tensor
+// holding a pool element is found by binary search over the table's pool offsets, which the
+// host checked to be descending (tensors in ascending id: tensor m at offset 0).
+__device__ __forceinline__ int tensor_of(const TensorTable& T, uint64_t e) {
+    int lo = 0, hi = T.n;  // first entry with off <= e (offsets descending)
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (T.off[mid] <= e) hi = mid; else lo = mid + 1;
+    }
+    return (lo < T.n && e < T.off[lo] + T.cnt[lo]) ? lo : -1;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads, 4)
+pack_correct_planned_kernel(const __grid_constant__ TensorTable T, void* __restrict__ pool, float* __restrict__ hg,
+                            void* __restrict__ staging, const uint64_t* __restrict__ plan,
+                            const uint64_t* __restrict__ coff, uint64_t total, uint64_t chunk, uint64_t nc,
+                            uint64_t per, float mom) {
+    const uint64_t k = plan[1];
+    for (uint64_t item = blockIdx.x; item < k * per; item += gridDim.x) {
+        const uint64_t c = plan[4 + item / per];
+        const uint64_t cb = c * chunk, clen = (c + 1 == nc) ? total - cb : chunk;
+        const uint64_t s0 = (item % per) * kTile;
+        if (s0 >= clen) continue;
+        const uint64_t e0 = cb + s0, e1 = cb + min(clen, s0 + kTile);
+        const uint64_t so = coff[c] - cb;  // staging index = pool index + so
+        for (uint64_t e = e0 + 8 * uint64_t(threadIdx.x); e < e1; e += 8 * uint64_t(kThreads)) {
+            const int t = tensor_of(T, e);
+            const float* src = t >= 0 ? static_cast<const float*>(T.ptr[t]) + (e - T.off[t]) : nullptr;
+            if (DT == GF_F16 && t >= 0 && e + 8 <= min(e1, T.off[t] + T.cnt[t]) && e % 8 == 0 &&
+                ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(hg + e)) & 31u) == 0 &&
+                ((reinterpret_cast<uintptr_t>(static_cast<uint16_t*>(pool) + e) |
+                  reinterpret_cast<uintptr_t>(static_cast<uint16_t*>(staging) + e + so)) & 15u) == 0) {
+                const gfd::F8 gv = gfd::ld32f_stream(src);
+                const gfd::F8 hv = gfd::ld32f(hg + e);
+                float hn[8];
+                uint4 ov;
+                bool nan;
+                correct8(gv, reinterpret_cast<const float*>(&hv), true, mom, hn, ov, nan);
+                gfd::st32f(hg + e, make_float4(hn[0], hn[1], hn[2], hn[3]), make_float4(hn[4], hn[5], hn[6], hn[7]));
+                gfd::st16(static_cast<uint16_t*>(pool) + e, ov);
+                gfd::st16(static_cast<uint16_t*>(staging) + e + so, ov);
+                continue;
+            }
+            for (uint64_t q = e; q < min(e + 8, e1); ++q) {  // edges: element by element
+                const int tq = tensor_of(T, q);
+                if (tq < 0) continue;  // another table's tensor (more than 256 tensors)
+                const float x = static_cast<const float*>(T.ptr[tq])[q - T.off[tq]];
+                if (DT == GF_F16) {
+                    const uint16_t w = gfd::enc(correct_elem(gfd::dec(gfd::enc(x)), hg + q, true, mom));
+                    static_cast<uint16_t*>(pool)[q] = w;
+                    static_cast<uint16_t*>(staging)[q + so] = w;
+                } else {
+                    const float w = correct_elem(x, hg + q, true, mom);
+                    static_cast<float*>(pool)[q] = w;
+                    static_cast<float*>(staging)[q + so] = w;
+                }
+            }
+        }
+    }
+}
+
 // Staging pack (dir=0) / write-back (dir=1) over the important chunks listed in the plan
 // (plan[4+j], j < plan[1]): grid.y walks the list, grid.x tiles a chunk; 16-B copies.
 // On write-back of an fp16 pool, the exact |x| sums of the (now global) chunk values are
@@ -517,13 +581,13 @@ int gf_csc_pack_correct(int dtype, void* pool, float* hg, void* staging,
                         uint64_t chunk, uint64_t nc, const float* const* src,
                         const uint64_t* pool_off, const uint64_t* count, int ntensors,
                         float momentum, uint64_t* nacc, void* stream) {
-    return gf_csc_pack_correct_part(dtype, pool, hg, staging, important, coff, total, chunk, nc, src, pool_off,
-                                    count, ntensors, momentum, nacc, 0, stream);
+    return gf_csc_pack_correct_part(dtype, pool, hg, staging, important, coff, nullptr, total, chunk, nc, src,
+                                    pool_off, count, ntensors, momentum, nacc, 0, stream);
 }
 
 int gf_csc_pack_correct_part(int dtype, void* pool, float* hg, void* staging,
-                             const uint8_t* important, const uint64_t* coff, uint64_t total,
-                             uint64_t chunk, uint64_t nc, const float* const* src,
+                             const uint8_t* important, const uint64_t* coff, const uint64_t* plan,
+                             uint64_t total, uint64_t chunk, uint64_t nc, const float* const* src,
                              const uint64_t* pool_off, const uint64_t* count, int ntensors,
                              float momentum, uint64_t* nacc, int part, void* stream) {
     if (part < 0 || part > 2) return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct_part: part is 0, 1 or 2");
@@ -531,9 +595,28 @@ int gf_csc_pack_correct_part(int dtype, void* pool, float* hg, void* staging,
         return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct: bad arguments");
     if (nacc && dtype != GF_F16) return gfi::fail(GF_ERR_CONFIG, "exact norm accumulation needs an fp16 pool");
     if (staging && !coff) return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct: staging needs coff");
-    (void)total;
+    bool descending = true;
+    for (int i = 1; i < ntensors; ++i) descending &= pool_off[i] < pool_off[i - 1];
+    if (part == 1 && plan && staging && descending) {  // the plan-driven form
+        const uint64_t last = total - (nc - 1) * chunk;
+        const uint64_t per = (std::max(chunk, last) + kTile - 1) / kTile;
+        return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
+                              [&](const TensorTable& T, uint64_t, int) {
+                                  const int g = gfi::sm_count() * 4;
+                                  if (dtype == GF_F16)
+                                      pack_correct_planned_kernel<GF_F16><<<g, kThreads, 0, gfi::S(stream)>>>(
+                                          T, pool, hg, staging, plan, coff, total, chunk, nc, per, momentum);
+                                  else
+                                      pack_correct_planned_kernel<GF_F32><<<g, kThreads, 0, gfi::S(stream)>>>(
+                                          T, pool, hg, staging, plan, coff, total, chunk, nc, per, momentum);
+                              });
+    }
     return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
                           [&](const TensorTable& T, uint64_t tiles, int grid) {
+                              // part 1 skips most tiles: a persistent grid (4 CTAs per SM) walks
+                              // them; part 2 keeps one tile per CTA, so the exchange running
+                              // beside it gets SMs as CTAs retire
+                              if (part == 1) grid = std::min(grid, gfi::sm_count() * 4);
                               if (dtype == GF_F16)
                                   pack_correct_kernel<GF_F16><<<grid, kThreads, 0, gfi::S(stream)>>>(
                                       T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc, part);

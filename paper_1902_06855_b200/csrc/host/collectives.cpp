@@ -57,7 +57,7 @@ void rooted(Communicator& comm, ScalarBuffer dev, int root, F&& launch) {
     Transport& tp = comm.transport();
     const std::uint32_t tag = device_tag(comm);
     cudaDeviceSynchronize();  // this rank's pending writes to its buffer are done
-    auto ptrs = ctx.exchange(dev.data, tag);
+    auto ptrs = ctx.exchange(dev.data, tag, (static_cast<std::uint64_t>(dev.byte_length()) << 1) | static_cast<std::uint64_t>(dev.type));
     const std::vector<std::byte> token(1);
     if (comm.rank() == root) {
         for (int r = 0; r < comm.world_size(); ++r)

@@ -241,20 +241,36 @@ void* DeviceContext::scratch(std::size_t bytes, int slot) {
     return s.first;
 }
 
-std::vector<void*> DeviceContext::exchange(void* mine, std::uint32_t tag) {
+std::vector<void*> DeviceContext::exchange(void* mine, std::uint32_t tag, std::uint64_t agree) {
     if (mode_ == Mode::kSolo) return {mine};
+    // every rank must describe the same collective (sizes, windows): the reference fails a
+    // mismatch at its first exchange (collectives.cpp:21-27); here, at the pointer exchange
+    auto check_agree = [&](auto get) {
+        for (int q = 0; q < world_; ++q)
+            if (get(q) != agree)
+                throw ProtocolError("collective mismatch across ranks at rank " + std::to_string(rank_) +
+                                    " (rank " + std::to_string(q) + " describes a different buffer / windows)");
+    };
     if (mode_ != Mode::kIpc) {
-        const auto all = allgather(tp_, reinterpret_cast<std::uintptr_t>(mine), tag);
+        struct Ptr {
+            std::uintptr_t p;
+            std::uint64_t agree;
+        };
+        const auto all = allgather(tp_, Ptr{reinterpret_cast<std::uintptr_t>(mine), agree}, tag);
+        check_agree([&](int q) { return all[static_cast<std::size_t>(q)].agree; });
         std::vector<void*> out;
-        for (auto p : all) out.push_back(reinterpret_cast<void*>(p));
+        for (auto& p : all) out.push_back(reinterpret_cast<void*>(p.p));
         return out;
     }
     struct Reg {
         char h[GF_IPC_HANDLE_BYTES];
         std::uint64_t off;
+        std::uint64_t agree;
     } r{};
     check(gf_ipc_export(mine, r.h, &r.off), "gf_ipc_export");
+    r.agree = agree;
     const auto all = allgather(tp_, r, tag);
+    check_agree([&](int q) { return all[static_cast<std::size_t>(q)].agree; });
     std::vector<void*> out(static_cast<std::size_t>(world_));
     for (int q = 0; q < world_; ++q) {
         if (q == rank_) {
@@ -287,7 +303,19 @@ void DeviceContext::ring_allreduce(ScalarBuffer buf, const std::vector<int>& rin
     const std::size_t es = element_size(buf.type);
     // Peers' buffers must share this buffer's 16-byte misalignment so one aligned base plus
     // shifted windows describes every rank; otherwise the collective runs in aligned scratch.
-    auto ptrs = exchange(buf.data, tag);
+    std::uint64_t agree = 1469598103934665603ull;  // FNV-1a of (type, windows): same on every rank
+    auto mix = [&](std::uint64_t v) {
+        for (int b = 0; b < 8; ++b) {
+            agree ^= (v >> (8 * b)) & 0xFFu;
+            agree *= 1099511628211ull;
+        }
+    };
+    mix(static_cast<std::uint64_t>(buf.type));
+    for (auto& w : windows) {
+        mix(w.first);
+        mix(w.second);
+    }
+    auto ptrs = exchange(buf.data, tag, agree);
     const std::uintptr_t mis = reinterpret_cast<std::uintptr_t>(buf.data) & 15u;
     bool same = mis % es == 0;
     for (void* p : ptrs) same &= (reinterpret_cast<std::uintptr_t>(p) & 15u) == mis;
@@ -307,7 +335,7 @@ void DeviceContext::ring_allreduce(ScalarBuffer buf, const std::vector<int>& rin
     } else {
         staged = static_cast<std::byte*>(scratch((hi - lo) * es, 1));
         cuda_ok(cudaMemcpyAsync(staged, buf.data + lo * es, (hi - lo) * es, cudaMemcpyDefault, st), "stage");
-        ptrs = exchange(staged, tag | 0x80u);
+        ptrs = exchange(staged, tag | 0x80u, agree);
         for (auto& w : windows) {
             ws.push_back(w.first - lo);
             wl.push_back(w.second);

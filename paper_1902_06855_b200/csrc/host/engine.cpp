@@ -488,8 +488,8 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
         return gf_csc_scatter(dt, pool, stage, e->plan[cur], e->coff[cur], T, chunk, nc, k_cur, e->nacc, s);
     };
     auto pack_correct = [&](int part, cudaStream_t st) {
-        return gf_csc_pack_correct_part(dt, pool, e->hg, solo ? nullptr : stage, e->imp[cur], e->coff[cur], T, chunk,
-                                        nc, grads, e->offs.data(), e->sizes.data(), e->m,
+        return gf_csc_pack_correct_part(dt, pool, e->hg, solo ? nullptr : stage, e->imp[cur], e->coff[cur],
+                                        e->plan[cur], T, chunk, nc, grads, e->offs.data(), e->sizes.data(), e->m,
                                         static_cast<float>(C.momentum), e->nacc, part, st);
     };
     if (solo) {

@@ -62,6 +62,24 @@ struct GradientPool::Device {
     float* norm_out = nullptr;
     float* norm_host = nullptr;  // pinned
     bool fresh_iteration = true;
+    // packs not launched yet: write_tensor only queues its copy; one multi-tensor pack launch
+    // covers every pending tensor when the pool's stream next has to be current
+    std::vector<const float*> pend_src;
+    std::vector<std::uint64_t> pend_off, pend_cnt;
+    bool pend_copies = false;
+    // staging slots follow the ascending tensor-id order (a flat gradient buffer's layout), so
+    // the descending-id writes of one contiguous host buffer extend one copy backwards: with
+    // async host input the copies of adjacent spans coalesce into one DMA
+    std::vector<std::size_t> slot_off;  // by id-1
+    float* cp_dst = nullptr;
+    const float* cp_src = nullptr;
+    std::size_t cp_bytes = 0;
+
+    void issue_copy() {
+        if (!cp_bytes) return;
+        cuda_ok(cudaMemcpyAsync(cp_dst, cp_src, cp_bytes, cudaMemcpyHostToDevice, copy), "H2D gradients");
+        cp_bytes = 0;
+    }
 
     Device(int dev, std::size_t bytes) : device(dev) {
         cuda_ok(cudaMalloc(&data, std::max<std::size_t>(bytes, 16)), "cudaMalloc pool");
@@ -118,22 +136,46 @@ GradientPool::GradientPool(const std::vector<std::size_t>& sizes, std::size_t ch
         1, static_cast<std::size_t>(std::llround(static_cast<double>(off) / static_cast<double>(chunk_size))));
     next_expected_id_ = m;
     cuda_ok(cudaGetDevice(&device_), "cudaGetDevice");
-    dev_ = std::make_unique<Device>(device_, total_elements_ * element_size(type));
-    data_ = dev_->data;
-    host_.assign(total_elements_ * element_size(type), std::byte{0});
-    host_valid_ = true;
+    // the device side (pool, streams, staging) is created on first use: constructing a pool
+    // is pure layout, as in the reference (acceptance criterion 1 times it)
+    host_valid_ = false;  // the host mirror is allocated on the first host read
 }
 
 GradientPool::GradientPool(GradientPool&& o) noexcept = default;
 
 GradientPool::~GradientPool() = default;
 
-void* GradientPool::stream() const { return dev_->stream; }
+GradientPool::Device& GradientPool::dev() {
+    if (!dev_) {
+        OnDevice g(device_);
+        dev_ = std::make_unique<Device>(device_, total_elements_ * element_size(element_type_));
+        data_ = dev_->data;
+        dev_->slot_off.resize(descs_.size());
+        std::size_t asc = 0;
+        for (std::size_t i = 0; i < descs_.size(); ++i) {
+            dev_->slot_off[i] = asc;
+            asc += descs_[i].element_count;
+        }
+    }
+    return *dev_;
+}
+
+void* GradientPool::stream() { return dev().stream; }
+
+std::byte* GradientPool::device_data() {
+    dev();
+    return data_;
+}
+
+void GradientPool::run_pending_work() {
+    flush_writes();
+    if (pending_work_) pending_work_();
+}
 
 void GradientPool::synchronize() {
     run_pending_work();
     OnDevice g(device_);
-    cuda_ok(cudaStreamSynchronize(dev_->stream), "pool stream");
+    cuda_ok(cudaStreamSynchronize(dev().stream), "pool stream");
 }
 
 const TensorDesc& GradientPool::desc(int tensor_id) const {
@@ -168,8 +210,9 @@ ScalarBuffer GradientPool::chunk_view(std::size_t c) {
 }
 
 void GradientPool::begin_iteration() {
-    Device& D = *dev_;
+    Device& D = dev();
     if (!D.fresh_iteration) {  // an abandoned iteration: retire its staging buffer like a full one
+        flush_writes();
         OnDevice g(device_);
         cuda_ok(cudaEventRecord(D.ev_packed[D.parity], D.stream), "event");
         D.packed_recorded[D.parity] = true;
@@ -192,7 +235,7 @@ std::vector<std::size_t> GradientPool::write_tensor(int tensor_id, std::span<con
         throw ConfigError("tensor " + std::to_string(tensor_id) + " length mismatch: " +
                           std::to_string(values.size()) + " vs " + std::to_string(d.element_count));
     OnDevice g(device_);
-    Device& D = *dev_;
+    Device& D = dev();
     const float* src = values.data();
     const std::size_t bytes = values.size() * sizeof(float);
     const Where where = locate(src);
@@ -209,21 +252,40 @@ std::vector<std::size_t> GradientPool::write_tensor(int tensor_id, std::span<con
             if (D.packed_recorded[D.parity]) cuda_ok(cudaStreamWaitEvent(D.copy, D.ev_packed[D.parity], 0), "wait");
             D.fresh_iteration = false;
         }
-        float* slot = D.staging(total_elements_) + d.pool_offset;
-        cuda_ok(cudaMemcpyAsync(slot, src, bytes, cudaMemcpyHostToDevice, D.copy), "H2D gradients");
-        cuda_ok(cudaEventRecord(D.ev_copy, D.copy), "event");
-        cuda_ok(cudaStreamWaitEvent(D.stream, D.ev_copy, 0), "wait");
-        // the span is the caller's again when we return: wait for a pinned DMA (pageable
-        // sources were staged by the driver before cudaMemcpyAsync returned)
-        if (where == Where::kPinned && !async_host_input_) cuda_ok(cudaEventSynchronize(D.ev_copy), "H2D");
+        float* slot = D.staging(total_elements_) + D.slot_off[static_cast<std::size_t>(tensor_id - 1)];
+        if (where == Where::kPinned && async_host_input_) {
+            // deferred: extends the pending copy when this span sits right before it (host and slot)
+            if (D.cp_bytes && src + values.size() == D.cp_src && slot + values.size() == D.cp_dst) {
+                D.cp_src = src;
+                D.cp_dst = slot;
+                D.cp_bytes += bytes;
+            } else {
+                D.issue_copy();
+                D.cp_src = src;
+                D.cp_dst = slot;
+                D.cp_bytes = bytes;
+            }
+        } else {
+            D.issue_copy();
+            cuda_ok(cudaMemcpyAsync(slot, src, bytes, cudaMemcpyHostToDevice, D.copy), "H2D gradients");
+            // the span is the caller's again when we return: wait for a pinned DMA (pageable
+            // sources were staged by the driver before cudaMemcpyAsync returned)
+            if (where == Where::kPinned) {
+                cuda_ok(cudaEventRecord(D.ev_copy, D.copy), "event");
+                cuda_ok(cudaEventSynchronize(D.ev_copy), "H2D");
+            }
+        }
         src = slot;
     }
-    const std::uint64_t off = d.pool_offset, cnt = d.element_count;
-    check(gf_pack(static_cast<int>(element_type_), data_, &src, &off, &cnt, 1, 1.0f, D.stream), "write_tensor");
+    D.pend_src.push_back(src);
+    D.pend_off.push_back(d.pool_offset);
+    D.pend_cnt.push_back(d.element_count);
+    if (where != Where::kDevice) D.pend_copies = true;
     host_valid_ = false;
     next_expected_id_ = tensor_id - 1;
     watermark_ = d.pool_offset + d.element_count;
     if (next_expected_id_ == 0) {  // the iteration's last tensor: its staging buffer is free once packed
+        flush_writes();
         cuda_ok(cudaEventRecord(D.ev_packed[D.parity], D.stream), "event");
         D.packed_recorded[D.parity] = true;
         D.parity ^= 1;
@@ -237,12 +299,30 @@ std::vector<std::size_t> GradientPool::write_tensor(int tensor_id, std::span<con
     return done;
 }
 
+void GradientPool::flush_writes() {
+    Device& D = dev();
+    if (D.pend_src.empty()) return;
+    OnDevice g(device_);
+    if (D.pend_copies) {  // the queued H2D copies come first
+        D.issue_copy();
+        cuda_ok(cudaEventRecord(D.ev_copy, D.copy), "event");
+        cuda_ok(cudaStreamWaitEvent(D.stream, D.ev_copy, 0), "wait");
+    }
+    check(gf_pack(static_cast<int>(element_type_), data_, D.pend_src.data(), D.pend_off.data(), D.pend_cnt.data(),
+                  static_cast<int>(D.pend_src.size()), 1.0f, D.stream),
+          "write_tensor");
+    D.pend_src.clear();
+    D.pend_off.clear();
+    D.pend_cnt.clear();
+    D.pend_copies = false;
+}
+
 void GradientPool::read_averaged(std::span<float> out, int world, bool wait) {
     if (out.size() != total_elements_) throw ConfigError("read_averaged: output does not match the pool layout");
     if (world < 1) throw ConfigError("read_averaged: world must be >= 1");
     run_pending_work();
     OnDevice g(device_);
-    Device& D = *dev_;
+    Device& D = dev();
     float* avg = D.averaged(total_elements_);
     const std::uint64_t off = 0, cnt = total_elements_;
     check(gf_unpack(static_cast<int>(element_type_), data_, &avg, &off, &cnt, 1, world, D.stream), "read_averaged");
@@ -252,10 +332,12 @@ void GradientPool::read_averaged(std::span<float> out, int world, bool wait) {
 
 void GradientPool::sync_host() {
     if (host_valid_) return;
+    if (host_.size() != total_elements_ * element_size(element_type_))
+        host_.resize(total_elements_ * element_size(element_type_));
     synchronize();
     OnDevice g(device_);
-    cuda_ok(cudaMemcpyAsync(host_.data(), data_, host_.size(), cudaMemcpyDeviceToHost, dev_->stream), "pool D2H");
-    cuda_ok(cudaStreamSynchronize(dev_->stream), "pool D2H");
+    cuda_ok(cudaMemcpyAsync(host_.data(), data_, host_.size(), cudaMemcpyDeviceToHost, dev().stream), "pool D2H");
+    cuda_ok(cudaStreamSynchronize(dev().stream), "pool D2H");
     host_valid_ = true;
 }
 
@@ -271,16 +353,16 @@ void GradientPool::set(std::size_t i, float v) {
     h.set(i, v);
     const std::size_t es = element_size(element_type_);
     OnDevice g(device_);
-    cuda_ok(cudaMemcpyAsync(data_ + i * es, host_.data() + i * es, es, cudaMemcpyHostToDevice, dev_->stream),
+    cuda_ok(cudaMemcpyAsync(data_ + i * es, host_.data() + i * es, es, cudaMemcpyHostToDevice, dev().stream),
             "pool set");
-    cuda_ok(cudaStreamSynchronize(dev_->stream), "pool set");
+    cuda_ok(cudaStreamSynchronize(dev().stream), "pool set");
 }
 
 float GradientPool::chunk_l1(std::size_t c) {
     const std::size_t b = chunk_begin(c), len = chunk_length(c);
     run_pending_work();
     OnDevice g(device_);
-    Device& D = *dev_;
+    Device& D = dev();
     // one-chunk launch of K3 (exact; bit-identical to the reference's fp64 loop)
     check(gf_chunk_norms(static_cast<int>(element_type_), data_ + b * element_size(element_type_), len, len, 1,
                          nullptr, 1, D.norm_out, D.stream),

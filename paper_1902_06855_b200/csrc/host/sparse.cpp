@@ -140,6 +140,7 @@ void SparseState::begin_iteration(std::uint64_t t) {
 
 void SparseState::flush_corrections() {
     if (run_hi_ == run_lo_) return;
+    pool_.flush_writes();  // the chunks' packs precede their correction on the pool stream
     OnDevice g(pool_.device());
     check(gf_csc_correct(static_cast<int>(pool_.element_type()), pool_.device_data(), d_hg_, d_imp_,
                          pool_.total_elements(), pool_.chunk_size(), pool_.num_chunks(), run_lo_, run_hi_ - run_lo_,
@@ -193,9 +194,8 @@ void SparseState::device_allreduce(Communicator& comm, std::vector<void*>& ranks
     DeviceContext& ctx = comm.device();
     if (ranks.empty()) {  // first use: every rank registers this buffer at the same call
         pool_.synchronize();
-        ranks = ctx.exchange(buf, (comm.acquire_collective_id() << 8) | phase);
+        ranks = ctx.exchange(buf, (comm.acquire_collective_id() << 8) | phase, (static_cast<std::uint64_t>(length) << 1) | static_cast<std::uint64_t>(type));
     }
-    (void)length;
     ctx.ring_allreduce_async(type, ranks, comm.ring_order(), windows, pool_.stream());
     detail::record_ring_payload(comm, type, windows, "ring");
 }

@@ -105,6 +105,7 @@ struct TcpTransport::Impl {
     std::unordered_map<std::uint64_t, std::deque<std::vector<std::byte>>> box;
     bool poisoned = false;
     std::string reason;
+    std::vector<char> closed;  // per peer: orderly EOF seen (frames already received stay readable)
 
     void wake() const {
         const std::uint64_t one = 1;
@@ -122,11 +123,21 @@ struct TcpTransport::Impl {
         box_cv.notify_all();
     }
 
-    void drop(int r, const std::string& why) {
+    void drop(int r, const std::string& why, bool orderly = false) {
         Peer& p = peers[static_cast<std::size_t>(r)];
         if (!p.open) return;
         p.open = false;
-        if (!stopping.load()) poison(why);
+        if (stopping.load()) return;
+        if (orderly) {  // the peer finished and closed: only waits on ITS frames can fail now
+            {
+                std::lock_guard lk(box_mu);
+                if (closed.size() < peers.size()) closed.resize(peers.size(), 0);
+                closed[static_cast<std::size_t>(r)] = 1;
+            }
+            box_cv.notify_all();
+            return;
+        }
+        poison(why);
     }
 
     // reads everything available on peer r; complete frames go to the mailbox
@@ -148,7 +159,7 @@ struct TcpTransport::Impl {
                 if (k < 0 && errno == EINTR) continue;
                 if (k < 0 && (errno == EAGAIN || errno == EWOULDBLOCK)) return;
                 if (k <= 0) {
-                    drop(r, "connection to rank " + std::to_string(r) + (k == 0 ? " closed" : " reset"));
+                    drop(r, "connection to rank " + std::to_string(r) + (k == 0 ? " closed" : " reset"), k == 0);
                     return;
                 }
             }
@@ -429,9 +440,13 @@ std::vector<std::byte> TcpTransport::take(int src, std::uint8_t type, std::uint3
         auto it = impl_->box.find(key);
         return it != impl_->box.end() && !it->second.empty();
     };
-    impl_->box_cv.wait_for(lk, timeout_, [&] { return ready() || impl_->poisoned; });
+    auto gone = [&] {
+        return static_cast<std::size_t>(src) < impl_->closed.size() && impl_->closed[static_cast<std::size_t>(src)];
+    };
+    impl_->box_cv.wait_for(lk, timeout_, [&] { return ready() || impl_->poisoned || gone(); });
     if (!ready()) {
         if (impl_->poisoned) throw TransportError(impl_->reason);
+        if (gone()) throw TransportError("connection to rank " + std::to_string(src) + " closed");
         throw TransportError("recv timeout at rank " + std::to_string(rank_) + " (src " + std::to_string(src) +
                              ", tag " + std::to_string(tag) + ")");
     }

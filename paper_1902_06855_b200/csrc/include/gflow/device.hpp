@@ -49,8 +49,9 @@ public:
     void activate() const;
 
     // Collective: every rank passes its own device buffer (same call order on all ranks).
-    // Returns rank r's buffer as addressable from this rank's GPU, for every r.
-    std::vector<void*> exchange(void* mine, std::uint32_t tag);
+    // Returns rank r's buffer as addressable from this rank's GPU, for every r. `agree` must be
+    // equal on every rank (a digest of what the collective covers), else ProtocolError.
+    std::vector<void*> exchange(void* mine, std::uint32_t tag, std::uint64_t agree = 0);
 
     // Collective in-place sum of `windows` (element ranges of buf) with the reference's
     // ring order; buf is a DEVICE view on this rank's GPU. Blocks until done; a peer

@@ -39,44 +39,46 @@ struct SegMap {  // routing of pool elements to their owners (explicit windows)
     uint64_t wlen[kMaxW];
 };
 
-// owner position and the end of its segment for pool element e (e inside the windows)
-__device__ __forceinline__ int seg_owner(const SegMap& m, uint64_t e, uint64_t& seg_end) {
+// Per-tile routing table in shared memory. A tile lies inside one tensor, hence inside one
+// window (windows are cut at tensor boundaries), so it meets at most world-1 segment
+// boundaries: one thread computes that window's segment_of starts (src/collectives.cpp:47-53,
+// one 64-bit division per tile) and each owner's destination base; every vector then finds its
+// owner with a few compares instead of divisions.
+struct TileRoute {
+    uint64_t start[GF_MAX_RANKS + 1];  // segment j of the tile's window: [start[j], start[j+1])
+    uint16_t* dst[GF_MAX_RANKS];       // owner j's destination base (pool indices)
+};
+
+__device__ __forceinline__ void tile_route(const SegMap& m, uint64_t e, TileRoute& r) {
     int lo = 0, hi = m.nwin;
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
         if (m.wstart[mid] <= e) lo = mid; else hi = mid;
     }
-    const uint64_t n = uint64_t(m.world), L = m.wlen[lo], x = e - m.wstart[lo];
-    const uint64_t base = L / n, rem = L % n, big = rem * (base + 1);
-    uint64_t j, j0;
-    if (x < big) {
-        j = x / (base + 1);
-        j0 = j * (base + 1);
-        seg_end = m.wstart[lo] + j0 + base + 1;
-    } else {
-        j = rem + (x - big) / base;
-        j0 = big + (j - rem) * base;
-        seg_end = m.wstart[lo] + j0 + base;
+    const uint64_t n = uint64_t(m.world), L = m.wlen[lo], ws = m.wstart[lo];
+    const uint64_t base = L / n, rem = L % n;
+    for (int j = 0; j <= m.world; ++j) r.start[j] = ws + uint64_t(j) * base + min(uint64_t(j), rem);
+    for (int j = 0; j < m.world; ++j) {
+        if (j == m.pos || m.diag == 1) {
+            r.dst[j] = reinterpret_cast<uint16_t*>(m.pool_local);
+        } else {  // inbox slot s of the owner at position j holds position j + 1 + s
+            const int slot = (m.pos - j - 1 + m.world) % m.world;
+            r.dst[j] = reinterpret_cast<uint16_t*>(m.inbox_by_pos[j]) + uint64_t(slot) * m.slot_elems;
+        }
     }
-    return int(j);
 }
 
-// where a packed element of segment owned by position j goes
-__device__ __forceinline__ uint16_t* route(const SegMap& m, int j, uint64_t e) {
-    if (j == m.pos || m.diag == 1) return reinterpret_cast<uint16_t*>(m.pool_local) + e;
-    const int slot = (m.pos - j - 1 + m.world) % m.world;
-    return reinterpret_cast<uint16_t*>(m.inbox_by_pos[j]) + uint64_t(slot) * m.slot_elems + e;
-}
-
-__device__ __forceinline__ void put_elem(const SegMap& m, uint64_t e, uint16_t h) {
-    uint64_t end;
-    *route(m, seg_owner(m, e, end), e) = h;
+__device__ __forceinline__ int tile_owner(const TileRoute& r, int world, uint64_t e) {
+    int j = 0;
+    while (j + 1 < world && r.start[j + 1] <= e) ++j;
+    return j;
 }
 
 template <int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
 pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ SegMap M, uint64_t total_tiles,
-                 uint64_t spread) {
+                 uint64_t spread, int fence) {
+    __shared__ TileRoute R;
     // CTA i packs tile (i * spread) mod tiles (spread coprime with tiles, ~tiles/N): consecutive
     // CTAs hit different segments, so every rank keeps all its peers' links busy at once
     // instead of streaming one owner's segment after another
@@ -87,6 +89,10 @@ pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ 
         const uint64_t len = min(kTile, T.cnt[t] - base);
         const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
         const uint64_t po = T.off[t] + base;
+        __syncthreads();  // the previous tile's readers of R are done
+        if (threadIdx.x == 0) tile_route(M, po, R);
+        __syncthreads();
+        auto put = [&](uint64_t e, uint16_t h) { R.dst[tile_owner(R, M.world, e)][e] = h; };
         uint64_t done = 0;
         if ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0 && po % 8 == 0) {
             const int nvec = int(len / 8);
@@ -106,132 +112,25 @@ pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ 
                 if (v < nvec) {
                     const uint4 h = gfd::enc8(a[k], b[k]);
                     const uint64_t e = po + 8 * uint64_t(v);
-                    uint64_t end;
-                    const int j = seg_owner(M, e, end);
-                    if (e + 8 <= end) {  // the whole vector belongs to one owner
-                        gfd::st16(route(M, j, e), h);
-                    } else {             // a segment boundary inside the vector
+                    const int j = tile_owner(R, M.world, e);
+                    if (e + 8 <= R.start[j + 1]) {  // the whole vector belongs to one owner
+                        gfd::st16(R.dst[j] + e, h);
+                    } else {                         // a segment boundary inside the vector
                         const uint32_t w[4] = {h.x, h.y, h.z, h.w};
 #pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            put_elem(M, e + q, uint16_t((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu));
+                        for (int q = 0; q < 8; ++q) put(e + q, uint16_t((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu));
                     }
                 }
             }
             done = uint64_t(nvec) * 8;
         }
-        for (uint64_t i = done + threadIdx.x; i < len; i += kThreads) put_elem(M, po + i, gfd::enc(s[i]));
+        for (uint64_t q = done + threadIdx.x; q < len; q += kThreads) put(po + q, gfd::enc(s[q]));
     }
-    // No fence: CTAs retire with their NVLink stores in flight. The kernel boundary orders
-    // all of them before rsp_kernel, whose release of the entry flag publishes them (the
-    // same ordering the ring relies on for the pack's local stores).
-}
-
-// ---- the routed pack with its stores staged through shared memory and written by TMA -----------
-// Each CTA encodes a tile into a shared-memory stage; one elected thread then issues bulk copies
-// (cp.async.bulk.global.shared::cta) of the tile's pieces to their owners — my pool or a peer's
-// inbox over NVLink. The threads go straight on to the next tile's HBM loads while the copy
-// engine drains the stage, so the NVLink write latency no longer throttles the SM's stores.
-// A vector that straddles a segment boundary is stored element by element (as the register
-// kernel does); the bulk pieces cover the whole vectors of each owner.
-constexpr int kTmaStages = 3;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-template <int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
-pack_push_tma_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ SegMap M, uint64_t total_tiles,
-                     uint64_t spread) {
-    extern __shared__ __align__(128) unsigned char stage_mem[];  // kTmaStages x kTile fp16
-    int it = 0;
-    for (uint64_t i = blockIdx.x; i < total_tiles; i += gridDim.x, ++it) {
-        const uint64_t tile = (i * spread) % total_tiles;
-        const int t = find_tensor(T, tile);
-        const uint64_t base = (tile - T.tiles[t]) * kTile;
-        const uint64_t len = min(kTile, T.cnt[t] - base);
-        const float* __restrict__ s = static_cast<const float*>(T.ptr[t]) + base;
-        const uint64_t po = T.off[t] + base;
-        uint16_t* buf = reinterpret_cast<uint16_t*>(stage_mem) + size_t(it % kTmaStages) * kTile;
-        uint64_t done = 0;
-        const bool vec = (reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0 && po % 8 == 0;
-        const int nvec = vec ? int(len / 8) : 0;
-        if (vec) {
-            float4 a[kVecPerThread], b[kVecPerThread];
-#pragma unroll
-            for (int k = 0; k < kVecPerThread; ++k) {
-                const int v = threadIdx.x + k * kThreads;
-                if (v < nvec) {
-                    const gfd::F8 f = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
-                    a[k] = f.lo;
-                    b[k] = f.hi;
-                }
-            }
-            // the stage this tile uses was last read by the bulk copies kTmaStages tiles ago
-            if (it >= kTmaStages && threadIdx.x == 0)
-                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaStages - 1) : "memory");
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < kVecPerThread; ++k) {
-                const int v = threadIdx.x + k * kThreads;
-                if (v < nvec) {
-                    const uint4 h = gfd::enc8(a[k], b[k]);
-                    const uint64_t e = po + 8 * uint64_t(v);
-                    uint64_t end;
-                    const int j = seg_owner(M, e, end);
-                    if (e + 8 <= end) {
-                        *reinterpret_cast<uint4*>(buf + 8 * v) = h;  // bulk-copied below
-                    } else {  // a segment boundary inside the vector: element stores
-                        const uint32_t w[4] = {h.x, h.y, h.z, h.w};
-#pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            put_elem(M, e + q, uint16_t((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu));
-                        (void)j;
-                    }
-                }
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                // pieces: maximal runs of whole vectors with one owner
-                const uint64_t hi = po + uint64_t(nvec) * 8;
-                uint64_t cur = po;
-                while (cur < hi) {
-                    uint64_t end;
-                    const int j = seg_owner(M, cur, end);
-                    if (cur + 8 > end) {  // straddling vector: already stored element-wise
-                        cur += 8;
-                        continue;
-                    }
-                    const uint64_t stop = min(hi, po + ((end - po) / 8) * 8);
-                    bulk_s2g(route(M, j, cur), buf + (cur - po), uint32_t((stop - cur) * 2));
-                    cur = stop;
-                }
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-            done = uint64_t(nvec) * 8;
-        }
-        for (uint64_t q = done + threadIdx.x; q < len; q += kThreads) put_elem(M, po + q, gfd::enc(s[q]));
-    }
-    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // all bulk writes performed
-}
-
-// Routed-pack form: direct register stores (default) or TMA-staged stores (GF_PACK_TMA=1).
-// Measured at N=2 (ResNet-50): 61 us register vs 69 us TMA-staged, and the TMA form takes 64 us
-// even with every store local — its per-tile load -> stage -> bulk-copy sequence is latency-bound
-// at 2 CTAs per SM, where the register kernel keeps 4 CTAs' loads in flight.
-bool pack_tma() {
-    static const bool v = [] {
-        const char* e = std::getenv("GF_PACK_TMA");
-        return e && std::strcmp(e, "1") == 0;
-    }();
-    return v;
+    // No fence by default: CTAs retire with their NVLink stores in flight. The kernel boundary
+    // orders all of them before rsp_kernel, whose release of the entry flag publishes them
+    // (the ordering argument and the stress test that backs it). GF_PUSH_FENCE=1
+    // adds a system-scope fence per thread — the provable form, for validation runs.
+    if (fence) __threadfence_system();
 }
 
 // CTAs per SM the routed pack is compiled for (register cap 65536 / (256 * MINB)); 4 measured
@@ -369,6 +268,14 @@ rsp_kernel(const __grid_constant__ RingArgs a, const char* __restrict__ inbox_lo
 
 // GF_PUSH_DIAG timing probes (results invalid by design): 1 every routed store local, 2 the
 // routed pack alone (no reduce / all-gather / unpack).
+int push_fence() {
+    static const int v = [] {
+        const char* e = std::getenv("GF_PUSH_FENCE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 int push_diag() {
     static const int v = [] {
         const char* e = std::getenv("GF_PUSH_DIAG");
@@ -394,31 +301,14 @@ int routed_pack(gf_comm* c, cudaStream_t s, uint64_t pool_heap_off, uint64_t inb
         M.wstart[w] = win_start[w];
         M.wlen[w] = win_len[w];
     }
-    const bool tma = pack_tma();
-    if (tma) {
-        static bool attr_set[64] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-            GF_CHECK_CUDA(cudaFuncSetAttribute(pack_push_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               int(kTmaStages * kTile * 2)));
-            attr_set[dev] = true;
-        }
-    }
     return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
                           [&](const TensorTable& T, uint64_t tiles, int grid) {
                               uint64_t spread = std::max<uint64_t>(1, tiles / uint64_t(c->world));
                               while (std::gcd(spread, tiles) != 1) ++spread;
-                              if (tma) {  // persistent: 2 CTAs per SM, each loops over its tiles
-                                  const int g = int(std::min<uint64_t>(tiles, uint64_t(gfi::sm_count()) * 2));
-                                  pack_push_tma_kernel<2><<<g, kThreads, kTmaStages * kTile * 2, s>>>(T, M, tiles,
-                                                                                                      spread);
-                                  return;
-                              }
                               switch (push_minb()) {
-                                  case 6: pack_push_kernel<6><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
-                                  case 8: pack_push_kernel<8><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
-                                  default: pack_push_kernel<4><<<grid, kThreads, 0, s>>>(T, M, tiles, spread); break;
+                                  case 6: pack_push_kernel<6><<<grid, kThreads, 0, s>>>(T, M, tiles, spread, push_fence()); break;
+                                  case 8: pack_push_kernel<8><<<grid, kThreads, 0, s>>>(T, M, tiles, spread, push_fence()); break;
+                                  default: pack_push_kernel<4><<<grid, kThreads, 0, s>>>(T, M, tiles, spread, push_fence()); break;
                               }
                           });
 }
