@@ -43,6 +43,9 @@ struct gf_comm {
     bool colocated = false;
     int grid_cap = 0;
     int max_blocks = 0;  // gf_comm_set_max_blocks (0: automatic)
+    // a second stream + fork/join events for kernels a collective runs side by side
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     uint64_t sel_inbox_off = UINT64_MAX;  // gf_comm_set_select_inbox (UINT64_MAX: pull protocol)
 };
 
