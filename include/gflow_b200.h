@@ -190,6 +190,9 @@ int gf_comm_set_timeout_ms(gf_comm* comm, uint64_t ms);
  * the same on every rank (CTA b pairs with CTA b). A CSC step caps its exchange so the rest of
  * the SMs keep packing beside it. */
 int gf_comm_set_max_blocks(gf_comm* comm, int max_blocks);
+/* CTA size (threads, multiple of 32, <= 512; 0: 512) of the CSC exchange kernels
+ * (gf_ring_allreduce_planned_scatter, gf_csc_exchange_pull). Same on every rank. */
+int gf_comm_set_block_threads(gf_comm* comm, int threads);
 /* GF_OK, or GF_ERR_TRANSPORT once a device-side wait timed out (comm is then poisoned). */
 int gf_comm_status(gf_comm* comm);
 /* Tracing: when on, CTA 0 of every NVLink ring launch stamps %globaltimer (ns) into a

@@ -76,6 +76,7 @@ SIGNATURES = {
     "gf_csc_pack_correct_part": [_i, _vp, _vp, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _vp, _vp, _vp, _i, _f, _vp,
                                  _i, _vp],
     "gf_comm_set_max_blocks": [_vp, _i],
+    "gf_comm_set_block_threads": [_vp, _i],
     "gf_csc_compact": [_i, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _vp],
     "gf_csc_scatter": [_i, _vp, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _vp, _vp],
     "gf_csc_plan": [_vp, _u64, _u64, _u64, _i, _u64, _vp, _vp, _vp],

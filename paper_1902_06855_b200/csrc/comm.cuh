@@ -42,10 +42,9 @@ struct gf_comm {
     // barrier-waiting CTAs fit on the SMs at once
     bool colocated = false;
     int grid_cap = 0;
-    int max_blocks = 0;  // gf_comm_set_max_blocks (0: automatic)
-    // a second stream + fork/join events for kernels a collective runs side by side
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int max_blocks = 0;     // gf_comm_set_max_blocks (0: automatic)
+    int block_threads = 0;  // gf_comm_set_block_threads: CTA size of the CSC exchange (0: 512)
+
     uint64_t sel_inbox_off = UINT64_MAX;  // gf_comm_set_select_inbox (UINT64_MAX: pull protocol)
 };
 

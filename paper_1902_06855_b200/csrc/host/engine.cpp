@@ -93,7 +93,8 @@ struct gf_engine {
     uint64_t* plan[2] = {};
     uint64_t* nacc = nullptr;
     uint64_t iteration = 0;
-    int xblocks = 0;  // CTAs of the CSC exchange (the packing of the other chunks runs beside it)
+    int xblocks = 0;   // CTAs of the CSC exchange (the packing of the other chunks runs beside it)
+    int xthreads = 0;  // their size (0: 512)
     // streams / events (created on the engine's device, non-blocking)
     cudaStream_t side = nullptr, comm_s = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_ready = nullptr, ev_done = nullptr, ev_sel = nullptr,
@@ -284,6 +285,7 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
     dense_windows(e);
     if (const char* xb = std::getenv("GF_CSC_XBLOCKS")) e->xblocks = std::max(0, std::atoi(xb));
     else e->xblocks = 64;
+    if (const char* xt = std::getenv("GF_CSC_XTHREADS")) e->xthreads = std::max(0, std::atoi(xt));
     // symmetric heap: [pool | (pull: 2nd pool) | (rspush: N-1 inbox slots) | (CSC: staging) | norms | (CSC N>1: select inbox)]
     const uint64_t pool_bytes = align_up(e->total * e->esz);
     e->pool_off = 0;
@@ -503,8 +505,10 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
         GF_ENG_OK(pack_correct(1, s));
         if (e->marks_on) {
             GF_ENG_OK(gf_comm_set_max_blocks(e->comm, e->xblocks));
+            GF_ENG_OK(gf_comm_set_block_threads(e->comm, e->xthreads));
             const int rc = exchange();
             gf_comm_set_max_blocks(e->comm, 0);
+            gf_comm_set_block_threads(e->comm, 0);
             GF_ENG_OK(rc);
             mark(e, "pack_correct_rest", s);
             GF_ENG_OK(pack_correct(2, s));
@@ -514,8 +518,10 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
             GF_ENG_OK(pack_correct(2, e->side));
             GF_ENG_CUDA(cudaEventRecord(e->ev_rest, e->side));
             GF_ENG_OK(gf_comm_set_max_blocks(e->comm, e->xblocks));
+            GF_ENG_OK(gf_comm_set_block_threads(e->comm, e->xthreads));
             const int rc = exchange();
             gf_comm_set_max_blocks(e->comm, 0);
+            gf_comm_set_block_threads(e->comm, 0);
             GF_ENG_OK(rc);
             GF_ENG_CUDA(cudaStreamWaitEvent(s, e->ev_rest, 0));
         }

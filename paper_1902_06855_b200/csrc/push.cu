@@ -32,7 +32,6 @@ namespace {
 
 struct SegMap {  // routing of pool elements to their owners (explicit windows)
     int nwin, world, pos, diag;  // diag: GF_PUSH_DIAG timing probe (1: every store local; results invalid)
-    int part;                    // 0 every vector; 1 my own segment's only; 2 the other owners' only
     uint64_t slot_elems;                 // elements per inbox slot (the pool span)
     char* pool_local;                    // my pool (fp16)
     char* inbox_by_pos[GF_MAX_RANKS];    // owner at ring position j: its inbox as mapped here
@@ -93,48 +92,34 @@ pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ 
         __syncthreads();  // the previous tile's readers of R are done
         if (threadIdx.x == 0) tile_route(M, po, R);
         __syncthreads();
-        if (M.part != 0) {  // a tile wholly inside / outside my segment is skipped by the other part
-            const bool mine = R.start[M.pos] <= po && po + len <= R.start[M.pos + 1];
-            const bool none = po + len <= R.start[M.pos] || R.start[M.pos + 1] <= po;
-            if ((M.part == 1 && none) || (M.part == 2 && mine)) continue;
-        }
-        auto wanted = [&](int j) { return M.part == 0 || (M.part == 1) == (j == M.pos); };
-        auto put = [&](uint64_t e, uint16_t h) {
-            const int j = tile_owner(R, M.world, e);
-            if (wanted(j)) R.dst[j][e] = h;
-        };
+        auto put = [&](uint64_t e, uint16_t h) { R.dst[tile_owner(R, M.world, e)][e] = h; };
         uint64_t done = 0;
         if ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0 && po % 8 == 0) {
             const int nvec = int(len / 8);
             float4 a[kVecPerThread], b[kVecPerThread];
-            int own[kVecPerThread];
 #pragma unroll
             for (int k = 0; k < kVecPerThread; ++k) {
                 const int v = threadIdx.x + k * kThreads;
-                own[k] = -1;
                 if (v < nvec) {
-                    const uint64_t e = po + 8 * uint64_t(v);
-                    const int j = tile_owner(R, M.world, e);
-                    const bool whole = e + 8 <= R.start[j + 1];
-                    if (!whole || wanted(j)) {
-                        own[k] = whole ? j : GF_MAX_RANKS;  // GF_MAX_RANKS: straddles a boundary
-                        const gfd::F8 f = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
-                        a[k] = f.lo;
-                        b[k] = f.hi;
-                    }
+                    const gfd::F8 f = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
+                    a[k] = f.lo;
+                    b[k] = f.hi;
                 }
             }
 #pragma unroll
             for (int k = 0; k < kVecPerThread; ++k) {
-                if (own[k] < 0) continue;
-                const uint64_t e = po + 8 * uint64_t(threadIdx.x + k * kThreads);
-                const uint4 h = gfd::enc8(a[k], b[k]);
-                if (own[k] < GF_MAX_RANKS) {  // the whole vector belongs to one owner
-                    gfd::st16(R.dst[own[k]] + e, h);
-                } else {                      // a segment boundary inside the vector
-                    const uint32_t w[4] = {h.x, h.y, h.z, h.w};
+                const int v = threadIdx.x + k * kThreads;
+                if (v < nvec) {
+                    const uint4 h = gfd::enc8(a[k], b[k]);
+                    const uint64_t e = po + 8 * uint64_t(v);
+                    const int j = tile_owner(R, M.world, e);
+                    if (e + 8 <= R.start[j + 1]) {  // the whole vector belongs to one owner
+                        gfd::st16(R.dst[j] + e, h);
+                    } else {                         // a segment boundary inside the vector
+                        const uint32_t w[4] = {h.x, h.y, h.z, h.w};
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) put(e + q, uint16_t((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu));
+                        for (int q = 0; q < 8; ++q) put(e + q, uint16_t((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu));
+                    }
                 }
             }
             done = uint64_t(nvec) * 8;
@@ -302,10 +287,9 @@ int push_diag() {
 // The routed pack of one group of <= kMaxW windows (the tensors inside them).
 int routed_pack(gf_comm* c, cudaStream_t s, uint64_t pool_heap_off, uint64_t inbox_heap_off, uint64_t slot_elems,
                 const float* const* src, const uint64_t* pool_off, const uint64_t* count, int ntensors,
-                const uint64_t* win_start, const uint64_t* win_len, int nwin, int part = 0) {
+                const uint64_t* win_start, const uint64_t* win_len, int nwin) {
     SegMap M;
     std::memset(&M, 0, sizeof(M));
-    M.part = part;
     M.nwin = nwin;
     M.world = c->world;
     M.pos = c->pos;
@@ -329,48 +313,16 @@ int routed_pack(gf_comm* c, cudaStream_t s, uint64_t pool_heap_off, uint64_t inb
                           });
 }
 
-// The routed pack as two concurrent grids (GF_PUSH_SPLIT=1): my own segment's vectors (HBM only)
-// on the caller's stream and the other owners' (the NVLink stores) on the communicator's side
-// stream, so the remote stores no longer share CTAs with the local ones.
-bool push_split() {
-    static const bool v = [] {
-        const char* e = std::getenv("GF_PUSH_SPLIT");
-        return e && std::strcmp(e, "1") == 0;
-    }();
-    return v;
-}
-
-int routed_pack_any(gf_comm* c, cudaStream_t s, uint64_t pool_heap_off, uint64_t inbox_heap_off, uint64_t slot_elems,
-                    const float* const* src, const uint64_t* pool_off, const uint64_t* count, int ntensors,
-                    const uint64_t* win_start, const uint64_t* win_len, int nwin) {
-    if (!push_split())
-        return routed_pack(c, s, pool_heap_off, inbox_heap_off, slot_elems, src, pool_off, count, ntensors, win_start,
-                           win_len, nwin, 0);
-    if (!c->side) {
-        GF_CHECK_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-        GF_CHECK_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-        GF_CHECK_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-    }
-    GF_CHECK_CUDA(cudaEventRecord(c->ev_fork, s));
-    GF_CHECK_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    if (int rc = routed_pack(c, c->side, pool_heap_off, inbox_heap_off, slot_elems, src, pool_off, count, ntensors,
-                             win_start, win_len, nwin, 2))
-        return rc;
-    if (int rc = routed_pack(c, s, pool_heap_off, inbox_heap_off, slot_elems, src, pool_off, count, ntensors,
-                             win_start, win_len, nwin, 1))
-        return rc;
-    GF_CHECK_CUDA(cudaEventRecord(c->ev_join, c->side));
-    GF_CHECK_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
-    return GF_OK;
-}
-
-// The unpack fused into rsp_kernel (default) or a separate unpack launch (GF_FUSE_UNPACK=0).
-bool fuse_unpack() {
-    static const bool v = [] {
+// The unpack fused into rsp_kernel or a separate unpack launch. Measured: fused wins
+// at N=2 (the own half is unpacked while the pushes drain; AlexNet 0.274 vs 0.285 ms), but from
+// N=4 the (N-1)/N of the pool unpacked after the exit barrier by the 1-CTA-per-SM grid costs more
+// than a separate full-grid unpack (ResNet-50 0.187 vs 0.178 ms). GF_FUSE_UNPACK=0/1 overrides.
+bool fuse_unpack(int world) {
+    static const int v = [] {
         const char* e = std::getenv("GF_FUSE_UNPACK");
-        return !(e && std::strcmp(e, "0") == 0);
+        return e ? std::atoi(e) : -1;
     }();
-    return v;
+    return v < 0 ? world == 2 : v != 0;
 }
 
 }  // namespace
@@ -413,7 +365,7 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
     const char* inbox_local = c->alloc + kFlagBytes + inbox_heap_off;
     // the unpack rides in rsp_kernel when the tensors fit its table and one launch covers the
     // windows (the usual case); otherwise a separate unpack follows
-    const bool fused = ntensors <= kStepMaxT && nwin <= kMaxW && fuse_unpack();
+    const bool fused = ntensors <= kStepMaxT && nwin <= kMaxW && fuse_unpack(c->world);
     StepTable TT;
     std::memset(&TT, 0, sizeof(TT));
     if (fused) {
@@ -441,9 +393,9 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
         }
         // 1. pack, routed to the owners
         gfi::phase("pack_push", s);
-        if (int rc = routed_pack_any(c, s, pool_heap_off, inbox_heap_off, slot_elems,
-                                     reinterpret_cast<const float* const*>(gsrc.data()), goff.data(), gcnt.data(),
-                                     int(gsrc.size()), win_start + first, win_len + first, nw))
+        if (int rc = routed_pack(c, s, pool_heap_off, inbox_heap_off, slot_elems,
+                                 reinterpret_cast<const float* const*>(gsrc.data()), goff.data(), gcnt.data(),
+                                 int(gsrc.size()), win_start + first, win_len + first, nw))
             return rc;
         if (push_diag() == 2) continue;  // timing probe: the routed pack alone (results invalid)
         // 2. local reduce + all-gather push (+ the unpack when fused)

@@ -462,7 +462,8 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
 }
 
 template <int DT, bool P2P>
-void launch_ring_dt(const RingArgs& a, dim3 grid, cudaStream_t s, size_t smem) {
+void launch_ring_dt(const RingArgs& a, dim3 grid, cudaStream_t s, size_t smem, int threads) {
+    const int kRingThreads = threads;  // the CTA size of this launch (<= the compiled 512)
     switch (a.world) {
         case 2: ring_kernel<DT, 2, P2P><<<grid, kRingThreads, smem, s>>>(a); break;
         case 3: ring_kernel<DT, 3, P2P><<<grid, kRingThreads, smem, s>>>(a); break;
@@ -474,11 +475,14 @@ void launch_ring_dt(const RingArgs& a, dim3 grid, cudaStream_t s, size_t smem) {
         default: ring_kernel<DT, 0, P2P><<<grid, kRingThreads, smem, s>>>(a); break;
     }
 }
-void launch_ring(int dtype, bool p2p, const RingArgs& a, dim3 grid, cudaStream_t s, size_t smem = 0) {
+void launch_ring(int dtype, bool p2p, const RingArgs& a, dim3 grid, cudaStream_t s, size_t smem = 0,
+                 int threads = kRingThreads) {
     if (dtype == GF_F16) {
-        if (p2p) launch_ring_dt<GF_F16, true>(a, grid, s, smem); else launch_ring_dt<GF_F16, false>(a, grid, s, smem);
+        if (p2p) launch_ring_dt<GF_F16, true>(a, grid, s, smem, threads);
+        else launch_ring_dt<GF_F16, false>(a, grid, s, smem, threads);
     } else {
-        if (p2p) launch_ring_dt<GF_F32, true>(a, grid, s, smem); else launch_ring_dt<GF_F32, false>(a, grid, s, smem);
+        if (p2p) launch_ring_dt<GF_F32, true>(a, grid, s, smem, threads);
+        else launch_ring_dt<GF_F32, false>(a, grid, s, smem, threads);
     }
 }
 
@@ -573,9 +577,6 @@ int gf_comm_destroy(gf_comm* c) {
     cudaDeviceSynchronize();
     for (int r = 0; r < c->world; ++r)
         if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->peer_alloc[r]);
-    if (c->side) cudaStreamDestroy(c->side);
-    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-    if (c->ev_join) cudaEventDestroy(c->ev_join);
     cudaFree(c->alloc);
     cudaFreeHost(c->err_host);
     delete c;
@@ -697,6 +698,13 @@ int gf_comm_set_timeout_ms(gf_comm* c, uint64_t ms) {
 int gf_comm_set_max_blocks(gf_comm* c, int max_blocks) {
     if (!c || max_blocks < 0) return gfi::fail(GF_ERR_CONFIG, "gf_comm_set_max_blocks: bad arguments");
     c->max_blocks = std::min(max_blocks, kMaxBlocks);
+    return GF_OK;
+}
+
+int gf_comm_set_block_threads(gf_comm* c, int threads) {
+    if (!c || threads < 0 || threads > kRingThreads || threads % 32 != 0)
+        return gfi::fail(GF_ERR_CONFIG, "gf_comm_set_block_threads: 0 (default 512) or a multiple of 32 up to 512");
+    c->block_threads = threads;
     return GF_OK;
 }
 
@@ -884,7 +892,8 @@ int gf_ring_allreduce_planned_scatter(gf_comm* c, int dtype, uint64_t stage_heap
     a.wb_chunk = chunk;
     a.wb_nc = nc;
     const uint64_t bound = c->heap_bytes > stage_heap_off ? (c->heap_bytes - stage_heap_off) / c->world : 0;
-    launch_ring(dtype, true, a, dim3(gfr::comm_blocks(c, bound)), gfi::S(stream), size_t(nc) * 8);
+    launch_ring(dtype, true, a, dim3(gfr::comm_blocks(c, bound)), gfi::S(stream), size_t(nc) * 8,
+                c->block_threads > 0 ? c->block_threads : kRingThreads);
     gfi::count_launch();
     return gfi::check_launch("gf_ring_allreduce_planned_scatter");
 }
@@ -911,11 +920,12 @@ int gf_csc_exchange_pull(gf_comm* c, uint64_t stage_heap_off, const uint64_t* pl
     const dim3 grid(gfr::comm_blocks(c, bound));
     const size_t smem = size_t(nc) * 8;
     cudaStream_t s = gfi::S(stream);
+    const int th = c->block_threads > 0 ? c->block_threads : kRingThreads;
     switch (c->world) {
-        case 2: csc_pull_kernel<2><<<grid, kRingThreads, smem, s>>>(a); break;
-        case 4: csc_pull_kernel<4><<<grid, kRingThreads, smem, s>>>(a); break;
-        case 8: csc_pull_kernel<8><<<grid, kRingThreads, smem, s>>>(a); break;
-        default: csc_pull_kernel<0><<<grid, kRingThreads, smem, s>>>(a); break;
+        case 2: csc_pull_kernel<2><<<grid, th, smem, s>>>(a); break;
+        case 4: csc_pull_kernel<4><<<grid, th, smem, s>>>(a); break;
+        case 8: csc_pull_kernel<8><<<grid, th, smem, s>>>(a); break;
+        default: csc_pull_kernel<0><<<grid, th, smem, s>>>(a); break;
     }
     gfi::count_launch();
     return gfi::check_launch("gf_csc_exchange_pull");

@@ -405,3 +405,14 @@ def test_colo_timeout_is_transport_error():
             capi.call("gf_ring_allreduce", comms[0], F32, 0, capi.u64_array([0]), capi.u64_array([8]), 1, streams[0])
     finally:
         close_raw(comms, streams)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("csc_mode", ["push", "pull"])
+def test_colo_csc_exchange_small_ctas(reference, world, csc_mode, monkeypatch):
+    """The CSC exchange with its grid capped and 256-thread CTAs (GF_CSC_XBLOCKS /
+    GF_CSC_XTHREADS, the engine's overlap knobs): same results as the reference."""
+    monkeypatch.setenv("GF_CSC_XBLOCKS", "8")
+    monkeypatch.setenv("GF_CSC_XTHREADS", "256")
+    sizes = [1000, 64, 3000, 5, 8192, 7777, 12000, 31, 2048, 4099]
+    run_csc_vs_reference(reference, sizes, world, 1000, 3000, 4, csc_mode, sparsity=0.75, warmup=1)
