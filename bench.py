@@ -368,6 +368,11 @@ class Run:
         out = {"ms": ms, "launches": int(launches), "host_enqueue_ms_per_step": round(host_enqueue_ms, 4),
                "kernel_timing": kernel_timing}
         out.update(self.roofline(seg_ms))
+        if self.world > 1:  # the whole step against NVLink: the ring's bytes over the step's time
+            sb = out["ring_bus_bytes"] / (ms / 1e3) / 1e9
+            out["step_bus"] = {"GBps": round(sb, 1), "frac_900": round(sb / NVLINK_GBS, 3),
+                               "bytes": int(out["ring_bus_bytes"]),
+                               "note": "2(N-1)/N x K (NCCL busBw convention) / whole step incl. pack and unpack"}
         if e2e and not args.no_e2e:
             out["e2e"] = self.e2e()
             if self.world == 1:
@@ -398,9 +403,14 @@ class Run:
             ring_bytes = ring_bus_bytes(esz, world, [staged])
         else:
             ring_bytes = ring_bus_bytes(esz, world, wlen)
-        for k in ("ring", "ring_scatter", "ring_unpack", "rsp"):
+        for k in ("ring", "ring_scatter", "ring_unpack"):
             algo[k] = ring_bytes if world > 1 else None
-        nvlink = ("ring", "ring_scatter", "ring_unpack", "rsp")
+        # rspush splits the ring's bytes: the routed pack pushes the reduce-scatter half (its
+        # binding bound at N>1: the HBM side is 6 B/el), rsp_kernel pushes the all-gather half
+        if world > 1 and not self.csc:
+            algo["rsp"] = ring_bytes / 2
+            algo["pack_push"] = ring_bytes / 2
+        nvlink = ("ring", "ring_scatter", "ring_unpack", "rsp") + (("pack_push",) if world > 1 else ())
         kernels = {}
         for k, v in seg_ms.items():
             d = {"ms": round(v, 4)}
@@ -440,9 +450,11 @@ class Run:
                 pass
         bus = None
         if world > 1:
-            rk = next((k for k in ("rsp", "ring", "ring_unpack", "ring_scatter") if k in seg_ms), None)
+            rk = next((k for k in ("ring", "ring_unpack", "ring_scatter") if k in seg_ms), None)
             if rk:
                 bus = round(ring_bytes / (seg_ms[rk] / 1e3) / 1e9, 1)
+            elif "rsp" in seg_ms and "pack_push" in seg_ms:  # the two kernels that carry the ring's bytes
+                bus = round(ring_bytes / ((seg_ms["rsp"] + seg_ms["pack_push"]) / 1e3) / 1e9, 1)
         return {"kernels": kernels, "roofline": roof, "bus_gbs": bus, "ring_bus_bytes": ring_bytes}
 
     def e2e(self):
@@ -730,7 +742,8 @@ def main():
             "exchange": exchange,
             "l2_policy": f"{run.n_sets} rotating input sets of {run.in_bytes >> 20} MiB (> 126 MB L2 in total)",
             "parity": res["parity"], "parity_detail": res.get("parity_detail"),
-            "bus_gbs": res["bus_gbs"], "kernels": res["kernels"], "kernel_timing": res["kernel_timing"],
+            "bus_gbs": res["bus_gbs"], "step_bus": res.get("step_bus"), "kernels": res["kernels"],
+            "kernel_timing": res["kernel_timing"],
             "roofline": res["roofline"], "cpu_baseline": res.get("cpu_baseline"), "e2e": res.get("e2e"),
             "e2e_api": res.get("e2e_api"),
             "nccl_allreduce": nccl, "gpu_launches": res["launches"], "clocks": clk,

@@ -190,7 +190,7 @@ def run_csc_vs_reference(reference, sizes, world, chunk, theta, steps, csc_mode,
         cw.close()
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 @pytest.mark.parametrize("csc_mode", ["push", "pull"])
 @pytest.mark.parametrize("theta", [0, 5000, THETA_INF])
 def test_colo_csc_engine_vs_reference(reference, world, csc_mode, theta):
@@ -210,11 +210,12 @@ def test_colo_alexnet_csc_full_vs_reference(reference, world, csc_mode):
     run_csc_vs_reference(reference, ALEXNET, world, 32000, THETA_INF, 3, csc_mode, full=True)
 
 
-def test_colo_resnet50_csc_theta_full_vs_reference(reference):
+@pytest.mark.parametrize("world,csc_mode", [(4, "push"), (8, "pull")])
+def test_colo_resnet50_csc_theta_full_vs_reference(reference, world, csc_mode):
     """BASELINE configs[3]: ResNet-50 CSC with a lazy-fusion threshold (1 MiB: many windows over
-    the staging buffer) and residual carry-over, 4 ranks, 3 iterations."""
+    the staging buffer) and residual carry-over, 3 iterations, at 4 and 8 ranks."""
     from oracle.oracle import RESNET50
-    run_csc_vs_reference(reference, RESNET50, 4, 32000, 1 << 20, 3, "push", full=True)
+    run_csc_vs_reference(reference, RESNET50, world, 32000, 1 << 20, 3, csc_mode, full=True)
 
 
 def test_colo_overlap_windows(oracle):
