@@ -283,8 +283,12 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
     if (mode == GF_DENSE_PULL && ntensors > GF_MAX_WINDOWS_PER_LAUNCH) mode = GF_DENSE_PUSH;  // 256-tensor table
     e->dense_mode = mode;
     dense_windows(e);
+    // the CSC exchange beside the packing of the unselected chunks: 64 CTAs of 256 threads, so
+    // that packing CTAs share the exchange's SMs (measured at N=2/4: 0.226 / 0.234 ms
+    // AlexNet CSC against 0.232 / 0.242 with 64 CTAs of 512 threads)
+    e->xblocks = 64;
+    e->xthreads = 256;
     if (const char* xb = std::getenv("GF_CSC_XBLOCKS")) e->xblocks = std::max(0, std::atoi(xb));
-    else e->xblocks = 64;
     if (const char* xt = std::getenv("GF_CSC_XTHREADS")) e->xthreads = std::max(0, std::atoi(xt));
     // symmetric heap: [pool | (pull: 2nd pool) | (rspush: N-1 inbox slots) | (CSC: staging) | norms | (CSC N>1: select inbox)]
     const uint64_t pool_bytes = align_up(e->total * e->esz);
