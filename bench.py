@@ -576,6 +576,9 @@ def nccl_compare(run):
     return {"ms": round(nms, 4), "busbw_GBps": round(2 * (w - 1) / w * run.total * 2 / (nms / 1e3) / 1e9, 1)}
 
 
+SELECT_PHASES = ["finalize+push", "entry_wait", "sum", "exit_wait", "topk", "plan"]
+
+
 def ring_trace(run):
     """Device timestamps of CTA 0 of the NVLink kernel (diagnostic, outside the timed region)."""
     import ctypes as C
@@ -592,6 +595,9 @@ def ring_trace(run):
                    ([t[5] - t[4], t[6] - t[5], t[7] - t[6], t[8] - t[7], t[9] - t[8], t[10] - t[9]]
                     if run.csc else []))
     capi.call("gf_comm_set_trace", run.sync.comm, 0)
+    if run.world == 1:  # no NVLink kernel: the selection's phases only
+        return {"select_phases_us": [round(statistics.median(r[j] for r in rec) / 1e3, 2) for j in range(3, 9)],
+                "select_phase_names": SELECT_PHASES}
     med = [statistics.median(r[j] for r in rec) / 1e3 for j in range(3)]
     out = {"entry_wait_us": round(run.allmax(med[0]), 2), "body_us": round(run.allmax(med[1]), 2),
            "exit_wait_us": round(run.allmax(med[2]), 2)}
@@ -601,6 +607,7 @@ def ring_trace(run):
     if run.csc:
         out["select_phases_us"] = [round(run.allmax(statistics.median(r[j] for r in rec) / 1e3), 2)
                                    for j in range(3, 9)]
+        out["select_phase_names"] = SELECT_PHASES
     return out
 
 
@@ -711,7 +718,7 @@ def main():
     run = Run(args, args.workload, world, rank, local, dist, allgather)
     res = run.measure(clocks=clocks)
     extra = {}
-    if args.trace and world > 1:
+    if args.trace and (world > 1 or run.csc):
         extra["ring_trace"] = ring_trace(run)
     if args.overlap > 0 and not run.csc:
         extra["overlap"] = dict(overlap_probe(run, args.overlap), sync_alone_ms=round(res["ms"], 4))

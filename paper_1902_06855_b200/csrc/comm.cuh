@@ -44,6 +44,9 @@ struct gf_comm {
     int grid_cap = 0;
     int max_blocks = 0;     // gf_comm_set_max_blocks (0: automatic)
     int block_threads = 0;  // gf_comm_set_block_threads: CTA size of the CSC exchange (0: 512)
+    // a second stream + events for kernels a collective runs beside each other (pipelined rspush)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev[8] = {};
 
     uint64_t sel_inbox_off = UINT64_MAX;  // gf_comm_set_select_inbox (UINT64_MAX: pull protocol)
 };

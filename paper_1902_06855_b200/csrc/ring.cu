@@ -548,6 +548,9 @@ int gf_comm_create(int world, int rank, int device, uint64_t heap_bytes, gf_comm
     c->world = world;
     c->rank = rank;
     c->device = device;
+    // GF_DIAG_NOWAIT=1: cross-GPU barriers signal but never wait (timeout 0). A traffic probe for
+    // ncu's kernel replay of ONE rank (scripts/diag/ncu_nvl.sh); every result is invalid.
+    if (const char* e = std::getenv("GF_DIAG_NOWAIT"); e && std::atoi(e) == 1) c->timeout_ns = 0;
     c->heap_bytes = (heap_bytes + 255) & ~uint64_t(255);
     for (int i = 0; i < world; ++i) c->ring[i] = i;
     c->pos = rank;
@@ -577,6 +580,9 @@ int gf_comm_destroy(gf_comm* c) {
     cudaDeviceSynchronize();
     for (int r = 0; r < c->world; ++r)
         if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->peer_alloc[r]);
+    if (c->side) cudaStreamDestroy(c->side);
+    for (cudaEvent_t e : c->ev)
+        if (e) cudaEventDestroy(e);
     cudaFree(c->alloc);
     cudaFreeHost(c->err_host);
     delete c;
@@ -691,7 +697,7 @@ int gf_comm_set_ring_order(gf_comm* c, const int* order) {
 
 int gf_comm_set_timeout_ms(gf_comm* c, uint64_t ms) {
     if (!c) return gfi::fail(GF_ERR_CONFIG, "null communicator");
-    c->timeout_ns = ms * 1000ull * 1000ull;
+    c->timeout_ns = std::max<uint64_t>(ms * 1000ull * 1000ull, 1);  // 0 is the no-wait probe
     return GF_OK;
 }
 

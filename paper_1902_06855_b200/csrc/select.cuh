@@ -68,20 +68,6 @@ struct SelShared {
 // Keys of up to kSelThreads * kKeysPerThread chunks stay in registers across the passes.
 constexpr int kKeysPerThread = 4;
 
-template <typename F>
-__device__ __forceinline__ void for_each_key(const float* norms, uint64_t nc, const uint32_t* kr, bool cached,
-                                             F&& fn) {
-    if (cached) {
-#pragma unroll
-        for (int q = 0; q < kKeysPerThread; ++q) {
-            const uint64_t i = threadIdx.x + uint64_t(q) * kSelThreads;
-            if (i < nc) fn(i, kr[q]);
-        }
-    } else {
-        for (uint64_t i = threadIdx.x; i < nc; i += kSelThreads) fn(i, norm_key(norms[i]));
-    }
-}
-
 inline __device__ void block_topk(const float* norms, uint64_t nc, uint64_t k, uint8_t* flags,
                            SelShared& sh) {
     const int tid = threadIdx.x;
@@ -103,10 +89,23 @@ inline __device__ void block_topk(const float* norms, uint64_t nc, uint64_t k, u
         const int shift = 24 - 8 * pass;
         for (int d = tid; d < 256; d += kSelThreads) sh.hist[d] = 0;
         __syncthreads();
-        for_each_key(norms, nc, kr, cached, [&](uint64_t, uint32_t key) {
-            const bool match = pass == 0 || (key >> (shift + 8)) == prefix;
-            if (match) atomicAdd(&sh.hist[(key >> shift) & 255u], 1u);
-        });
+        // Warp-aggregated: chunk norms share a few exponents, so most keys of a pass fall into one
+        // or two digits and per-key shared atomics would serialise on one address.
+        auto count = [&](bool valid, uint32_t key) {
+            valid = valid && (pass == 0 || (key >> (shift + 8)) == prefix);
+            const uint32_t d = (key >> shift) & 255u;
+            const unsigned same = __match_any_sync(0xFFFFFFFFu, valid ? d : 0xFFFFFFFFu);
+            if (valid && __ffs(same) - 1 == (tid & 31)) atomicAdd(&sh.hist[d], unsigned(__popc(same)));
+        };
+        if (cached) {
+#pragma unroll
+            for (int q = 0; q < kKeysPerThread; ++q) count(tid + uint64_t(q) * kSelThreads < nc, kr[q]);
+        } else {
+            for (uint64_t base = 0; base < nc; base += kSelThreads) {
+                const uint64_t i = base + tid;
+                count(i < nc, i < nc ? norm_key(norms[i]) : 0u);
+            }
+        }
         __syncthreads();
         if (tid < 32) {
             // warp 0: lane l owns digits 255-8l .. 248-8l (descending); find the digit where
