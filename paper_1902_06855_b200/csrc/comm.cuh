@@ -7,6 +7,9 @@
 //   [0, kFlagWords)                 ring barrier flags  flags[cta][src_rank]   (peers write)
 //   [kFlagWords, +kMaxBlocks)       per-CTA epoch counters (local)
 //   [+kMaxBlocks, +32)              ring work/done counters (local)
+//   kPipeGenOff   [kMaxBlocks]                  pipe kernel per-CTA generations (local)
+//   kPipeRsOff    [kPipeUnits][GF_MAX_RANKS]    pipe RS flags: unit u of my segment from rank r (peers write)
+//   kPipeAgOff    [GF_MAX_RANKS][kPipeUnits]    pipe AG flags: unit u of the owner at position j (peers write)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -23,7 +26,12 @@ constexpr int kMaxW = GF_MAX_WINDOWS_PER_LAUNCH;
 constexpr int kRingThreads = 512;
 constexpr uint64_t kFlagWords = uint64_t(kMaxBlocks) * GF_MAX_RANKS;
 constexpr uint64_t kRingFlagBytes = (kFlagWords + kMaxBlocks + 32) * sizeof(uint64_t);
-constexpr uint64_t kFlagBytes = kRingFlagBytes;
+constexpr uint64_t kPipeUnits = 4096;  // units per owner of one pipe step (pipe.cu)
+constexpr uint64_t kPipeGenOff = kRingFlagBytes;
+constexpr uint64_t kPipeRsOff = kPipeGenOff + uint64_t(kMaxBlocks) * sizeof(uint64_t);
+constexpr uint64_t kPipeAgOff = kPipeRsOff + kPipeUnits * GF_MAX_RANKS * sizeof(uint64_t);
+constexpr uint64_t kFlagBytes = kPipeAgOff + uint64_t(GF_MAX_RANKS) * kPipeUnits * sizeof(uint64_t);
+static_assert(kFlagBytes % 256 == 0, "the symmetric heap stays 256-byte aligned");
 
 struct gf_comm {
     int world = 0, rank = 0, device = 0, pos = 0;
@@ -44,10 +52,6 @@ struct gf_comm {
     int grid_cap = 0;
     int max_blocks = 0;     // gf_comm_set_max_blocks (0: automatic)
     int block_threads = 0;  // gf_comm_set_block_threads: CTA size of the CSC exchange (0: 512)
-    // a second stream + events for kernels a collective runs beside each other (pipelined rspush)
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev[8] = {};
-
     uint64_t sel_inbox_off = UINT64_MAX;  // gf_comm_set_select_inbox (UINT64_MAX: pull protocol)
 };
 

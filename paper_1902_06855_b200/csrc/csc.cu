@@ -333,50 +333,75 @@ __device__ __forceinline__ int tensor_of(const TensorTable& T, uint64_t e) {
     return (lo < T.n && e < T.off[lo] + T.cnt[lo]) ? lo : -1;
 }
 
+// Staging element s <-> pool element: s lies in important chunk q = min(s / chunk, k - 1) of the
+// plan (the staging buffer holds the chunks packed ascending, all `chunk` long except the final
+// pool chunk, which is last when selected).
+__device__ __forceinline__ uint64_t staged_to_pool(const uint64_t* plan, uint64_t k, uint64_t chunk, uint64_t s) {
+    const uint64_t q = min(s / chunk, k - 1);
+    return plan[4 + q] * chunk + (s - q * chunk);
+}
+
+// The grid sweeps the staging index space [0, plan[0]) in 8-element vectors (kPlannedU per
+// thread, every load in flight before the math); each vector maps to its pool element through
+// the plan. Work is proportional to the staged data only.
+constexpr int kPlannedU = 2;
 template <int DT>
 __global__ void __launch_bounds__(kThreads, 4)
 pack_correct_planned_kernel(const __grid_constant__ TensorTable T, void* __restrict__ pool, float* __restrict__ hg,
-                            void* __restrict__ staging, const uint64_t* __restrict__ plan,
-                            const uint64_t* __restrict__ coff, uint64_t total, uint64_t chunk, uint64_t nc,
-                            uint64_t per, float mom) {
-    const uint64_t k = plan[1];
-    for (uint64_t item = blockIdx.x; item < k * per; item += gridDim.x) {
-        const uint64_t c = plan[4 + item / per];
-        const uint64_t cb = c * chunk, clen = (c + 1 == nc) ? total - cb : chunk;
-        const uint64_t s0 = (item % per) * kTile;
-        if (s0 >= clen) continue;
-        const uint64_t e0 = cb + s0, e1 = cb + min(clen, s0 + kTile);
-        const uint64_t so = coff[c] - cb;  // staging index = pool index + so
-        for (uint64_t e = e0 + 8 * uint64_t(threadIdx.x); e < e1; e += 8 * uint64_t(kThreads)) {
+                            void* __restrict__ staging, const uint64_t* __restrict__ plan, uint64_t chunk, float mom) {
+    const uint64_t staged = plan[0], k = plan[1];
+    if (k == 0) return;
+    const uint64_t nv = (staged + 7) / 8, G = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t v0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v0 < nv; v0 += G * kPlannedU) {
+        gfd::F8 gv[kPlannedU], hv[kPlannedU];
+        uint64_t pe[kPlannedU];
+        bool fast[kPlannedU];
+#pragma unroll
+        for (int u = 0; u < kPlannedU; ++u) {
+            const uint64_t v = v0 + uint64_t(u) * G, s = v * 8;
+            fast[u] = false;
+            pe[u] = 0;
+            if (v >= nv) continue;
+            const uint64_t e = staged_to_pool(plan, k, chunk, s);
+            pe[u] = e;
             const int t = tensor_of(T, e);
-            const float* src = t >= 0 ? static_cast<const float*>(T.ptr[t]) + (e - T.off[t]) : nullptr;
-            if (DT == GF_F16 && t >= 0 && e + 8 <= min(e1, T.off[t] + T.cnt[t]) && e % 8 == 0 &&
-                ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(hg + e)) & 31u) == 0 &&
-                ((reinterpret_cast<uintptr_t>(static_cast<uint16_t*>(pool) + e) |
-                  reinterpret_cast<uintptr_t>(static_cast<uint16_t*>(staging) + e + so)) & 15u) == 0) {
-                const gfd::F8 gv = gfd::ld32f_stream(src);
-                const gfd::F8 hv = gfd::ld32f(hg + e);
+            if (DT != GF_F16 || t < 0 || chunk % 8 != 0 || s + 8 > staged || e % 8 != 0 ||
+                e + 8 > T.off[t] + T.cnt[t])
+                continue;
+            const float* src = static_cast<const float*>(T.ptr[t]) + (e - T.off[t]);
+            if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(hg + e)) & 31u) != 0) continue;
+            fast[u] = true;
+            gv[u] = gfd::ld32f_stream(src);
+            hv[u] = gfd::ld32f(hg + e);
+        }
+#pragma unroll
+        for (int u = 0; u < kPlannedU; ++u) {
+            const uint64_t v = v0 + uint64_t(u) * G;
+            if (v >= nv) continue;
+            if (fast[u]) {
+                const uint64_t e = pe[u];
                 float hn[8];
                 uint4 ov;
                 bool nan;
-                correct8(gv, reinterpret_cast<const float*>(&hv), true, mom, hn, ov, nan);
+                correct8(gv[u], reinterpret_cast<const float*>(&hv[u]), true, mom, hn, ov, nan);
                 gfd::st32f(hg + e, make_float4(hn[0], hn[1], hn[2], hn[3]), make_float4(hn[4], hn[5], hn[6], hn[7]));
                 gfd::st16(static_cast<uint16_t*>(pool) + e, ov);
-                gfd::st16(static_cast<uint16_t*>(staging) + e + so, ov);
+                gfd::st16(static_cast<uint16_t*>(staging) + v * 8, ov);
                 continue;
             }
-            for (uint64_t q = e; q < min(e + 8, e1); ++q) {  // edges: element by element
+            for (uint64_t s = v * 8; s < min(v * 8 + 8, staged); ++s) {  // element by element
+                const uint64_t q = staged_to_pool(plan, k, chunk, s);
                 const int tq = tensor_of(T, q);
                 if (tq < 0) continue;  // another table's tensor (more than 256 tensors)
                 const float x = static_cast<const float*>(T.ptr[tq])[q - T.off[tq]];
                 if (DT == GF_F16) {
                     const uint16_t w = gfd::enc(correct_elem(gfd::dec(gfd::enc(x)), hg + q, true, mom));
                     static_cast<uint16_t*>(pool)[q] = w;
-                    static_cast<uint16_t*>(staging)[q + so] = w;
+                    static_cast<uint16_t*>(staging)[s] = w;
                 } else {
                     const float w = correct_elem(x, hg + q, true, mom);
                     static_cast<float*>(pool)[q] = w;
-                    static_cast<float*>(staging)[q + so] = w;
+                    static_cast<float*>(staging)[s] = w;
                 }
             }
         }
@@ -598,17 +623,15 @@ int gf_csc_pack_correct_part(int dtype, void* pool, float* hg, void* staging,
     bool descending = true;
     for (int i = 1; i < ntensors; ++i) descending &= pool_off[i] < pool_off[i - 1];
     if (part == 1 && plan && staging && descending) {  // the plan-driven form
-        const uint64_t last = total - (nc - 1) * chunk;
-        const uint64_t per = (std::max(chunk, last) + kTile - 1) / kTile;
         return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
                               [&](const TensorTable& T, uint64_t, int) {
                                   const int g = gfi::sm_count() * 4;
                                   if (dtype == GF_F16)
                                       pack_correct_planned_kernel<GF_F16><<<g, kThreads, 0, gfi::S(stream)>>>(
-                                          T, pool, hg, staging, plan, coff, total, chunk, nc, per, momentum);
+                                          T, pool, hg, staging, plan, chunk, momentum);
                                   else
                                       pack_correct_planned_kernel<GF_F32><<<g, kThreads, 0, gfi::S(stream)>>>(
-                                          T, pool, hg, staging, plan, coff, total, chunk, nc, per, momentum);
+                                          T, pool, hg, staging, plan, chunk, momentum);
                               });
     }
     return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,

@@ -97,8 +97,9 @@ struct gf_engine {
     int xthreads = 0;  // their size (0: 512)
     // streams / events (created on the engine's device, non-blocking)
     cudaStream_t side = nullptr, comm_s = nullptr;
+    cudaStream_t hp = nullptr;  // highest priority: the CSC critical path (selected chunks + exchange)
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_ready = nullptr, ev_done = nullptr, ev_sel = nullptr,
-                ev_rest = nullptr;
+                ev_rest = nullptr, ev_x = nullptr;
     // overlap state
     bool ov_on = false;
     std::vector<const float*> ov_grad;
@@ -159,7 +160,10 @@ void dense_windows(gf_engine* e) {
 int create_streams(gf_engine* e) {
     GF_ENG_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
     GF_ENG_CUDA(cudaStreamCreateWithFlags(&e->comm_s, cudaStreamNonBlocking));
-    for (cudaEvent_t* ev : {&e->ev_a, &e->ev_b, &e->ev_ready, &e->ev_done, &e->ev_sel, &e->ev_rest})
+    int least = 0, greatest = 0;
+    GF_ENG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    GF_ENG_CUDA(cudaStreamCreateWithPriority(&e->hp, cudaStreamNonBlocking, greatest));
+    for (cudaEvent_t* ev : {&e->ev_a, &e->ev_b, &e->ev_ready, &e->ev_done, &e->ev_sel, &e->ev_rest, &e->ev_x})
         GF_ENG_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     return GF_OK;
 }
@@ -253,7 +257,7 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
     if (cfg->dtype != GF_F16 && cfg->dtype != GF_F32) return gfi::fail(GF_ERR_CONFIG, "gf_engine_create: bad dtype");
     if (cfg->world < 1 || cfg->world > GF_MAX_RANKS || cfg->rank < 0 || cfg->rank >= cfg->world)
         return gfi::fail(GF_ERR_CONFIG, "gf_engine_create: rank/world out of range");
-    if (cfg->dense_mode < GF_DENSE_AUTO || cfg->dense_mode > GF_DENSE_PUSH || cfg->csc_mode < GF_CSC_PUSH ||
+    if (cfg->dense_mode < GF_DENSE_AUTO || cfg->dense_mode > GF_DENSE_PIPE || cfg->csc_mode < GF_CSC_PUSH ||
         cfg->csc_mode > GF_CSC_PULL)
         return gfi::fail(GF_ERR_CONFIG, "gf_engine_create: bad dense_mode / csc_mode");
     if (cfg->csc && (cfg->final_sparsity < 0.0 || cfg->final_sparsity >= 1.0))
@@ -279,7 +283,8 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
     int mode = cfg->dense_mode;
     if (mode == GF_DENSE_AUTO)  // measured: rspush ahead at 2 and 4 ranks; fp16 pools only
         mode = cfg->dtype == GF_F16 ? GF_DENSE_RSPUSH : (W == 2 ? GF_DENSE_PULL : GF_DENSE_PUSH);
-    if (mode == GF_DENSE_RSPUSH && cfg->dtype != GF_F16) mode = GF_DENSE_PUSH;
+    if ((mode == GF_DENSE_RSPUSH || mode == GF_DENSE_PIPE) && cfg->dtype != GF_F16) mode = GF_DENSE_PUSH;
+    if (mode == GF_DENSE_PIPE && (ntensors > GF_MAX_WINDOWS_PER_LAUNCH || W == 1)) mode = GF_DENSE_RSPUSH;
     if (mode == GF_DENSE_PULL && ntensors > GF_MAX_WINDOWS_PER_LAUNCH) mode = GF_DENSE_PUSH;  // 256-tensor table
     e->dense_mode = mode;
     dense_windows(e);
@@ -300,7 +305,7 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
         e->pull_pools[1] = at;
         at += pool_bytes;
     }
-    if (!cfg->csc && W > 1 && mode == GF_DENSE_RSPUSH) {
+    if (!cfg->csc && W > 1 && (mode == GF_DENSE_RSPUSH || mode == GF_DENSE_PIPE)) {
         e->push_inbox = at;  // slot stride: a multiple of 8 elements (16-byte aligned slots)
         at += align_up(uint64_t(W - 1) * align_up(e->total, 8) * e->esz);
     }
@@ -333,11 +338,13 @@ int gf_engine_destroy(gf_engine* e) {
     DevGuard g(e->cfg.device);
     if (e->side) cudaStreamSynchronize(e->side);
     if (e->comm_s) cudaStreamSynchronize(e->comm_s);
-    for (cudaEvent_t ev : {e->ev_a, e->ev_b, e->ev_ready, e->ev_done, e->ev_sel, e->ev_rest})
+    if (e->hp) cudaStreamSynchronize(e->hp);
+    for (cudaEvent_t ev : {e->ev_a, e->ev_b, e->ev_ready, e->ev_done, e->ev_sel, e->ev_rest, e->ev_x})
         if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
     if (e->side) cudaStreamDestroy(e->side);
     if (e->comm_s) cudaStreamDestroy(e->comm_s);
+    if (e->hp) cudaStreamDestroy(e->hp);
     if (e->state) cudaFree(e->state);
     if (e->comm) gf_comm_destroy(e->comm);
     delete e;
@@ -425,6 +432,11 @@ int gf_engine_dense_step(gf_engine* e, const float* const* grads, float* const* 
         e->last_pool = e->heap_base + e->pool_off;
         rc = gf_sync_step_dense_push(e->comm, dt, e->pool_off, e->push_inbox, grads, out, offs, cnts, m, e->ws.data(),
                                      e->wl.data(), nw, s);
+    } else if (e->dense_mode == GF_DENSE_PIPE) {
+        e->last_pool = e->heap_base + e->pool_off;
+        mark(e, "pipe", s);
+        rc = gf_sync_step_dense_pipe(e->comm, dt, e->pool_off, e->push_inbox, grads, out, offs, cnts, m, e->ws.data(),
+                                     e->wl.data(), nw, s);
     } else if (e->dense_mode == GF_DENSE_PULL) {
         // two pools used alternately: the next step's entry barrier orders the peers' last
         // reads of a pool before its reuse, so no exit barrier (GF_RSAG_NO_EXIT_BARRIER)
@@ -456,6 +468,14 @@ int gf_engine_dense_step(gf_engine* e, const float* const* grads, float* const* 
     return rc;
 }
 
+int csc_order() {  // GF_CSC_ORDER=0: the previous launch order (A/B measurement)
+    static const int v = [] {
+        const char* x = std::getenv("GF_CSC_ORDER");
+        return x ? std::atoi(x) : 1;
+    }();
+    return v;
+}
+
 int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
     if (!e || !grads) return gfi::fail(GF_ERR_CONFIG, "gf_engine_csc_step: null argument");
     if (!e->cfg.csc) return gfi::fail(GF_ERR_CONFIG, "gf_engine_csc_step on a dense engine");
@@ -476,22 +496,22 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
                                : gflow::selection_count(gflow::sparsity_at(e->iteration, C.warmup_iters, C.final_sparsity),
                                                         nc);
     const bool fused_wb = !solo && e->nacc && chunk % 8 == 0 && nc <= 6144;
-    auto exchange = [&]() -> int {
+    auto exchange = [&](cudaStream_t xs) -> int {
         if (fused_wb && C.csc_mode == GF_CSC_PULL) {
             // pull RS + pull AG straight into the pool (+ exact L1); the staging buffer is next
             // rewritten after gf_csc_select's barrier, so no exit barrier is needed
-            mark(e, "ring_scatter", s);
-            return gf_csc_exchange_pull(e->comm, e->stage_off, e->plan[cur], pool, chunk, nc, e->nacc, s);
+            mark(e, "ring_scatter", xs);
+            return gf_csc_exchange_pull(e->comm, e->stage_off, e->plan[cur], pool, chunk, nc, e->nacc, xs);
         }
         if (fused_wb) {  // exchange + write-back + exact L1 of the exchanged chunks, one launch
-            mark(e, "ring_scatter", s);
+            mark(e, "ring_scatter", xs);
             return gf_ring_allreduce_planned_scatter(e->comm, dt, e->stage_off, e->plan[cur], pool, chunk, nc,
-                                                     e->nacc, s);
+                                                     e->nacc, xs);
         }
-        mark(e, "ring", s);
-        GF_ENG_OK(gf_ring_allreduce_planned(e->comm, dt, e->stage_off, e->plan[cur], s));
-        mark(e, "scatter", s);
-        return gf_csc_scatter(dt, pool, stage, e->plan[cur], e->coff[cur], T, chunk, nc, k_cur, e->nacc, s);
+        mark(e, "ring", xs);
+        GF_ENG_OK(gf_ring_allreduce_planned(e->comm, dt, e->stage_off, e->plan[cur], xs));
+        mark(e, "scatter", xs);
+        return gf_csc_scatter(dt, pool, stage, e->plan[cur], e->coff[cur], T, chunk, nc, k_cur, e->nacc, xs);
     };
     auto pack_correct = [&](int part, cudaStream_t st) {
         return gf_csc_pack_correct_part(dt, pool, e->hg, solo ? nullptr : stage, e->imp[cur], e->coff[cur],
@@ -505,28 +525,42 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
         // the staged (important) chunks first; their exchange then runs beside the correction
         // of the other chunks (disjoint pool / hg / nacc elements), its grid capped so that the
         // packing CTAs keep the rest of the SMs
-        mark(e, "pack_correct_sel", s);
-        GF_ENG_OK(pack_correct(1, s));
-        if (e->marks_on) {
+        auto capped_exchange = [&](cudaStream_t xs) {
             GF_ENG_OK(gf_comm_set_max_blocks(e->comm, e->xblocks));
             GF_ENG_OK(gf_comm_set_block_threads(e->comm, e->xthreads));
-            const int rc = exchange();
+            const int rc = exchange(xs);
             gf_comm_set_max_blocks(e->comm, 0);
             gf_comm_set_block_threads(e->comm, 0);
-            GF_ENG_OK(rc);
+            return rc;
+        };
+        if (e->marks_on) {  // per-kernel timing: one stream, kernels in order
+            mark(e, "pack_correct_sel", s);
+            GF_ENG_OK(pack_correct(1, s));
+            GF_ENG_OK(capped_exchange(s));
             mark(e, "pack_correct_rest", s);
             GF_ENG_OK(pack_correct(2, s));
-        } else {
+        } else if (csc_order() == 0) {  // previous order (measurement): selected, then the rest beside the exchange
+            GF_ENG_OK(pack_correct(1, s));
             GF_ENG_CUDA(cudaEventRecord(e->ev_sel, s));
             GF_ENG_CUDA(cudaStreamWaitEvent(e->side, e->ev_sel, 0));
             GF_ENG_OK(pack_correct(2, e->side));
             GF_ENG_CUDA(cudaEventRecord(e->ev_rest, e->side));
-            GF_ENG_OK(gf_comm_set_max_blocks(e->comm, e->xblocks));
-            GF_ENG_OK(gf_comm_set_block_threads(e->comm, e->xthreads));
-            const int rc = exchange();
-            gf_comm_set_max_blocks(e->comm, 0);
-            gf_comm_set_block_threads(e->comm, 0);
-            GF_ENG_OK(rc);
+            GF_ENG_OK(capped_exchange(s));
+            GF_ENG_CUDA(cudaStreamWaitEvent(s, e->ev_rest, 0));
+        } else {
+            // The other chunks' correction starts at once on the side stream; the selected
+            // chunks' pack and their exchange — the step's critical path — run on the
+            // highest-priority stream, so the block scheduler hands them SMs first and the
+            // other chunks' tiles fill the rest. Disjoint chunks: no ordering between the two.
+            GF_ENG_CUDA(cudaEventRecord(e->ev_sel, s));
+            GF_ENG_CUDA(cudaStreamWaitEvent(e->hp, e->ev_sel, 0));
+            GF_ENG_CUDA(cudaStreamWaitEvent(e->side, e->ev_sel, 0));
+            GF_ENG_OK(pack_correct(1, e->hp));
+            GF_ENG_OK(capped_exchange(e->hp));
+            GF_ENG_CUDA(cudaEventRecord(e->ev_x, e->hp));
+            GF_ENG_OK(pack_correct(2, e->side));
+            GF_ENG_CUDA(cudaEventRecord(e->ev_rest, e->side));
+            GF_ENG_CUDA(cudaStreamWaitEvent(s, e->ev_x, 0));
             GF_ENG_CUDA(cudaStreamWaitEvent(s, e->ev_rest, 0));
         }
     }

@@ -32,7 +32,6 @@ namespace {
 
 struct SegMap {  // routing of pool elements to their owners (explicit windows)
     int nwin, world, pos, diag;  // diag: GF_PUSH_DIAG timing probe (1: every store local; results invalid)
-    uint32_t part_lo, part_hi;   // the piece of every segment this launch packs (0,0: whole)
     uint64_t slot_elems;                 // elements per inbox slot (the pool span)
     char* pool_local;                    // my pool (fp16)
     char* inbox_by_pos[GF_MAX_RANKS];    // owner at ring position j: its inbox as mapped here
@@ -47,7 +46,6 @@ struct SegMap {  // routing of pool elements to their owners (explicit windows)
 // owner with a few compares instead of divisions.
 struct TileRoute {
     uint64_t start[GF_MAX_RANKS + 1];  // segment j of the tile's window: [start[j], start[j+1])
-    uint64_t lo[GF_MAX_RANKS], hi[GF_MAX_RANKS];  // the launch's piece of segment j
     uint16_t* dst[GF_MAX_RANKS];       // owner j's destination base (pool indices)
 };
 
@@ -60,10 +58,6 @@ __device__ __forceinline__ void tile_route(const SegMap& m, uint64_t e, TileRout
     const uint64_t n = uint64_t(m.world), L = m.wlen[lo], ws = m.wstart[lo];
     const uint64_t base = L / n, rem = L % n;
     for (int j = 0; j <= m.world; ++j) r.start[j] = ws + uint64_t(j) * base + min(uint64_t(j), rem);
-    for (int j = 0; j < m.world; ++j) {
-        r.lo[j] = m.part_hi ? part_cut(r.start[j], r.start[j + 1], m.part_lo) : r.start[j];
-        r.hi[j] = m.part_hi ? part_cut(r.start[j], r.start[j + 1], m.part_hi) : r.start[j + 1];
-    }
     for (int j = 0; j < m.world; ++j) {
         if (j == m.pos || m.diag == 1) {
             r.dst[j] = reinterpret_cast<uint16_t*>(m.pool_local);
@@ -98,48 +92,34 @@ pack_push_kernel(const __grid_constant__ TensorTable T, const __grid_constant__ 
         __syncthreads();  // the previous tile's readers of R are done
         if (threadIdx.x == 0) tile_route(M, po, R);
         __syncthreads();
-        if (M.part_hi) {  // a tile meeting no piece range of this launch is skipped whole
-            bool any = false;
-            for (int j = 0; j < M.world; ++j) any |= R.lo[j] < po + len && po < R.hi[j];
-            if (!any) continue;
-        }
-        auto in_piece = [&](int j, uint64_t e) { return R.lo[j] <= e && e < R.hi[j]; };
-        auto put = [&](uint64_t e, uint16_t h) {
-            const int j = tile_owner(R, M.world, e);
-            if (in_piece(j, e)) R.dst[j][e] = h;
-        };
+        auto put = [&](uint64_t e, uint16_t h) { R.dst[tile_owner(R, M.world, e)][e] = h; };
         uint64_t done = 0;
         if ((reinterpret_cast<uintptr_t>(T.ptr[t]) & 31u) == 0 && po % 8 == 0) {
             const int nvec = int(len / 8);
             float4 a[kVecPerThread], b[kVecPerThread];
-            int own[kVecPerThread];  // owner of a whole vector, GF_MAX_RANKS: straddles, -1: not this piece
 #pragma unroll
             for (int k = 0; k < kVecPerThread; ++k) {
                 const int v = threadIdx.x + k * kThreads;
-                own[k] = -1;
                 if (v < nvec) {
-                    const uint64_t e = po + 8 * uint64_t(v);
-                    const int j = tile_owner(R, M.world, e);
-                    if (e + 8 > R.start[j + 1]) own[k] = GF_MAX_RANKS;
-                    else if (!M.part_hi || (R.lo[j] <= e && e < R.hi[j])) own[k] = j;  // cuts are 8-aligned
-                    if (own[k] >= 0) {
-                        const gfd::F8 f = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
-                        a[k] = f.lo;
-                        b[k] = f.hi;
-                    }
+                    const gfd::F8 f = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
+                    a[k] = f.lo;
+                    b[k] = f.hi;
                 }
             }
 #pragma unroll
             for (int k = 0; k < kVecPerThread; ++k) {
-                if (own[k] < 0) continue;
-                const uint64_t e = po + 8 * uint64_t(threadIdx.x + k * kThreads);
-                const uint4 h = gfd::enc8(a[k], b[k]);
-                if (own[k] < GF_MAX_RANKS) {  // the whole vector belongs to one owner
-                    gfd::st16(R.dst[own[k]] + e, h);
-                } else {                      // a segment boundary inside the vector
-                    const uint32_t w[4] = {h.x, h.y, h.z, h.w};
+                const int v = threadIdx.x + k * kThreads;
+                if (v < nvec) {
+                    const uint4 h = gfd::enc8(a[k], b[k]);
+                    const uint64_t e = po + 8 * uint64_t(v);
+                    const int j = tile_owner(R, M.world, e);
+                    if (e + 8 <= R.start[j + 1]) {  // the whole vector belongs to one owner
+                        gfd::st16(R.dst[j] + e, h);
+                    } else {                         // a segment boundary inside the vector
+                        const uint32_t w[4] = {h.x, h.y, h.z, h.w};
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) put(e + q, uint16_t((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu));
+                        for (int q = 0; q < 8; ++q) put(e + q, uint16_t((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu));
+                    }
                 }
             }
             done = uint64_t(nvec) * 8;
@@ -307,12 +287,9 @@ int push_diag() {
 // The routed pack of one group of <= kMaxW windows (the tensors inside them).
 int routed_pack(gf_comm* c, cudaStream_t s, uint64_t pool_heap_off, uint64_t inbox_heap_off, uint64_t slot_elems,
                 const float* const* src, const uint64_t* pool_off, const uint64_t* count, int ntensors,
-                const uint64_t* win_start, const uint64_t* win_len, int nwin, uint32_t part_lo = 0,
-                uint32_t part_hi = 0) {
+                const uint64_t* win_start, const uint64_t* win_len, int nwin) {
     SegMap M;
     std::memset(&M, 0, sizeof(M));
-    M.part_lo = part_lo;
-    M.part_hi = part_hi;
     M.nwin = nwin;
     M.world = c->world;
     M.pos = c->pos;
@@ -334,25 +311,6 @@ int routed_pack(gf_comm* c, cudaStream_t s, uint64_t pool_heap_off, uint64_t inb
                                   default: pack_push_kernel<4><<<grid, kThreads, 0, s>>>(T, M, tiles, spread, push_fence()); break;
                               }
                           });
-}
-
-// Pipelined rspush (GF_PUSH_PIECES = P > 1): P pieces of every segment, and the CTAs of
-// rsp_kernel while a piece's pack runs beside it (GF_PUSH_RSP_BLOCKS).
-int push_pieces() {
-    static const int v = [] {
-        const char* e = std::getenv("GF_PUSH_PIECES");
-        const int x = e ? std::atoi(e) : 1;
-        return std::min(std::max(x, 1), 16);
-    }();
-    return v;
-}
-int push_rsp_blocks() {
-    static const int v = [] {
-        const char* e = std::getenv("GF_PUSH_RSP_BLOCKS");
-        const int x = e ? std::atoi(e) : 64;
-        return std::max(x, 1);
-    }();
-    return v;
 }
 
 // The unpack fused into rsp_kernel or a separate unpack launch. Measured: fused wins
@@ -416,19 +374,7 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
     }
     const float inv = 1.0f / static_cast<float>(c->world);
     // Windows go in groups of <= kMaxW per launch pair; windows are cut at tensor boundaries,
-    // so every tensor belongs to exactly one group. Within a group the step can be pipelined in
-    // P pieces of every segment (GF_PUSH_PIECES): piece p+1's routed pack runs on the
-    // communicator's side stream while rsp_kernel reduces and pushes piece p (its grid capped so
-    // the packing CTAs keep SMs); pieces change no element's summation order.
-    const int P = nwin <= kMaxW ? push_pieces() : 1;
-    if (P > 1 && !c->side) {
-        // the reduce/all-gather pieces run at the highest stream priority: the block scheduler
-        // then hands them SMs ahead of the pending CTAs of the next piece's pack
-        int least = 0, greatest = 0;
-        GF_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        GF_CHECK_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, greatest));
-        for (cudaEvent_t& e : c->ev) GF_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
+    // so every tensor belongs to exactly one group.
     std::vector<const void*> gsrc;
     std::vector<uint64_t> goff, gcnt;
     for (int first = 0; first < nwin; first += kMaxW) {
@@ -445,6 +391,14 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
             goff.push_back(pool_off[i]);
             gcnt.push_back(count[i]);
         }
+        // 1. pack, routed to the owners
+        gfi::phase("pack_push", s);
+        if (int rc = routed_pack(c, s, pool_heap_off, inbox_heap_off, slot_elems,
+                                 reinterpret_cast<const float* const*>(gsrc.data()), goff.data(), gcnt.data(),
+                                 int(gsrc.size()), win_start + first, win_len + first, nw))
+            return rc;
+        if (push_diag() == 2) continue;  // timing probe: the routed pack alone (results invalid)
+        // 2. local reduce + all-gather push (+ the unpack when fused)
         RingArgs a;
         std::memset(&a, 0, sizeof(a));
         a.nwin = nw;
@@ -455,51 +409,21 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
             max_seg += (a.wlen[w] + c->world - 1) / c->world;
         }
         fill_common(c, a, pool_heap_off);
-        int grid = gfr::comm_blocks(c, max_seg * 2);
-        if (P > 1) grid = std::min(grid, push_rsp_blocks());
+        const int grid = gfr::comm_blocks(c, max_seg * 2);
+        gfi::phase("rsp", s);
         const uint64_t sb = slot_elems * 2;
-        auto pack = [&](cudaStream_t st, uint32_t lo, uint32_t hi) {
-            return routed_pack(c, st, pool_heap_off, inbox_heap_off, slot_elems,
-                               reinterpret_cast<const float* const*>(gsrc.data()), goff.data(), gcnt.data(),
-                               int(gsrc.size()), win_start + first, win_len + first, nw, lo, hi);
-        };
-        auto cut = [&](int p) { return uint32_t((uint64_t(kPieceOne) * uint64_t(p)) / uint64_t(P)); };
-        // The routed packs of the pieces go back to back on the caller's stream; piece p's
-        // reduce/all-gather (rsp_kernel) waits for piece p's pack only and runs on the
-        // high-priority side stream beside the packs of the later pieces. The caller's stream
-        // rejoins after the last piece, so the next step's pack (which rewrites the peers'
-        // inboxes) follows every read of this step (rsp's exit barrier).
-        cudaStream_t rs = P > 1 ? c->side : s;
-        for (int p = 0; p < P; ++p) {
-            // 1. the routed pack of piece p (of everything when P == 1)
-            gfi::phase("pack_push", s);
-            if (int rc = pack(s, P > 1 ? cut(p) : 0, P > 1 ? cut(p + 1) : 0)) return rc;
-            if (push_diag() == 2) continue;  // timing probe: the routed pack alone (results invalid)
-            if (P > 1) {
-                GF_CHECK_CUDA(cudaEventRecord(c->ev[0], s));
-                GF_CHECK_CUDA(cudaStreamWaitEvent(rs, c->ev[0], 0));
-            }
-            // 2. local reduce + all-gather push (+ the unpack when fused) of piece p
-            a.part_lo = P > 1 ? cut(p) : 0;
-            a.part_hi = P > 1 ? cut(p + 1) : 0;
-            gfi::phase("rsp", rs);
 #define GF_RSP(NT_)                                                                                  \
-    if (fused) rsp_kernel<NT_, true><<<grid, kRingThreads, 0, rs>>>(a, inbox_local, sb, TT, inv);    \
-    else rsp_kernel<NT_, false><<<grid, kRingThreads, 0, rs>>>(a, inbox_local, sb, TT, inv);
-            switch (c->world) {
-                case 2: GF_RSP(2) break;
-                case 4: GF_RSP(4) break;
-                case 8: GF_RSP(8) break;
-                default: GF_RSP(0) break;
-            }
+    if (fused) rsp_kernel<NT_, true><<<grid, kRingThreads, 0, s>>>(a, inbox_local, sb, TT, inv);     \
+    else rsp_kernel<NT_, false><<<grid, kRingThreads, 0, s>>>(a, inbox_local, sb, TT, inv);
+        switch (c->world) {
+            case 2: GF_RSP(2) break;
+            case 4: GF_RSP(4) break;
+            case 8: GF_RSP(8) break;
+            default: GF_RSP(0) break;
+        }
 #undef GF_RSP
-            gfi::count_launch();
-            if (int rc = gfi::check_launch("gf_sync_step_dense_push")) return rc;
-        }
-        if (P > 1 && push_diag() != 2) {
-            GF_CHECK_CUDA(cudaEventRecord(c->ev[1], rs));
-            GF_CHECK_CUDA(cudaStreamWaitEvent(s, c->ev[1], 0));
-        }
+        gfi::count_launch();
+        if (int rc = gfi::check_launch("gf_sync_step_dense_push")) return rc;
     }
     if (fused || push_diag() == 2) return GF_OK;
     // 3. unpack

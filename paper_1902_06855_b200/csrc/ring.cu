@@ -381,11 +381,15 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
     // Finalize this iteration's local norms from the exact accumulators written by
     // pack_correct (unimportant chunks) and scatter (important chunks): chunk_l1 +
     // x1/N (sparse.cpp:176-184), then re-arm the accumulators for the next iteration.
+    // World 1: the finalized norms are the sums; they go straight into `red` (shared memory)
+    // and the sum phase below is skipped.
+    const bool solo = n == 1;
     if (a.nacc[0] || a.nacc[a.rank]) {
         const float inv_world = 1.0f / float(n);
         for (int r = a.p2p ? a.rank : 0; r < (a.p2p ? a.rank + 1 : n); ++r) {
             for (uint64_t i = threadIdx.x; i < a.nc; i += gfs::kSelThreads) {
                 const uint64_t S = a.nacc[r][i];
+                const bool imp = a.imp_cur[i] != 0;  // both loads in flight together
                 float v;
                 if (S >> 63) {
                     v = gfd::u2f(0x7FC00000u);
@@ -397,8 +401,9 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
                     for (uint64_t e = 0; e < len; ++e) d = __dadd_rn(d, fabs(double(gfd::dec(a.pool[r][b + e]))));
                     v = __double2float_rn(d);
                 }
-                if (a.imp_cur[i]) v = gfd::mul(v, inv_world);
+                if (imp) v = gfd::mul(v, inv_world);
                 a.norms[r][i] = v;
+                if (solo) red[i] = v;
                 a.nacc[r][i] = 0;
             }
         }
@@ -419,7 +424,8 @@ __global__ void __launch_bounds__(gfs::kSelThreads) select_kernel(const __grid_c
     if (inbox && threadIdx.x == 0) a.epochs[0] = epoch + 1;
     if (tr) a.trace[2] = gfd::globaltimer_ns();
     const uint64_t base = a.nc / uint64_t(n), rem = a.nc % uint64_t(n);
-    for (uint64_t i = threadIdx.x; i < a.nc; i += gfs::kSelThreads) {
+    const bool have_red = solo && (a.nacc[0] != nullptr);
+    for (uint64_t i = threadIdx.x; i < a.nc && !have_red; i += gfs::kSelThreads) {
         // segment index of element i under segment_of(nc, n, .) (collectives.cpp:47-53)
         const uint64_t big = rem * (base + 1);
         const int j = int(i < big ? i / (base + 1) : rem + (i - big) / base);
@@ -580,9 +586,6 @@ int gf_comm_destroy(gf_comm* c) {
     cudaDeviceSynchronize();
     for (int r = 0; r < c->world; ++r)
         if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->peer_alloc[r]);
-    if (c->side) cudaStreamDestroy(c->side);
-    for (cudaEvent_t e : c->ev)
-        if (e) cudaEventDestroy(e);
     cudaFree(c->alloc);
     cudaFreeHost(c->err_host);
     delete c;

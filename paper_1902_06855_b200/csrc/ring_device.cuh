@@ -18,7 +18,6 @@ struct RingArgs {
     char* bufs[GF_MAX_RANKS];            // buffer base of each RANK (peer-mapped)
     int ring[GF_MAX_RANKS];              // rank at each ring position
     int world, rank, pos;
-    uint32_t part_lo, part_hi;           // a piece of every segment (units of 1/kPieceOne); 0,0 = whole
     int nwin;                            // >= 0 explicit windows; -1: read plan
     uint64_t* flags_local;
     uint64_t* flags_peer[GF_MAX_RANKS];  // by rank
@@ -38,17 +37,6 @@ struct RingArgs {
     uint64_t wstart[kMaxW];
     uint64_t wlen[kMaxW];
 };
-
-// Piece [q_lo, q_hi) (units of 1/kPieceOne) of segment [e0, e1): cut points are rounded down to
-// a multiple of 8 elements (16-byte fp16 vectors) and clamped to the segment. The routed pack
-// and rsp_kernel of a pipelined rspush step (push.cu) cut every segment the same way.
-constexpr uint32_t kPieceOne = 1024;
-__host__ __device__ inline uint64_t part_cut(uint64_t e0, uint64_t e1, uint32_t q) {
-    if (q == 0) return e0;
-    if (q >= kPieceOne) return e1;
-    uint64_t c = ((e0 + (e1 - e0) * q / kPieceOne) / 8) * 8;
-    return c < e0 ? e0 : (c > e1 ? e1 : c);
-}
 
 // ---- cross-GPU barrier (CTA b <-> CTA b of every peer) ------------------------
 // release_writes: the CTA's earlier global stores (incl. pushes into peers) must be visible
@@ -196,13 +184,8 @@ __device__ __forceinline__ void flat_build(const RingArgs& a, int n, int p, Flat
         uint64_t cnt = 0;
         if (w < a.nwin) {
             const uint64_t wl = a.wlen[w], base = wl / uint64_t(n), rem = wl % uint64_t(n), up = uint64_t(p);
-            uint64_t e0 = a.wstart[w] + up * base + min(up, rem);  // segment_of (collectives.cpp:47-53)
-            uint64_t e1 = e0 + base + (up < rem ? 1 : 0);
-            if (a.part_hi != 0) {  // one piece of the segment
-                const uint64_t s0 = e0, s1 = e1;
-                e0 = part_cut(s0, s1, a.part_lo);
-                e1 = part_cut(s0, s1, a.part_hi);
-            }
+            const uint64_t e0 = a.wstart[w] + up * base + min(up, rem);  // segment_of (collectives.cpp:47-53)
+            const uint64_t e1 = e0 + base + (up < rem ? 1 : 0);
             const uint64_t v0 = (e0 + VE - 1) / VE, v1 = e1 / VE;
             f.e0[w] = e0;
             f.e1[w] = e1;

@@ -28,7 +28,7 @@ from . import capi
 F32, F16 = capi.GF_F32, capi.GF_F16
 THETA_INF = capi.THETA_INF
 _DENSE = {"auto": capi.GF_DENSE_AUTO, "rspush": capi.GF_DENSE_RSPUSH, "pull": capi.GF_DENSE_PULL,
-          "push": capi.GF_DENSE_PUSH}
+          "push": capi.GF_DENSE_PUSH, "pipe": capi.GF_DENSE_PIPE}
 _DENSE_NAME = {v: k for k, v in _DENSE.items()}
 _CSC = {"push": capi.GF_CSC_PUSH, "pull": capi.GF_CSC_PULL}
 _STATE = {"pool": capi.GF_STATE_POOL, "hg": capi.GF_STATE_HG, "hu": capi.GF_STATE_HU, "w": capi.GF_STATE_W,
@@ -119,7 +119,7 @@ class GradSync:
                  lr=0.01, allgather=None, timeout_ms=30000, dense_mode="auto", csc_mode="push",
                  _connect=True):
         if dense_mode not in _DENSE:
-            raise capi.ConfigError(f"dense_mode {dense_mode!r}: auto, rspush, pull or push")
+            raise capi.ConfigError(f"dense_mode {dense_mode!r}: auto, rspush, pipe, pull or push")
         if csc_mode not in _CSC:
             raise capi.ConfigError(f"csc_mode {csc_mode!r}: pull or push")
         self.layout = PoolLayout.build(sizes, chunk)
@@ -154,6 +154,14 @@ class GradSync:
         barriers included, run unchanged; launch each rank's steps on its own stream."""
         ranks = [cls(sizes, rank=r, world=world, device=device, _connect=False, **kw) for r in range(world)]
         capi.call("gf_engine_connect_colocated", (C.c_void_p * world)(*[g.eng.value for g in ranks]), world)
+        return ranks
+
+    @classmethod
+    def local(cls, world, sizes, devices=None, **kw):
+        """`world` ranks in THIS process, rank r on devices[r] (peer access, gf_engine_connect_local)."""
+        devices = list(range(world)) if devices is None else list(devices)
+        ranks = [cls(sizes, rank=r, world=world, device=devices[r], _connect=False, **kw) for r in range(world)]
+        capi.call("gf_engine_connect_local", (C.c_void_p * world)(*[g.eng.value for g in ranks]), world)
         return ranks
 
     def info(self):
