@@ -468,14 +468,6 @@ int gf_engine_dense_step(gf_engine* e, const float* const* grads, float* const* 
     return rc;
 }
 
-int csc_order() {  // GF_CSC_ORDER=0: the previous launch order (A/B measurement)
-    static const int v = [] {
-        const char* x = std::getenv("GF_CSC_ORDER");
-        return x ? std::atoi(x) : 1;
-    }();
-    return v;
-}
-
 int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
     if (!e || !grads) return gfi::fail(GF_ERR_CONFIG, "gf_engine_csc_step: null argument");
     if (!e->cfg.csc) return gfi::fail(GF_ERR_CONFIG, "gf_engine_csc_step on a dense engine");
@@ -539,14 +531,6 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
             GF_ENG_OK(capped_exchange(s));
             mark(e, "pack_correct_rest", s);
             GF_ENG_OK(pack_correct(2, s));
-        } else if (csc_order() == 0) {  // previous order (measurement): selected, then the rest beside the exchange
-            GF_ENG_OK(pack_correct(1, s));
-            GF_ENG_CUDA(cudaEventRecord(e->ev_sel, s));
-            GF_ENG_CUDA(cudaStreamWaitEvent(e->side, e->ev_sel, 0));
-            GF_ENG_OK(pack_correct(2, e->side));
-            GF_ENG_CUDA(cudaEventRecord(e->ev_rest, e->side));
-            GF_ENG_OK(capped_exchange(s));
-            GF_ENG_CUDA(cudaStreamWaitEvent(s, e->ev_rest, 0));
         } else {
             // The other chunks' correction starts at once on the side stream; the selected
             // chunks' pack and their exchange — the step's critical path — run on the

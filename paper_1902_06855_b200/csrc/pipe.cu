@@ -97,27 +97,42 @@ __device__ __forceinline__ int table_at(const PipeTable& T, uint64_t e) {
     return lo;
 }
 
-// spin until *f >= v (threads that call it), bounded by the communicator timeout
+// Poll until *f >= v, bounded by the communicator timeout. Relaxed polls with exponential
+// __nanosleep backoff (hundreds of CTAs wait at once: acquire-polling at system scope in a
+// tight loop was measured to starve the producers), then one acquire fence.
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
 __device__ __forceinline__ bool wait_ge(const PipeArgs& A, const uint64_t* f, uint64_t v) {
-    if (A.timeout_ns == 0 || gfd::ld_acquire_sys(f) >= v) return true;  // 0: GF_DIAG_NOWAIT probe
-    const uint64_t t0 = gfd::globaltimer_ns();
-    uint32_t spins = 0;
-    while (gfd::ld_acquire_sys(f) < v) {
-        if ((++spins & 255u) == 0) {
-            if (*reinterpret_cast<volatile int*>(A.err) != 0) return false;
-            if (gfd::globaltimer_ns() - t0 > A.timeout_ns) {
-                *reinterpret_cast<volatile int*>(A.err) = 1;
-                return false;
+    if (A.timeout_ns == 0) return true;  // GF_DIAG_NOWAIT probe
+    if (ld_relaxed_sys(f) < v) {
+        const uint64_t t0 = gfd::globaltimer_ns();
+        unsigned ns = 32;
+        uint32_t spins = 0;
+        while (ld_relaxed_sys(f) < v) {
+            __nanosleep(ns);
+            ns = min(ns * 2, 512u);
+            if ((++spins & 63u) == 0) {
+                if (*reinterpret_cast<volatile int*>(A.err) != 0) return false;
+                if (gfd::globaltimer_ns() - t0 > A.timeout_ns) {
+                    *reinterpret_cast<volatile int*>(A.err) = 1;
+                    return false;
+                }
             }
         }
     }
+    fence_acq_rel_sys();  // acquire: the stores published before the flag are visible from here on
     return true;
 }
 
-// publish: the CTA's earlier stores, then flag = v (called by the signalling thread after bar.sync)
+// publish (one thread, after bar.sync): release fence over the CTA's stores, then the flag
 __device__ __forceinline__ void publish(uint64_t* flag, uint64_t v) {
-    __threadfence_system();
-    gfd::st_release_sys(flag, v);
+    fence_acq_rel_sys();
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
 }
 
 // producer: pack pool range [a, b) of my gradients into dst (pool indices)
@@ -318,7 +333,9 @@ pipe_kernel(const __grid_constant__ PipeArgs A, const __grid_constant__ PipeTabl
         // consume the units of my segment
         const uint64_t* rs = A.rs_by_pos[A.pos];
         for (uint32_t u = uint32_t(int(blockIdx.x) - P); u < U; u += uint32_t(C)) {
-            if (threadIdx.x < n && !wait_ge(A, rs + uint64_t(u) * GF_MAX_RANKS + A.ring[threadIdx.x], g1)) s_ok = 0;
+            if (threadIdx.x == 0)
+                for (int t = 0; t < n && s_ok; ++t)
+                    if (!wait_ge(A, rs + uint64_t(u) * GF_MAX_RANKS + A.ring[t], g1)) s_ok = 0;
             __syncthreads();
             if (!s_ok) return;
             uint64_t a, b;

@@ -527,6 +527,16 @@ bool lazy_module_loading() {
     return m == CU_MODULE_LAZY_LOADING;
 }
 
+// GF_DIAG_NOWAIT=1: cross-GPU barriers and flags signal but never wait (timeout 0). A traffic
+// probe for ncu's serialised kernel replay (scripts/ncu_nvlink.py); every result is invalid.
+bool diag_nowait() {
+    static const bool v = [] {
+        const char* e = std::getenv("GF_DIAG_NOWAIT");
+        return e && std::atoi(e) == 1;
+    }();
+    return v;
+}
+
 bool valid_ring(const int* order, int world) {
     bool seen[GF_MAX_RANKS] = {};
     for (int i = 0; i < world; ++i) {
@@ -554,9 +564,7 @@ int gf_comm_create(int world, int rank, int device, uint64_t heap_bytes, gf_comm
     c->world = world;
     c->rank = rank;
     c->device = device;
-    // GF_DIAG_NOWAIT=1: cross-GPU barriers signal but never wait (timeout 0). A traffic probe for
-    // ncu's kernel replay of ONE rank (scripts/diag/ncu_nvl.sh); every result is invalid.
-    if (const char* e = std::getenv("GF_DIAG_NOWAIT"); e && std::atoi(e) == 1) c->timeout_ns = 0;
+    if (diag_nowait()) c->timeout_ns = 0;
     c->heap_bytes = (heap_bytes + 255) & ~uint64_t(255);
     for (int i = 0; i < world; ++i) c->ring[i] = i;
     c->pos = rank;
@@ -700,6 +708,7 @@ int gf_comm_set_ring_order(gf_comm* c, const int* order) {
 
 int gf_comm_set_timeout_ms(gf_comm* c, uint64_t ms) {
     if (!c) return gfi::fail(GF_ERR_CONFIG, "null communicator");
+    if (diag_nowait()) return GF_OK;  // the probe keeps timeout 0
     c->timeout_ns = std::max<uint64_t>(ms * 1000ull * 1000ull, 1);  // 0 is the no-wait probe
     return GF_OK;
 }

@@ -183,9 +183,20 @@ inline __device__ void block_plan(const uint8_t* flags, uint64_t total, uint64_t
             len = (c + 1 == nc) ? total - c * chunk : chunk;
             one = 1;
         }
-        uint64_t tot_len, tot_cnt;
-        const uint64_t ex = block_excl_scan<uint64_t>(len, &tot_len, sh.u64s);
-        const uint64_t exc = block_excl_scan<uint64_t>(one, &tot_cnt, sh.u64s);
+        // one scan of (len << 20 | one): a round holds <= kSelThreads chunks (< 2^20), and the
+        // lengths of a round sum below 2^44 whenever its chunks fit in memory; otherwise two scans
+        uint64_t ex, exc, tot_len, tot_cnt;
+        if (total <= (uint64_t(1) << 43)) {
+            uint64_t tot;
+            const uint64_t x = block_excl_scan<uint64_t>((len << 20) | one, &tot, sh.u64s);
+            ex = x >> 20;
+            exc = x & 0xFFFFFu;
+            tot_len = tot >> 20;
+            tot_cnt = tot & 0xFFFFFu;
+        } else {
+            ex = block_excl_scan<uint64_t>(len, &tot_len, sh.u64s);
+            exc = block_excl_scan<uint64_t>(one, &tot_cnt, sh.u64s);
+        }
         if (c < nc) coff[c] = carry_len + ex;
         if (one) plan[4 + carry_cnt + exc] = c;  // ascending list of important chunks
         carry_len += tot_len;

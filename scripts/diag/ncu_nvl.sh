@@ -6,9 +6,9 @@ M=gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,nvltx__bytes_data_use
 export GF_DIAG_NOWAIT=1 WORLD_SIZE=$N
 for wl in $WLS; do
   for mode in $MODES; do
-    MODE=$mode WORKLOAD=$wl timeout 300 /usr/local/cuda/bin/ncu --metrics $M --clock-control none --devices 0 \
+    STEPS=8 MODE=$mode WORKLOAD=$wl timeout 300 /usr/local/cuda/bin/ncu --metrics $M --clock-control none --devices 0 \
       -k 'regex:pack_push|rsp_kernel|pipe_kernel|rsag|ring_kernel|csc_pull|select_kernel|pack_correct|unpack_kernel|pack_kernel' \
-      -s 6 -c 30 --csv --log-file ${P}_${wl}_${mode}.csv python -u scripts/ncu_nvlink.py > ${P}_${wl}_${mode}.log 2>&1
+      -s 4 -c 40 --csv --log-file ${P}_${wl}_${mode}.csv python -u scripts/ncu_nvlink.py > ${P}_${wl}_${mode}.log 2>&1
     echo "$wl $mode rc=$?"
   done
 done
