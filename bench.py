@@ -681,7 +681,7 @@ def main():
     ap.add_argument("--trace", action="store_true", help="report NVLink kernel CTA-0 timestamps (diagnostic)")
     ap.add_argument("--overlap", type=float, default=0.0, metavar="BACKWARD_MS",
                     help="also measure the dense sync overlapped with a synthetic backward of this many ms")
-    ap.add_argument("--dense-mode", default="auto", choices=["auto", "pull", "push", "rspush", "pipe"],
+    ap.add_argument("--dense-mode", default="auto", choices=["auto", "pull", "push", "rspush"],
                     help="dense N>1: rspush (pack pushes the reduce-scatter operands to their owners, "
                          "local reduce + all-gather push, unpack), pull (pack + pull RS/AG fused with "
                          "unpack), push (pack + push-pull ring + unpack); auto = rspush")

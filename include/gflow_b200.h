@@ -37,7 +37,6 @@
  *  gf_ring_allreduce_colocated      same, all ranks' buffers on one device   src/collectives.cpp:55-97
  *  gf_ring_allreduce_unpack         ring_allreduce of the windows + the update read g = get(i)*(1/N)
  *                                   src/collectives.cpp:55-97, src/trainer.cpp:332-347
- *  gf_sync_step_dense_pipe          the same as one kernel, unit-pipelined (same call sites)
  *  gf_sync_step_dense_push          the same with the reduce-scatter pushed by the pack (write_tensor
  *                                   src/gradient_pool.cpp:78-105 + ring_allreduce_on src/collectives.cpp:55-97)
  *  gf_sync_step_dense               one dense iteration: write_tensor x m + FusionEngine windows +
@@ -280,17 +279,6 @@ int gf_sync_step_dense_push(gf_comm* comm, int dtype, uint64_t pool_heap_off, ui
                             const float* const* src, float* const* dst, const uint64_t* pool_off,
                             const uint64_t* count, int ntensors, const uint64_t* win_start,
                             const uint64_t* win_len, int nwin, void* stream);
-/* The same step as gf_sync_step_dense_push (same inbox layout, same results bit for bit) as ONE
- * kernel per rank: the owned segments are cut into units; producer CTAs pack every unit and
- * store it at its owner (pool or inbox slot) and publish a per-unit flag; consumer CTAs reduce
- * each unit of their segment as soon as every rank published it, push the sums into every pool,
- * unpack them and publish; producers then unpack the other owners' units as they land. The
- * all-gather of early units overlaps the reduce-scatter of later ones (pipe.cu). fp16,
- * 1..256 tensors tiling the windows, 1..256 windows. */
-int gf_sync_step_dense_pipe(gf_comm* comm, int dtype, uint64_t pool_heap_off, uint64_t inbox_heap_off,
-                            const float* const* src, float* const* dst, const uint64_t* pool_off,
-                            const uint64_t* count, int ntensors, const uint64_t* win_start,
-                            const uint64_t* win_len, int nwin, void* stream);
 /* Emulation of `world` ranks whose buffers all live on the current device (no waits). */
 int gf_ring_allreduce_colocated(int dtype, void* const* bufs, int world, const int* ring_order,
                                 const uint64_t* win_start, const uint64_t* win_len, int nwin,
@@ -354,7 +342,7 @@ int gf_synth_grads(int rank, int step, const uint64_t* sizes, int ntensors, floa
  * captured into a CUDA graph. Gradient/output tables are HOST arrays of per-tensor DEVICE
  * pointers in ascending tensor id (id 1 first), as the reference's write_tensor(id, span). */
 typedef struct gf_engine gf_engine;
-enum { GF_DENSE_AUTO = 0, GF_DENSE_RSPUSH = 1, GF_DENSE_PULL = 2, GF_DENSE_PUSH = 3, GF_DENSE_PIPE = 4 };
+enum { GF_DENSE_AUTO = 0, GF_DENSE_RSPUSH = 1, GF_DENSE_PULL = 2, GF_DENSE_PUSH = 3 };
 enum { GF_CSC_PUSH = 0, GF_CSC_PULL = 1 };
 typedef struct {
     int world, rank, device, dtype;

@@ -22,7 +22,7 @@ GF_F32, GF_F16 = 0, 1
 GF_MAX_RANKS = 16
 GF_IPC_HANDLE_BYTES = 64
 GF_RSAG_NO_EXIT_BARRIER = 1
-GF_DENSE_AUTO, GF_DENSE_RSPUSH, GF_DENSE_PULL, GF_DENSE_PUSH, GF_DENSE_PIPE = range(5)
+GF_DENSE_AUTO, GF_DENSE_RSPUSH, GF_DENSE_PULL, GF_DENSE_PUSH = range(4)
 GF_CSC_PUSH, GF_CSC_PULL = range(2)
 (GF_STATE_POOL, GF_STATE_HG, GF_STATE_HU, GF_STATE_W, GF_STATE_IMP_NEXT, GF_STATE_NORMS, GF_STATE_NACC,
  GF_STATE_PLAN_NEXT, GF_STATE_IMP_CUR, GF_STATE_PLAN_CUR) = range(10)
@@ -105,7 +105,6 @@ SIGNATURES = {
     "gf_ring_allreduce_ptrs": [_vp, _i, _vp, _vp, _vp, _i, _vp],
     "gf_sync_step_dense": [_vp, _i, _u64, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _vp],
     "gf_sync_step_dense_push": [_vp, _i, _u64, _u64, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _vp],
-    "gf_sync_step_dense_pipe": [_vp, _i, _u64, _u64, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _vp],
     "gf_ring_allreduce_unpack": [_vp, _i, _u64, _vp, _vp, _vp, _i, _vp, _vp, _i, _i, _vp],
     "gf_ipc_export": [_vp, _vp, _u64p],
     "gf_ipc_open": [_vp, _vp, C.POINTER(_vp)],

@@ -7,9 +7,6 @@
 //   [0, kFlagWords)                 ring barrier flags  flags[cta][src_rank]   (peers write)
 //   [kFlagWords, +kMaxBlocks)       per-CTA epoch counters (local)
 //   [+kMaxBlocks, +32)              ring work/done counters (local)
-//   kPipeGenOff   [kMaxBlocks]                  pipe kernel per-CTA generations (local)
-//   kPipeRsOff    [kPipeUnits][GF_MAX_RANKS]    pipe RS flags: unit u of my segment from rank r (peers write)
-//   kPipeAgOff    [GF_MAX_RANKS][kPipeUnits]    pipe AG flags: unit u of the owner at position j (peers write)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -26,11 +23,7 @@ constexpr int kMaxW = GF_MAX_WINDOWS_PER_LAUNCH;
 constexpr int kRingThreads = 512;
 constexpr uint64_t kFlagWords = uint64_t(kMaxBlocks) * GF_MAX_RANKS;
 constexpr uint64_t kRingFlagBytes = (kFlagWords + kMaxBlocks + 32) * sizeof(uint64_t);
-constexpr uint64_t kPipeUnits = 4096;  // units per owner of one pipe step (pipe.cu)
-constexpr uint64_t kPipeGenOff = kRingFlagBytes;
-constexpr uint64_t kPipeRsOff = kPipeGenOff + uint64_t(kMaxBlocks) * sizeof(uint64_t);
-constexpr uint64_t kPipeAgOff = kPipeRsOff + kPipeUnits * GF_MAX_RANKS * sizeof(uint64_t);
-constexpr uint64_t kFlagBytes = kPipeAgOff + uint64_t(GF_MAX_RANKS) * kPipeUnits * sizeof(uint64_t);
+constexpr uint64_t kFlagBytes = kRingFlagBytes;
 static_assert(kFlagBytes % 256 == 0, "the symmetric heap stays 256-byte aligned");
 
 struct gf_comm {

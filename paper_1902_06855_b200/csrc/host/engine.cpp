@@ -257,7 +257,7 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
     if (cfg->dtype != GF_F16 && cfg->dtype != GF_F32) return gfi::fail(GF_ERR_CONFIG, "gf_engine_create: bad dtype");
     if (cfg->world < 1 || cfg->world > GF_MAX_RANKS || cfg->rank < 0 || cfg->rank >= cfg->world)
         return gfi::fail(GF_ERR_CONFIG, "gf_engine_create: rank/world out of range");
-    if (cfg->dense_mode < GF_DENSE_AUTO || cfg->dense_mode > GF_DENSE_PIPE || cfg->csc_mode < GF_CSC_PUSH ||
+    if (cfg->dense_mode < GF_DENSE_AUTO || cfg->dense_mode > GF_DENSE_PUSH || cfg->csc_mode < GF_CSC_PUSH ||
         cfg->csc_mode > GF_CSC_PULL)
         return gfi::fail(GF_ERR_CONFIG, "gf_engine_create: bad dense_mode / csc_mode");
     if (cfg->csc && (cfg->final_sparsity < 0.0 || cfg->final_sparsity >= 1.0))
@@ -283,8 +283,7 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
     int mode = cfg->dense_mode;
     if (mode == GF_DENSE_AUTO)  // measured: rspush ahead at 2 and 4 ranks; fp16 pools only
         mode = cfg->dtype == GF_F16 ? GF_DENSE_RSPUSH : (W == 2 ? GF_DENSE_PULL : GF_DENSE_PUSH);
-    if ((mode == GF_DENSE_RSPUSH || mode == GF_DENSE_PIPE) && cfg->dtype != GF_F16) mode = GF_DENSE_PUSH;
-    if (mode == GF_DENSE_PIPE && (ntensors > GF_MAX_WINDOWS_PER_LAUNCH || W == 1)) mode = GF_DENSE_RSPUSH;
+    if (mode == GF_DENSE_RSPUSH && cfg->dtype != GF_F16) mode = GF_DENSE_PUSH;
     if (mode == GF_DENSE_PULL && ntensors > GF_MAX_WINDOWS_PER_LAUNCH) mode = GF_DENSE_PUSH;  // 256-tensor table
     e->dense_mode = mode;
     dense_windows(e);
@@ -305,7 +304,7 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
         e->pull_pools[1] = at;
         at += pool_bytes;
     }
-    if (!cfg->csc && W > 1 && (mode == GF_DENSE_RSPUSH || mode == GF_DENSE_PIPE)) {
+    if (!cfg->csc && W > 1 && mode == GF_DENSE_RSPUSH) {
         e->push_inbox = at;  // slot stride: a multiple of 8 elements (16-byte aligned slots)
         at += align_up(uint64_t(W - 1) * align_up(e->total, 8) * e->esz);
     }
@@ -431,11 +430,6 @@ int gf_engine_dense_step(gf_engine* e, const float* const* grads, float* const* 
     } else if (e->dense_mode == GF_DENSE_RSPUSH) {
         e->last_pool = e->heap_base + e->pool_off;
         rc = gf_sync_step_dense_push(e->comm, dt, e->pool_off, e->push_inbox, grads, out, offs, cnts, m, e->ws.data(),
-                                     e->wl.data(), nw, s);
-    } else if (e->dense_mode == GF_DENSE_PIPE) {
-        e->last_pool = e->heap_base + e->pool_off;
-        mark(e, "pipe", s);
-        rc = gf_sync_step_dense_pipe(e->comm, dt, e->pool_off, e->push_inbox, grads, out, offs, cnts, m, e->ws.data(),
                                      e->wl.data(), nw, s);
     } else if (e->dense_mode == GF_DENSE_PULL) {
         // two pools used alternately: the next step's entry barrier orders the peers' last

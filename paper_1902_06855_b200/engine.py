@@ -28,7 +28,7 @@ from . import capi
 F32, F16 = capi.GF_F32, capi.GF_F16
 THETA_INF = capi.THETA_INF
 _DENSE = {"auto": capi.GF_DENSE_AUTO, "rspush": capi.GF_DENSE_RSPUSH, "pull": capi.GF_DENSE_PULL,
-          "push": capi.GF_DENSE_PUSH, "pipe": capi.GF_DENSE_PIPE}
+          "push": capi.GF_DENSE_PUSH}
 _DENSE_NAME = {v: k for k, v in _DENSE.items()}
 _CSC = {"push": capi.GF_CSC_PUSH, "pull": capi.GF_CSC_PULL}
 _STATE = {"pool": capi.GF_STATE_POOL, "hg": capi.GF_STATE_HG, "hu": capi.GF_STATE_HU, "w": capi.GF_STATE_W,
@@ -119,7 +119,7 @@ class GradSync:
                  lr=0.01, allgather=None, timeout_ms=30000, dense_mode="auto", csc_mode="push",
                  _connect=True):
         if dense_mode not in _DENSE:
-            raise capi.ConfigError(f"dense_mode {dense_mode!r}: auto, rspush, pipe, pull or push")
+            raise capi.ConfigError(f"dense_mode {dense_mode!r}: auto, rspush, pull or push")
         if csc_mode not in _CSC:
             raise capi.ConfigError(f"csc_mode {csc_mode!r}: pull or push")
         self.layout = PoolLayout.build(sizes, chunk)

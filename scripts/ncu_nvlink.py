@@ -2,7 +2,7 @@
 """NVLink bytes per launch of the multi-GPU kernels, from ncu's nvltx/nvlrx counters.
 
 ONE process drives N ranks on N GPUs (peer access, GradSync.local), each running the engine's
-step for MODE (rspush | pipe | pull | push | csc-push | csc-pull) on WORKLOAD's seeded
+step for MODE (rspush | pull | push | csc-push | csc-pull) on WORKLOAD's seeded
 gradients. Run with GF_DIAG_NOWAIT=1: the cross-GPU barriers and flags signal but never wait, so
 ncu can serialise and replay each kernel (replays re-issue the same stores into the peers'
 buffers). Every result is invalid by design; only the traffic and the kernel durations without

@@ -68,7 +68,7 @@ def check_dense(o, W, sizes, dtype, theta, grads, pools_got, outs_got, ring=None
 
 
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
-@pytest.mark.parametrize("mode,dtype", [("rspush", F16), ("pipe", F16), ("pull", F16), ("push", F16), ("pull", F32),
+@pytest.mark.parametrize("mode,dtype", [("rspush", F16), ("pull", F16), ("push", F16), ("pull", F32),
                                         ("push", F32)])
 @pytest.mark.parametrize("case", ["ragged", "many"])
 def test_colo_dense_modes(oracle, world, mode, dtype, case):
@@ -80,7 +80,7 @@ def test_colo_dense_modes(oracle, world, mode, dtype, case):
     total = sum(sizes)
     for theta in thetas:
         cw = ColoWorld(world, sizes, dtype=dtype, theta=theta, dense_mode=mode)
-        fallback = {"pull": "push", "pipe": "rspush"}  # beyond one 256-tensor table
+        fallback = {"pull": "push"}  # beyond one 256-tensor table
         assert cw.ranks[0].dense_mode == (mode if len(sizes) <= 256 else fallback.get(mode, mode))
         try:
             for it in range(3):
@@ -95,8 +95,7 @@ def test_colo_dense_modes(oracle, world, mode, dtype, case):
             cw.close()
 
 
-@pytest.mark.parametrize("world,mode", [(1, "auto"), (2, "auto"), (4, "auto"), (8, "auto"), (2, "pipe"), (4, "pipe"),
-                                        (8, "pipe")])
+@pytest.mark.parametrize("world,mode", [(1, "auto"), (2, "auto"), (4, "auto"), (8, "auto"), (2, "push"), (4, "pull")])
 def test_colo_resnet50_full_vs_reference(oracle, reference, world, mode):
     """BASELINE configs[1]: ResNet-50, all 161 tensors, dense fp16 lazy allreduce (theta 64 MiB
     = one window), through the default engine path (one-pass kernel at N=1, rspush at N>1),
@@ -124,7 +123,7 @@ def test_colo_resnet50_full_vs_reference(oracle, reference, world, mode):
         cw.close()
 
 
-@pytest.mark.parametrize("mode", ["rspush", "pipe", "push"])
+@pytest.mark.parametrize("mode", ["rspush", "push"])
 def test_colo_alexnet_4rank_full_vs_reference(oracle, reference, mode):
     """BASELINE configs[0]: the AlexNet gradient set (61.1M params, 16 tensors), fp16 lazy
     allreduce, theta = inf, 4 ranks — the reference's own oracle run — bit-exact."""
