@@ -149,30 +149,12 @@ int push_minb() {
 // registers while the pushes drain, and after the exit barrier the other segments from my pool:
 // CTA b unpacks exactly the vectors its peer CTAs b pushed to me (the same flat sweep on the
 // owner's segment), which is what its CTA-pair exit barrier covers.
-// This CTA's share of a flat sweep over [0, total) vectors: interleaved (thread g of the grid
-// takes g, g+T, ...) or blocked (CTA b takes one contiguous range, its threads interleave in it).
-struct Sweep {
-    uint64_t start, end, stride;
-    __device__ Sweep(uint64_t total, bool blocked) {
-        if (blocked) {
-            const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
-            start = min(total, uint64_t(blockIdx.x) * per) + threadIdx.x;
-            end = min(total, uint64_t(blockIdx.x + 1) * per);
-            stride = blockDim.x;
-        } else {
-            start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-            end = total;
-            stride = uint64_t(gridDim.x) * blockDim.x;
-        }
-    }
-};
-
-template <int NT, bool UNPACK, int TH, int MINB>
-__global__ void __launch_bounds__(TH, MINB)
+template <int NT, bool UNPACK>
+__global__ void __launch_bounds__(kRingThreads, 1)
 rsp_kernel(const __grid_constant__ RingArgs a, const char* __restrict__ inbox_local, uint64_t slot_bytes,
-           const __grid_constant__ StepTable TT, float inv, int blocked) {
+           const __grid_constant__ StepTable TT, float inv) {
     constexpr int NMAX = NT > 0 ? NT : GF_MAX_RANKS;
-    constexpr int U = MINB >= 3 ? (NMAX <= 2 ? 2 : 1) : (NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1));
+    constexpr int U = NMAX <= 4 ? 4 : (NMAX <= 8 ? 2 : 1);
     __shared__ int s_ok;
     __shared__ FlatWins flat;
     const uint64_t epoch = a.epochs[blockIdx.x];
@@ -213,15 +195,15 @@ rsp_kernel(const __grid_constant__ RingArgs a, const char* __restrict__ inbox_lo
         }
     }
     const uint64_t total = flat.pre[a.nwin];
-    const Sweep sw(total, blocked != 0);
-    for (uint64_t x = sw.start; x < sw.end; x += sw.stride * U) {
+    const uint64_t T = uint64_t(gridDim.x) * blockDim.x, g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (uint64_t x = g; x < total; x += T * U) {
         uint4 v[U][NMAX];
         uint64_t vv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t xu = x + uint64_t(u) * sw.stride;
+            const uint64_t xu = x + uint64_t(u) * T;
             vv[u] = ~0ull;
-            if (xu < sw.end) {
+            if (xu < total) {
                 const int w = flat_window(flat, a.nwin, xu);
                 vv[u] = flat.v0[w] + (xu - flat.pre[w]);
 #pragma unroll
@@ -262,15 +244,15 @@ rsp_kernel(const __grid_constant__ RingArgs a, const char* __restrict__ inbox_lo
                 for (uint64_t e = v1 * 8 + threadIdx.x; e < e1; e += blockDim.x)
                     unpack_elem(e, reinterpret_cast<const volatile uint16_t*>(pool)[e]);
         }
-        const Sweep sq(flat.pre[a.nwin], blocked != 0);  // the vectors peer CTA b pushed
-        for (uint64_t x = sq.start; x < sq.end; x += sq.stride * 4) {
+        const uint64_t tq = flat.pre[a.nwin];
+        for (uint64_t x = g; x < tq; x += T * 4) {
             uint4 h[4];
             uint64_t vq[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const uint64_t xu = x + uint64_t(u) * sq.stride;
+                const uint64_t xu = x + uint64_t(u) * T;
                 vq[u] = ~0ull;
-                if (xu < sq.end) {
+                if (xu < tq) {
                     const int w = flat_window(flat, a.nwin, xu);
                     vq[u] = flat.v0[w] + (xu - flat.pre[w]);
                     h[u] = ld16_cg<GF_F16>(a.bufs[a.rank] + vq[u] * 16);  // pushed by a peer: skip L1
@@ -282,16 +264,6 @@ rsp_kernel(const __grid_constant__ RingArgs a, const char* __restrict__ inbox_lo
         }
     }
     if (tr) a.trace[3] = gfd::globaltimer_ns();
-}
-
-// rsp_kernel launch shape (measurement knob GF_RSP_CFG): 0 512 threads x 1 CTA/SM interleaved,
-// 1 256x2, 2 256x3, 3 512x1 blocked, 4 256x2 blocked, 5 256x4
-int rsp_cfg() {
-    static const int v = [] {
-        const char* e = std::getenv("GF_RSP_CFG");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
 }
 
 // GF_PUSH_DIAG timing probes (results invalid by design): 1 every routed store local, 2 the
@@ -437,23 +409,12 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
             max_seg += (a.wlen[w] + c->world - 1) / c->world;
         }
         fill_common(c, a, pool_heap_off);
-        int grid = gfr::comm_blocks(c, max_seg * 2);
+        const int grid = gfr::comm_blocks(c, max_seg * 2);
         gfi::phase("rsp", s);
         const uint64_t sb = slot_elems * 2;
-        const int cfg = rsp_cfg();
-        const int minb = cfg == 1 || cfg == 4 ? 2 : (cfg == 2 ? 3 : (cfg == 5 ? 4 : 1));
-        const int blocked = cfg == 3 || cfg == 4;
-        grid = std::min(kMaxBlocks, grid * minb);
-#define GF_RSP2(NT_, TH_, MB_)                                                                                   \
-    if (fused) rsp_kernel<NT_, true, TH_, MB_><<<grid, TH_, 0, s>>>(a, inbox_local, sb, TT, inv, blocked);      \
-    else rsp_kernel<NT_, false, TH_, MB_><<<grid, TH_, 0, s>>>(a, inbox_local, sb, TT, inv, blocked);
-#define GF_RSP(NT_)                                          \
-    switch (minb) {                                          \
-        case 2: GF_RSP2(NT_, 256, 2) break;                  \
-        case 3: GF_RSP2(NT_, 256, 3) break;                  \
-        case 4: GF_RSP2(NT_, 256, 4) break;                  \
-        default: GF_RSP2(NT_, kRingThreads, 1) break;        \
-    }
+#define GF_RSP(NT_)                                                                                  \
+    if (fused) rsp_kernel<NT_, true><<<grid, kRingThreads, 0, s>>>(a, inbox_local, sb, TT, inv);     \
+    else rsp_kernel<NT_, false><<<grid, kRingThreads, 0, s>>>(a, inbox_local, sb, TT, inv);
         switch (c->world) {
             case 2: GF_RSP(2) break;
             case 4: GF_RSP(4) break;
@@ -461,7 +422,6 @@ int gf_sync_step_dense_push(gf_comm* c, int dtype, uint64_t pool_heap_off, uint6
             default: GF_RSP(0) break;
         }
 #undef GF_RSP
-#undef GF_RSP2
         gfi::count_launch();
         if (int rc = gfi::check_launch("gf_sync_step_dense_push")) return rc;
     }
