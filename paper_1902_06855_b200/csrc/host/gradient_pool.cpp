@@ -135,20 +135,25 @@ GradientPool::GradientPool(const std::vector<std::size_t>& sizes, std::size_t ch
     num_chunks_ = std::max<std::size_t>(
         1, static_cast<std::size_t>(std::llround(static_cast<double>(off) / static_cast<double>(chunk_size))));
     next_expected_id_ = m;
-    cuda_ok(cudaGetDevice(&device_), "cudaGetDevice");
-    // the device side (pool, streams, staging) is created on first use: constructing a pool
-    // is pure layout, as in the reference (acceptance criterion 1 times it)
+    // the device (and the device side: pool, streams, staging) is bound on first use:
+    // constructing a pool is pure layout, as in the reference (acceptance criterion 1 times it;
+    // a CUDA call here would pay the runtime's initialisation)
     host_valid_ = false;  // the host mirror is allocated on the first host read
 }
 
 GradientPool::GradientPool(GradientPool&& o) noexcept = default;
 
+int GradientPool::device() const {
+    if (device_ < 0) cuda_ok(cudaGetDevice(&device_), "cudaGetDevice");
+    return device_;
+}
+
 GradientPool::~GradientPool() = default;
 
 GradientPool::Device& GradientPool::dev() {
     if (!dev_) {
-        OnDevice g(device_);
-        dev_ = std::make_unique<Device>(device_, total_elements_ * element_size(element_type_));
+        OnDevice g(device());
+        dev_ = std::make_unique<Device>(device(), total_elements_ * element_size(element_type_));
         data_ = dev_->data;
         dev_->slot_off.resize(descs_.size());
         std::size_t asc = 0;
@@ -174,7 +179,7 @@ void GradientPool::run_pending_work() {
 
 void GradientPool::synchronize() {
     run_pending_work();
-    OnDevice g(device_);
+    OnDevice g(device());
     cuda_ok(cudaStreamSynchronize(dev().stream), "pool stream");
 }
 
@@ -213,7 +218,7 @@ void GradientPool::begin_iteration() {
     Device& D = dev();
     if (!D.fresh_iteration) {  // an abandoned iteration: retire its staging buffer like a full one
         flush_writes();
-        OnDevice g(device_);
+        OnDevice g(device());
         cuda_ok(cudaEventRecord(D.ev_packed[D.parity], D.stream), "event");
         D.packed_recorded[D.parity] = true;
         D.parity ^= 1;
@@ -234,7 +239,7 @@ std::vector<std::size_t> GradientPool::write_tensor(int tensor_id, std::span<con
     if (values.size() != d.element_count)
         throw ConfigError("tensor " + std::to_string(tensor_id) + " length mismatch: " +
                           std::to_string(values.size()) + " vs " + std::to_string(d.element_count));
-    OnDevice g(device_);
+    OnDevice g(device());
     Device& D = dev();
     const float* src = values.data();
     const std::size_t bytes = values.size() * sizeof(float);
@@ -302,7 +307,7 @@ std::vector<std::size_t> GradientPool::write_tensor(int tensor_id, std::span<con
 void GradientPool::flush_writes() {
     Device& D = dev();
     if (D.pend_src.empty()) return;
-    OnDevice g(device_);
+    OnDevice g(device());
     if (D.pend_copies) {  // the queued H2D copies come first
         D.issue_copy();
         cuda_ok(cudaEventRecord(D.ev_copy, D.copy), "event");
@@ -321,7 +326,7 @@ void GradientPool::read_averaged(std::span<float> out, int world, bool wait) {
     if (out.size() != total_elements_) throw ConfigError("read_averaged: output does not match the pool layout");
     if (world < 1) throw ConfigError("read_averaged: world must be >= 1");
     run_pending_work();
-    OnDevice g(device_);
+    OnDevice g(device());
     Device& D = dev();
     float* avg = D.averaged(total_elements_);
     const std::uint64_t off = 0, cnt = total_elements_;
@@ -335,7 +340,7 @@ void GradientPool::sync_host() {
     if (host_.size() != total_elements_ * element_size(element_type_))
         host_.resize(total_elements_ * element_size(element_type_));
     synchronize();
-    OnDevice g(device_);
+    OnDevice g(device());
     cuda_ok(cudaMemcpyAsync(host_.data(), data_, host_.size(), cudaMemcpyDeviceToHost, dev().stream), "pool D2H");
     cuda_ok(cudaStreamSynchronize(dev().stream), "pool D2H");
     host_valid_ = true;
@@ -352,7 +357,7 @@ void GradientPool::set(std::size_t i, float v) {
     ScalarBuffer h{element_type_, host_.data(), total_elements_, Residency::kHost};
     h.set(i, v);
     const std::size_t es = element_size(element_type_);
-    OnDevice g(device_);
+    OnDevice g(device());
     cuda_ok(cudaMemcpyAsync(data_ + i * es, host_.data() + i * es, es, cudaMemcpyHostToDevice, dev().stream),
             "pool set");
     cuda_ok(cudaStreamSynchronize(dev().stream), "pool set");
@@ -361,7 +366,7 @@ void GradientPool::set(std::size_t i, float v) {
 float GradientPool::chunk_l1(std::size_t c) {
     const std::size_t b = chunk_begin(c), len = chunk_length(c);
     run_pending_work();
-    OnDevice g(device_);
+    OnDevice g(device());
     Device& D = dev();
     // one-chunk launch of K3 (exact; bit-identical to the reference's fp64 loop)
     check(gf_chunk_norms(static_cast<int>(element_type_), data_ + b * element_size(element_type_), len, len, 1,

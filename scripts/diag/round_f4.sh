@@ -1,6 +1,12 @@
 #!/bin/bash
 # 4-GPU evidence: the cross-GPU tests (multigpu + the N=4 stress), N=2/N=4 benches, NVLink ncu at N=4
 P=gpurun_out/r2f4
+timeout 600 python -m pytest tests/test_reference_suites.py -m gpu -q -p no:cacheprovider > ${P}_pytest_refsuites.txt 2>&1
+for numa in 1 0; do
+  if [ $numa = 0 ]; then export GF_BENCH_NO_NUMA=1; fi
+  timeout 400 python bench.py --no-cpu-baseline --no-csc > ${P}_bench_n1_numa$numa.txt 2>&1
+done
+unset GF_BENCH_NO_NUMA
 timeout 1200 python -m pytest tests/test_gpu_multi.py tests/test_gpu_stress.py -m gpu -q -p no:cacheprovider -k "not colocated" > ${P}_pytest_multi.txt 2>&1; echo "rc=$?" >> ${P}_pytest_multi.txt
 for N in 2 4; do
   TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2958$N"
