@@ -504,9 +504,29 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
                                         e->plan[cur], T, chunk, nc, grads, e->offs.data(), e->sizes.data(), e->m,
                                         static_cast<float>(C.momentum), e->nacc, part, st);
     };
-    if (solo) {
+    auto update = [&](cudaStream_t us) {
+        return gf_csc_sgd_update(dt, pool, e->plan[cur], T, chunk, nc, k_cur, W, static_cast<float>(C.momentum),
+                                 static_cast<float>(C.learning_rate), e->hu, e->w, us);
+    };
+    // world 1 with exact norms: the update of the selected chunks needs only their packed values
+    const bool solo_split = solo && e->nacc && !e->marks_on;
+    if (solo && !solo_split) {
         mark(e, "pack_correct", s);
         GF_ENG_OK(pack_correct(0, s));
+    } else if (solo_split) {
+        // The selected chunks' pack_correct and then their momentum update (the collective is the
+        // identity: the pool holds g_avg) on the highest-priority stream, beside the other chunks'
+        // pack_correct from the step's start (disjoint elements); the selection follows both.
+        GF_ENG_CUDA(cudaEventRecord(e->ev_sel, s));
+        GF_ENG_CUDA(cudaStreamWaitEvent(e->hp, e->ev_sel, 0));
+        GF_ENG_CUDA(cudaStreamWaitEvent(e->side, e->ev_sel, 0));
+        GF_ENG_OK(pack_correct(1, e->hp));
+        GF_ENG_OK(update(e->hp));
+        GF_ENG_CUDA(cudaEventRecord(e->ev_x, e->hp));
+        GF_ENG_OK(pack_correct(2, e->side));
+        GF_ENG_CUDA(cudaEventRecord(e->ev_rest, e->side));
+        GF_ENG_CUDA(cudaStreamWaitEvent(s, e->ev_x, 0));
+        GF_ENG_CUDA(cudaStreamWaitEvent(s, e->ev_rest, 0));
     } else {
         // the staged (important) chunks first; their exchange then runs beside the correction
         // of the other chunks (disjoint pool / hg / nacc elements), its grid capped so that the
@@ -553,11 +573,9 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
         return gf_csc_select(e->comm, e->norms_off, nc, k, e->imp[nxt], T, chunk, dt, C.theta_bytes, e->coff[nxt],
                              e->plan[nxt], e->nacc, e->nacc ? pool : nullptr, e->nacc ? e->imp[cur] : nullptr, s);
     };
-    auto update = [&](cudaStream_t us) {
-        return gf_csc_sgd_update(dt, pool, e->plan[cur], T, chunk, nc, k_cur, W, static_cast<float>(C.momentum),
-                                 static_cast<float>(C.learning_rate), e->hu, e->w, us);
-    };
-    if (e->marks_on) {  // per-kernel timing: one stream, kernels in order
+    if (solo_split) {  // the update already ran beside the packing
+        GF_ENG_OK(select());
+    } else if (e->marks_on) {  // per-kernel timing: one stream, kernels in order
         mark(e, "select", s);
         GF_ENG_OK(select());
         mark(e, "sgd_update", s);

@@ -57,8 +57,11 @@ __device__ __forceinline__ T block_excl_scan(T v, T* total, T* warp_sums /*[32]*
     return warp_off + x - v;
 }
 
+constexpr int kSelBins = 2048;  // radix digits of 11, 11 and 10 bits: three passes over 32-bit keys
+static_assert(kSelBins == 2 * kSelThreads, "two histogram bins per thread in the digit search");
+
 struct SelShared {
-    unsigned hist[256];
+    unsigned hist[kSelBins];
     uint64_t u64s[32];
     unsigned digit;
     unsigned long long rem;
@@ -85,15 +88,17 @@ inline __device__ void block_topk(const float* norms, uint64_t nc, uint64_t k, u
     }
     uint32_t prefix = 0;
     unsigned long long remaining = k;
-    for (int pass = 0; pass < 4; ++pass) {
-        const int shift = 24 - 8 * pass;
-        for (int d = tid; d < 256; d += kSelThreads) sh.hist[d] = 0;
+    for (int pass = 0; pass < 3; ++pass) {
+        const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);  // digits [31:21], [20:10], [9:0]
+        const uint32_t dmask = pass == 2 ? 1023u : 2047u;
+        sh.hist[tid] = 0;
+        sh.hist[tid + kSelThreads] = 0;
         __syncthreads();
         // Warp-aggregated: chunk norms share a few exponents, so most keys of a pass fall into one
         // or two digits and per-key shared atomics would serialise on one address.
         auto count = [&](bool valid, uint32_t key) {
-            valid = valid && (pass == 0 || (key >> (shift + 8)) == prefix);
-            const uint32_t d = (key >> shift) & 255u;
+            valid = valid && (pass == 0 || (key >> (pass == 1 ? 21 : 10)) == prefix);
+            const uint32_t d = (key >> shift) & dmask;
             const unsigned same = __match_any_sync(0xFFFFFFFFu, valid ? d : 0xFFFFFFFFu);
             if (valid && __ffs(same) - 1 == (tid & 31)) atomicAdd(&sh.hist[d], unsigned(__popc(same)));
         };
@@ -107,38 +112,24 @@ inline __device__ void block_topk(const float* norms, uint64_t nc, uint64_t k, u
             }
         }
         __syncthreads();
-        if (tid < 32) {
-            // warp 0: lane l owns digits 255-8l .. 248-8l (descending); find the digit where
-            // the descending cumulative count first reaches `remaining`.
-            unsigned c[8];
-            unsigned tot = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                c[j] = sh.hist[255 - 8 * tid - j];
-                tot += c[j];
-            }
-            unsigned incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                if (tid >= o) incl += y;
-            }
-            const unsigned excl = incl - tot;
-            const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl >= remaining);
-            const int L = hit ? __ffs(hit) - 1 : 31;
-            if (tid == L) {
-                unsigned long long cum = excl;
-                int d = 255 - 8 * L;
-                for (int j = 0; j < 8; ++j, --d) {
-                    if (cum + c[j] >= remaining || d == 0) break;
-                    cum += c[j];
-                }
-                sh.digit = unsigned(d);
-                sh.rem = remaining - cum;
+        // thread t owns digits hi = top - 2t and hi - 1 (descending); one block scan finds the
+        // digit where the descending cumulative count first reaches `remaining`
+        const int top = int(dmask);
+        const int dhi = top - 2 * tid, dlo = dhi - 1;
+        const uint64_t chi = dhi >= 0 ? sh.hist[dhi] : 0, clo = dlo >= 0 ? sh.hist[dlo] : 0;
+        uint64_t total;
+        const uint64_t excl = block_excl_scan<uint64_t>(chi + clo, &total, sh.u64s);
+        if (excl < remaining && remaining <= excl + chi + clo) {  // exactly one thread
+            if (excl + chi >= remaining) {
+                sh.digit = unsigned(dhi);
+                sh.rem = remaining - excl;
+            } else {
+                sh.digit = unsigned(dlo);
+                sh.rem = remaining - excl - chi;
             }
         }
         __syncthreads();
-        prefix = (prefix << 8) | sh.digit;
+        prefix = (prefix << (pass == 2 ? 10 : 11)) | sh.digit;
         remaining = sh.rem;
         __syncthreads();
     }
