@@ -45,6 +45,8 @@
  *                                   (src/trainer.cpp:297-347), FusionEngine (src/fusion.cpp:25-123),
  *                                   SparseState (src/sparse.cpp:57-224)
  *  gf_csc_exchange_pull             sparse_exchange ring + write-back (pull form) src/sparse.cpp:106-170
+ *  gf_csc_pack_correct_routed       correction_pre_allreduce + staging pack, routed to the exchange owners
+ *                                   src/sparse.cpp:57-79, :129-140
  *  gf_csc_select                    select_next_important (norm allreduce + top-k) src/sparse.cpp:172-204
  *  gf_ring_traffic                  TrafficStats record_send/recv of the ring include/gflow/transport.hpp:48-91, src/collectives.cpp:69-96
  *  gf_oracle_allreduce_ptrs         oracle_allreduce                         src/collectives.cpp:203-226
@@ -299,6 +301,20 @@ int gf_ring_allreduce_colocated_planned(int dtype, void* const* bufs, int world,
  * switch together; UINT64_MAX switches back. The caller must not rewrite its norms or
  * inbox before its next exchange (the CSC step order guarantees it). */
 int gf_comm_set_select_inbox(gf_comm* comm, uint64_t inbox_heap_off);
+/* Switches this communicator's CSC exchange to the routed form: world-1 inbox slots of
+ * slot_elems fp16 elements (a multiple of 8, >= the staging capacity) at inbox_heap_off (same
+ * offset on every rank); gf_csc_pack_correct_routed stores every staged element at the owner of
+ * its exchange segment (my staging, or my slot of the owner's inbox over NVLink), so
+ * gf_csc_exchange_pull reduces from local memory and pulls only the all-gather. Same results.
+ * All ranks switch together; UINT64_MAX switches back. */
+int gf_comm_set_csc_inbox(gf_comm* comm, uint64_t inbox_heap_off, uint64_t slot_elems);
+/* Part 1 of gf_csc_pack_correct_part (the chunks of the device-side `plan`, fp16, tensors in
+ * ascending id) with every staged element routed to its exchange owner (gf_comm_set_csc_inbox);
+ * the staging buffer is at stage_heap_off in the symmetric heap. */
+int gf_csc_pack_correct_routed(gf_comm* comm, void* pool, float* hg, uint64_t stage_heap_off,
+                               const uint64_t* plan, uint64_t chunk, const float* const* src,
+                               const uint64_t* pool_off, const uint64_t* count, int ntensors,
+                               float momentum, void* stream);
 int gf_csc_select(gf_comm* comm, uint64_t norms_off, uint64_t nc, uint64_t k,
                   uint8_t* flags, uint64_t total, uint64_t chunk, int dtype, uint64_t theta,
                   uint64_t* coff, uint64_t* plan, uint64_t* nacc, const void* pool,

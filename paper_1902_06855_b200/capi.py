@@ -96,6 +96,8 @@ SIGNATURES = {
     "gf_comm_trace": [_vp, _vp],
     "gf_comm_trace_n": [_vp, _vp, _i],
     "gf_comm_set_select_inbox": [_vp, _u64],
+    "gf_comm_set_csc_inbox": [_vp, _u64, _u64],
+    "gf_csc_pack_correct_routed": [_vp, _vp, _vp, _u64, _vp, _u64, _vp, _vp, _vp, _i, _f, _vp],
     "gf_comm_rank": [_vp],
     "gf_comm_world": [_vp],
     "gf_ring_allreduce": [_vp, _i, _u64, _vp, _vp, _i, _vp],

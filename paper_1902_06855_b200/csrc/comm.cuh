@@ -46,6 +46,10 @@ struct gf_comm {
     int max_blocks = 0;     // gf_comm_set_max_blocks (0: automatic)
     int block_threads = 0;  // gf_comm_set_block_threads: CTA size of the CSC exchange (0: 512)
     uint64_t sel_inbox_off = UINT64_MAX;  // gf_comm_set_select_inbox (UINT64_MAX: pull protocol)
+    // gf_comm_set_csc_inbox: the routed CSC exchange (UINT64_MAX: off). World-1 slots of
+    // csc_slot_elems fp16 elements; slot t of the owner at position j holds position j + 1 + t.
+    uint64_t csc_inbox_off = UINT64_MAX;
+    uint64_t csc_slot_elems = 0;
 };
 
 namespace {

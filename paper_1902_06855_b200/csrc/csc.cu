@@ -21,7 +21,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
+#include "comm.cuh"
 #include "gf_device.cuh"
 #include "gf_internal.cuh"
 #include "select.cuh"
@@ -341,6 +343,26 @@ __device__ __forceinline__ uint64_t staged_to_pool(const uint64_t* plan, uint64_
     return plan[4 + q] * chunk + (s - q * chunk);
 }
 
+// Routing of staged elements to the owner of their exchange segment (gf_csc_pack_correct_routed):
+// the planned windows over the staging index space (plan[2] windows of plan[3] elements, the
+// last shorter) are split by segment_of (src/collectives.cpp:47-53); element s of segment j goes
+// to my staging when j is my ring position, else into my slot of owner j's inbox (slot t of the
+// owner at position j holds position j + 1 + t, the rspush layout). world == 0: no routing.
+struct StageRoute {
+    int world, pos;
+    uint16_t* dst_by_pos[GF_MAX_RANKS];  // where an element of segment j is stored (staging indices)
+};
+
+// owner position of staging element s, and the end of its segment
+__device__ __forceinline__ int stage_owner(const StageRoute& R, const uint64_t* plan, uint64_t s, uint64_t& seg_end) {
+    const uint64_t staged = plan[0], nwin = plan[2], stride = plan[3];
+    const uint64_t w = min(s / stride, nwin - 1), ws = w * stride, wl = (w + 1 == nwin) ? staged - ws : stride;
+    const uint64_t n = uint64_t(R.world), base = wl / n, rem = wl % n, off = s - ws, big = rem * (base + 1);
+    const uint64_t j = off < big ? off / (base + 1) : rem + (off - big) / base;  // off >= big implies base > 0
+    seg_end = ws + j * base + min(j, rem) + base + (j < rem ? 1 : 0);
+    return int(j);
+}
+
 // The grid sweeps the staging index space [0, plan[0]) in 8-element vectors (kPlannedU per
 // thread, every load in flight before the math); each vector maps to its pool element through
 // the plan. Work is proportional to the staged data only.
@@ -348,7 +370,8 @@ constexpr int kPlannedU = 2;
 template <int DT>
 __global__ void __launch_bounds__(kThreads, 4)
 pack_correct_planned_kernel(const __grid_constant__ TensorTable T, void* __restrict__ pool, float* __restrict__ hg,
-                            void* __restrict__ staging, const uint64_t* __restrict__ plan, uint64_t chunk, float mom) {
+                            void* __restrict__ staging, const uint64_t* __restrict__ plan, uint64_t chunk, float mom,
+                            const __grid_constant__ StageRoute R) {
     const uint64_t staged = plan[0], k = plan[1];
     if (k == 0) return;
     const uint64_t nv = (staged + 7) / 8, G = uint64_t(gridDim.x) * blockDim.x;
@@ -386,7 +409,22 @@ pack_correct_planned_kernel(const __grid_constant__ TensorTable T, void* __restr
                 correct8(gv[u], reinterpret_cast<const float*>(&hv[u]), true, mom, hn, ov, nan);
                 gfd::st32f(hg + e, make_float4(hn[0], hn[1], hn[2], hn[3]), make_float4(hn[4], hn[5], hn[6], hn[7]));
                 gfd::st16(static_cast<uint16_t*>(pool) + e, ov);
-                gfd::st16(static_cast<uint16_t*>(staging) + v * 8, ov);
+                if (R.world == 0) {
+                    gfd::st16(static_cast<uint16_t*>(staging) + v * 8, ov);
+                } else {
+                    uint64_t seg_end;
+                    const int j = stage_owner(R, plan, v * 8, seg_end);
+                    if (v * 8 + 8 <= seg_end) {
+                        gfd::st16(R.dst_by_pos[j] + v * 8, ov);
+                    } else {  // a segment boundary inside the vector
+                        const uint32_t w[4] = {ov.x, ov.y, ov.z, ov.w};
+                        for (int q = 0; q < 8; ++q) {
+                            uint64_t se;
+                            const int jq = stage_owner(R, plan, v * 8 + q, se);
+                            R.dst_by_pos[jq][v * 8 + q] = uint16_t((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu);
+                        }
+                    }
+                }
                 continue;
             }
             for (uint64_t s = v * 8; s < min(v * 8 + 8, staged); ++s) {  // element by element
@@ -397,7 +435,12 @@ pack_correct_planned_kernel(const __grid_constant__ TensorTable T, void* __restr
                 if (DT == GF_F16) {
                     const uint16_t w = gfd::enc(correct_elem(gfd::dec(gfd::enc(x)), hg + q, true, mom));
                     static_cast<uint16_t*>(pool)[q] = w;
-                    static_cast<uint16_t*>(staging)[s] = w;
+                    if (R.world == 0) {
+                        static_cast<uint16_t*>(staging)[s] = w;
+                    } else {
+                        uint64_t se;
+                        R.dst_by_pos[stage_owner(R, plan, s, se)][s] = w;
+                    }
                 } else {
                     const float w = correct_elem(x, hg + q, true, mom);
                     static_cast<float*>(pool)[q] = w;
@@ -628,10 +671,10 @@ int gf_csc_pack_correct_part(int dtype, void* pool, float* hg, void* staging,
                                   const int g = gfi::sm_count() * 4;
                                   if (dtype == GF_F16)
                                       pack_correct_planned_kernel<GF_F16><<<g, kThreads, 0, gfi::S(stream)>>>(
-                                          T, pool, hg, staging, plan, chunk, momentum);
+                                          T, pool, hg, staging, plan, chunk, momentum, StageRoute{});
                                   else
                                       pack_correct_planned_kernel<GF_F32><<<g, kThreads, 0, gfi::S(stream)>>>(
-                                          T, pool, hg, staging, plan, chunk, momentum);
+                                          T, pool, hg, staging, plan, chunk, momentum, StageRoute{});
                               });
     }
     return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
@@ -646,6 +689,38 @@ int gf_csc_pack_correct_part(int dtype, void* pool, float* hg, void* staging,
                               else
                                   pack_correct_kernel<GF_F32><<<grid, kThreads, 0, gfi::S(stream)>>>(
                                       T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc, part);
+                          });
+}
+
+int gf_csc_pack_correct_routed(gf_comm* c, void* pool, float* hg, uint64_t stage_heap_off, const uint64_t* plan,
+                               uint64_t chunk, const float* const* src, const uint64_t* pool_off, const uint64_t* count,
+                               int ntensors, float momentum, void* stream) {
+    if (int rc = comm_ready(c)) return rc;
+    if (c->csc_inbox_off == UINT64_MAX)
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct_routed: no CSC inbox (gf_comm_set_csc_inbox)");
+    if (!pool || !hg || !plan || !src || !pool_off || !count || ntensors < 1 || chunk == 0 || chunk % 8 != 0)
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct_routed: fp16, chunk % 8 == 0, >= 1 tensor");
+    for (int i = 1; i < ntensors; ++i)
+        if (pool_off[i] >= pool_off[i - 1])
+            return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct_routed: tensors in ascending id (descending offsets)");
+    if (stage_heap_off % 16 != 0 || stage_heap_off + c->csc_slot_elems * 2 > c->heap_bytes)
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct_routed: staging outside the heap or not 16-B aligned");
+    StageRoute R;
+    std::memset(&R, 0, sizeof(R));
+    R.world = c->world;
+    R.pos = c->pos;
+    for (int j = 0; j < c->world; ++j) {
+        char* base = c->peer_alloc[c->ring[j]] + kFlagBytes;
+        R.dst_by_pos[j] = j == c->pos ? reinterpret_cast<uint16_t*>(c->alloc + kFlagBytes + stage_heap_off)
+                                      : reinterpret_cast<uint16_t*>(base + c->csc_inbox_off) +
+                                            uint64_t((c->pos - j - 1 + c->world) % c->world) * c->csc_slot_elems;
+    }
+    DeviceGuard g(c->device);
+    void* staging = c->alloc + kFlagBytes + stage_heap_off;
+    return for_each_table(reinterpret_cast<const void* const*>(src), pool_off, count, ntensors,
+                          [&](const TensorTable& T, uint64_t, int) {
+                              pack_correct_planned_kernel<GF_F16><<<gfi::sm_count() * 4, kThreads, 0, gfi::S(stream)>>>(
+                                  T, pool, hg, staging, plan, chunk, momentum, R);
                           });
 }
 

@@ -79,6 +79,7 @@ struct gf_engine {
     // symmetric heap layout (bytes)
     uint64_t pool_off = 0, pull_pools[2] = {0, 0}, push_inbox = UINT64_MAX, stage_off = 0, norms_off = 0,
              inbox_off = 0, heap = 0;
+    uint64_t csc_inbox = UINT64_MAX, csc_slot = 0;  // routed CSC exchange (csc_mode PULL, fp16)
     int pull_flip = 0;
     bool pull_two_pools = false;
     gf_comm* comm = nullptr;
@@ -195,6 +196,7 @@ int alloc_csc_state(gf_engine* e) {
 
 int after_connect(gf_engine* e) {
     if (e->cfg.csc && e->cfg.world > 1) GF_ENG_OK(gf_comm_set_select_inbox(e->comm, e->inbox_off));
+    if (e->csc_inbox != UINT64_MAX) GF_ENG_OK(gf_comm_set_csc_inbox(e->comm, e->csc_inbox, e->csc_slot));
     return GF_OK;
 }
 
@@ -310,6 +312,14 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
     }
     e->stage_off = at;
     e->norms_off = e->stage_off + (cfg->csc ? pool_bytes : 0);
+    // the routed CSC exchange (pull form, fp16 with exact norms): world-1 inbox slots of the
+    // staging capacity; the selected chunks' pack stores every staged element at its owner
+    if (cfg->csc && W > 1 && cfg->csc_mode == GF_CSC_PULL && cfg->dtype == GF_F16 && cfg->chunk % 8 == 0 &&
+        e->nc <= 6144) {
+        e->csc_slot = align_up(e->total, 8);
+        e->csc_inbox = e->norms_off;
+        e->norms_off += align_up(uint64_t(W - 1) * e->csc_slot * 2);
+    }
     e->inbox_off = e->norms_off + align_up(e->nc * 4);
     e->heap = e->inbox_off + ((cfg->csc && W > 1) ? align_up(uint64_t(W) * e->nc * 4) : 0);
     DevGuard g(cfg->device);
@@ -500,6 +510,9 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
         return gf_csc_scatter(dt, pool, stage, e->plan[cur], e->coff[cur], T, chunk, nc, k_cur, e->nacc, xs);
     };
     auto pack_correct = [&](int part, cudaStream_t st) {
+        if (part == 1 && e->csc_inbox != UINT64_MAX)  // routed to the exchange owners
+            return gf_csc_pack_correct_routed(e->comm, pool, e->hg, e->stage_off, e->plan[cur], chunk, grads,
+                                              e->offs.data(), e->sizes.data(), e->m, static_cast<float>(C.momentum), st);
         return gf_csc_pack_correct_part(dt, pool, e->hg, solo ? nullptr : stage, e->imp[cur], e->coff[cur],
                                         e->plan[cur], T, chunk, nc, grads, e->offs.data(), e->sizes.data(), e->m,
                                         static_cast<float>(C.momentum), e->nacc, part, st);

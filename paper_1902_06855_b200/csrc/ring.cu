@@ -273,7 +273,10 @@ __global__ void __launch_bounds__(kRingThreads) csc_pull_kernel(const __grid_con
     const int nwin = int(a.plan[2]);
     const char* src[NMAX];
 #pragma unroll
-    for (int t = 0; t < NMAX; ++t) src[t] = (t < n) ? a.bufs[a.ring[(a.pos + t) % n]] : nullptr;
+    for (int t = 0; t < NMAX; ++t)
+        src[t] = t >= n ? nullptr
+                        : (a.csc_inbox == nullptr ? a.bufs[a.ring[(a.pos + t) % n]]
+                                                  : (t == 0 ? a.bufs[a.rank] : a.csc_inbox + uint64_t(t - 1) * a.csc_slot_bytes));
     auto seg = [&](int w, int j, uint64_t& e0, uint64_t& e1) {  // segment_of (collectives.cpp:47-53)
         const uint64_t ws = uint64_t(w) * stride, wl = (w == nwin - 1) ? staged - ws : stride;
         const uint64_t base = wl / uint64_t(n), rem = wl % uint64_t(n), uj = uint64_t(j);
@@ -756,6 +759,18 @@ int gf_comm_set_select_inbox(gf_comm* c, uint64_t inbox_heap_off) {
     return GF_OK;
 }
 
+int gf_comm_set_csc_inbox(gf_comm* c, uint64_t inbox_heap_off, uint64_t slot_elems) {
+    if (!c) return gfi::fail(GF_ERR_CONFIG, "null communicator");
+    if (inbox_heap_off != UINT64_MAX &&
+        (inbox_heap_off % 16 != 0 || slot_elems % 8 != 0 || slot_elems == 0 ||
+         inbox_heap_off + uint64_t(c->world - 1) * slot_elems * 2 > c->heap_bytes))
+        return gfi::fail(GF_ERR_CONFIG, "gf_comm_set_csc_inbox: world-1 slots of slot_elems (multiple of 8) fp16 "
+                                        "elements at a 16-B aligned offset inside the heap");
+    c->csc_inbox_off = inbox_heap_off;
+    c->csc_slot_elems = inbox_heap_off == UINT64_MAX ? 0 : slot_elems;
+    return GF_OK;
+}
+
 int gf_comm_trace_n(gf_comm* c, uint64_t* out, int n) {
     if (!c || !out || n < 0 || n > 16) return gfi::fail(GF_ERR_CONFIG, "gf_comm_trace_n: bad arguments");
     const volatile uint64_t* t =
@@ -934,6 +949,10 @@ int gf_csc_exchange_pull(gf_comm* c, uint64_t stage_heap_off, const uint64_t* pl
     a.wb_nacc = nacc;
     a.wb_chunk = chunk;
     a.wb_nc = nc;
+    if (c->csc_inbox_off != UINT64_MAX) {
+        a.csc_inbox = c->alloc + kFlagBytes + c->csc_inbox_off;
+        a.csc_slot_bytes = c->csc_slot_elems * 2;
+    }
     const uint64_t bound = c->heap_bytes > stage_heap_off ? (c->heap_bytes - stage_heap_off) / c->world : 0;
     const dim3 grid(gfr::comm_blocks(c, bound));
     const size_t smem = size_t(nc) * 8;

@@ -34,6 +34,10 @@ struct RingArgs {
     char* wb_pool;
     uint64_t* wb_nacc;
     uint64_t wb_chunk, wb_nc;
+    // routed CSC exchange (gf_comm_set_csc_inbox): the reduce-scatter's operands are local, my
+    // staging buffer and my inbox slots (ring order from my position); null: pulled from the peers
+    const char* csc_inbox;
+    uint64_t csc_slot_bytes;
     uint64_t wstart[kMaxW];
     uint64_t wlen[kMaxW];
 };
