@@ -707,9 +707,10 @@ def main():
                     help="dense N>1: rspush (pack pushes the reduce-scatter operands to their owners, "
                          "local reduce + all-gather push, unpack), pull (pack + pull RS/AG fused with "
                          "unpack), push (pack + push-pull ring + unpack); auto = rspush")
-    ap.add_argument("--csc-mode", default="push", choices=["pull", "push"],
-                    help="CSC N>1 exchange: pull (pull RS/AG straight into the pool) or push "
-                         "(push-pull ring + fused write-back)")
+    ap.add_argument("--csc-mode", default="auto", choices=["auto", "pull", "push"],
+                    help="CSC N>1 exchange: pull (selected chunks routed to their owners by the pack, "
+                         "local RS + pull AG straight into the pool) or push (push-pull ring + fused "
+                         "write-back); auto = pull from 4 ranks, else push")
     args = ap.parse_args()
 
     world = env_int("WORLD_SIZE", 1)
@@ -746,7 +747,7 @@ def main():
     if args.overlap > 0 and not run.csc:
         extra["overlap"] = dict(overlap_probe(run, args.overlap), sync_alone_ms=round(res["ms"], 4))
     nccl = nccl_compare(run) if world > 1 else None
-    exchange = "none (N=1)" if world == 1 else (args.csc_mode if run.csc else run.sync.dense_mode)
+    exchange = "none (N=1)" if world == 1 else (run.sync.csc_mode if run.csc else run.sync.dense_mode)
     run.close()
 
     csc_sub = None
@@ -757,7 +758,7 @@ def main():
         csc_sub = {"workload": CSC_SUB, "config": config_of(CSC_SUB, crun.wl, world), "value": round(c["ms"], 4),
                    "unit": "ms", "kernels": c["kernels"], "roofline": c["roofline"], "bus_gbs": c["bus_gbs"],
                    "select_us": round(sel * 1e3, 2) if sel else None, "gpu_launches": c["launches"],
-                   "exchange": "none (N=1)" if world == 1 else args.csc_mode,
+                   "exchange": "none (N=1)" if world == 1 else crun.sync.csc_mode,
                    "parity": c["parity"], "parity_detail": c.get("parity_detail"),
                    "cpu_baseline": c.get("cpu_baseline")}
         crun.close()

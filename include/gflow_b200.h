@@ -359,14 +359,14 @@ int gf_synth_grads(int rank, int step, const uint64_t* sizes, int ntensors, floa
  * pointers in ascending tensor id (id 1 first), as the reference's write_tensor(id, span). */
 typedef struct gf_engine gf_engine;
 enum { GF_DENSE_AUTO = 0, GF_DENSE_RSPUSH = 1, GF_DENSE_PULL = 2, GF_DENSE_PUSH = 3 };
-enum { GF_CSC_PUSH = 0, GF_CSC_PULL = 1 };
+enum { GF_CSC_PUSH = 0, GF_CSC_PULL = 1, GF_CSC_AUTO = 2 };
 typedef struct {
     int world, rank, device, dtype;
     uint64_t theta_bytes;     /* FusionConfig::threshold_bytes (fusion.hpp:27-30) */
     uint64_t chunk;           /* GradientPool chunk size (gradient_pool.hpp:16) */
     int csc;                  /* 0: dense lazy allreduce; 1: CSC (TrainOptions::csc) */
     int dense_mode;           /* GF_DENSE_*: N>1 dense exchange (AUTO = RSPUSH for fp16) */
-    int csc_mode;             /* GF_CSC_*: N>1 CSC exchange form */
+    int csc_mode;             /* GF_CSC_*: N>1 CSC exchange form (AUTO: routed PULL from 4 ranks, else PUSH) */
     double final_sparsity;    /* SparseConfig (sparse.hpp:21-26) */
     uint64_t warmup_iters;
     double momentum, learning_rate;
@@ -377,6 +377,7 @@ typedef struct {
     int nwin;                 /* dense theta windows per iteration */
     int dense_mode;           /* resolved GF_DENSE_* */
     uint64_t iteration;       /* CSC iterations run */
+    int csc_mode;             /* resolved GF_CSC_* */
 } gf_engine_info;
 enum { GF_STATE_POOL = 0, GF_STATE_HG, GF_STATE_HU, GF_STATE_W, GF_STATE_IMP_NEXT, GF_STATE_NORMS,
        GF_STATE_NACC, GF_STATE_PLAN_NEXT, GF_STATE_IMP_CUR, GF_STATE_PLAN_CUR };

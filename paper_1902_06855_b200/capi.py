@@ -23,7 +23,7 @@ GF_MAX_RANKS = 16
 GF_IPC_HANDLE_BYTES = 64
 GF_RSAG_NO_EXIT_BARRIER = 1
 GF_DENSE_AUTO, GF_DENSE_RSPUSH, GF_DENSE_PULL, GF_DENSE_PUSH = range(4)
-GF_CSC_PUSH, GF_CSC_PULL = range(2)
+GF_CSC_PUSH, GF_CSC_PULL, GF_CSC_AUTO = range(3)
 (GF_STATE_POOL, GF_STATE_HG, GF_STATE_HU, GF_STATE_W, GF_STATE_IMP_NEXT, GF_STATE_NORMS, GF_STATE_NACC,
  GF_STATE_PLAN_NEXT, GF_STATE_IMP_CUR, GF_STATE_PLAN_CUR) = range(10)
 THETA_INF = (1 << 64) - 1
@@ -158,7 +158,7 @@ class EngineConfig(C.Structure):
 class EngineInfo(C.Structure):
     """gf_engine_info (include/gflow_b200.h)."""
     _fields_ = [("total", C.c_uint64), ("num_chunks", C.c_uint64), ("heap_bytes", C.c_uint64),
-                ("nwin", C.c_int), ("dense_mode", C.c_int), ("iteration", C.c_uint64)]
+                ("nwin", C.c_int), ("dense_mode", C.c_int), ("iteration", C.c_uint64), ("csc_mode", C.c_int)]
 
 
 def header_symbols() -> list[str]:

@@ -244,7 +244,7 @@ void gf_engine_config_init(gf_engine_config* c) {
     c->theta_bytes = 64ull << 20;
     c->chunk = 32000;
     c->dense_mode = GF_DENSE_AUTO;
-    c->csc_mode = GF_CSC_PUSH;
+    c->csc_mode = GF_CSC_AUTO;
     c->final_sparsity = 0.9;
     c->momentum = 0.9;
     c->learning_rate = 0.01;
@@ -260,7 +260,7 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
     if (cfg->world < 1 || cfg->world > GF_MAX_RANKS || cfg->rank < 0 || cfg->rank >= cfg->world)
         return gfi::fail(GF_ERR_CONFIG, "gf_engine_create: rank/world out of range");
     if (cfg->dense_mode < GF_DENSE_AUTO || cfg->dense_mode > GF_DENSE_PUSH || cfg->csc_mode < GF_CSC_PUSH ||
-        cfg->csc_mode > GF_CSC_PULL)
+        cfg->csc_mode > GF_CSC_AUTO)
         return gfi::fail(GF_ERR_CONFIG, "gf_engine_create: bad dense_mode / csc_mode");
     if (cfg->csc && (cfg->final_sparsity < 0.0 || cfg->final_sparsity >= 1.0))
         return gfi::fail(GF_ERR_CONFIG, "final_sparsity must be in [0, 1)");  // sparse.cpp:28-33
@@ -314,8 +314,11 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
     e->norms_off = e->stage_off + (cfg->csc ? pool_bytes : 0);
     // the routed CSC exchange (pull form, fp16 with exact norms): world-1 inbox slots of the
     // staging capacity; the selected chunks' pack stores every staged element at its owner
-    if (cfg->csc && W > 1 && cfg->csc_mode == GF_CSC_PULL && cfg->dtype == GF_F16 && cfg->chunk % 8 == 0 &&
-        e->nc <= 6144) {
+    const bool routable = cfg->csc && W > 1 && cfg->dtype == GF_F16 && cfg->chunk % 8 == 0 && e->nc <= 6144;
+    // AUTO, measured: the routed pull exchange from 4 ranks (ResNet-50 / AlexNet CSC
+    // at N=4: 0.117 / 0.207 ms vs 0.135 / 0.228 push); at N=2 both forms are within 3 %
+    if (e->cfg.csc_mode == GF_CSC_AUTO) e->cfg.csc_mode = (routable && W >= 4) ? GF_CSC_PULL : GF_CSC_PUSH;
+    if (routable && e->cfg.csc_mode == GF_CSC_PULL) {
         e->csc_slot = align_up(e->total, 8);
         e->csc_inbox = e->norms_off;
         e->norms_off += align_up(uint64_t(W - 1) * e->csc_slot * 2);
@@ -392,6 +395,7 @@ int gf_engine_info_get(gf_engine* e, gf_engine_info* out) {
     out->heap_bytes = e->heap;
     out->nwin = static_cast<int>(e->ws.size());
     out->dense_mode = e->dense_mode;
+    out->csc_mode = e->cfg.csc_mode;
     out->iteration = e->iteration;
     return GF_OK;
 }
@@ -521,25 +525,9 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
         return gf_csc_sgd_update(dt, pool, e->plan[cur], T, chunk, nc, k_cur, W, static_cast<float>(C.momentum),
                                  static_cast<float>(C.learning_rate), e->hu, e->w, us);
     };
-    // world 1 with exact norms: the update of the selected chunks needs only their packed values
-    const bool solo_split = solo && e->nacc && !e->marks_on;
-    if (solo && !solo_split) {
+    if (solo) {
         mark(e, "pack_correct", s);
         GF_ENG_OK(pack_correct(0, s));
-    } else if (solo_split) {
-        // The selected chunks' pack_correct and then their momentum update (the collective is the
-        // identity: the pool holds g_avg) on the highest-priority stream, beside the other chunks'
-        // pack_correct from the step's start (disjoint elements); the selection follows both.
-        GF_ENG_CUDA(cudaEventRecord(e->ev_sel, s));
-        GF_ENG_CUDA(cudaStreamWaitEvent(e->hp, e->ev_sel, 0));
-        GF_ENG_CUDA(cudaStreamWaitEvent(e->side, e->ev_sel, 0));
-        GF_ENG_OK(pack_correct(1, e->hp));
-        GF_ENG_OK(update(e->hp));
-        GF_ENG_CUDA(cudaEventRecord(e->ev_x, e->hp));
-        GF_ENG_OK(pack_correct(2, e->side));
-        GF_ENG_CUDA(cudaEventRecord(e->ev_rest, e->side));
-        GF_ENG_CUDA(cudaStreamWaitEvent(s, e->ev_x, 0));
-        GF_ENG_CUDA(cudaStreamWaitEvent(s, e->ev_rest, 0));
     } else {
         // the staged (important) chunks first; their exchange then runs beside the correction
         // of the other chunks (disjoint pool / hg / nacc elements), its grid capped so that the
@@ -586,9 +574,7 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
         return gf_csc_select(e->comm, e->norms_off, nc, k, e->imp[nxt], T, chunk, dt, C.theta_bytes, e->coff[nxt],
                              e->plan[nxt], e->nacc, e->nacc ? pool : nullptr, e->nacc ? e->imp[cur] : nullptr, s);
     };
-    if (solo_split) {  // the update already ran beside the packing
-        GF_ENG_OK(select());
-    } else if (e->marks_on) {  // per-kernel timing: one stream, kernels in order
+    if (e->marks_on) {  // per-kernel timing: one stream, kernels in order
         mark(e, "select", s);
         GF_ENG_OK(select());
         mark(e, "sgd_update", s);

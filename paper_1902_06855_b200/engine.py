@@ -30,7 +30,8 @@ THETA_INF = capi.THETA_INF
 _DENSE = {"auto": capi.GF_DENSE_AUTO, "rspush": capi.GF_DENSE_RSPUSH, "pull": capi.GF_DENSE_PULL,
           "push": capi.GF_DENSE_PUSH}
 _DENSE_NAME = {v: k for k, v in _DENSE.items()}
-_CSC = {"push": capi.GF_CSC_PUSH, "pull": capi.GF_CSC_PULL}
+_CSC = {"push": capi.GF_CSC_PUSH, "pull": capi.GF_CSC_PULL, "auto": capi.GF_CSC_AUTO}
+_CSC_NAME = {v: k for k, v in _CSC.items()}
 _STATE = {"pool": capi.GF_STATE_POOL, "hg": capi.GF_STATE_HG, "hu": capi.GF_STATE_HU, "w": capi.GF_STATE_W,
           "imp_next": capi.GF_STATE_IMP_NEXT, "norms": capi.GF_STATE_NORMS, "nacc": capi.GF_STATE_NACC,
           "plan_next": capi.GF_STATE_PLAN_NEXT, "imp_cur": capi.GF_STATE_IMP_CUR, "plan_cur": capi.GF_STATE_PLAN_CUR}
@@ -116,12 +117,12 @@ class GradSync:
 
     def __init__(self, sizes, rank=0, world=1, device=0, dtype=F16, theta=64 << 20,
                  chunk=32000, csc=False, final_sparsity=0.9, warmup_iters=0, momentum=0.9,
-                 lr=0.01, allgather=None, timeout_ms=30000, dense_mode="auto", csc_mode="push",
+                 lr=0.01, allgather=None, timeout_ms=30000, dense_mode="auto", csc_mode="auto",
                  _connect=True):
         if dense_mode not in _DENSE:
             raise capi.ConfigError(f"dense_mode {dense_mode!r}: auto, rspush, pull or push")
         if csc_mode not in _CSC:
-            raise capi.ConfigError(f"csc_mode {csc_mode!r}: pull or push")
+            raise capi.ConfigError(f"csc_mode {csc_mode!r}: auto, pull or push")
         self.layout = PoolLayout.build(sizes, chunk)
         self.rank, self.world, self.device, self.dtype = rank, world, device, dtype
         self.esz = 2 if dtype == F16 else 4
@@ -145,6 +146,7 @@ class GradSync:
             capi.call("gf_comm_export_handle", self.comm, h)
             capi.call("gf_engine_connect_ipc", self.eng, b"".join(allgather(bytes(h))))
         self.dense_mode = _DENSE_NAME[self.info().dense_mode] if not csc else None
+        self.csc_mode = _CSC_NAME[self.info().csc_mode] if csc else None
         self._names = C.create_string_buffer(1024)
         self._ms = (C.c_float * 64)()
 

@@ -60,7 +60,7 @@ def test_engine_config_defaults():
     cfg = capi.EngineConfig()
     capi.lib().gf_engine_config_init(C.byref(cfg))
     assert (cfg.world, cfg.rank, cfg.dtype, cfg.theta_bytes, cfg.chunk) == (1, 0, capi.GF_F16, 64 << 20, 32000)
-    assert (cfg.csc, cfg.dense_mode, cfg.csc_mode) == (0, capi.GF_DENSE_AUTO, capi.GF_CSC_PUSH)
+    assert (cfg.csc, cfg.dense_mode, cfg.csc_mode) == (0, capi.GF_DENSE_AUTO, capi.GF_CSC_AUTO)
     assert (cfg.momentum, cfg.learning_rate, cfg.timeout_ms) == (0.9, 0.01, 30000)
     with pytest.raises(capi.ConfigError):
         capi.call("gf_engine_create", C.byref(cfg), capi.u64_array([]), 0, C.byref(C.c_void_p()))
