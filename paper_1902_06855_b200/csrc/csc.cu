@@ -29,6 +29,7 @@
 #include "select.cuh"
 #include "tensor_table.cuh"
 
+
 namespace {
 
 constexpr int kNormThreads = 256;
@@ -230,7 +231,7 @@ __device__ __forceinline__ void correct8(const gfd::F8& gv, const float* hp, boo
 // K2 over one 8192-element tile of tensor table entry (tile index `tile`), by NTH threads.
 // part: 0 every chunk, 1 the important chunks only, 2 the unimportant ones only (the CSC step
 // runs part 1 first, so the exchange of the staged chunks overlaps part 2).
-template <int DT, int NTH>
+template <int DT, int NTH, int U>  // U: vectors per thread in flight before the math
 __device__ __forceinline__ void pack_correct_tile(const TensorTable& T, uint64_t tile, void* __restrict__ pool,
                                                   float* __restrict__ hg, void* __restrict__ staging,
                                                   const uint8_t* __restrict__ imp, const uint64_t* __restrict__ coff,
@@ -256,30 +257,54 @@ __device__ __forceinline__ void pack_correct_tile(const TensorTable& T, uint64_t
         uint16_t* __restrict__ d = static_cast<uint16_t*>(pool) + po;
         uint16_t* __restrict__ stg = static_cast<uint16_t*>(staging);
         const int nvec = int(len / 8);
-        for (int v0 = 0; v0 < nvec; v0 += NTH) {
-            const int v = v0 + threadIdx.x;
-            const bool act = v < nvec;
-            uint64_t c = 0, units = 0;
-            bool im = true, nan = false;
-            if (act) {
-                c = min((po + 8 * uint64_t(v)) / chunk, nc - 1);
-                im = imp[c] != 0;
+        // The tile's chunks: with chunk >= kTile a tile meets at most two (c0 and c0 + 1, split at
+        // element cb), so a vector's chunk and importance come from two compares, not a 64-bit
+        // division and a dependent flag load per vector
+        const uint64_t c0 = min(po / chunk, nc - 1), cb = (c0 + 1) * chunk;
+        const bool two = chunk >= kTile && c0 + 1 < nc;
+        const bool im0 = imp[c0] != 0, im1 = two ? imp[c0 + 1] != 0 : im0;
+        auto chunk_of = [&](uint64_t pi) {
+            return chunk >= kTile ? ((two && pi >= cb) ? c0 + 1 : c0) : min(pi / chunk, nc - 1);
+        };
+        for (int v0 = 0; v0 < nvec; v0 += U * NTH) {
+            gfd::F8 gv[U], hv[U];
+            uint64_t c[U];
+            bool im[U], mine[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int v = v0 + u * NTH + threadIdx.x;
+                const bool act = v < nvec;
+                c[u] = 0;
+                im[u] = true;
+                if (act) {
+                    const uint64_t pi = po + 8 * uint64_t(v);
+                    c[u] = chunk_of(pi);
+                    im[u] = chunk >= kTile ? (c[u] == c0 ? im0 : im1) : imp[c[u]] != 0;
+                }
+                mine[u] = act && (part == 0 || (part == 1) == im[u]);
+                if (mine[u]) {
+                    gv[u] = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
+                    hv[u] = gfd::ld32f(hg + po + 8 * uint64_t(v));
+                }
             }
-            const bool mine = act && (part == 0 || (part == 1) == im);
-            if (mine) {
-                const uint64_t pi = po + 8 * uint64_t(v);
-                const gfd::F8 gv = gfd::ld32f_stream(s + 8 * v);  // LDG.E.256
-                const gfd::F8 hv = gfd::ld32f(hg + pi);
-                float hn[8];
-                uint4 ov;
-                correct8(gv, reinterpret_cast<const float*>(&hv), im, mom, hn, ov, nan);
-                gfd::st32f(hg + pi, make_float4(hn[0], hn[1], hn[2], hn[3]),
-                           make_float4(hn[4], hn[5], hn[6], hn[7]));
-                gfd::st16(d + 8 * v, ov);
-                if (im && stg) gfd::st16(stg + coff[c] + (pi - c * chunk), ov);
-                if ((!im || !stg) && nacc) units = units8(nan ? make_uint4(0, 0, 0, 0) : ov);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int v = v0 + u * NTH + threadIdx.x;
+                uint64_t units = 0;
+                bool nan = false;
+                if (mine[u]) {
+                    const uint64_t pi = po + 8 * uint64_t(v);
+                    float hn[8];
+                    uint4 ov;
+                    correct8(gv[u], reinterpret_cast<const float*>(&hv[u]), im[u], mom, hn, ov, nan);
+                    gfd::st32f(hg + pi, make_float4(hn[0], hn[1], hn[2], hn[3]),
+                               make_float4(hn[4], hn[5], hn[6], hn[7]));
+                    gfd::st16(d + 8 * v, ov);
+                    if (im[u] && stg) gfd::st16(stg + coff[c[u]] + (pi - c[u] * chunk), ov);
+                    if ((!im[u] || !stg) && nacc) units = units8(nan ? make_uint4(0, 0, 0, 0) : ov);
+                }
+                if (nacc) nacc_add(nacc, c[u], units, nan, mine[u] && (!im[u] || !stg));
             }
-            if (nacc) nacc_add(nacc, c, units, nan, mine && (!im || !stg));
         }
         done = uint64_t(nvec) * 8;
     }
@@ -310,7 +335,7 @@ __device__ __forceinline__ void pack_correct_tile(const TensorTable& T, uint64_t
 // every chunk when staging is null: world 1, where the pool already holds the exchanged sums).
 // 4 CTAs per SM (64 registers): measured best (AlexNet CSC: 154 us; 168 us at 78 registers
 // and 3 CTAs per SM; 160 us at 5 CTAs per SM, which spills)
-template <int DT>
+template <int DT, int U>
 __global__ void __launch_bounds__(kThreads, 4)
 pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ pool,
                     float* __restrict__ hg, void* __restrict__ staging,
@@ -318,7 +343,7 @@ pack_correct_kernel(const __grid_constant__ TensorTable T, void* __restrict__ po
                     uint64_t chunk, uint64_t nc, float mom, uint64_t total_tiles,
                     uint64_t* __restrict__ nacc, int part) {
     for (uint64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x)
-        pack_correct_tile<DT, kThreads>(T, tile, pool, hg, staging, imp, coff, chunk, nc, mom, nacc, part);
+        pack_correct_tile<DT, kThreads, U>(T, tile, pool, hg, staging, imp, coff, chunk, nc, mom, nacc, part);
 }
 
 // K2 part 1 driven by the plan: only the important chunks (plan[4 .. 4+plan[1])), each cut into
@@ -333,6 +358,14 @@ __device__ __forceinline__ int tensor_of(const TensorTable& T, uint64_t e) {
         if (T.off[mid] <= e) hi = mid; else lo = mid + 1;
     }
     return (lo < T.n && e < T.off[lo] + T.cnt[lo]) ? lo : -1;
+}
+
+int k2_unroll() {  // GF_K2_U: K2 vectors per thread in flight (measurement knob; 1 or 2)
+    static const int v = [] {
+        const char* e = std::getenv("GF_K2_U");
+        return e && std::atoi(e) == 2 ? 2 : 1;
+    }();
+    return v;
 }
 
 // Staging element s <-> pool element: s lies in important chunk q = min(s / chunk, k - 1) of the
@@ -683,11 +716,14 @@ int gf_csc_pack_correct_part(int dtype, void* pool, float* hg, void* staging,
                               // them; part 2 keeps one tile per CTA, so the exchange running
                               // beside it gets SMs as CTAs retire
                               if (part == 1) grid = std::min(grid, gfi::sm_count() * 4);
-                              if (dtype == GF_F16)
-                                  pack_correct_kernel<GF_F16><<<grid, kThreads, 0, gfi::S(stream)>>>(
+                              if (dtype == GF_F16 && k2_unroll() == 2)
+                                  pack_correct_kernel<GF_F16, 2><<<grid, kThreads, 0, gfi::S(stream)>>>(
+                                      T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc, part);
+                              else if (dtype == GF_F16)
+                                  pack_correct_kernel<GF_F16, 1><<<grid, kThreads, 0, gfi::S(stream)>>>(
                                       T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc, part);
                               else
-                                  pack_correct_kernel<GF_F32><<<grid, kThreads, 0, gfi::S(stream)>>>(
+                                  pack_correct_kernel<GF_F32, 1><<<grid, kThreads, 0, gfi::S(stream)>>>(
                                       T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc, part);
                           });
 }
