@@ -333,6 +333,8 @@ __device__ __forceinline__ void pack_correct_tile(const TensorTable& T, uint64_t
 
 // K2: fused pack + correction + compaction (+ exact norms of the unimportant chunks; of
 // every chunk when staging is null: world 1, where the pool already holds the exchanged sums).
+// U = 1 vector per thread per pass: 2 in flight spills at the 64-register cap (measured, AlexNet
+// CSC N=1: 172 vs 152 us).
 // 4 CTAs per SM (64 registers): measured best (AlexNet CSC: 154 us; 168 us at 78 registers
 // and 3 CTAs per SM; 160 us at 5 CTAs per SM, which spills)
 template <int DT, int U>
@@ -358,14 +360,6 @@ __device__ __forceinline__ int tensor_of(const TensorTable& T, uint64_t e) {
         if (T.off[mid] <= e) hi = mid; else lo = mid + 1;
     }
     return (lo < T.n && e < T.off[lo] + T.cnt[lo]) ? lo : -1;
-}
-
-int k2_unroll() {  // GF_K2_U: K2 vectors per thread in flight (measurement knob; 1 or 2)
-    static const int v = [] {
-        const char* e = std::getenv("GF_K2_U");
-        return e && std::atoi(e) == 2 ? 2 : 1;
-    }();
-    return v;
 }
 
 // Staging element s <-> pool element: s lies in important chunk q = min(s / chunk, k - 1) of the
@@ -716,10 +710,7 @@ int gf_csc_pack_correct_part(int dtype, void* pool, float* hg, void* staging,
                               // them; part 2 keeps one tile per CTA, so the exchange running
                               // beside it gets SMs as CTAs retire
                               if (part == 1) grid = std::min(grid, gfi::sm_count() * 4);
-                              if (dtype == GF_F16 && k2_unroll() == 2)
-                                  pack_correct_kernel<GF_F16, 2><<<grid, kThreads, 0, gfi::S(stream)>>>(
-                                      T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc, part);
-                              else if (dtype == GF_F16)
+                              if (dtype == GF_F16)
                                   pack_correct_kernel<GF_F16, 1><<<grid, kThreads, 0, gfi::S(stream)>>>(
                                       T, pool, hg, staging, important, coff, chunk, nc, momentum, tiles, nacc, part);
                               else
@@ -736,9 +727,14 @@ int gf_csc_pack_correct_routed(gf_comm* c, void* pool, float* hg, uint64_t stage
         return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct_routed: no CSC inbox (gf_comm_set_csc_inbox)");
     if (!pool || !hg || !plan || !src || !pool_off || !count || ntensors < 1 || chunk == 0 || chunk % 8 != 0)
         return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct_routed: fp16, chunk % 8 == 0, >= 1 tensor");
-    for (int i = 1; i < ntensors; ++i)
-        if (pool_off[i] >= pool_off[i - 1])
+    uint64_t span = 0;
+    for (int i = 0; i < ntensors; ++i) {
+        if (i > 0 && pool_off[i] >= pool_off[i - 1])
             return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct_routed: tensors in ascending id (descending offsets)");
+        span = std::max(span, pool_off[i] + count[i]);
+    }
+    if (span > c->csc_slot_elems)  // every staged element must fit an inbox slot
+        return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct_routed: the pool is larger than the CSC inbox slots");
     if (stage_heap_off % 16 != 0 || stage_heap_off + c->csc_slot_elems * 2 > c->heap_bytes)
         return gfi::fail(GF_ERR_CONFIG, "gf_csc_pack_correct_routed: staging outside the heap or not 16-B aligned");
     StageRoute R;
