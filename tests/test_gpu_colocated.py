@@ -201,6 +201,48 @@ def test_colo_csc_engine_vs_reference(reference, world, csc_mode, theta):
     run_csc_vs_reference(reference, sizes, world, 1000, theta, 5, csc_mode, sparsity=0.75, warmup=2)
 
 
+@pytest.mark.parametrize("world,want", [(2, "push"), (3, "push"), (4, "pull"), (8, "pull")])
+def test_colo_csc_mode_auto_resolution(world, want):
+    """csc_mode auto: the routed pull exchange from 4 ranks, the ring below."""
+    cw = ColoWorld(world, RAGGED, csc=True)
+    try:
+        assert cw.ranks[0].csc_mode == want
+    finally:
+        cw.close()
+
+
+def test_colo_routed_csc_config_errors():
+    """gf_comm_set_csc_inbox / gf_csc_pack_correct_routed reject what would overrun the heap or
+    the inbox slots (ConfigError, nothing launched), and the routed pack needs the inbox set."""
+    import ctypes as C
+    import torch
+    from paper_1902_06855_b200 import capi
+    heap = 1 << 20
+    comms, bases, streams = raw_comms(2, heap)
+    try:
+        with pytest.raises(capi.ConfigError):  # slots past the heap
+            capi.call("gf_comm_set_csc_inbox", comms[0], heap - 1024, 4096)
+        with pytest.raises(capi.ConfigError):  # slot length not a multiple of 8
+            capi.call("gf_comm_set_csc_inbox", comms[0], 0, 1001)
+        g = torch.zeros(5000, device="cuda")
+        hg = torch.zeros(5000, device="cuda")
+        pool = torch.zeros(5000, dtype=torch.float16, device="cuda")
+        plan = torch.zeros(8, dtype=torch.int64, device="cuda")
+        args = lambda c: (c, pool.data_ptr(), hg.data_ptr(), 0, plan.data_ptr(), 1000,  # noqa: E731
+                          (C.c_void_p * 1)(g.data_ptr()), capi.u64_array([0]), capi.u64_array([5000]), 1,
+                          np.float32(0.9), streams[0])
+        with pytest.raises(capi.ConfigError):  # no inbox configured
+            capi.call("gf_csc_pack_correct_routed", *args(comms[0]))
+        capi.call("gf_comm_set_csc_inbox", comms[0], 1 << 16, 4096)
+        with pytest.raises(capi.ConfigError):  # a 5000-element pool does not fit 4096-element slots
+            capi.call("gf_csc_pack_correct_routed", *args(comms[0]))
+        capi.call("gf_comm_set_csc_inbox", comms[0], 2 ** 64 - 1, 0)  # switched back off
+        with pytest.raises(capi.ConfigError):
+            capi.call("gf_csc_pack_correct_routed", *args(comms[0]))
+    finally:
+        close_raw(comms, streams)
+
+
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("csc_mode", ["push", "pull"])
 def test_colo_alexnet_csc_full_vs_reference(reference, world, csc_mode):
