@@ -197,6 +197,8 @@ __device__ void csc_pull_range(const RingArgs& a, const char* const* src, int n,
                     h = reinterpret_cast<const uint16_t*>(src[0])[i];
                     for (int t = 1; t < n; ++t) h = gfd::acc16(reinterpret_cast<const uint16_t*>(src[t])[i], h);
                     local[i] = h;
+                    if (a.csc_push_ag)  // the all-gather as posted writes into every peer's staging
+                        for (int t = 1; t < n; ++t) reinterpret_cast<uint16_t*>(a.bufs[a.ring[(a.pos + t) % n]])[i] = h;
                 } else {
                     h = reinterpret_cast<const volatile uint16_t*>(src[0])[i];
                 }
@@ -244,6 +246,10 @@ __device__ void csc_pull_range(const RingArgs& a, const char* const* src, int n,
                     for (int t = 1; t < NS; ++t)
                         if (t < n) acc = gfd::acc16x8(x[u][t], acc);
                     gfd::st16_keep(local + vv * 8, acc);  // the peers pull it next
+                    if (a.csc_push_ag)
+#pragma unroll
+                        for (int t = 1; t < NMAX; ++t)
+                            if (t < n) gfd::st16(a.bufs[a.ring[(a.pos + t) % n]] + vv * 16, acc);
                 }
                 const uint64_t d = wb_target(a, list, k, vv * 8, c);
                 gfd::st16(reinterpret_cast<uint16_t*>(a.wb_pool) + d, acc);
@@ -296,7 +302,7 @@ __global__ void __launch_bounds__(kRingThreads) csc_pull_kernel(const __grid_con
             const int q = (a.pos + j) % n;
             uint64_t e0, e1;
             seg(w, q, e0, e1);
-            const char* owner[1] = {a.bufs[a.ring[q]]};
+            const char* owner[1] = {a.csc_push_ag ? a.bufs[a.rank] : a.bufs[a.ring[q]]};  // pushed here / pulled
             csc_pull_range<NT, false>(a, owner, n, wb_list, k, e0, e1, wg.lg, wg.LT, wg.edge_cta);
         }
     }
@@ -532,6 +538,14 @@ bool lazy_module_loading() {
 
 // GF_DIAG_NOWAIT=1: cross-GPU barriers and flags signal but never wait (timeout 0). A traffic
 // probe for ncu's serialised kernel replay (scripts/ncu_nvlink.py); every result is invalid.
+int csc_push_ag() {  // GF_CSC_PUSH_AG=1: the routed exchange's all-gather pushed by the owners (A/B)
+    static const int v = [] {
+        const char* e = std::getenv("GF_CSC_PUSH_AG");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 bool diag_nowait() {
     static const bool v = [] {
         const char* e = std::getenv("GF_DIAG_NOWAIT");
@@ -952,6 +966,7 @@ int gf_csc_exchange_pull(gf_comm* c, uint64_t stage_heap_off, const uint64_t* pl
     if (c->csc_inbox_off != UINT64_MAX) {
         a.csc_inbox = c->alloc + kFlagBytes + c->csc_inbox_off;
         a.csc_slot_bytes = c->csc_slot_elems * 2;
+        a.csc_push_ag = csc_push_ag();
     }
     const uint64_t bound = c->heap_bytes > stage_heap_off ? (c->heap_bytes - stage_heap_off) / c->world : 0;
     const dim3 grid(gfr::comm_blocks(c, bound));

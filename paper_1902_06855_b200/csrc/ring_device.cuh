@@ -38,6 +38,7 @@ struct RingArgs {
     // staging buffer and my inbox slots (ring order from my position); null: pulled from the peers
     const char* csc_inbox;
     uint64_t csc_slot_bytes;
+    int csc_push_ag;  // ... and the owners push the all-gather into every staging (read locally)
     uint64_t wstart[kMaxW];
     uint64_t wlen[kMaxW];
 };
