@@ -12,8 +12,10 @@
 //                            the unpack fused in
 //                    PULL    gf_pack -> gf_ring_allreduce_unpack (two pools used alternately)
 //                    PUSH    gf_pack -> gf_ring_allreduce -> gf_unpack
-//   CSC              gf_csc_pack_correct -> exchange + write-back + exact L1 (pull or push form)
-//                    -> gf_csc_select (next set) beside gf_csc_sgd_update on a second stream
+//   CSC              the other chunks' gf_csc_pack_correct_part on a side stream, beside the
+//                    selected chunks' pack (routed to the exchange owners from 4 ranks) and the
+//                    exchange + write-back + exact L1 (ring or routed form) on a highest-priority
+//                    stream -> gf_csc_select (next set) beside gf_csc_sgd_update
 //
 // Every FusionEngine theta window of an iteration goes into ONE flattened launch (they are all
 // known up front); the overlap API (begin_iteration / tensor_complete / finalize) launches
@@ -315,8 +317,8 @@ int gf_engine_create(const gf_engine_config* cfg, const uint64_t* sizes, int nte
     // the routed CSC exchange (pull form, fp16 with exact norms): world-1 inbox slots of the
     // staging capacity; the selected chunks' pack stores every staged element at its owner
     const bool routable = cfg->csc && W > 1 && cfg->dtype == GF_F16 && cfg->chunk % 8 == 0 && e->nc <= 6144;
-    // AUTO, measured: the routed pull exchange from 4 ranks (ResNet-50 / AlexNet CSC
-    // at N=4: 0.117 / 0.207 ms vs 0.135 / 0.228 push); at N=2 both forms are within 3 %
+    // AUTO, measured: the routed exchange from 4 ranks (ResNet-50 CSC at N=4:
+    // 0.117-0.128 ms vs 0.122-0.135 with the ring); at N=2 the ring is ahead on ResNet-50
     if (e->cfg.csc_mode == GF_CSC_AUTO) e->cfg.csc_mode = (routable && W >= 4) ? GF_CSC_PULL : GF_CSC_PUSH;
     if (routable && e->cfg.csc_mode == GF_CSC_PULL) {
         e->csc_slot = align_up(e->total, 8);
@@ -498,8 +500,10 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
     const bool fused_wb = !solo && e->nacc && chunk % 8 == 0 && nc <= 6144;
     auto exchange = [&](cudaStream_t xs) -> int {
         if (fused_wb && C.csc_mode == GF_CSC_PULL) {
-            // pull RS + pull AG straight into the pool (+ exact L1); the staging buffer is next
-            // rewritten after gf_csc_select's barrier, so no exit barrier is needed
+            // routed (csc_inbox set): local RS from my staging + inbox slots, the AG pushed into
+            // every staging and written back locally; otherwise pull RS + pull AG straight into the
+            // pool. Either way + the exact L1; the staging buffer is next rewritten after
+            // gf_csc_select's barrier, so no exit barrier is needed
             mark(e, "ring_scatter", xs);
             return gf_csc_exchange_pull(e->comm, e->stage_off, e->plan[cur], pool, chunk, nc, e->nacc, xs);
         }
@@ -529,8 +533,8 @@ int gf_engine_csc_step(gf_engine* e, const float* const* grads, void* stream) {
         mark(e, "pack_correct", s);
         GF_ENG_OK(pack_correct(0, s));
     } else {
-        // the staged (important) chunks first; their exchange then runs beside the correction
-        // of the other chunks (disjoint pool / hg / nacc elements), its grid capped so that the
+        // the staged (important) chunks and their exchange beside the correction of the other
+        // chunks (disjoint pool / hg / nacc elements), the exchange's grid capped so that the
         // packing CTAs keep the rest of the SMs
         auto capped_exchange = [&](cudaStream_t xs) {
             GF_ENG_OK(gf_comm_set_max_blocks(e->comm, e->xblocks));
