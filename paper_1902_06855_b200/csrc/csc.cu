@@ -478,65 +478,6 @@ pack_correct_planned_kernel(const __grid_constant__ TensorTable T, void* __restr
     }
 }
 
-// K6' over the staging index space (gf_csc_sgd_update, fp16, chunk % 8 == 0): the grid sweeps the
-// plan's staged elements [0, plan[0]) in 8-element vectors, kSgdFlatU per thread in flight, each
-// mapped to its pool element through the plan — one persistent grid instead of a CTA grid per chunk.
-constexpr int kSgdFlatU = 2;
-__global__ void __launch_bounds__(256)
-csc_sgd_flat_kernel(const uint16_t* __restrict__ pool, const uint64_t* __restrict__ plan, uint64_t chunk, float inv,
-                    float mom, float lr, float* __restrict__ hu, float* __restrict__ w) {
-    const uint64_t staged = plan[0], k = plan[1];
-    if (k == 0) return;
-    const uint64_t nv = staged / 8, G = uint64_t(gridDim.x) * blockDim.x;
-    for (uint64_t v0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v0 < nv; v0 += G * kSgdFlatU) {
-        uint4 x[kSgdFlatU];
-        gfd::F8 h[kSgdFlatU], ww[kSgdFlatU];
-        uint64_t e[kSgdFlatU];
-#pragma unroll
-        for (int u = 0; u < kSgdFlatU; ++u) {
-            const uint64_t v = v0 + uint64_t(u) * G;
-            if (v < nv) {
-                e[u] = staged_to_pool(plan, k, chunk, v * 8);
-                x[u] = gfd::ld16_stream(pool + e[u]);
-                h[u] = gfd::ld32f(hu + e[u]);
-                ww[u] = gfd::ld32f(w + e[u]);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kSgdFlatU; ++u) {
-            if (v0 + uint64_t(u) * G >= nv) continue;
-            float* hp = reinterpret_cast<float*>(&h[u]);
-            float* wp = reinterpret_cast<float*>(&ww[u]);
-            const uint32_t xs[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {  // csc_update (sparse.cpp:206-224), as csc_sgd_kernel
-                const float g = gfd::mul(gfd::dec(uint16_t((xs[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu)), inv);
-                const float uu = gfd::add(gfd::mul(mom, hp[q]), gfd::mul(lr, g));
-                hp[q] = uu;
-                wp[q] = gfd::sub(wp[q], uu);
-            }
-            gfd::st32f(hu + e[u], h[u].lo, h[u].hi);
-            gfd::st32f(w + e[u], ww[u].lo, ww[u].hi);
-        }
-    }
-    // the staged tail (< 8 elements: the final pool chunk's odd length), element by element
-    for (uint64_t s = nv * 8 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < staged; s += G) {
-        const uint64_t q = staged_to_pool(plan, k, chunk, s);
-        const float g = gfd::mul(gfd::dec(pool[q]), inv);
-        const float uu = gfd::add(gfd::mul(mom, hu[q]), gfd::mul(lr, g));
-        hu[q] = uu;
-        w[q] = gfd::sub(w[q], uu);
-    }
-}
-
-int sgd_flat() {  // GF_SGD_FLAT=1: the staged-space sweep (A/B measurement)
-    static const int v = [] {
-        const char* x = std::getenv("GF_SGD_FLAT");
-        return x ? std::atoi(x) : 0;
-    }();
-    return v;
-}
-
 // Staging pack (dir=0) / write-back (dir=1) over the important chunks listed in the plan
 // (plan[4+j], j < plan[1]): grid.y walks the list, grid.x tiles a chunk; 16-B copies.
 // On write-back of an fp16 pool, the exact |x| sums of the (now global) chunk values are
@@ -839,11 +780,7 @@ int gf_csc_sgd_update(int dtype, const void* pool, const uint64_t* plan, uint64_
     const uint64_t longest = std::max<uint64_t>(chunk, total - (nc - 1) * chunk);
     const int gx = int(std::max<uint64_t>(1, std::min<uint64_t>((longest / 8 + 256 * kSgdU - 1) / (256 * kSgdU), 64)));
     const dim3 grid(gx, grid_y(max_chunks, nc));
-    if (dtype == GF_F16 && sgd_flat() && chunk % 8 == 0 && (reinterpret_cast<uintptr_t>(pool) & 15u) == 0 &&
-        ((reinterpret_cast<uintptr_t>(hu) | reinterpret_cast<uintptr_t>(w)) & 31u) == 0)
-        csc_sgd_flat_kernel<<<gfi::sm_count() * 3, 256, 0, gfi::S(stream)>>>(
-            static_cast<const uint16_t*>(pool), plan, chunk, inv, momentum, lr, hu, w);
-    else if (dtype == GF_F16)
+    if (dtype == GF_F16)
         csc_sgd_kernel<GF_F16><<<grid, 256, 0, gfi::S(stream)>>>(pool, plan, total, chunk, nc, inv, momentum, lr, hu, w);
     else
         csc_sgd_kernel<GF_F32><<<grid, 256, 0, gfi::S(stream)>>>(pool, plan, total, chunk, nc, inv, momentum, lr, hu, w);

@@ -270,13 +270,30 @@ __device__ __forceinline__ void sgd_elem(const void* pool, uint64_t i, float inv
     hu[i] = u;
     w[i] = gfd::sub(w[i], u);
 }
+// vec (fp16, pool 16-B and hu/w 32-B aligned): 8 elements per thread step — one 16-byte pool load
+// and 32-byte hu/w loads/stores — with the per-element recurrence of sgd_elem; the tail scalar.
 template <int DT>
 __global__ void dense_sgd_kernel(const void* __restrict__ pool, uint64_t total, float inv_world,
-                                 float mom, float lr, float* __restrict__ hu, float* __restrict__ w) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        sgd_elem<DT>(pool, i, inv_world, mom, lr, hu, w);
+                                 float mom, float lr, float* __restrict__ hu, float* __restrict__ w, int vec) {
+    const uint64_t T = uint64_t(gridDim.x) * blockDim.x, g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nvec = (DT == GF_F16 && vec) ? total / 8 : 0;
+    for (uint64_t v = g; v < nvec; v += T) {
+        const uint4 x = gfd::ld16_stream(static_cast<const uint16_t*>(pool) + 8 * v);
+        gfd::F8 h = gfd::ld32f(hu + 8 * v), ww = gfd::ld32f(w + 8 * v);
+        float* hp = reinterpret_cast<float*>(&h);
+        float* wp = reinterpret_cast<float*>(&ww);
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float gk = gfd::mul(gfd::dec(uint16_t((xs[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu)), inv_world);
+            const float u = gfd::add(gfd::mul(mom, hp[k]), gfd::mul(lr, gk));
+            hp[k] = u;
+            wp[k] = gfd::sub(wp[k], u);
+        }
+        gfd::st32f(hu + 8 * v, h.lo, h.hi);
+        gfd::st32f(w + 8 * v, ww.lo, ww.hi);
     }
+    for (uint64_t i = nvec * 8 + g; i < total; i += T) sgd_elem<DT>(pool, i, inv_world, mom, lr, hu, w);
 }
 }  // namespace
 
@@ -373,9 +390,11 @@ int gf_dense_sgd_update(int dtype, const void* pool, uint64_t total, int world, 
     if (total == 0) return GF_OK;
     const float inv = 1.0f / static_cast<float>(world);
     if (dtype == GF_F16)
-        dense_sgd_kernel<GF_F16><<<grid_for(total, 256), 256, 0, gfi::S(stream)>>>(pool, total, inv, momentum, lr, hu, w);
+        dense_sgd_kernel<GF_F16><<<grid_for((total + 7) / 8, 256), 256, 0, gfi::S(stream)>>>(
+            pool, total, inv, momentum, lr, hu, w,
+            ((reinterpret_cast<uintptr_t>(pool) & 15u) | ((reinterpret_cast<uintptr_t>(hu) | reinterpret_cast<uintptr_t>(w)) & 31u)) == 0);
     else
-        dense_sgd_kernel<GF_F32><<<grid_for(total, 256), 256, 0, gfi::S(stream)>>>(pool, total, inv, momentum, lr, hu, w);
+        dense_sgd_kernel<GF_F32><<<grid_for(total, 256), 256, 0, gfi::S(stream)>>>(pool, total, inv, momentum, lr, hu, w, 0);
     gfi::count_launch();
     return gfi::check_launch("gf_dense_sgd_update");
 }
@@ -383,59 +402,114 @@ int gf_dense_sgd_update(int dtype, const void* pool, uint64_t total, int world, 
 }  // extern "C"
 
 // ---- rooted helpers for the host-orchestrated oracle/broadcast collectives ---------------
+// The peer-mapped buffers travel in kernel parameter space (no device pointer array, no
+// allocation per call). fp16/fp32 sums go 16 bytes at a time when every buffer is 16-byte
+// aligned, with the same per-element operation and operand order as the scalar form.
 namespace {
+struct RankPtrs {
+    char* p[GF_MAX_RANKS];
+};
+bool all_aligned16(void* const* bufs, int n) {
+    for (int r = 0; r < n; ++r)
+        if ((reinterpret_cast<uintptr_t>(bufs[r]) & 15u) != 0) return false;
+    return true;
+}
+
+// oracle_allreduce (collectives.cpp:203-226): rank 0 accumulates ranks 1..N-1 in order, then
+// every rank gets the sum. vec: elements [0, nvec*VE) as 16-byte vectors, the rest scalar.
 template <int DT>
-__global__ void oracle_sum_kernel(char* const* __restrict__ bufs_in, int world, uint64_t len) {
-    // bufs_in: device array of world pointers (peer-mapped). oracle_allreduce
-    // (collectives.cpp:203-226): rank 0 accumulates ranks 1..N-1 in order, then all get it.
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < len;
-         i += uint64_t(gridDim.x) * blockDim.x) {
+__global__ void oracle_sum_kernel(const __grid_constant__ RankPtrs B, int world, uint64_t len, int vec) {
+    constexpr int VE = DT == GF_F16 ? 8 : 4;
+    const uint64_t T = uint64_t(gridDim.x) * blockDim.x, g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nvec = vec ? len / VE : 0;
+    for (uint64_t v = g; v < nvec; v += T) {
+        uint4 acc = gfd::ld16(B.p[0] + v * 16);
+        for (int r = 1; r < world; ++r) {
+            const uint4 x = gfd::ld16(B.p[r] + v * 16);
+            acc = DT == GF_F16 ? gfd::acc16x8(acc, x) : gfd::acc32x4(acc, x);  // acc16(acc, x) per element
+        }
+        for (int r = 0; r < world; ++r) gfd::st16(B.p[r] + v * 16, acc);
+    }
+    for (uint64_t i = nvec * VE + g; i < len; i += T) {
         if (DT == GF_F16) {
-            uint16_t acc = reinterpret_cast<const uint16_t*>(bufs_in[0])[i];
-            for (int r = 1; r < world; ++r) acc = gfd::acc16(acc, reinterpret_cast<const uint16_t*>(bufs_in[r])[i]);
-            for (int r = 0; r < world; ++r) reinterpret_cast<uint16_t*>(bufs_in[r])[i] = acc;
+            uint16_t acc = reinterpret_cast<const uint16_t*>(B.p[0])[i];
+            for (int r = 1; r < world; ++r) acc = gfd::acc16(acc, reinterpret_cast<const uint16_t*>(B.p[r])[i]);
+            for (int r = 0; r < world; ++r) reinterpret_cast<uint16_t*>(B.p[r])[i] = acc;
         } else {
-            float acc = reinterpret_cast<const float*>(bufs_in[0])[i];
-            for (int r = 1; r < world; ++r) acc = gfd::add(acc, reinterpret_cast<const float*>(bufs_in[r])[i]);
-            for (int r = 0; r < world; ++r) reinterpret_cast<float*>(bufs_in[r])[i] = acc;
+            float acc = reinterpret_cast<const float*>(B.p[0])[i];
+            for (int r = 1; r < world; ++r) acc = gfd::add(acc, reinterpret_cast<const float*>(B.p[r])[i]);
+            for (int r = 0; r < world; ++r) reinterpret_cast<float*>(B.p[r])[i] = acc;
         }
     }
 }
+
 // ring_reduce_on (collectives.cpp:99-144) end state, one pass over every position's buffer
-// (bufs in ring-position order): segment j's chain starts raw at position j; position j+k
-// keeps the partial sum of positions j..j+k (what its RS step left), the root every full sum.
+// (B in ring-position order): segment j's chain starts raw at position j; position j+k keeps
+// the partial sum of positions j..j+k (what its RS step left), the root every full sum.
 template <int DT>
-__global__ void ring_reduce_kernel(char* const* __restrict__ bufs, int n, int root, uint64_t len) {
-    const uint64_t base = len / uint64_t(n), rem = len % uint64_t(n), big = rem * (base + 1);
-    for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < len;
-         e += uint64_t(gridDim.x) * blockDim.x) {
-        const int j = int(e < big ? e / (base + 1) : rem + (e - big) / base);
-        if (DT == GF_F16) {
-            uint16_t acc = reinterpret_cast<const uint16_t*>(bufs[j])[e];
-            for (int k = 1; k < n; ++k) {
-                uint16_t* b = reinterpret_cast<uint16_t*>(bufs[(j + k) % n]);
-                acc = gfd::acc16(b[e], acc);
-                b[e] = acc;
-            }
-            reinterpret_cast<uint16_t*>(bufs[root])[e] = acc;
-        } else {
-            float acc = reinterpret_cast<const float*>(bufs[j])[e];
-            for (int k = 1; k < n; ++k) {
-                float* b = reinterpret_cast<float*>(bufs[(j + k) % n]);
-                acc = gfd::add(b[e], acc);
-                b[e] = acc;
-            }
-            reinterpret_cast<float*>(bufs[root])[e] = acc;
+__device__ __forceinline__ void ring_reduce_elem(const RankPtrs& B, int n, int root, int j, uint64_t e) {
+    if (DT == GF_F16) {
+        uint16_t acc = reinterpret_cast<const uint16_t*>(B.p[j])[e];
+        for (int k = 1; k < n; ++k) {
+            uint16_t* b = reinterpret_cast<uint16_t*>(B.p[(j + k) % n]);
+            acc = gfd::acc16(b[e], acc);
+            b[e] = acc;
         }
+        reinterpret_cast<uint16_t*>(B.p[root])[e] = acc;
+    } else {
+        float acc = reinterpret_cast<const float*>(B.p[j])[e];
+        for (int k = 1; k < n; ++k) {
+            float* b = reinterpret_cast<float*>(B.p[(j + k) % n]);
+            acc = gfd::add(b[e], acc);
+            b[e] = acc;
+        }
+        reinterpret_cast<float*>(B.p[root])[e] = acc;
     }
 }
-__global__ void bcast_kernel(char* const* __restrict__ bufs_in, int world, int root, uint64_t bytes) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < bytes;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        const char v = bufs_in[root][i];
-        for (int r = 0; r < world; ++r)
-            if (r != root) bufs_in[r][i] = v;
+template <int DT>
+__global__ void ring_reduce_kernel(const __grid_constant__ RankPtrs B, int n, int root, uint64_t len, int vec) {
+    constexpr int VE = DT == GF_F16 ? 8 : 4;
+    const uint64_t base = len / uint64_t(n), rem = len % uint64_t(n), big = rem * (base + 1);
+    auto seg = [&](uint64_t e) { return int(e < big ? e / (base + 1) : rem + (e - big) / base); };
+    const uint64_t T = uint64_t(gridDim.x) * blockDim.x, g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nvec = vec ? len / VE : 0;
+    for (uint64_t v = g; v < nvec; v += T) {
+        const uint64_t e = v * VE;
+        const int j = seg(e);
+        if (seg(e + VE - 1) != j) {  // a segment boundary inside the vector: element by element
+            for (int q = 0; q < VE; ++q) ring_reduce_elem<DT>(B, n, root, seg(e + q), e + q);
+            continue;
+        }
+        uint4 acc = gfd::ld16(B.p[j] + v * 16);
+        for (int k = 1; k < n; ++k) {
+            char* b = B.p[(j + k) % n] + v * 16;
+            acc = DT == GF_F16 ? gfd::acc16x8(gfd::ld16(b), acc) : gfd::acc32x4(gfd::ld16(b), acc);
+            gfd::st16(b, acc);
+        }
+        gfd::st16(B.p[root] + v * 16, acc);
     }
+    for (uint64_t e = nvec * VE + g; e < len; e += T) ring_reduce_elem<DT>(B, n, root, seg(e), e);
+}
+
+__global__ void bcast_kernel(const __grid_constant__ RankPtrs B, int world, int root, uint64_t bytes, int vec) {
+    const uint64_t T = uint64_t(gridDim.x) * blockDim.x, g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nvec = vec ? bytes / 16 : 0;
+    for (uint64_t v = g; v < nvec; v += T) {
+        const uint4 x = gfd::ld16(B.p[root] + v * 16);
+        for (int r = 0; r < world; ++r)
+            if (r != root) gfd::st16(B.p[r] + v * 16, x);
+    }
+    for (uint64_t i = nvec * 16 + g; i < bytes; i += T) {
+        const char v = B.p[root][i];
+        for (int r = 0; r < world; ++r)
+            if (r != root) B.p[r][i] = v;
+    }
+}
+
+RankPtrs rank_ptrs(void* const* bufs, int n) {
+    RankPtrs B{};
+    for (int r = 0; r < n; ++r) B.p[r] = static_cast<char*>(bufs[r]);
+    return B;
 }
 }  // namespace
 
@@ -445,48 +519,40 @@ int gf_oracle_allreduce_ptrs(int dtype, void* const* bufs, int world, uint64_t l
     if (!gfi::valid_dtype(dtype) || !bufs || world < 1 || world > GF_MAX_RANKS)
         return gfi::fail(GF_ERR_CONFIG, "gf_oracle_allreduce_ptrs: bad arguments");
     if (world == 1 || len == 0) return GF_OK;
-    char** dptrs = nullptr;
-    GF_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dptrs), sizeof(char*) * world, gfi::S(stream)));
-    GF_CHECK_CUDA(cudaMemcpyAsync(dptrs, bufs, sizeof(char*) * world, cudaMemcpyHostToDevice, gfi::S(stream)));
+    const RankPtrs B = rank_ptrs(bufs, world);
+    const int vec = all_aligned16(bufs, world);
+    const int grid = grid_for((len + 7) / 8, 256);
     if (dtype == GF_F16)
-        oracle_sum_kernel<GF_F16><<<grid_for(len, 256), 256, 0, gfi::S(stream)>>>(dptrs, world, len);
+        oracle_sum_kernel<GF_F16><<<grid, 256, 0, gfi::S(stream)>>>(B, world, len, vec);
     else
-        oracle_sum_kernel<GF_F32><<<grid_for(len, 256), 256, 0, gfi::S(stream)>>>(dptrs, world, len);
+        oracle_sum_kernel<GF_F32><<<grid, 256, 0, gfi::S(stream)>>>(B, world, len, vec);
     gfi::count_launch();
-    const int rc = gfi::check_launch("gf_oracle_allreduce_ptrs");
-    cudaFreeAsync(dptrs, gfi::S(stream));
-    return rc;
+    return gfi::check_launch("gf_oracle_allreduce_ptrs");
 }
 
 int gf_ring_reduce_ptrs(int dtype, void* const* bufs, int n, int root_pos, uint64_t len, void* stream) {
     if (!gfi::valid_dtype(dtype) || !bufs || n < 1 || n > GF_MAX_RANKS || root_pos < 0 || root_pos >= n)
         return gfi::fail(GF_ERR_CONFIG, "gf_ring_reduce_ptrs: bad arguments");
     if (n == 1 || len == 0) return GF_OK;
-    char** dptrs = nullptr;
-    GF_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dptrs), sizeof(char*) * n, gfi::S(stream)));
-    GF_CHECK_CUDA(cudaMemcpyAsync(dptrs, bufs, sizeof(char*) * n, cudaMemcpyHostToDevice, gfi::S(stream)));
+    const RankPtrs B = rank_ptrs(bufs, n);
+    const int vec = all_aligned16(bufs, n);
+    const int grid = grid_for((len + 7) / 8, 256);
     if (dtype == GF_F16)
-        ring_reduce_kernel<GF_F16><<<grid_for(len, 256), 256, 0, gfi::S(stream)>>>(dptrs, n, root_pos, len);
+        ring_reduce_kernel<GF_F16><<<grid, 256, 0, gfi::S(stream)>>>(B, n, root_pos, len, vec);
     else
-        ring_reduce_kernel<GF_F32><<<grid_for(len, 256), 256, 0, gfi::S(stream)>>>(dptrs, n, root_pos, len);
+        ring_reduce_kernel<GF_F32><<<grid, 256, 0, gfi::S(stream)>>>(B, n, root_pos, len, vec);
     gfi::count_launch();
-    const int rc = gfi::check_launch("gf_ring_reduce_ptrs");
-    cudaFreeAsync(dptrs, gfi::S(stream));
-    return rc;
+    return gfi::check_launch("gf_ring_reduce_ptrs");
 }
 
 int gf_broadcast_ptrs(void* const* bufs, int world, int root, uint64_t bytes, void* stream) {
     if (!bufs || world < 1 || world > GF_MAX_RANKS || root < 0 || root >= world)
         return gfi::fail(GF_ERR_CONFIG, "gf_broadcast_ptrs: bad arguments");
     if (world == 1 || bytes == 0) return GF_OK;
-    char** dptrs = nullptr;
-    GF_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dptrs), sizeof(char*) * world, gfi::S(stream)));
-    GF_CHECK_CUDA(cudaMemcpyAsync(dptrs, bufs, sizeof(char*) * world, cudaMemcpyHostToDevice, gfi::S(stream)));
-    bcast_kernel<<<grid_for(bytes, 256), 256, 0, gfi::S(stream)>>>(dptrs, world, root, bytes);
+    bcast_kernel<<<grid_for((bytes + 15) / 16, 256), 256, 0, gfi::S(stream)>>>(rank_ptrs(bufs, world), world, root,
+                                                                              bytes, all_aligned16(bufs, world));
     gfi::count_launch();
-    const int rc = gfi::check_launch("gf_broadcast_ptrs");
-    cudaFreeAsync(dptrs, gfi::S(stream));
-    return rc;
+    return gfi::check_launch("gf_broadcast_ptrs");
 }
 
 }  // extern "C"
