@@ -277,7 +277,7 @@ __global__ void dense_sgd_kernel(const void* __restrict__ pool, uint64_t total, 
                                  float mom, float lr, float* __restrict__ hu, float* __restrict__ w, int vec) {
     const uint64_t T = uint64_t(gridDim.x) * blockDim.x, g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t nvec = (DT == GF_F16 && vec) ? total / 8 : 0;
-    for (uint64_t v = g; v < nvec; v += T) {
+    if constexpr (DT == GF_F16) for (uint64_t v = g; v < nvec; v += T) {
         const uint4 x = gfd::ld16_stream(static_cast<const uint16_t*>(pool) + 8 * v);
         gfd::F8 h = gfd::ld32f(hu + 8 * v), ww = gfd::ld32f(w + 8 * v);
         float* hp = reinterpret_cast<float*>(&h);
