@@ -100,3 +100,15 @@ def test_bench_reference_arm_two_ranks():
     d = lines[0]
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["unit"] == "ms" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "reference" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_bench_numa_bind_is_best_effort():
+    """bench.numa_bind never raises: without a GPU (or sysfs/affinity rights) it returns None and
+    leaves the process affinity alone."""
+    import torch
+    import bench
+    before = os.sched_getaffinity(0)
+    out = bench.numa_bind(torch, 0)
+    assert out is None or (set(out) == {"gpu_pci", "numa_node", "cpus"} and out["cpus"] >= 1)
+    if out is None:
+        assert os.sched_getaffinity(0) == before
