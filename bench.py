@@ -420,6 +420,9 @@ class Run:
         if self.csc:
             staged = int(self.read_state("plan_cur", np.uint64)[0])
             algo["pack_correct"] = total * 14 + (staged * 2 if world > 1 else 0)
+            # N>1: the selected chunks (g, hg in; hg, pool, staging out) and the others (g, hg in; hg, pool out)
+            algo["pack_correct_sel"] = staged * 16
+            algo["pack_correct_rest"] = (total - staged) * 14
             algo["scatter"] = staged * 4
             algo["sgd_update"] = staged * 18
             ring_bytes = ring_bus_bytes(esz, world, [staged])
@@ -461,7 +464,8 @@ class Run:
                 with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
                     tr = json.load(f)
                 kname = {"pack": "pack_kernel", "pack_unpack": "pack_kernel", "unpack": "unpack_kernel",
-                         "pack_correct": "pack_correct_kernel", "sgd_update": "csc_sgd_kernel",
+                         "pack_correct": "pack_correct_kernel", "pack_correct_rest": "pack_correct_kernel",
+                         "sgd_update": "csc_sgd_kernel",
                          "scatter": "compact_kernel", "select": "select_kernel", "pack_push": "pack_push_kernel",
                          "rsp": "rsp_kernel"}.get(dom)
                 ent = tr.get(self.workload, {}).get(kname or "", {})
