@@ -376,7 +376,7 @@ __device__ __forceinline__ uint64_t staged_to_pool(const uint64_t* plan, uint64_
 // to my staging when j is my ring position, else into my slot of owner j's inbox (slot t of the
 // owner at position j holds position j + 1 + t, the rspush layout). world == 0: no routing.
 struct StageRoute {
-    int world, pos;
+    int world;
     uint16_t* dst_by_pos[GF_MAX_RANKS];  // where an element of segment j is stored (staging indices)
 };
 
@@ -740,7 +740,6 @@ int gf_csc_pack_correct_routed(gf_comm* c, void* pool, float* hg, uint64_t stage
     StageRoute R;
     std::memset(&R, 0, sizeof(R));
     R.world = c->world;
-    R.pos = c->pos;
     for (int j = 0; j < c->world; ++j) {
         char* base = c->peer_alloc[c->ring[j]] + kFlagBytes;
         R.dst_by_pos[j] = j == c->pos ? reinterpret_cast<uint16_t*>(c->alloc + kFlagBytes + stage_heap_off)
